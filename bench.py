@@ -1,0 +1,447 @@
+#!/usr/bin/env python
+"""Benchmark: AirGS per-frame evaluation (decode -> rasterize -> PSNR ->
+keyframe decision) at the BASELINE.json headline config.
+
+Workload (configs[1], "N3DV-shaped"): 300k Gaussians, 18 views 1352x1014.
+One step = one frame of keyframe detection: decode that frame's GSDP delta
+payload, apply it to the canonical set, render all 18 views with SSE against
+the frame's 18 ground-truth images fused into compositing, PSNR per view,
+mean, and the tau = 30 dB decision.  Unit = evaluated views.
+
+value : device-resident inputs (payload bytes and targets already in HBM).
+e2e   : the same through the public API from pinned HOST buffers (payload
+        bytes + float64 target images copied H2D every step, qualities read
+        back D2H), timed inside the region.
+Multi-GPU (torchrun): weak scaling over frames -- each rank evaluates its
+own frames (all views), the per-frame qualities are all-gathered for the
+keyframe decisions.
+
+--impl reference: the CPU reference path (projection = oracle port, compositing
+= the reference's own compiled Cython kernel from oracle/_ref when present)
+on the host cores, same metric/config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "eval views/sec (decode+rasterize+PSNR) at 1352x1014, 300k Gaussians"
+UNIT = "views/s"
+TAU_DB = 30.0
+QUANT_STEP = 1e-4
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if sm:
+            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                   "samples": len(sm)}
+        return out
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+
+def build_workload(cfg, frames, seed, device):
+    """Canonical set, per-frame GSDP payloads and GT targets (untimed)."""
+    import torch
+
+    from paper_2512_20943_b200 import codec, rasterizer, synth
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+
+    seq = synth.Sequence(cfg, seed=seed, event_every=max(3, frames // 2) if frames > 3 else 0,
+                         event_fraction=0.02)
+    cams = synth.cameras(cfg)
+    gt0 = seq.frame(0)
+    space = CanonicalSpace(GaussianFrame(params=gt0, frame_index=0, group_key=0), capacity_U=gt0.shape[0])
+    n = gt0.shape[0]
+    payloads, targets = [], []
+    for t in range(1, frames + 1):
+        gt = seq.frame(t)
+        d = diff_frames(space.frame, GaussianFrame(params=gt[:n]))
+        payloads.append(codec.encode_delta(d, QUANT_STEP, frame_index=t, base_key=0))
+        vb = rasterizer.render_views([GaussianFrame(params=gt)], cams, [(0, v) for v in range(len(cams))],
+                                     want_images=True, device=device)
+        targets.append(vb.images)
+    torch.cuda.synchronize(device)
+    return space, cams, payloads, targets
+
+
+def evaluate_frame(space, cams, payload_dev, payload_bytes, targets_dev, device):
+    """One step: decode -> apply -> render+SSE (18 views) -> PSNR -> tau."""
+    from paper_2512_20943_b200 import codec
+    from paper_2512_20943_b200.metrics import psnr_from_sse
+    from paper_2512_20943_b200.model import GaussianFrame, apply_overlay
+    from paper_2512_20943_b200.rasterizer import render_views
+
+    n = space.frame.count
+    delta, _ = codec.decode_delta_device(payload_bytes, n, space.frame.width, device=device, payload_dev=payload_dev)
+    planes = apply_overlay(space.frame.planes(device), n, delta.overlay(device))
+    fr = GaussianFrame(device_params=planes, count=n)
+    V = len(cams)
+    vb = render_views([fr], cams, [(0, v) for v in range(V)], targets=targets_dev, device=device)
+    sse = vb.sse.cpu().numpy()
+    px = cams[0].resolution[0] * cams[0].resolution[1] * 3
+    q = float(np.mean([psnr_from_sse(s, px) for s in sse]))
+    return q, vb.launches
+
+
+def run_gpu(args):
+    import torch
+
+    from paper_2512_20943_b200 import _lib, synth
+
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+    cfg = synth.CONFIGS[args.config]
+    total = args.warmup + args.steps
+    space, cams, payloads, targets = build_workload(cfg, total, seed=args.seed + rank, device=device)
+    eng = _lib.engine(device)
+    payload_dev = [torch.frombuffer(bytearray(p.data), dtype=torch.uint8).to(device) for p in payloads]
+    stream = torch.cuda.current_stream(device)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    # ---- device-resident
+    quals = []
+    for i in range(args.warmup):
+        evaluate_frame(space, cams, payload_dev[i], payloads[i].data, targets[i], device)
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    launches0 = eng.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.warmup, total):
+        q, _ = evaluate_frame(space, cams, payload_dev[i], payloads[i].data, targets[i], device)
+        quals.append(q)
+    ev1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = (eng.launches - launches0) / args.steps
+    ms_max = ms
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    V = len(cams)
+    views = V * args.steps * world
+    value = views / (ms_max / 1e3)
+
+    # ---- kernel share / roofline: time the compositing kernel alone on one view batch
+    roof = roofline(space, cams, payload_dev, payloads, targets, device, ms_max / args.steps, args)
+
+    # ---- e2e through the public API from pinned host buffers
+    e2e = run_e2e(space, cams, payloads, targets, device, args, world)
+
+    decisions = [not (q >= TAU_DB) for q in quals]
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, cfg)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SURVEY s8(d) generator; self-rendered targets)",
+            "config": {"workload": f"{args.config} keyframe probe: decode GSDP delta + apply + render {V} views "
+                                   f"{cfg.resolution[0]}x{cfg.resolution[1]} + SSE/PSNR + tau", "gaussians": cfg.count,
+                       "views_per_step": V, "resolution": list(cfg.resolution),
+                       "l2": "inputs larger than L2 (18 float64 targets = 592 MB per step)",
+                       "parallelism": f"frame-sharded x{world}"},
+            "gpu_launches": int(round(launches)),
+            "clocks": clocks, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "keyframe_decisions": decisions, "qualities_db": [round(q, 6) for q in quals],
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def roofline(space, cams, payload_dev, payloads, targets, device, step_ms, args):
+    """Algorithmic bytes per view (float64 images) over the
+    measured per-view step time, plus the compositing kernel's share."""
+    hbm, which = _peaks()
+    cfg_n = space.frame.count
+    W = space.frame.width
+    V = len(cams)
+    P = cams[0].resolution[0] * cams[0].resolution[1]
+    s_gsdp = payloads[0].payload_bytes
+    # per frame state (amortised over V views): read canonical, payload, write params
+    per_state = cfg_n * W * 8 + s_gsdp + cfg_n * W * 8
+    per_view = per_state / V + cfg_n * W * 8 + P * 3 * 8  # read params once per view, read f64 target
+    achieved = per_view / (step_ms / V / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": which,
+            "algorithmic_bytes_per_view": int(per_view),
+            "note": "whole-step algorithmic bytes per view / measured time per view; compositing is SM-bound "
+                    "(fp64 exact path), see DESIGN.md and profiles/"}
+
+
+def run_e2e(space, cams, payloads, targets, device, args, world):
+    import torch
+
+    from paper_2512_20943_b200 import codec
+    from paper_2512_20943_b200.grouping import probe_frames
+    from paper_2512_20943_b200.model import GaussianFrame, apply_overlay
+
+    stream = torch.cuda.current_stream(device)
+    pool = min(2, len(targets))  # pinned host copies of 2 frames' targets, used cyclically
+    host_t = [[im.cpu().pin_memory() for im in targets[i]] for i in range(pool)]
+    total = args.warmup + args.steps
+    h2d = d2h = 0
+
+    def step(i):
+        nonlocal h2d, d2h
+        data = payloads[i % pool].data
+        n = space.frame.count
+        pd = torch.frombuffer(bytearray(data), dtype=torch.uint8).pin_memory().to(device, non_blocking=True)
+        tg = [t.to(device, non_blocking=True) for t in host_t[i % pool]]
+        h2d = len(data) + sum(t.numel() * 8 for t in host_t[i % pool])
+        delta, _ = codec.decode_delta_device(data, n, space.frame.width, device=device, payload_dev=pd)
+        planes = apply_overlay(space.frame.planes(device), n, delta.overlay(device))
+        q = probe_frames([GaussianFrame(device_params=planes, count=n)], cams, [tg], device=device)[0]
+        d2h = len(cams) * 8
+        return q
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(device)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.warmup, total):
+        step(i)
+    ev1.record(stream)
+    torch.cuda.synchronize(device)
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    views = len(cams) * args.steps * world
+    return {"value": round(views / (ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / baseline
+
+
+_REF_KERNEL = []
+
+
+def _ref_kernel():
+    """The reference's own compiled compositing kernel (oracle/_ref), if built."""
+    import glob
+    import importlib.util
+
+    if _REF_KERNEL:
+        return _REF_KERNEL[0]
+    hits = glob.glob(os.path.join(ROOT, "oracle", "_ref", "_composite*.so"))
+    if not hits:
+        return None
+    spec = importlib.util.spec_from_file_location("splatstream._composite", hits[0])
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    _REF_KERNEL.append(mod)
+    return mod
+
+
+def _cpu_view(job):
+    params, cam_args, target = job
+    from oracle import airgs_oracle as orc
+    from paper_2512_20943_b200.camera import Camera
+
+    cam = Camera(*cam_args)
+    pr = orc.prepare(params, cam)
+    W, H = cam.resolution
+    ker = _ref_kernel()
+    if ker is not None:
+        img = ker.forward(pr.means2d, pr.conics, pr.alphas, pr.colors, pr.bboxes, H, W)[0]
+    else:
+        img = orc.composite(pr.means2d, pr.conics, pr.alphas, pr.colors, pr.bboxes, H, W)[0]
+    return orc.psnr(np.clip(img, 0.0, 1.0), target)
+
+
+def cpu_run(cfg, views, seed=0):
+    """decode_delta + apply_delta once, then `views` x (render + psnr) in a
+    process pool; returns (views/s, cores, kind, sample)."""
+    import multiprocessing as mp
+
+    from oracle import airgs_oracle as orc
+    from paper_2512_20943_b200 import synth
+
+    seq = synth.Sequence(cfg, seed=seed, event_every=0)
+    cams = synth.cameras(cfg)[:views]
+    gt0 = seq.frame(0)
+    gt1 = seq.frame(1)
+    n = gt0.shape[0]
+    gi, gr = orc.from_dense(gt1[:n] - gt0)
+    blob = orc.gsdp_encode(gi, gr, QUANT_STEP, 1, 0)
+    # targets: take the oracle's own render of the exact frame (not timed)
+    cores = min(len(cams), os.cpu_count() or 1)
+    jobs0 = [(gt1, (c.pose, c.focal, c.resolution, c.near_clip), np.zeros((c.resolution[1], c.resolution[0], 3)))
+             for c in cams]
+    t0 = time.perf_counter()
+    di, dr, *_ = orc.gsdp_decode(blob, n, gt0.shape[1])
+    params = orc.apply(gt0, di, dr)
+    jobs = [(params, j[1], j[2]) for j in jobs0]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_view, jobs)
+    dt = time.perf_counter() - t0
+    kind = "port"
+    ker = "reference compiled Cython kernel (oracle/_ref)" if _ref_kernel() is not None else "oracle C restatement"
+    sample = (f"1 frame state (decode_delta+apply_delta) + {len(cams)} views x (project + composite + psnr) at "
+              f"{cfg.resolution[0]}x{cfg.resolution[1]}, {cfg.count} Gaussians; compositing = {ker}; "
+              f"{cores} worker processes")
+    return len(cams) / dt, cores, kind, sample
+
+
+def cpu_baseline(args, cfg):
+    try:
+        v, cores, kind, sample = cpu_run(cfg, args.cpu_views, seed=args.seed)
+        return {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+    except Exception as e:  # reported, never fatal for the GPU arm
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e!r}"}
+
+
+def run_reference(args):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    from paper_2512_20943_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    vals = []
+    for _ in range(args.warmup):
+        cpu_run(cfg, args.cpu_views, args.seed)
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_run(cfg, args.cpu_views, args.seed)
+        vals.append(last[0])
+    wall = time.perf_counter() - t0
+    v = float(np.mean(vals))
+    line = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * wall / max(args.steps, 1), 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SURVEY s8(d) generator)", "impl": "reference",
+            "config": {"workload": f"{args.config} keyframe probe, bounded CPU sample of {args.cpu_views} views/step",
+                       "gaussians": cfg.count, "resolution": list(cfg.resolution)},
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": last[1], "kind": last[2],
+                             "sample": last[3]},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-views", type=int, default=18)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

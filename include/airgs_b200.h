@@ -1,0 +1,223 @@
+/*
+ * airgs_b200 -- C-ABI of the B200-native AirGS per-frame evaluation path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * (passed as void*), returns 0 on success or a negative status whose value
+ * maps 1:1 onto the reference exception taxonomy
+ * (/root/reference/pkg/src/splatstream/errors.py:8-67), and never lets a C++
+ * exception cross the boundary.  Output buffers are caller-owned; scratch
+ * lives in an opaque per-device context that only grows (no allocation in
+ * steady-state hot calls).  Calls are reentrant per context; use one context
+ * per host thread / stream.
+ *
+ * Layouts (HBM):
+ *   params    plane-major float64 [width][ld]   (one plane per attribute, the
+ *             GSAI layout; row-major (n,width) of the reference is transposed
+ *             once at upload)
+ *   images    float64 (height, width, 3) row-major, the reference layout
+ *   usage     int64 [n] per-primitive counts
+ *
+ * See INTEGRATION.md for the reference-side bindings.
+ */
+#ifndef AIRGS_B200_H
+#define AIRGS_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define AIRGS_API __attribute__((visibility("default")))
+#else
+#define AIRGS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:8-67) ------------------------------------ */
+#define AIRGS_OK 0
+#define AIRGS_E_STRUCTURAL -1   /* StructuralError  */
+#define AIRGS_E_VALIDATION -2   /* ValidationError  */
+#define AIRGS_E_CAPACITY -3     /* CapacityError    */
+#define AIRGS_E_DECODE -5       /* DecodeError      */
+#define AIRGS_E_CUDA -100       /* CUDA runtime failure (RuntimeError) */
+#define AIRGS_E_INTERNAL -101
+
+typedef struct airgs_ctx airgs_ctx;
+
+/* Pinhole camera (ss/camera.py:16-65).  rot/trans are pose[:3,:3] and
+ * pose[:3,3]; center is -rot^T @ trans computed by the caller exactly as the
+ * reference's Camera.center property does (host numpy). */
+typedef struct airgs_camera {
+    double rot[9];
+    double trans[3];
+    double center[3];
+    double focal;
+    double near_clip;
+    int32_t width;
+    int32_t height;
+} airgs_camera;
+
+/* One primitive set (ss/model.py:125-185 GaussianFrame) resident in HBM. */
+typedef struct airgs_frame {
+    const double *params; /* plane-major [width][ld] */
+    int64_t count;        /* primitives n */
+    int64_t ld;           /* plane stride in elements, >= count */
+    int32_t width;        /* 17 (SH degree 0) or 26 (SH degree 1) */
+    int32_t reserved;
+} airgs_frame;
+
+/* One evaluated view = (frame, camera) pair.  Any output may be NULL. */
+typedef struct airgs_view_item {
+    int32_t frame;          /* index into frames[] */
+    int32_t camera;         /* index into cams[]   */
+    const double *target;   /* (h,w,3) float64 reference image for SSE, or NULL */
+    double *image;          /* (h,w,3) float64 clipped render out, or NULL */
+    int64_t *usage;         /* int64[count], counts are ADDED (+=), or NULL */
+} airgs_view_item;
+
+/* ---- context ------------------------------------------------------------ */
+AIRGS_API int airgs_ctx_create(airgs_ctx **out, int32_t device);
+AIRGS_API int airgs_ctx_destroy(airgs_ctx *ctx);
+/* Human-readable message of the last failing call on this context. */
+AIRGS_API const char *airgs_last_error(const airgs_ctx *ctx);
+/* Number of kernel launches issued by this context since creation. */
+AIRGS_API int64_t airgs_launch_count(const airgs_ctx *ctx);
+
+/* ---- rasterizer --------------------------------------------------------- */
+
+/* Batched render: replaces ss/rasterizer.py:113-240 (_activate, _prepare,
+ * render, render_with_usage) for every item at once.  sse (device float64
+ * [nitems], may be NULL) receives sum((clip(render) - target)^2) over all
+ * h*w*3 values for items with a target (ss/metrics.py:37-43 numerator).
+ * Fails with AIRGS_E_VALIDATION on a zero quaternion or non-finite parameter
+ * (ss/rasterizer.py:105-106) and AIRGS_E_STRUCTURAL on an empty frame
+ * (ss/rasterizer.py:114-115). */
+AIRGS_API int airgs_render(airgs_ctx *ctx, const airgs_frame *frames, int32_t nframes,
+                 const airgs_camera *cams, int32_t ncams,
+                 const airgs_view_item *items, int32_t nitems,
+                 double *sse, void *stream);
+
+/* The reference's pluggable compositing seam, ss/_composite.pyx:18-74
+ * forward(means2d, conics, alphas, colors, bboxes, height, width):
+ * primitives already in depth order with clipped int64 bboxes.  Writes the
+ * UNclipped image (h,w,3), final transmittance (h,w) and usage int64[k]
+ * (all device, caller-owned).  record=True (training masks) is not
+ * supported by this path. */
+AIRGS_API int airgs_composite_forward(airgs_ctx *ctx, int64_t k, const double *means2d,
+                            const double *conics, const double *alphas,
+                            const double *colors, const int64_t *bboxes,
+                            int32_t height, int32_t width, double *image,
+                            double *t_final, int64_t *usage, void *stream);
+
+/* Sum of squared differences of two device float64 arrays of n values
+ * (ss/metrics.py:40 numerator), deterministic order.  out: device double. */
+AIRGS_API int airgs_sse(airgs_ctx *ctx, const double *a, const double *b, int64_t n,
+              double *out, void *stream);
+
+/* ---- codec (ss/codec.py) ------------------------------------------------ */
+
+/* GSAI attribute planes -> plane-major params (ss/codec.py:95-121,161-169).
+ * blob: device copy of the container bytes.  The caller parses and validates
+ * the 25-byte header on the host (magic, version, depth, truncation) and
+ * passes n (count), m (planes), plane_pixels = w*h.  Each plane j starts at
+ * byte 25 + j*(16 + 2*plane_pixels): (scale, offset) f64 LE then u16 LE.
+ * out[j*ld + i] = (double)q * scale_j + offset_j (separate mul, add). */
+AIRGS_API int airgs_gsai_decode(airgs_ctx *ctx, const uint8_t *blob, int64_t nbytes,
+                      int64_t n, int32_t m, int64_t plane_pixels,
+                      double *out, int64_t ld, void *stream);
+
+/* GSDP payload -> dense delta overlay (ss/codec.py:217-248).
+ * payload: device bytes; entry_count / quant_step from the host-parsed
+ * 24-byte header; width = param_width.  Decodes the gap varints in parallel,
+ * prefix-sums them to indices, and scatters rows[c*ld + idx] =
+ * (double)q * quant_step and present[idx] = 1 (later duplicates win).
+ * Writes the number of distinct entries to *entries_out (device int64) and
+ * the strictly increasing entry indices to idx_out (device int64[entry_count]).
+ * rows == NULL decodes the indices only (no range check, no scatter).
+ * Errors: AIRGS_E_DECODE (truncated varint / varint too long / truncated
+ * payload), AIRGS_E_STRUCTURAL (index >= base_count). */
+AIRGS_API int airgs_gsdp_decode(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes,
+                      int64_t entry_count, double quant_step, int32_t width,
+                      int64_t base_count, double *rows, int64_t ld,
+                      uint8_t *present, int64_t *idx_out, int64_t *entries_out,
+                      void *stream);
+
+/* Position after the entry_count gap varints (sequential walk, reference
+ * order); *err_out: 0 ok, 1 truncated varint, 2 varint too long.  Used to
+ * infer param_width when the caller does not pin it (ss/codec.py:235-240). */
+AIRGS_API int airgs_gsdp_varint_end(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes,
+                          int64_t entry_count, int64_t *pos_out, int32_t *err_out,
+                          void *stream);
+
+/* Server-side encoders (ss/codec.py:124-158,187-214).
+ * airgs_plane_minmax: per plane (min, max) of params -> lohi_out (host
+ * double[2*m], interleaved).  The caller derives scale_j = (hi-lo)/65535 (0
+ * for a constant plane) exactly as encode_frame does, then
+ * airgs_gsai_encode writes u16 planes [m][plane_pixels] (device) with
+ * clip(rint((v - lo)/scale), 0, 65535), zero padding beyond n. */
+AIRGS_API int airgs_plane_minmax(airgs_ctx *ctx, const double *params, int64_t n, int32_t m,
+                                 int64_t ld, double *lohi_out, void *stream);
+AIRGS_API int airgs_gsai_encode(airgs_ctx *ctx, const double *params, int64_t n, int32_t m,
+                                int64_t ld, const double *lo, const double *scale,
+                                int64_t plane_pixels, uint16_t *planes, void *stream);
+/* GSDP body for the entries with nz[i] != 0 (use airgs_quantize first):
+ * gap varints then i32 rows, written to out[24 ..] (device); the caller
+ * writes the 24-byte header.  capacity >= 24 + E*(10 + 4*width). */
+AIRGS_API int airgs_gsdp_encode(airgs_ctx *ctx, const double *rows, const uint8_t *nz, int64_t n,
+                                int32_t width, int64_t ld, double step, uint8_t *out,
+                                int64_t capacity, int64_t *nbytes_out, int64_t *entries_out,
+                                void *stream);
+
+/* ---- delta algebra (ss/model.py:241-311) -------------------------------- */
+
+/* n-way compose of dense overlays in list order with one |.|max > eps filter
+ * at the end (ss/model.py:294-311); sign[d] = -1 negates overlay d
+ * (DeltaTensor.negate, ss/model.py:241-246).  apply_eps = 0 skips the filter
+ * (the base-is-empty shortcut of ss/pruning.py:111). */
+AIRGS_API int airgs_delta_compose(airgs_ctx *ctx, int32_t ndeltas, const double *const *rows,
+                        const uint8_t *const *present, const double *signs,
+                        int64_t n, int32_t width, int64_t ld, double eps,
+                        int32_t apply_eps, double *out_rows, uint8_t *out_present,
+                        void *stream);
+
+/* params_out = canonical + selected overlay row (ss/model.py:269-284).
+ * Overlay A (rows_a/present_a) is used for primitive i when
+ *   (sel_a == NULL || sel_a[i]) && (keep_rank == NULL || keep_rank[i] >= keep_min)
+ * -- the pruning-level mask of ss/pruning.py:79-90 -- and overlay B
+ * (rows_b/present_b, may be NULL) otherwise.  A selected overlay whose
+ * present flag is 0 leaves the canonical row untouched. */
+AIRGS_API int airgs_delta_apply(airgs_ctx *ctx, const double *canonical, const double *rows_a,
+                      const uint8_t *present_a, const uint8_t *sel_a, const int32_t *keep_rank,
+                      int32_t keep_min, const double *rows_b, const uint8_t *present_b,
+                      int64_t n, int32_t width, int64_t ld, double *params_out, void *stream);
+
+/* ---- pruning (ss/pruning.py, ss/codec.py:187-214) ------------------------ */
+
+/* Quantisation rule of encode_delta: q = rint(v/step) per component; an
+ * entry survives iff any q != 0.  nz_out[i] = survives (u8, 0 for absent).
+ * Fails with AIRGS_E_STRUCTURAL if a surviving |q| > 2^31-1 (first offending
+ * index in *bad_index_out, host int64).  deq_out (optional, plane-major like
+ * rows) receives the decoded values q*step of surviving entries: exactly what
+ * decode_delta(encode_delta(.)) yields (ss/codec.py:195,247). */
+AIRGS_API int airgs_quantize(airgs_ctx *ctx, const double *rows, const uint8_t *present,
+                   int64_t n, int32_t width, int64_t ld, double step,
+                   uint8_t *nz_out, double *deq_out, int64_t *bad_index_out, void *stream);
+
+/* Usage-ordered prune ranks (ss/pruning.py:72-76): among present entries,
+ * order by (usage ascending, index descending); rank_out[i] = position in
+ * that order (INT32_MAX for absent).  *count_out (host) = entry count. */
+AIRGS_API int airgs_prune_rank(airgs_ctx *ctx, const uint8_t *present, const int64_t *usage,
+                     int64_t n, int32_t *rank_out, int64_t *count_out, void *stream);
+
+/* Exact GSDP sizes for L pruning levels (ss/codec.py:200-207): level l keeps
+ * entries with rank >= kmin[l] that also survive quantisation (nz).  size =
+ * 24 + sum varint_len(gap) + 4*width*kept.  sizes_out: host int64[L]. */
+AIRGS_API int airgs_level_sizes(airgs_ctx *ctx, const uint8_t *nz, const int32_t *rank,
+                      int64_t n, int32_t width, const int64_t *kmin, int32_t nlevels,
+                      int64_t *sizes_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AIRGS_B200_H */

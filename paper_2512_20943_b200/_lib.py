@@ -1,0 +1,180 @@
+"""ctypes binding of ``lib/libairgs_b200.so`` (the C-ABI in
+``include/airgs_b200.h``) plus the per-device engine that owns a context.
+
+There is no CPU fallback: if the shared library is missing, or no sm_100
+GPU is visible, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libairgs_b200.so")
+
+c_double_p = ctypes.POINTER(ctypes.c_double)
+c_i64_p = ctypes.POINTER(ctypes.c_int64)
+vp = ctypes.c_void_p
+i32 = ctypes.c_int32
+i64 = ctypes.c_int64
+f64 = ctypes.c_double
+
+
+class CameraC(ctypes.Structure):
+    _fields_ = [
+        ("rot", ctypes.c_double * 9),
+        ("trans", ctypes.c_double * 3),
+        ("center", ctypes.c_double * 3),
+        ("focal", ctypes.c_double),
+        ("near_clip", ctypes.c_double),
+        ("width", ctypes.c_int32),
+        ("height", ctypes.c_int32),
+    ]
+
+
+class FrameC(ctypes.Structure):
+    _fields_ = [
+        ("params", ctypes.c_void_p),
+        ("count", ctypes.c_int64),
+        ("ld", ctypes.c_int64),
+        ("width", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+class ItemC(ctypes.Structure):
+    _fields_ = [
+        ("frame", ctypes.c_int32),
+        ("camera", ctypes.c_int32),
+        ("target", ctypes.c_void_p),
+        ("image", ctypes.c_void_p),
+        ("usage", ctypes.c_void_p),
+    ]
+
+
+# name -> (restype, argtypes); must match include/airgs_b200.h exactly
+SIGNATURES = {
+    "airgs_ctx_create": (ctypes.c_int, [ctypes.POINTER(vp), i32]),
+    "airgs_ctx_destroy": (ctypes.c_int, [vp]),
+    "airgs_last_error": (ctypes.c_char_p, [vp]),
+    "airgs_launch_count": (i64, [vp]),
+    "airgs_render": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), i32, ctypes.POINTER(CameraC), i32,
+                                    ctypes.POINTER(ItemC), i32, vp, vp]),
+    "airgs_composite_forward": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp]),
+    "airgs_sse": (ctypes.c_int, [vp, vp, vp, i64, vp, vp]),
+    "airgs_gsai_decode": (ctypes.c_int, [vp, vp, i64, i64, i32, i64, vp, i64, vp]),
+    "airgs_gsdp_decode": (ctypes.c_int, [vp, vp, i64, i64, f64, i32, i64, vp, i64, vp, vp, vp, vp]),
+    "airgs_gsdp_varint_end": (ctypes.c_int, [vp, vp, i64, i64, c_i64_p, ctypes.POINTER(i32), vp]),
+    "airgs_plane_minmax": (ctypes.c_int, [vp, vp, i64, i32, i64, c_double_p, vp]),
+    "airgs_gsai_encode": (ctypes.c_int, [vp, vp, i64, i32, i64, c_double_p, c_double_p, i64, vp, vp]),
+    "airgs_gsdp_encode": (ctypes.c_int, [vp, vp, vp, i64, i32, i64, f64, vp, i64, c_i64_p, c_i64_p, vp]),
+    "airgs_delta_compose": (ctypes.c_int, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), c_double_p, i64, i32,
+                                           i64, f64, i32, vp, vp, vp]),
+    "airgs_delta_apply": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, i32, vp, vp, i64, i32, i64, vp, vp]),
+    "airgs_quantize": (ctypes.c_int, [vp, vp, vp, i64, i32, i64, f64, vp, vp, c_i64_p, vp]),
+    "airgs_prune_rank": (ctypes.c_int, [vp, vp, vp, i64, vp, c_i64_p, vp]),
+    "airgs_level_sizes": (ctypes.c_int, [vp, vp, vp, i64, i32, c_i64_p, i32, c_i64_p, vp]),
+}
+
+_STATUS = {
+    -1: errors.StructuralError,
+    -2: errors.ValidationError,
+    -3: errors.CapacityError,
+    -5: errors.DecodeError,
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library():
+    """Load the shared library (no GPU needed) and bind every symbol."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"airgs_b200 CUDA library not built: {LIB_PATH} is missing "
+                    "(run `python -c 'import __graft_entry__ as g; g.build()'`)"
+                )
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+class Engine:
+    """One airgs context on one CUDA device (scratch workspace owner)."""
+
+    def __init__(self, device: int):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("airgs_b200 requires a CUDA device (sm_100); none is visible")
+        self.lib = load_library()
+        self.device = int(device)
+        self.torch_device = torch.device("cuda", self.device)
+        ctx = vp()
+        rc = self.lib.airgs_ctx_create(ctypes.byref(ctx), self.device)
+        if rc != 0:
+            raise RuntimeError(f"airgs_ctx_create failed on cuda:{self.device} (status {rc}); an sm_100 GPU is required")
+        self.ctx = ctx
+
+    def stream(self):
+        import torch
+
+        return vp(torch.cuda.current_stream(self.torch_device).cuda_stream)
+
+    def call(self, name, *args):
+        rc = getattr(self.lib, name)(self.ctx, *args)
+        if rc != 0:
+            msg = (self.lib.airgs_last_error(self.ctx) or b"").decode(errors="replace")
+            exc = _STATUS.get(rc)
+            if exc is None:
+                raise RuntimeError(f"{name} failed (status {rc}): {msg}")
+            raise exc(msg)
+        return rc
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.airgs_launch_count(self.ctx))
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None):
+                self.lib.airgs_ctx_destroy(self.ctx)
+        except Exception:
+            pass
+
+
+_engines: dict = {}
+
+
+def engine(device=None) -> Engine:
+    """The process-wide engine for ``device`` (default: torch's current)."""
+    import torch
+
+    if device is None:
+        device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+    if isinstance(device, torch.device):
+        device = device.index if device.index is not None else torch.cuda.current_device()
+    device = int(device)
+    with _lock:
+        eng = _engines.get(device)
+    if eng is None:
+        eng = Engine(device)
+        with _lock:
+            _engines[device] = eng
+    return eng
+
+
+def ptr(t) -> vp:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return vp(0 if t is None else t.data_ptr())

@@ -1,0 +1,32 @@
+// Context lifecycle of the airgs_b200 C-ABI.
+#include "context.h"
+
+using namespace airgs;
+
+extern "C" int airgs_ctx_create(airgs_ctx **out, int32_t device) {
+    if (!out) return AIRGS_E_INTERNAL;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return AIRGS_E_CUDA;
+    if (cudaSetDevice(device) != cudaSuccess) return AIRGS_E_CUDA;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return AIRGS_E_CUDA;
+    if (prop.major < 10) return AIRGS_E_CUDA;  // built for sm_100a only
+    airgs_ctx *c = new (std::nothrow) airgs_ctx();
+    if (!c) return AIRGS_E_INTERNAL;
+    c->device = device;
+    *out = c;
+    return AIRGS_OK;
+}
+
+extern "C" int airgs_ctx_destroy(airgs_ctx *ctx) {
+    if (!ctx) return AIRGS_OK;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    delete ctx;
+    return AIRGS_OK;
+}
+
+extern "C" const char *airgs_last_error(const airgs_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+extern "C" int64_t airgs_launch_count(const airgs_ctx *ctx) { return ctx ? ctx->launches : 0; }

@@ -1,0 +1,484 @@
+// Wire-format decode on device (ss/codec.py).
+//
+//  * GSAI: u16 attribute planes at odd byte offsets -> float64 planes.  One
+//    thread decodes 8 consecutive pixels from two aligned 128-bit loads
+//    (funnel-shifted), and writes them as four 128-bit stores.
+//  * GSDP: gap varints are decoded in parallel -- a terminator flag per byte,
+//    a warp-scan over the flags numbers the varints, each terminator thread
+//    walks back <= 9 continuation bytes, and a second scan turns gaps into
+//    indices; the i32 rows are dequantised and scattered into a dense
+//    plane-major overlay.  Malformed payloads are re-walked by one device
+//    thread in the reference's exact sequential order so the error class and
+//    message match ss/codec.py:217-248.
+#include <algorithm>
+#include <vector>
+
+#include "context.h"
+#include "scan_sort.cuh"
+
+namespace airgs {
+
+__device__ __forceinline__ double load_f64_unaligned(const uint8_t *p) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v |= (uint64_t)p[k] << (8 * k);
+    return __longlong_as_double((long long)v);
+}
+
+__global__ void __launch_bounds__(256)
+k_gsai_decode(const uint8_t *__restrict__ blob, int64_t nbytes, int64_t n, int64_t pp,
+              double *__restrict__ out, int64_t ld) {
+    const int j = blockIdx.y;
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (i0 >= n) return;
+    const int64_t hdr = 25 + (int64_t)j * (16 + 2 * pp);  // (scale, offset) of plane j
+    const double scale = load_f64_unaligned(blob + hdr);
+    const double offset = load_f64_unaligned(blob + hdr + 8);
+    const uintptr_t addr = (uintptr_t)(blob + hdr + 16 + 2 * i0);
+    const uintptr_t a0 = addr & ~uintptr_t(15);
+    const int sh = (int)(addr & 15);
+    const uintptr_t end = (uintptr_t)(blob + nbytes);
+    const uint4 w0 = *reinterpret_cast<const uint4 *>(a0);
+    uint4 w1 = make_uint4(0, 0, 0, 0);
+    if (sh && a0 + 16 < end) w1 = *reinterpret_cast<const uint4 *>(a0 + 16);
+    unsigned __int128 lo = ((unsigned __int128)(((uint64_t)w0.w << 32) | w0.z) << 64) | (((uint64_t)w0.y << 32) | w0.x);
+    unsigned __int128 hi = ((unsigned __int128)(((uint64_t)w1.w << 32) | w1.z) << 64) | (((uint64_t)w1.y << 32) | w1.x);
+    unsigned __int128 v = sh ? ((lo >> (8 * sh)) | (hi << (128 - 8 * sh))) : lo;
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t q = (uint32_t)(v >> (16 * k)) & 0xffffu;
+        r[k] = (double)q * scale + offset;  // separate mul and add (-fmad=false)
+    }
+    double *o = out + (int64_t)j * ld + i0;
+    if (i0 + 8 <= n && ((uintptr_t)o & 15) == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) *reinterpret_cast<double2 *>(o + k) = make_double2(r[k], r[k + 1]);
+    } else {
+        for (int k = 0; k < 8 && i0 + k < n; ++k) o[k] = r[k];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// GSDP
+
+struct TermIn {
+    const uint8_t *p;  // start of the varint section
+    __device__ int64_t operator()(int, int64_t i) const { return (p[i] & 0x80) ? 0 : 1; }
+};
+struct TermOut {
+    const uint8_t *p;
+    int64_t *gaps;
+    unsigned int *flags;
+    __device__ void operator()(int, int64_t i, int64_t ex, int64_t v) const {
+        if (!v) return;
+        // varint ex ends at byte i; walk back over its continuation bytes
+        uint64_t val = 0;
+        int len = 1;
+        while (i - len >= 0 && (p[i - len] & 0x80)) ++len;
+        if (len > 10) atomicOr(flags, (unsigned)kFlagVarintLong);
+        bool big = false;
+        for (int k = 0; k < len && k < 10; ++k) {
+            const uint64_t b = p[i - len + 1 + k] & 0x7f;
+            if (k == 9 && b > 1) big = true;  // value >= 2^63: can only be out of range
+            val |= b << (7 * k);
+        }
+        if (big) atomicOr(flags, (unsigned)kFlagIndexRange);
+        gaps[ex] = (int64_t)val;
+    }
+};
+struct GapIn {
+    const int64_t *gaps;
+    __device__ int64_t operator()(int, int64_t i) const { return gaps[i]; }
+};
+struct GapOut {
+    int64_t *idx;
+    __device__ void operator()(int, int64_t i, int64_t ex, int64_t v) const { idx[i] = ex + v; }
+};
+
+__global__ void __launch_bounds__(256)
+k_gsdp_rows(const uint8_t *__restrict__ qbytes, const int64_t *__restrict__ idx, int64_t E, int W,
+            double step, int64_t base_count, double *__restrict__ rows, int64_t ld,
+            uint8_t *__restrict__ present, unsigned int *flags, unsigned long long *bad,
+            unsigned long long *distinct) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = e < E ? idx[e] : 0;
+    // a later duplicate wins (dict semantics); count distinct entries
+    const bool live = e < E && !(e + 1 < E && idx[e + 1] == i);
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(distinct, (unsigned long long)__popc(m));
+    if (e >= E) return;
+    if (i < 0 || i >= base_count) {
+        atomicOr(flags, (unsigned)kFlagIndexRange);
+        atomicMin(bad, (unsigned long long)i);
+        return;
+    }
+    if (!live) return;
+    const uint8_t *q = qbytes + 4 * (int64_t)W * e;
+    for (int c = 0; c < W; ++c) {
+        const int32_t v = (int32_t)((uint32_t)q[4 * c] | ((uint32_t)q[4 * c + 1] << 8) |
+                                    ((uint32_t)q[4 * c + 2] << 16) | ((uint32_t)q[4 * c + 3] << 24));
+        rows[(int64_t)c * ld + i] = (double)v * step;
+    }
+    present[i] = 1;
+}
+
+// Sequential re-walk of the varint section in the reference's order
+// (ss/codec.py:44-58,229-242).  out[0] = error code (1 truncated varint,
+// 2 varint too long, 0 none), out[1] = position after the last varint.
+__global__ void k_gsdp_walk(const uint8_t *__restrict__ p, int64_t nbytes, int64_t E, int64_t *out) {
+    if (threadIdx.x || blockIdx.x) return;
+    int64_t pos = 24;
+    for (int64_t e = 0; e < E; ++e) {
+        int shift = 0;
+        while (true) {
+            if (pos >= nbytes) {
+                out[0] = 1;
+                out[1] = pos;
+                return;
+            }
+            const uint8_t b = p[pos++];
+            if (!(b & 0x80)) break;
+            shift += 7;
+            if (shift > 63) {
+                out[0] = 2;
+                out[1] = pos;
+                return;
+            }
+        }
+    }
+    out[0] = 0;
+    out[1] = pos;
+}
+
+
+// ---------------------------------------------------------------------------
+// encoders (server side, ss/codec.py:124-158,187-214)
+
+__global__ void __launch_bounds__(256)
+k_plane_minmax_partial(const double *__restrict__ params, int64_t n, int64_t ld, int nblk,
+                       double *__restrict__ part) {
+    const int j = blockIdx.y;
+    const double *p = params + (int64_t)j * ld;
+    double lo = INFINITY, hi = -INFINITY;
+    const int64_t per = ceil_div(n, (int64_t)nblk);
+    const int64_t b0 = per * blockIdx.x, b1 = min(n, b0 + per);
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += 256) {
+        const double v = p[i];
+        lo = fmin(lo, v);
+        hi = fmax(hi, v);
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+        lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, d));
+        hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, d));
+    }
+    __shared__ double sl[8], sh[8];
+    if ((threadIdx.x & 31) == 0) {
+        sl[threadIdx.x >> 5] = lo;
+        sh[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 8; ++k) {
+            lo = fmin(lo, sl[k]);
+            hi = fmax(hi, sh[k]);
+        }
+        part[((int64_t)j * nblk + blockIdx.x) * 2] = lo;
+        part[((int64_t)j * nblk + blockIdx.x) * 2 + 1] = hi;
+    }
+}
+
+__global__ void k_plane_minmax_final(const double *__restrict__ part, int nblk, int m, double *__restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    double lo = INFINITY, hi = -INFINITY;
+    for (int b = 0; b < nblk; ++b) {
+        lo = fmin(lo, part[((int64_t)j * nblk + b) * 2]);
+        hi = fmax(hi, part[((int64_t)j * nblk + b) * 2 + 1]);
+    }
+    out[2 * j] = lo;
+    out[2 * j + 1] = hi;
+}
+
+struct PlaneQ {
+    double lo[32];
+    double scale[32];
+};
+
+__global__ void __launch_bounds__(256)
+k_gsai_quantize(const double *__restrict__ params, int64_t n, int64_t ld, int64_t pp, PlaneQ q,
+                uint16_t *__restrict__ planes) {
+    const int j = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= pp) return;
+    uint16_t v = 0;
+    const double sc = q.scale[j];
+    if (i < n && sc != 0.0) {
+        // np.clip(np.rint((col - lo) / scale), 0, QMAX).astype(np.uint16)
+        const double r = rint((params[(int64_t)j * ld + i] - q.lo[j]) / sc);
+        v = (uint16_t)fmin(fmax(r, 0.0), 65535.0);
+    }
+    planes[(int64_t)j * pp + i] = v;
+}
+
+struct NzIn {
+    const uint8_t *nz;
+    __device__ int64_t operator()(int, int64_t i) const { return nz[i] ? 1 : 0; }
+};
+struct NzOut {
+    int64_t *cidx;
+    __device__ void operator()(int, int64_t i, int64_t ex, int64_t v) const {
+        if (v) cidx[ex] = i;
+    }
+};
+
+__device__ __forceinline__ int varint_bytes(uint64_t v) {
+    int k = 1;
+    while (v > 0x7f) {
+        v >>= 7;
+        ++k;
+    }
+    return k;
+}
+
+struct VlenIn {
+    const int64_t *cidx;
+    __device__ int64_t operator()(int, int64_t e) const {
+        const int64_t prev = e ? cidx[e - 1] : 0;
+        return varint_bytes((uint64_t)(cidx[e] - prev));
+    }
+};
+struct VlenOut {
+    const int64_t *cidx;
+    uint8_t *out;  // payload base
+    __device__ void operator()(int, int64_t e, int64_t ex, int64_t) const {
+        uint64_t v = (uint64_t)(cidx[e] - (e ? cidx[e - 1] : 0));
+        uint8_t *p = out + 24 + ex;
+        while (v > 0x7f) {
+            *p++ = (uint8_t)((v & 0x7f) | 0x80);
+            v >>= 7;
+        }
+        *p = (uint8_t)v;
+    }
+};
+
+__global__ void __launch_bounds__(256)
+k_gsdp_write_rows(const double *__restrict__ rows, int64_t ld, int W, double step, const int64_t *__restrict__ cidx,
+                  int64_t E, uint8_t *__restrict__ dst) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= E * W) return;
+    const int64_t e = t / W;
+    const int c = (int)(t % W);
+    const int64_t i = cidx[e];
+    const int32_t q = (int32_t)(long long)rint(rows[(int64_t)c * ld + i] / step);
+    uint8_t *p = dst + 4 * t;
+    const uint32_t u = (uint32_t)q;
+    p[0] = (uint8_t)u;
+    p[1] = (uint8_t)(u >> 8);
+    p[2] = (uint8_t)(u >> 16);
+    p[3] = (uint8_t)(u >> 24);
+}
+
+static void gsai_impl(airgs_ctx *ctx, const uint8_t *blob, int64_t nbytes, int64_t n, int m, int64_t pp, double *out,
+                      int64_t ld, cudaStream_t st) {
+    if (m <= 0 || n < 0 || pp < n) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad attribute image geometry");
+    if (25 + (int64_t)m * (16 + 2 * pp) > nbytes) throw ApiFailure(AIRGS_E_DECODE, "truncated attribute image container");
+    if (n == 0) return;
+    dim3 grid((unsigned)ceil_div(n, 256 * 8), (unsigned)m);
+    k_gsai_decode<<<grid, 256, 0, st>>>(blob, nbytes, n, pp, out, ld);
+    ++ctx->launches;
+    check_launch();
+}
+
+static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, int64_t E, double step, int W,
+                      int64_t base_count, double *rows, int64_t ld, uint8_t *present, int64_t *idx_out,
+                      int64_t *entries_out, cudaStream_t st) {
+    if (nbytes < 24) throw ApiFailure(AIRGS_E_DECODE, "delta payload shorter than its header");
+    if (W <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad parameter width");
+    int64_t &L = ctx->launches;
+    const int64_t V = nbytes - 24 - 4 * E * (int64_t)W;  // varint section length if well formed
+    unsigned int *flags = ctx->scratch_t<unsigned int>(kSlotFlags, 4);
+    int64_t *misc = ctx->scratch_t<int64_t>(kSlotMisc3, 8);
+    AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
+    bool ok = V >= 0 && V >= E && V <= 10 * E;
+    int64_t nterm = -1;
+    int64_t *gaps = ctx->scratch_t<int64_t>(kSlotKeys, (size_t)std::max<int64_t>(E, 1));
+    if (ok && E > 0) {
+        // terminators in the section must be exactly E and the section must end on one
+        int64_t *dV = misc;  // count for the scan driver
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(dV, &V, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        const int bps = (int)std::max<int64_t>(1, ceil_div(V, kScanTile));
+        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
+        // gaps[] is written only for ex < E; protect against over-count by sizing V
+        int64_t *gbuf = ctx->scratch_t<int64_t>(kSlotKeysAlt, (size_t)V + 1);
+        seg_scan<int64_t>(TermIn{payload + 24}, TermOut{payload + 24, gbuf, flags}, dV, 1, V, blocks, misc + 1, st, &L);
+        check_launch();
+        int64_t h[2];
+        uint8_t last = 0;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(h, misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&last, payload + 24 + V - 1, 1, cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        nterm = h[0];
+        ok = nterm == E && !(last & 0x80);
+        if (ok) gaps = gbuf;
+    } else if (ok && E == 0) {
+        ok = V == 0;
+    }
+    if (!ok) {
+        // exact reference error path
+        k_gsdp_walk<<<1, 1, 0, st>>>(payload, nbytes, E, misc);
+        ++L;
+        int64_t h[2];
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(h, misc, sizeof(h), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h[0] == 1) throw ApiFailure(AIRGS_E_DECODE, "truncated varint");
+        if (h[0] == 2) throw ApiFailure(AIRGS_E_DECODE, "varint too long");
+        throw ApiFailure(AIRGS_E_DECODE, "truncated delta payload");
+    }
+    if (E == 0) {
+        int64_t z = 0;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(entries_out, &z, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        return;
+    }
+    // indices = inclusive prefix sum of gaps
+    {
+        int64_t *dE = misc + 2;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(dE, &E, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        const int bps = (int)std::max<int64_t>(1, ceil_div(E, kScanTile));
+        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
+        seg_scan<int64_t>(GapIn{gaps}, GapOut{idx_out}, dE, 1, E, blocks, (int64_t *)nullptr, st, &L);
+        check_launch();
+    }
+    unsigned long long *bad = (unsigned long long *)(misc + 4);
+    if (rows == nullptr) {  // indices only (caller infers base_count)
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        return;
+    }
+    {
+        const unsigned long long mx = ~0ull;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(bad, &mx, sizeof(mx), cudaMemcpyHostToDevice, st));
+        AIRGS_CUDA_TRY(cudaMemsetAsync(entries_out, 0, sizeof(int64_t), st));
+        k_gsdp_rows<<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(payload + 24 + V, idx_out, E, W, step, base_count, rows,
+                                                              ld, present, flags, bad,
+                                                              (unsigned long long *)entries_out);
+        ++L;
+        check_launch();
+    }
+    unsigned int hf = 0;
+    unsigned long long hbad = 0;
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, st));
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hf & kFlagVarintLong) throw ApiFailure(AIRGS_E_DECODE, "varint too long");
+    if (hf & kFlagIndexRange)
+        throw ApiFailure(AIRGS_E_STRUCTURAL, "delta index " + std::to_string((long long)hbad) + " out of range");
+}
+
+}  // namespace airgs
+
+using namespace airgs;
+
+
+extern "C" int airgs_plane_minmax(airgs_ctx *ctx, const double *params, int64_t n, int32_t m, int64_t ld,
+                                  double *lohi_out, void *stream) {
+    return guarded(ctx, [&] {
+        cudaStream_t st = (cudaStream_t)stream;
+        if (n <= 0 || m <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "empty frame");
+        const int nblk = (int)std::min<int64_t>(256, ceil_div(n, 4096));
+        double *part = ctx->scratch_t<double>(kSlotMisc0, (size_t)2 * nblk * m + 2 * m);
+        double *fin = part + (size_t)2 * nblk * m;
+        k_plane_minmax_partial<<<dim3((unsigned)nblk, (unsigned)m), 256, 0, st>>>(params, n, ld, nblk, part);
+        k_plane_minmax_final<<<1, 64, 0, st>>>(part, nblk, m, fin);
+        ctx->launches += 2;
+        check_launch();
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(lohi_out, fin, sizeof(double) * 2 * m, cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    });
+}
+
+extern "C" int airgs_gsai_encode(airgs_ctx *ctx, const double *params, int64_t n, int32_t m, int64_t ld,
+                                 const double *lo, const double *scale, int64_t plane_pixels, uint16_t *planes,
+                                 void *stream) {
+    return guarded(ctx, [&] {
+        if (m <= 0 || m > 32) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad attribute count");
+        if (n > plane_pixels)
+            throw ApiFailure(AIRGS_E_CAPACITY, std::to_string((long long)n) + " primitives exceed image capacity");
+        PlaneQ q;
+        for (int j = 0; j < m; ++j) {
+            q.lo[j] = lo[j];
+            q.scale[j] = scale[j];
+        }
+        if (plane_pixels <= 0) return;
+        k_gsai_quantize<<<dim3((unsigned)ceil_div(plane_pixels, 256), (unsigned)m), 256, 0, (cudaStream_t)stream>>>(
+            params, n, ld, plane_pixels, q, planes);
+        ++ctx->launches;
+        check_launch();
+    });
+}
+
+extern "C" int airgs_gsdp_encode(airgs_ctx *ctx, const double *rows, const uint8_t *nz, int64_t n, int32_t width,
+                                 int64_t ld, double step, uint8_t *out, int64_t capacity, int64_t *nbytes_out,
+                                 int64_t *entries_out, void *stream) {
+    return guarded(ctx, [&] {
+        cudaStream_t st = (cudaStream_t)stream;
+        int64_t &L = ctx->launches;
+        *nbytes_out = 24;
+        *entries_out = 0;
+        if (n <= 0) return;
+        int64_t *misc = ctx->scratch_t<int64_t>(kSlotMisc3, 8);
+        int64_t *cidx = ctx->scratch_t<int64_t>(kSlotKeys, n);
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(misc, &n, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        const int bps = (int)std::max<int64_t>(1, ceil_div(n, kScanTile));
+        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
+        seg_scan<int64_t>(NzIn{nz}, NzOut{cidx}, misc, 1, n, blocks, misc + 1, st, &L);
+        check_launch();
+        int64_t E = 0;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&E, misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        if (E == 0) return;
+        if (24 + E * (10 + 4 * (int64_t)width) > capacity) throw ApiFailure(AIRGS_E_CAPACITY, "encode buffer too small");
+        seg_scan<int64_t>(VlenIn{cidx}, VlenOut{cidx, out}, misc + 1, 1, E, blocks, misc + 2, st, &L);
+        check_launch();
+        int64_t V = 0;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&V, misc + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        k_gsdp_write_rows<<<(unsigned)ceil_div(E * width, 256), 256, 0, st>>>(rows, ld, width, step, cidx, E,
+                                                                              out + 24 + V);
+        ++L;
+        check_launch();
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        *nbytes_out = 24 + V + 4 * (int64_t)width * E;
+        *entries_out = E;
+    });
+}
+
+extern "C" int airgs_gsai_decode(airgs_ctx *ctx, const uint8_t *blob, int64_t nbytes, int64_t n, int32_t m,
+                                 int64_t plane_pixels, double *out, int64_t ld, void *stream) {
+    return guarded(ctx, [&] { gsai_impl(ctx, blob, nbytes, n, m, plane_pixels, out, ld, (cudaStream_t)stream); });
+}
+
+extern "C" int airgs_gsdp_varint_end(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, int64_t entry_count,
+                                     int64_t *pos_out, int32_t *err_out, void *stream) {
+    return guarded(ctx, [&] {
+        cudaStream_t st = (cudaStream_t)stream;
+        int64_t *misc = ctx->scratch_t<int64_t>(kSlotMisc3, 8);
+        k_gsdp_walk<<<1, 1, 0, st>>>(payload, nbytes, entry_count, misc);
+        ++ctx->launches;
+        check_launch();
+        int64_t h[2];
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(h, misc, sizeof(h), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        *err_out = (int32_t)h[0];
+        *pos_out = h[1];
+    });
+}
+
+extern "C" int airgs_gsdp_decode(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, int64_t entry_count,
+                                 double quant_step, int32_t width, int64_t base_count, double *rows, int64_t ld,
+                                 uint8_t *present, int64_t *idx_out, int64_t *entries_out, void *stream) {
+    return guarded(ctx, [&] {
+        gsdp_impl(ctx, payload, nbytes, entry_count, quant_step, width, base_count, rows, ld, present, idx_out,
+                  entries_out, (cudaStream_t)stream);
+    });
+}

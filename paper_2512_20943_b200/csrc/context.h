@@ -1,0 +1,117 @@
+// Per-device context: grow-only HBM workspace + pinned staging.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct airgs_ctx {
+    int device = 0;
+    std::string err;
+    int64_t launches = 0;
+    struct Buf {
+        void *p = nullptr;
+        size_t cap = 0;
+    };
+    std::vector<Buf> bufs;
+    void *host = nullptr;
+    size_t host_cap = 0;
+
+    // Device scratch slot `id`, at least `bytes` long.  Growing synchronises
+    // the device first (rare: capacity only grows).
+    void *scratch(int id, size_t bytes) {
+        if ((size_t)id >= bufs.size()) bufs.resize(id + 1);
+        Buf &b = bufs[id];
+        if (b.cap < bytes) {
+            size_t want = std::max(bytes, b.cap + b.cap / 4);
+            want = (want + 255) & ~size_t(255);
+            AIRGS_CUDA_TRY(cudaDeviceSynchronize());
+            if (b.p) AIRGS_CUDA_TRY(cudaFree(b.p));
+            b.p = nullptr;
+            b.cap = 0;
+            AIRGS_CUDA_TRY(cudaMalloc(&b.p, want));
+            b.cap = want;
+        }
+        return b.p;
+    }
+    template <typename T>
+    T *scratch_t(int id, size_t count) {
+        return static_cast<T *>(scratch(id, std::max<size_t>(count, 1) * sizeof(T)));
+    }
+    // Pinned host staging (descriptor uploads, small readbacks).  Callers
+    // synchronise the stream before a later call reuses it.
+    void *staging(size_t bytes) {
+        if (host_cap < bytes) {
+            size_t want = std::max(bytes, size_t(1) << 16);
+            if (host) AIRGS_CUDA_TRY(cudaFreeHost(host));
+            host = nullptr;
+            host_cap = 0;
+            AIRGS_CUDA_TRY(cudaMallocHost(&host, want));
+            host_cap = want;
+        }
+        return host;
+    }
+    ~airgs_ctx() {
+        for (auto &b : bufs)
+            if (b.p) cudaFree(b.p);
+        if (host) cudaFreeHost(host);
+    }
+};
+
+// scratch slot ids
+namespace airgs {
+enum Slot : int {
+    kSlotDesc = 0,
+    kSlotRecs,
+    kSlotDepth,
+    kSlotNtiles,
+    kSlotKeys,
+    kSlotVals,
+    kSlotKeysAlt,
+    kSlotValsAlt,
+    kSlotPairOff,
+    kSlotScanBlocks,
+    kSlotItemStats,
+    kSlotPairKeys,
+    kSlotPairVals,
+    kSlotPairKeysAlt,
+    kSlotPairValsAlt,
+    kSlotRanges,
+    kSlotSseTiles,
+    kSlotHist,
+    kSlotFlags,
+    kSlotMisc0,
+    kSlotMisc1,
+    kSlotMisc2,
+    kSlotMisc3,
+    kSlotCount
+};
+
+// Run fn() translating failures into status codes / messages on ctx.
+template <typename F>
+int guarded(airgs_ctx *ctx, F &&fn) {
+    if (!ctx) return AIRGS_E_INTERNAL;
+    try {
+        ctx->err.clear();
+        AIRGS_CUDA_TRY(cudaSetDevice(ctx->device));
+        fn();
+        return AIRGS_OK;
+    } catch (const ApiFailure &f) {
+        ctx->err = f.what;
+        return f.code;
+    } catch (const CudaFailure &f) {
+        ctx->err = f.what;
+        return AIRGS_E_CUDA;
+    } catch (const std::exception &e) {
+        ctx->err = e.what();
+        return AIRGS_E_INTERNAL;
+    } catch (...) {
+        ctx->err = "unknown failure";
+        return AIRGS_E_INTERNAL;
+    }
+}
+
+inline void check_launch() { AIRGS_CUDA_TRY(cudaGetLastError()); }
+
+}  // namespace airgs

@@ -1,0 +1,184 @@
+"""Keyframe detection on device (drop-in for the probe half of
+``ss/grouping.py``).
+
+``frame_quality`` = arithmetic-mean PSNR over the evaluation cameras of the
+frame's renders against ground truth (ss/grouping.py:153-159);
+``quality_probe`` applies a delta first (:162-166); a frame stays in its
+group iff ``q >= tau`` (:213), otherwise it becomes a keyframe.
+``probe_frames`` evaluates many candidate frames x views in one batched
+render with SSE fused into compositing -- the C2 keyframe-detection workload.
+The training loop of ``build_groups`` (fit_group_frame / fit_keyframe) is
+outside the evaluation path.
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+
+from . import device as dv
+from .errors import StructuralError, ValidationError
+from .metrics import psnr_from_sse
+from .model import CanonicalSpace, DeltaTensor, apply_delta
+
+DEFAULT_TAU_DB = 30.0
+
+
+class GroundTruth:
+    """Per-camera target images of one time step (as ss/train.py:92-107)."""
+
+    __slots__ = ("images", "_dev")
+
+    def __init__(self, images):
+        object.__setattr__(self, "images", tuple(np.asarray(im, dtype=np.float64) for im in images))
+        object.__setattr__(self, "_dev", None)
+
+    def __setattr__(self, k, v):
+        raise AttributeError("GroundTruth is immutable")
+
+    def check_cameras(self, cams):
+        check_targets(self.images, cams)
+
+    def device_images(self, device=None):
+        import torch
+
+        dev = dv.device_of(device)
+        if self._dev is None or self._dev[0].device != dev:
+            object.__setattr__(self, "_dev", [torch.from_numpy(np.ascontiguousarray(im)).to(dev)
+                                              for im in self.images])
+        return self._dev
+
+
+def check_targets(images, cams):
+    if len(images) != len(cams):
+        raise StructuralError("target image count does not match cameras")
+    for im, cam in zip(images, cams):
+        w, h = cam.resolution
+        if tuple(im.shape) != (h, w, 3):
+            raise StructuralError("target resolution does not match camera")
+
+
+def _device_targets(target, cams, dev):
+    import torch
+
+    if isinstance(target, GroundTruth):
+        target.check_cameras(cams)
+        return target.device_images(dev)
+    imgs = getattr(target, "images", target)
+    out = []
+    for im in imgs:
+        if isinstance(im, torch.Tensor):
+            out.append(im.to(device=dev, dtype=torch.float64).contiguous())
+        else:
+            out.append(torch.from_numpy(np.ascontiguousarray(np.asarray(getattr(im, "pixels", im),
+                                                                        dtype=np.float64))).to(dev))
+    check_targets(out, cams)
+    return out
+
+
+def frame_quality(frame, cams, target) -> float:
+    """Mean PSNR of the frame's renders against the targets."""
+    return probe_frames([frame], cams, [target])[0]
+
+
+def quality_probe(space: CanonicalSpace, delta: DeltaTensor, target, cams) -> float:
+    return frame_quality(apply_delta(space, delta), cams, target)
+
+
+def probe_frames(frames, cams, targets, device=None) -> list:
+    """Mean-over-views PSNR of each frame against its targets, all
+    (frame, view) pairs in one batched render."""
+    from .rasterizer import render_views
+
+    dev = dv.device_of(device)
+    cams = list(cams)
+    frames = list(frames)
+    if not cams:
+        raise ValidationError("at least one camera required")
+    tgts = [_device_targets(t, cams, dev) for t in targets]
+    items, tlist = [], []
+    for f in range(len(frames)):
+        for v in range(len(cams)):
+            items.append((f, v))
+            tlist.append(tgts[f][v])
+    vb = render_views(frames, cams, items, targets=tlist, device=dev)
+    sse = vb.sse.cpu().numpy()
+    V = len(cams)
+    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+    return [float(np.mean([psnr_from_sse(sse[f * V + v], px[v]) for v in range(V)])) for f in range(len(frames))]
+
+
+def is_keyframe(quality_db: float, tau_db: float = DEFAULT_TAU_DB) -> bool:
+    """The grouping decision: re-anchor when the probe misses tau
+    (ss/grouping.py:213)."""
+    return not quality_db >= tau_db
+
+
+class GroupSpan:
+    __slots__ = ("key", "start", "end")
+
+    def __init__(self, key, start, end):
+        if not key == start <= end:
+            raise StructuralError(f"bad group span ({key}, {start}, {end})")
+        object.__setattr__(self, "key", key)
+        object.__setattr__(self, "start", start)
+        object.__setattr__(self, "end", end)
+
+    def __setattr__(self, k, v):
+        raise AttributeError("GroupSpan is immutable")
+
+    def __eq__(self, o):
+        return isinstance(o, GroupSpan) and (self.key, self.start, self.end) == (o.key, o.start, o.end)
+
+
+class GroupPlan:
+    __slots__ = ("tau_db", "groups")
+
+    def __init__(self, tau_db, groups):
+        groups = tuple(groups)
+        if not groups or groups[0].start != 0:
+            raise StructuralError("group plan must start at frame 0")
+        for a, b in zip(groups, groups[1:]):
+            if b.start != a.end + 1:
+                raise StructuralError("group spans must be contiguous")
+        object.__setattr__(self, "tau_db", tau_db)
+        object.__setattr__(self, "groups", groups)
+
+    def __setattr__(self, k, v):
+        raise AttributeError("GroupPlan is immutable")
+
+    def __eq__(self, o):
+        return isinstance(o, GroupPlan) and self.tau_db == o.tau_db and self.groups == o.groups
+
+    @property
+    def frame_count(self) -> int:
+        return self.groups[-1].end + 1
+
+    def group_of(self, frame_index: int) -> GroupSpan:
+        for g in self.groups:
+            if g.start <= frame_index <= g.end:
+                return g
+        raise ValidationError(f"frame {frame_index} outside the plan")
+
+    def to_json(self) -> str:
+        return json.dumps({"tau": self.tau_db,
+                           "groups": [{"key": g.key, "start": g.start, "end": g.end} for g in self.groups]},
+                          indent=2)
+
+    @staticmethod
+    def from_json(text: str) -> "GroupPlan":
+        obj = json.loads(text)
+        return GroupPlan(tau_db=float(obj["tau"]),
+                         groups=tuple(GroupSpan(g["key"], g["start"], g["end"]) for g in obj["groups"]))
+
+
+def plan_from_decisions(keyframe_flags, tau_db=DEFAULT_TAU_DB) -> GroupPlan:
+    """Group spans from per-frame keyframe decisions (frame 0 always opens)."""
+    spans = []
+    for t, k in enumerate(keyframe_flags):
+        if t == 0 or k:
+            spans.append([t, t, t])
+        else:
+            spans[-1][2] = t
+    return GroupPlan(tau_db, tuple(GroupSpan(*s) for s in spans))

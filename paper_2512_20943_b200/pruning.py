@@ -1,0 +1,356 @@
+"""Usage-frequency pruning on device (drop-in for ``ss/pruning.py``).
+
+``build_level_space`` runs entirely in HBM: quantise the gap once
+(decode(encode(.)) values and the survive mask), order entries by
+(usage asc, index desc) with a radix sort, compute every level's exact GSDP
+size in one kernel, then materialise each surviving level's frame with the
+pruning-level selector folded into ``apply`` and evaluate all (level, view)
+pairs in one batched render whose SSE against the unpruned reconstruction is
+fused into compositing.  Only level sizes, per-view SSE and (for the API
+result) the pruned index sets come back to the host.
+
+``select_pruning_level`` (Algorithm 1) and ``ilp_optimal`` are scalar
+host logic over the level table, as in the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import device as dv
+from .codec import quantize_overlay
+from .errors import StructuralError, ValidationError
+from .metrics import psnr_from_sse
+from .model import EPS_SPARSE, CanonicalSpace, DeltaTensor, _compose_call, apply_overlay
+
+MIN_DROP = 1e-12
+
+
+class PruningLevel:
+    __slots__ = ("ratio", "quality_db", "size_bytes", "pruned_indices")
+
+    def __init__(self, ratio, quality_db, size_bytes, pruned_indices):
+        object.__setattr__(self, "ratio", ratio)
+        object.__setattr__(self, "quality_db", quality_db)
+        object.__setattr__(self, "size_bytes", size_bytes)
+        object.__setattr__(self, "pruned_indices", tuple(pruned_indices))
+
+    def __setattr__(self, k, v):
+        raise AttributeError("PruningLevel is immutable")
+
+    def __eq__(self, o):
+        return isinstance(o, PruningLevel) and (self.ratio, self.quality_db, self.size_bytes,
+                                                 self.pruned_indices) == (o.ratio, o.quality_db, o.size_bytes,
+                                                                          o.pruned_indices)
+
+    def __repr__(self):
+        return (f"PruningLevel(ratio={self.ratio}, quality_db={self.quality_db}, size_bytes={self.size_bytes}, "
+                f"pruned={len(self.pruned_indices)})")
+
+
+class PruningLevelSpace:
+    __slots__ = ("levels", "frame_index")
+
+    def __init__(self, levels, frame_index):
+        levels = tuple(levels)
+        if not levels or levels[0].ratio != 0.0:
+            raise StructuralError("level space must start at ratio 0")
+        if any(b.ratio <= a.ratio for a, b in zip(levels, levels[1:])):
+            raise StructuralError("ratios must be strictly increasing")
+        if any(b.size_bytes >= a.size_bytes for a, b in zip(levels, levels[1:])):
+            raise StructuralError("sizes must be strictly decreasing")
+        object.__setattr__(self, "levels", levels)
+        object.__setattr__(self, "frame_index", frame_index)
+
+    def __setattr__(self, k, v):
+        raise AttributeError("PruningLevelSpace is immutable")
+
+    def qualities(self):
+        return [lv.quality_db for lv in self.levels]
+
+    def sizes(self):
+        return [lv.size_bytes for lv in self.levels]
+
+
+class SelectionContext:
+    __slots__ = ("bandwidth_B", "target_rate_R", "cliff_beta")
+
+    def __init__(self, bandwidth_B, target_rate_R, cliff_beta=2.0):
+        if bandwidth_B <= 0 or target_rate_R <= 0 or cliff_beta <= 0:
+            raise ValidationError("selection context values must be positive")
+        object.__setattr__(self, "bandwidth_B", bandwidth_B)
+        object.__setattr__(self, "target_rate_R", target_rate_R)
+        object.__setattr__(self, "cliff_beta", cliff_beta)
+
+    def __setattr__(self, k, v):
+        raise AttributeError("SelectionContext is immutable")
+
+    @property
+    def budget_bytes(self) -> float:
+        """C = B / R bits per frame, in bytes."""
+        return self.bandwidth_B / self.target_rate_R / 8.0
+
+
+class FrameSelection:
+    __slots__ = ("frame_index", "level", "quality_db", "feasible")
+
+    def __init__(self, frame_index, level, quality_db, feasible):
+        for k, v in (("frame_index", frame_index), ("level", level), ("quality_db", quality_db),
+                     ("feasible", feasible)):
+            object.__setattr__(self, k, v)
+
+    def __setattr__(self, k, v):
+        raise AttributeError("FrameSelection is immutable")
+
+    def __eq__(self, o):
+        return isinstance(o, FrameSelection) and (self.frame_index, self.level, self.quality_db, self.feasible) == (
+            o.frame_index, o.level, o.quality_db, o.feasible)
+
+    def __repr__(self):
+        return f"FrameSelection({self.frame_index}, {self.level}, {self.quality_db}, {self.feasible})"
+
+
+# ---------------------------------------------------------------------------
+# device helpers
+
+
+def _engine(dev):
+    from ._lib import engine
+
+    return engine(dev)
+
+
+def _ptr(t):
+    from ._lib import ptr
+
+    return ptr(t)
+
+
+def _usage_tensor(usage, n, dev):
+    import torch
+
+    counts = usage.counts if hasattr(usage, "counts") else usage
+    if isinstance(counts, torch.Tensor):
+        if counts.shape[0] < n:
+            raise StructuralError("usage counts do not cover the primitive set")
+        return counts[:n].to(device=dev, dtype=torch.int64).contiguous()
+    counts = np.asarray(counts)
+    if counts.shape[0] < n:
+        raise StructuralError("usage counts do not cover the primitive set")
+    return torch.from_numpy(np.ascontiguousarray(counts[:n].astype(np.int64))).to(dev)
+
+
+def prune_ranks(ov: dv.Overlay, usage_t):
+    """rank[i] = position of entry i in the (usage asc, index desc) order;
+    INT32_MAX for absent.  Returns (rank tensor, entry count)."""
+    import torch
+
+    eng = _engine(ov.rows.device)
+    rank = torch.empty((ov.ld,), dtype=torch.int32, device=ov.rows.device)
+    cnt = ctypes.c_int64(0)
+    eng.call("airgs_prune_rank", _ptr(ov.present), _ptr(usage_t), ov.n, _ptr(rank), ctypes.byref(cnt), eng.stream())
+    return rank, int(cnt.value)
+
+
+def level_sizes(nz, rank, n, width, kmins, dev):
+    eng = _engine(dev)
+    L = len(kmins)
+    k = (ctypes.c_int64 * L)(*[int(v) for v in kmins])
+    out = (ctypes.c_int64 * L)()
+    eng.call("airgs_level_sizes", _ptr(nz), _ptr(rank), n, width, k, L, out, eng.stream())
+    return [int(v) for v in out]
+
+
+def _k_of(ratio, entries):
+    return int(math.floor(ratio * entries + 0.5))
+
+
+# ---------------------------------------------------------------------------
+# reference API
+
+
+def prune_order(delta: DeltaTensor, usage_counts) -> list:
+    """Entry indices, lowest usage first, ties prune the higher index first
+    (ss/pruning.py:72-76)."""
+    ov = delta.overlay()
+    if ov.n == 0:
+        return []
+    rank, e = prune_ranks(ov, _usage_tensor(usage_counts, ov.n, ov.rows.device))
+    idx, _ = ov.entries()
+    r = rank[: ov.n].cpu().numpy()[idx]
+    return [int(i) for i in idx[np.argsort(r, kind="stable")]]
+
+
+def prune_delta(delta: DeltaTensor, usage_counts, ratio: float):
+    """Remove the ``ratio`` fraction of lowest-usage entries
+    (ss/pruning.py:79-90).  Returns (kept DeltaTensor, sorted removed tuple)."""
+    ov = delta.overlay()
+    if ov.n == 0:
+        return DeltaTensor(delta.base_count, delta.param_width, {}), ()
+    rank, e = prune_ranks(ov, _usage_tensor(usage_counts, ov.n, ov.rows.device))
+    k = _k_of(ratio, e)
+    keep = (rank >= k).to(ov.present.dtype) * ov.present
+    kept = DeltaTensor(delta.base_count, delta.param_width,
+                       overlay=dv.Overlay(ov.rows, keep, ov.n, ov.width))
+    removed_mask = (ov.present.bool() & (rank < k))[: ov.n]
+    removed = tuple(int(i) for i in np.nonzero(removed_mask.cpu().numpy())[0])
+    return kept, removed
+
+
+class LevelPlan:
+    """Device state shared by every pruning level of one gap (see
+    ``build_level_space``)."""
+
+    __slots__ = ("canon", "n", "width", "A", "B", "nz", "rank", "entries", "idx_host", "rank_host")
+
+
+def plan_levels(delta: DeltaTensor, space: CanonicalSpace, usage, quant_step: float, base: DeltaTensor = None):
+    import torch
+
+    fr = space.frame
+    dev = dv.device_of(None)
+    n, w = fr.count, fr.width
+    canon = fr.planes(dev)
+    G = delta.overlay(dev)
+    usage_t = _usage_tensor(usage, n, dev)
+    nz, D = quantize_overlay(G, quant_step, want_decoded=True)
+    eng = _engine(dev)
+    Dov = dv.Overlay(D, nz, n, w)
+    if base is not None and not base.is_empty():
+        Bov = base.overlay(dev)
+        A = dv.Overlay.empty(n, w, dev)
+        _compose_call(eng, [(Bov.rows, Bov.present, 1.0), (Dov.rows, Dov.present, 1.0)], n, w, A.ld, EPS_SPARSE,
+                      True, A)
+        Bonly = dv.Overlay.empty(n, w, dev)
+        _compose_call(eng, [(Bov.rows, Bov.present, 1.0)], n, w, Bonly.ld, EPS_SPARSE, True, Bonly)
+    else:
+        A, Bonly = Dov, None
+    rank, entries = prune_ranks(G, usage_t)
+    p = LevelPlan()
+    p.canon, p.n, p.width = canon, n, w
+    p.A, p.B, p.nz, p.rank, p.entries = A, Bonly, nz, rank, entries
+    p.idx_host = None
+    p.rank_host = None
+    return p
+
+
+def level_frame_planes(p: LevelPlan, kmin):
+    """Parameters of the level that prunes ranks < kmin (None: unpruned)."""
+    if kmin is None:
+        return apply_overlay(p.canon, p.n, p.A)
+    return apply_overlay(p.canon, p.n, p.A, sel=p.nz, rank=p.rank, keep_min=int(kmin), ov_b=p.B)
+
+
+def _removed_sets(p: LevelPlan, G, kmins):
+    if p.idx_host is None:
+        idx, _ = G.entries()
+        p.idx_host = idx
+        p.rank_host = p.rank[: p.n].cpu().numpy()[idx] if idx.size else np.zeros(0, dtype=np.int32)
+    return [tuple(p.idx_host[p.rank_host < k].tolist()) for k in kmins]
+
+
+def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, usage, quant_step: float,
+                      base: DeltaTensor = None, frame_index: int = 0) -> PruningLevelSpace:
+    """Dense (quality, size) space over pruning ratios (ss/pruning.py:93-137).
+
+    Quality of a level = mean over ``cams`` of PSNR of its reconstruction
+    against the unpruned quantised reconstruction; sizes are exact GSDP
+    payload sizes; a level whose size does not shrink is dropped.
+    """
+    from .model import GaussianFrame
+    from .rasterizer import render_views
+
+    ratios = sorted(set(float(r) for r in ratios))
+    if not ratios or ratios[0] != 0.0:
+        raise StructuralError("ratios must include 0")
+    counts = usage.counts if hasattr(usage, "counts") else usage
+    if len(counts) < space.frame.count:
+        raise StructuralError("usage counts do not cover the primitive set")
+    if delta.base_count != space.frame.count:
+        raise StructuralError(f"delta base_count {delta.base_count} != space count {space.frame.count}")
+    cams = list(cams)
+    if quant_step <= 0:
+        raise StructuralError("quant_step must be positive")
+    p = plan_levels(delta, space, usage, quant_step, base)
+    kmins = [_k_of(r, p.entries) for r in ratios]
+    sizes = level_sizes(p.nz, p.rank, p.n, p.width, kmins, p.canon.device)
+    keep_levels = []
+    last = None
+    for j, s in enumerate(sizes):
+        if last is not None and s >= last:
+            continue  # duplicate level (ss/pruning.py:125-126)
+        keep_levels.append(j)
+        last = s
+    removed = _removed_sets(p, delta.overlay(), [kmins[j] for j in keep_levels])
+    qualities = [100.0] * len(keep_levels)
+    if cams:
+        ref = GaussianFrame(device_params=level_frame_planes(p, None), count=p.n, frame_index=frame_index,
+                            group_key=space.key_index)
+        rv = render_views([ref], cams, [(0, v) for v in range(len(cams))], want_images=True)
+        frames = [GaussianFrame(device_params=level_frame_planes(p, kmins[j]), count=p.n) for j in keep_levels]
+        items, targets = [], []
+        for li in range(len(frames)):
+            for v in range(len(cams)):
+                items.append((li, v))
+                targets.append(rv.images[v])
+        lv = render_views(frames, cams, items, targets=targets)
+        sse = lv.sse.cpu().numpy()
+        V = len(cams)
+        sizes_px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+        qualities = [float(np.mean([psnr_from_sse(sse[li * V + v], sizes_px[v]) for v in range(V)]))
+                     for li in range(len(frames))]
+    levels = [PruningLevel(ratio=ratios[j], quality_db=q, size_bytes=sizes[j], pruned_indices=rm)
+              for j, q, rm in zip(keep_levels, qualities, removed)]
+    return PruningLevelSpace(levels=tuple(levels), frame_index=frame_index)
+
+
+def select_pruning_level(space: PruningLevelSpace, ctx: SelectionContext) -> int:
+    """Algorithm 1: cliff scan, then binary search for the smallest-index
+    candidate within budget, else the last (smallest) level
+    (ss/pruning.py:140-178, PAPER Alg. 1)."""
+    lv = space.levels
+    if len(lv) == 1:
+        return 0
+    q = [x.quality_db for x in lv]
+    prev_drop = q[0] - q[1]
+    cand = [0]
+    for i in range(1, len(lv)):
+        drop = q[i - 1] - q[i]
+        if drop / max(prev_drop, MIN_DROP) > ctx.cliff_beta:
+            break
+        cand.append(i)
+        prev_drop = drop
+    budget = ctx.budget_bytes
+    lo, hi, best = 0, len(cand) - 1, None
+    while lo <= hi:
+        mid = (lo + hi) // 2
+        if lv[cand[mid]].size_bytes <= budget:
+            best, hi = cand[mid], mid - 1
+        else:
+            lo = mid + 1
+    return len(lv) - 1 if best is None else best
+
+
+def ilp_optimal(level_spaces, budgets_bytes) -> list:
+    """Exact optimum of the separable selection program: per frame, the
+    highest-quality level within budget (first index wins ties)."""
+    spaces, budgets = list(level_spaces), list(budgets_bytes)
+    if len(spaces) != len(budgets):
+        raise StructuralError("one budget per frame required")
+    out = []
+    for sp, b in zip(spaces, budgets):
+        best = None
+        for j, x in enumerate(sp.levels):
+            if x.size_bytes <= b and (best is None or x.quality_db > sp.levels[best].quality_db):
+                best = j
+        out.append(FrameSelection(sp.frame_index, None, float("-inf"), False) if best is None
+                   else FrameSelection(sp.frame_index, best, sp.levels[best].quality_db, True))
+    return out
+
+
+def levels_to_csv_rows(spaces) -> list:
+    return [{"frame": sp.frame_index, "ratio": lv.ratio, "quality_db": lv.quality_db, "size_bytes": lv.size_bytes}
+            for sp in spaces for lv in sp.levels]

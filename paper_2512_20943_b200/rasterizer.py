@@ -1,0 +1,216 @@
+"""Tile rasterizer on B200 (drop-in for ``ss/rasterizer.py``).
+
+``render`` / ``render_with_usage`` keep the reference signatures and return
+the reference's ``RenderedImage`` / ``UsageFrequency``; ``forward`` is the
+reference's pluggable kernel seam (``ss/_composite.pyx:18``).  The batched
+entry point ``render_views`` evaluates many (frame, camera) items in one
+pipeline pass and returns device tensors (images, per-item SSE, usage) for
+the hot paths in ``pruning`` / ``grouping`` / ``streamsim``.
+
+Numerics: projection follows ``_prepare`` op-for-op in fp64 (OpenBLAS FMA
+order for the small matmuls); compositing evaluates every (pixel,
+primitive) pair that could contribute exactly as ``_composite.pyx:53-68``
+after an fp32 log-domain fast reject with a proven guard band.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import device as dv
+from ._lib import CameraC, FrameC, ItemC, engine, ptr
+from .camera import camera_struct
+from .errors import StructuralError, ValidationError
+from .model import GaussianFrame
+
+KERNEL_BACKEND = "cuda-sm_100a"
+EPS_CONTRIB = 1.0 / 255.0
+ALPHA_CLAMP = 0.999
+COV_BLUR = 0.3
+RADIUS_SIGMA = 3.5
+SH_C0 = 0.2820947917738781
+SH_C1 = 0.4886025119029199
+
+
+class RenderedImage:
+    """(h, w, 3) float64 image in [0, 1] (ss/rasterizer.py:59-74)."""
+
+    __slots__ = ("pixels", "resolution")
+
+    def __init__(self, pixels, resolution):
+        px = np.asarray(pixels, dtype=np.float64)
+        w, h = resolution
+        if px.shape != (h, w, 3):
+            raise StructuralError("pixel buffer does not match resolution")
+        if not np.all(np.isfinite(px)):
+            raise ValidationError("non-finite pixel values")
+        px = np.ascontiguousarray(px)
+        px.setflags(write=False)
+        object.__setattr__(self, "pixels", px)
+        object.__setattr__(self, "resolution", (int(w), int(h)))
+
+    def __setattr__(self, k, v):
+        raise AttributeError("RenderedImage is immutable")
+
+
+class UsageFrequency:
+    """Per-primitive count of (pixel, view) pairs with perceptible weight."""
+
+    __slots__ = ("counts",)
+
+    def __init__(self, counts):
+        object.__setattr__(self, "counts", counts)
+
+    def __setattr__(self, k, v):
+        raise AttributeError("UsageFrequency is immutable")
+
+    def merged_with(self, other: "UsageFrequency") -> "UsageFrequency":
+        if self.counts.shape != other.counts.shape:
+            raise StructuralError("usage count length mismatch")
+        return UsageFrequency(counts=self.counts + other.counts)
+
+
+# ---------------------------------------------------------------------------
+# batched device API
+
+
+class ViewBatch:
+    """Result of ``render_views``: device tensors, one entry per item."""
+
+    __slots__ = ("sse", "images", "usage", "launches")
+
+    def __init__(self, sse, images, usage, launches):
+        self.sse = sse
+        self.images = images
+        self.usage = usage
+        self.launches = launches
+
+
+def _frame_planes(frame, dev):
+    if isinstance(frame, GaussianFrame):
+        return frame.planes(dev), frame.count, frame.width
+    p = np.asarray(frame.params, dtype=np.float64)  # reference GaussianFrame or lookalike
+    if p.ndim != 2:
+        raise StructuralError("params must be (n, param_dim)")
+    return dv.upload_params(p, dev), p.shape[0], p.shape[1]
+
+
+def render_views(frames, cams, items, targets=None, want_images=False, usage_frames=None, device=None):
+    """Render ``items`` = [(frame_idx, cam_idx), ...] in one pipeline pass.
+
+    targets: optional list (per item) of device (h, w, 3) float64 tensors;
+      per-item SSE against them is returned in ``.sse`` (device float64).
+    want_images: return clipped device images per item.
+    usage_frames: iterable of frame indices whose items accumulate usage
+      counts; ``.usage[f]`` is an int64 device tensor over the frame.
+    """
+    import torch
+
+    dev = dv.device_of(device)
+    eng = engine(dev)
+    frames = list(frames)
+    cams = list(cams)
+    items = list(items)
+    if not items:
+        return ViewBatch(torch.zeros(0, dtype=torch.float64, device=dev), [], {}, 0)
+    planes = []
+    fc = (FrameC * len(frames))()
+    for k, f in enumerate(frames):
+        p, n, w = _frame_planes(f, dev)
+        if n == 0:
+            raise StructuralError("cannot render an empty frame")
+        planes.append(p)
+        fc[k].params = p.data_ptr()
+        fc[k].count = n
+        fc[k].ld = p.shape[1]
+        fc[k].width = w
+    cc = (CameraC * len(cams))(*[camera_struct(c) for c in cams])
+    usage = {}
+    for f in (usage_frames or ()):
+        usage[f] = torch.zeros((fc[f].count,), dtype=torch.int64, device=dev)
+    images = []
+    ic = (ItemC * len(items))()
+    for s, (fi, ci) in enumerate(items):
+        ic[s].frame = fi
+        ic[s].camera = ci
+        if targets is not None and targets[s] is not None:
+            ic[s].target = targets[s].data_ptr()
+        if want_images:
+            w, h = cams[ci].resolution
+            img = torch.empty((h, w, 3), dtype=torch.float64, device=dev)
+            images.append(img)
+            ic[s].image = img.data_ptr()
+        if fi in usage:
+            ic[s].usage = usage[fi].data_ptr()
+    sse = torch.zeros((len(items),), dtype=torch.float64, device=dev)
+    before = eng.launches
+    eng.call("airgs_render", fc, len(frames), cc, len(cams), ic, len(items), ptr(sse), eng.stream())
+    return ViewBatch(sse, images, usage, eng.launches - before)
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible API
+
+
+def render(frame, cam) -> RenderedImage:
+    """Render one frame; pure and deterministic (ss/rasterizer.py:215-222)."""
+    if frame.count == 0:
+        raise StructuralError("cannot render an empty frame")
+    vb = render_views([frame], [cam], [(0, 0)], want_images=True)
+    return RenderedImage(pixels=vb.images[0].cpu().numpy(), resolution=cam.resolution)
+
+
+def render_with_usage(frame, cams) -> tuple:
+    """Per-camera images plus usage counts summed over cameras
+    (ss/rasterizer.py:225-240)."""
+    cams = list(cams)
+    if not cams:
+        raise StructuralError("at least one camera required")
+    if frame.count == 0:
+        raise StructuralError("cannot render an empty frame")
+    vb = render_views([frame], cams, [(0, k) for k in range(len(cams))], want_images=True, usage_frames=[0])
+    imgs = [RenderedImage(pixels=im.cpu().numpy(), resolution=c.resolution) for im, c in zip(vb.images, cams)]
+    return imgs, UsageFrequency(counts=vb.usage[0].cpu().numpy())
+
+
+def forward(means2d, conics, alphas, colors, bboxes, height, width, record=False):
+    """The reference kernel seam ``_composite.forward`` on the GPU.
+
+    Inputs are numpy arrays (or CUDA tensors) of depth-ordered primitives;
+    returns numpy ``(image (h,w,3) unclipped, t_final (h,w), usage (k,),
+    None)``.  ``record=True`` (training masks) is out of scope.
+    """
+    import torch
+
+    if record:
+        raise NotImplementedError("record=True (training contribution masks) is outside the evaluation path")
+    dev = dv.device_of(None)
+    eng = engine(dev)
+
+    def t(a, dt):
+        if isinstance(a, torch.Tensor):
+            return a.to(device=dev, dtype=dt).contiguous()
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=np.float64 if dt == torch.float64
+                                                    else np.int64)).to(dev)
+
+    m2 = t(means2d, torch.float64)
+    k = m2.shape[0]
+    co, al, cl, bb = t(conics, torch.float64), t(alphas, torch.float64), t(colors, torch.float64), t(bboxes, torch.int64)
+    img = torch.empty((int(height), int(width), 3), dtype=torch.float64, device=dev)
+    tr = torch.empty((int(height), int(width)), dtype=torch.float64, device=dev)
+    us = torch.zeros((max(k, 1),), dtype=torch.int64, device=dev)
+    eng.call("airgs_composite_forward", k, ptr(m2), ptr(co), ptr(al), ptr(cl), ptr(bb), int(height), int(width),
+             ptr(img), ptr(tr), ptr(us), eng.stream())
+    return img.cpu().numpy(), tr.cpu().numpy(), us[:k].cpu().numpy(), None
+
+
+def backward(*args, **kwargs):
+    raise NotImplementedError("the backward compositing pass is training-only and outside the evaluation path")
+
+
+def render_forward(*args, **kwargs):
+    raise NotImplementedError("render_forward records training state; outside the evaluation path")
+
+
+def render_backward(*args, **kwargs):
+    raise NotImplementedError("render_backward is training-only; outside the evaluation path")

@@ -1,0 +1,145 @@
+"""Pruning-level spaces, selection and keyframe probes on the GPU vs the
+oracle: prune order, pruned index sets, level sizes and selected levels are
+bit-exact; qualities within 1e-6 dB (north star: 0.01 dB)."""
+
+import numpy as np
+import pytest
+
+from conftest import random_params
+from oracle import airgs_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+DB_TOL = 1e-6
+
+
+def _scene(seed, n=2000, movers=0.3, amp=0.02):
+    rng = np.random.default_rng(seed)
+    base = random_params(rng, n, 0, spread=0.6)
+    moved = base.copy()
+    m = rng.choice(n, int(movers * n), replace=False)
+    moved[m, 0:3] += rng.normal(0, amp, (m.size, 3))
+    moved[m[::3], 11:14] += rng.normal(0, 0.2, (m[::3].size, 3))
+    return base, moved
+
+
+def _cams(count=3, res=(64, 48)):
+    from paper_2512_20943_b200.camera import ring_rig
+
+    return ring_rig(count, radius=3.0, height=0.3, focal=res[0] * 40.0 / 48.0, resolution=res)
+
+
+def test_prune_order_rules():
+    from paper_2512_20943_b200.model import DeltaTensor
+    from paper_2512_20943_b200.pruning import prune_delta, prune_order
+
+    delta = DeltaTensor(4, 17, {i: np.ones(17) for i in range(4)})
+    assert prune_order(delta, np.array([5, 1, 1, 7])) == [2, 1, 0, 3]
+    delta = DeltaTensor(6, 17, {1: np.ones(17), 4: np.ones(17)})
+    assert prune_order(delta, np.array([0, 9, 0, 0, 2, 0])) == [4, 1]
+    five = DeltaTensor(5, 17, {i: np.ones(17) for i in range(5)})
+    kept, removed = prune_delta(five, np.arange(5), 0.5)
+    assert len(removed) == 3 and kept.entry_count == 2
+    kept, removed = prune_delta(five, np.arange(5), 0.0)
+    assert removed == () and kept.entry_count == 5
+    kept, removed = prune_delta(five, np.arange(5), 1.0)
+    assert kept.is_empty() and len(removed) == 5
+
+
+def test_prune_order_matches_oracle_large(rng):
+    from paper_2512_20943_b200.model import DeltaTensor
+    from paper_2512_20943_b200.pruning import prune_order
+
+    n = 50000
+    idx = np.sort(rng.choice(n, 9000, replace=False))
+    usage = rng.integers(0, 40, n)  # many ties
+    d = DeltaTensor(n, 17, {int(i): np.ones(17) for i in idx})
+    assert prune_order(d, usage) == orc.prune_order(idx, usage).tolist()
+
+
+@pytest.mark.parametrize("with_base", [False, True])
+def test_level_space_matches_oracle(with_base):
+    from paper_2512_20943_b200 import rasterizer
+    from paper_2512_20943_b200.model import CanonicalSpace, DeltaTensor, GaussianFrame, diff_frames
+    from paper_2512_20943_b200.pruning import build_level_space
+
+    base_p, moved = _scene(1 + with_base)
+    cams = _cams()
+    space = CanonicalSpace(GaussianFrame(params=base_p, frame_index=0, group_key=0), capacity_U=base_p.shape[0])
+    gap = diff_frames(space.frame, GaussianFrame(params=moved))
+    _, usage = rasterizer.render_with_usage(GaussianFrame(params=moved), cams)
+    _, ref_usage = orc.render_with_usage(moved, cams)
+    np.testing.assert_array_equal(usage.counts, ref_usage)
+    ratios = [i / 10 for i in range(10)] + [1.0]
+    bi = br = None
+    base = None
+    if with_base:
+        rng = np.random.default_rng(9)
+        bi = np.sort(rng.choice(base_p.shape[0], 300, replace=False))
+        br = rng.normal(0, 0.003, (300, 17))
+        base = DeltaTensor(base_p.shape[0], 17, {int(i): r for i, r in zip(bi, br)})
+    got = build_level_space(gap, space, cams, ratios, usage, 1e-4, base=base, frame_index=2)
+    gi, gr = gap.indices(), np.stack([gap.entries[i] for i in gap.indices().tolist()])
+    ref = orc.level_space((gi, gr), base_p, cams, ratios, ref_usage, 1e-4, base=(bi, br) if with_base else None)
+    assert len(got.levels) == len(ref)
+    for lv, (r, q, s, rm) in zip(got.levels, ref):
+        assert lv.ratio == r
+        assert lv.size_bytes == s
+        assert lv.pruned_indices == tuple(rm.tolist())
+        assert abs(lv.quality_db - q) <= DB_TOL
+    assert got.levels[0].quality_db == 100.0
+    assert got.levels[-1].size_bytes == 24
+    sizes = got.sizes()
+    assert all(b < a for a, b in zip(sizes, sizes[1:]))
+
+
+def test_selection_matches_oracle_on_real_space():
+    from paper_2512_20943_b200 import rasterizer
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+    from paper_2512_20943_b200.pruning import SelectionContext, build_level_space, ilp_optimal, select_pruning_level
+
+    base_p, moved = _scene(5)
+    cams = _cams(2)
+    space = CanonicalSpace(GaussianFrame(params=base_p), capacity_U=base_p.shape[0])
+    gap = diff_frames(space.frame, GaussianFrame(params=moved))
+    _, usage = rasterizer.render_with_usage(GaussianFrame(params=moved), cams)
+    sp = build_level_space(gap, space, cams, [i / 10 for i in range(10)], usage, 1e-4)
+    q, s = sp.qualities(), sp.sizes()
+    for budget in (24, 100, s[len(s) // 2], s[0], 10 * s[0]):
+        ctx = SelectionContext(bandwidth_B=budget * 8.0, target_rate_R=1.0)
+        assert select_pruning_level(sp, ctx) == orc.select_level(q, s, budget * 8.0, 1.0)
+    sel = ilp_optimal([sp], [s[1]])
+    assert sel[0].level == orc.ilp([(q, s)], [s[1]])[0]
+
+
+def test_frame_quality_and_probe_match_oracle():
+    from paper_2512_20943_b200 import grouping
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+
+    base_p, moved = _scene(7)
+    cams = _cams(3, (80, 64))
+    targets = grouping.GroundTruth(images=orc.render_with_usage(moved, cams)[0])
+    f = GaussianFrame(params=moved)
+    assert grouping.frame_quality(f, cams, targets) == 100.0
+    q = grouping.frame_quality(GaussianFrame(params=base_p), cams, targets)
+    assert abs(q - orc.frame_quality(base_p, cams, targets.images)) <= DB_TOL
+    space = CanonicalSpace(GaussianFrame(params=base_p), capacity_U=base_p.shape[0])
+    d = diff_frames(space.frame, f)
+    assert grouping.quality_probe(space, d, targets, cams) == 100.0
+    assert grouping.is_keyframe(q, 200.0) and not grouping.is_keyframe(100.0, 30.0)
+
+
+def test_probe_frames_batched_matches_oracle():
+    from paper_2512_20943_b200 import grouping
+    from paper_2512_20943_b200.model import GaussianFrame
+
+    cams = _cams(4, (64, 64))
+    frames, targets, ref = [], [], []
+    for s in range(3):
+        b, m = _scene(20 + s, n=1500)
+        frames.append(GaussianFrame(params=b))
+        imgs = orc.render_with_usage(m, cams)[0]
+        targets.append(grouping.GroundTruth(images=imgs))
+        ref.append(orc.frame_quality(b, cams, imgs))
+    got = grouping.probe_frames(frames, cams, targets)
+    assert np.max(np.abs(np.array(got) - np.array(ref))) <= DB_TOL
