@@ -14,7 +14,7 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libairgs_b200.so")
+LIB_PATH = os.environ.get("AIRGS_B200_LIB") or os.path.join(_HERE, "lib", "libairgs_b200.so")
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 c_i64_p = ctypes.POINTER(ctypes.c_int64)

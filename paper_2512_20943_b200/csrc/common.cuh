@@ -34,7 +34,9 @@ struct __align__(16) Rec {
     double al;            // activated opacity
     double cr, cg, cbl;   // activated colour
     int32_t x0, x1, y0, y1;  // clipped bbox [x0,x1) x [y0,y1)
-    int32_t pad[2];
+    // half extents of the AABB of the ellipse e <= ln(al/EPS) (+ outward pad):
+    // no pixel centre outside it can pass the weight test
+    float hx, hy;
 };
 static_assert(sizeof(Rec) == 96, "Rec layout");
 

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "context.h"
+#include "exp_table.h"
 #include "scan_sort.cuh"
 
 namespace airgs {
@@ -53,36 +54,35 @@ __device__ __forceinline__ double sigmoid_ref(double x) {
     return 0.5 * (1.0 + tanh(0.5 * x));  // ss/model.py:63-64
 }
 
-__global__ void __launch_bounds__(128) k_project(ProjArgs a) {
+// Orderable 64-bit key of a double (monotone for all finite values).
+__device__ __forceinline__ unsigned long long order_key(double z) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(z);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+constexpr int kProjThreads = 128;
+
+__global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
     const int f = blockIdx.y;
     const airgs_frame fr = a.frames[f];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= fr.count) return;
     const int ib = a.frame_item_ptr[f], ie = a.frame_item_ptr[f + 1];
-    if (ib == ie) return;
-    const double *P = fr.params + i;
+    if (ib == ie || (int64_t)blockIdx.x * blockDim.x >= fr.count) return;  // block-uniform
+    const bool active = i < fr.count;
     const int64_t ld = fr.ld;
     const int W = fr.width;
     double p[26];
 #pragma unroll
-    for (int c = 0; c < 14; ++c) p[c] = P[c * ld];
-    const int nsh = W - 14;
-    for (int c = 0; c < nsh; ++c) p[14 + c] = P[(14 + c) * ld];
+    for (int c = 0; c < 26; ++c) p[c] = (active && c < W) ? fr.params[i + c * ld] : 0.0;
 
     // _activate (ss/rasterizer.py:100-110)
-    const double qw = p[3], qx = p[4], qy = p[5], qz = p[6];
-    const double qn = sqrt(((qw * qw + qx * qx) + qy * qy) + qz * qz);
+    const double qn = sqrt(((p[3] * p[3] + p[4] * p[4]) + p[5] * p[5]) + p[6] * p[6]);
     bool finite = true;
-    for (int c = 0; c < W; ++c) finite &= isfinite(p[c]);
-    if (qn == 0.0 || !finite) {
-        atomicOr(a.flags, (unsigned)kFlagInvalidParam);
-        for (int it = ib; it < ie; ++it) {
-            const int item = a.frame_items[it];
-            a.ntiles[item * a.stride + i] = 0;
-        }
-        return;
-    }
-    const double w_ = qw / qn, x_ = qx / qn, y_ = qy / qn, z_ = qz / qn;
+#pragma unroll
+    for (int c = 0; c < 26; ++c) finite &= isfinite(p[c]);
+    const bool valid = active && qn != 0.0 && finite;
+    if (active && !valid) atomicOr(a.flags, (unsigned)kFlagInvalidParam);
+    const double w_ = p[3] / qn, x_ = p[4] / qn, y_ = p[5] / qn, z_ = p[6] / qn;
     const double s0 = exp(2.0 * p[7]), s1 = exp(2.0 * p[8]), s2 = exp(2.0 * p[9]);
     const double alpha = sigmoid_ref(p[10]);
     // quat_to_matrix (ss/model.py:72-85), elementwise, no fusion
@@ -97,95 +97,129 @@ __global__ void __launch_bounds__(128) k_project(ProjArgs a) {
     m[7] = 2.0 * (y_ * z_ + w_ * x_);
     m[8] = 1.0 - 2.0 * (x_ * x_ + y_ * y_);
     // cov3d = (R * s2) @ R^T  (ss/rasterizer.py:159), full 3x3 (not symmetric in fp)
-    double rs[9];
-    for (int r = 0; r < 3; ++r) {
-        rs[3 * r + 0] = m[3 * r + 0] * s0;
-        rs[3 * r + 1] = m[3 * r + 1] * s1;
-        rs[3 * r + 2] = m[3 * r + 2] * s2;
-    }
     double cv[9];
+#pragma unroll
     for (int r = 0; r < 3; ++r)
+#pragma unroll
         for (int c = 0; c < 3; ++c)
-            cv[3 * r + c] = dot3_blas(rs[3 * r], rs[3 * r + 1], rs[3 * r + 2], m[3 * c], m[3 * c + 1],
+            cv[3 * r + c] = dot3_blas(m[3 * r] * s0, m[3 * r + 1] * s1, m[3 * r + 2] * s2, m[3 * c], m[3 * c + 1],
                                       m[3 * c + 2]);
-    const bool live = alpha > kEpsContrib;
+    const bool live = valid && alpha > kEpsContrib;
+    // SH degree 0: colour is view independent -- compute once
+    double col0[3] = {0.0, 0.0, 0.0};
+    if (W == 17 && live) {
+        col0[0] = sigmoid_ref(p[11] + kShC0 * p[14]);
+        col0[1] = sigmoid_ref(p[12] + kShC0 * p[15]);
+        col0[2] = sigmoid_ref(p[13] + kShC0 * p[16]);
+    }
+    __shared__ unsigned long long red_min[kProjThreads / 32], red_max[kProjThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
     for (int it = ib; it < ie; ++it) {
         const int item = a.frame_items[it];
         const int64_t o = (int64_t)item * a.stride + i;
         const airgs_camera &cam = a.cams[a.item_cam[item]];
         const double *R = cam.rot;
-        const double tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
-        if (!(tz > cam.near_clip) || !live) {
-            a.ntiles[o] = 0;
-            continue;
-        }
-        const double tx = dot3_blas(p[0], p[1], p[2], R[0], R[1], R[2]) + cam.trans[0];
-        const double ty = dot3_blas(p[0], p[1], p[2], R[3], R[4], R[5]) + cam.trans[1];
-        const double f = cam.focal;
-        const double mx = f * tx / tz + 0.5 * (double)cam.width;
-        const double my = f * ty / tz + 0.5 * (double)cam.height;
-        // J (2x3) @ R_wc with the reference's explicit zeros
-        const double j00 = f / tz;
-        const double zz = tz * tz;
-        const double j02 = -f * tx / zz;
-        const double j12 = -f * ty / zz;
-        double M[6];
-        for (int c = 0; c < 3; ++c) {
-            M[c] = dot3_blas(j00, 0.0, j02, R[c], R[3 + c], R[6 + c]);
-            M[3 + c] = dot3_blas(0.0, j00, j12, R[c], R[3 + c], R[6 + c]);
-        }
-        double MC[6];
-        for (int r = 0; r < 2; ++r)
-            for (int c = 0; c < 3; ++c)
-                MC[3 * r + c] = dot3_blas(M[3 * r], M[3 * r + 1], M[3 * r + 2], cv[c], cv[3 + c], cv[6 + c]);
-        const double a2 = dot3_blas(MC[0], MC[1], MC[2], M[0], M[1], M[2]) + kCovBlur;
-        const double b2 = dot3_blas(MC[0], MC[1], MC[2], M[3], M[4], M[5]);
-        const double c2 = dot3_blas(MC[3], MC[4], MC[5], M[3], M[4], M[5]) + kCovBlur;
-        const double det = a2 * c2 - b2 * b2;
-        Rec rec;
-        rec.mx = mx;
-        rec.my = my;
-        rec.ca = c2 / det;
-        rec.cb = -b2 / det;
-        rec.cc = a2 / det;
-        const double dd = a2 - c2;
-        const double eig = 0.5 * (a2 + c2) + sqrt(fmax(0.25 * (dd * dd) + b2 * b2, 0.0));
-        const double rad = kRadiusSigma * sqrt(eig);
-        const double Wd = (double)cam.width, Hd = (double)cam.height;
-        rec.x0 = (int32_t)fmin(fmax(floor(mx - rad), 0.0), Wd);
-        rec.x1 = (int32_t)fmin(fmax(ceil(mx + rad) + 1.0, 0.0), Wd);
-        rec.y0 = (int32_t)fmin(fmax(floor(my - rad), 0.0), Hd);
-        rec.y1 = (int32_t)fmin(fmax(ceil(my + rad) + 1.0, 0.0), Hd);
-        // colour (ss/rasterizer.py:183-198)
-        const double d0 = p[0] - cam.center[0], d1 = p[1] - cam.center[1], d2 = p[2] - cam.center[2];
-        double lr = p[11] + kShC0 * p[14];
-        double lg = p[12] + kShC0 * p[15];
-        double lb = p[13] + kShC0 * p[16];
-        if (W == 26) {
-            double dn = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
-            if (dn == 0.0) dn = 1.0;
-            const double h0 = d0 / dn, h1 = d1 / dn, h2 = d2 / dn;
-            lr = lr + kShC1 * ((-h1 * p[17] + h2 * p[20]) - h0 * p[23]);
-            lg = lg + kShC1 * ((-h1 * p[18] + h2 * p[21]) - h0 * p[24]);
-            lb = lb + kShC1 * ((-h1 * p[19] + h2 * p[22]) - h0 * p[25]);
-        }
-        rec.cr = sigmoid_ref(lr);
-        rec.cg = sigmoid_ref(lg);
-        rec.cbl = sigmoid_ref(lb);
-        rec.al = alpha;
-        rec.pad[0] = rec.pad[1] = 0;
-        a.recs[o] = rec;
+        unsigned long long zkey_min = ~0ull, zkey_max = 0ull;
         int nt = 0;
-        if (rec.x1 > rec.x0 && rec.y1 > rec.y0)
-            nt = ((rec.x1 - 1) / kTile - rec.x0 / kTile + 1) * ((rec.y1 - 1) / kTile - rec.y0 / kTile + 1);
-        a.ntiles[o] = nt;
-        if (nt > 0) {
-            const unsigned long long zb = (unsigned long long)__double_as_longlong(tz);
-            a.depth[o] = zb;
-            atomicMin(a.zmin + item, zb);
-            atomicMax(a.zmax + item, zb);
+        double tz = 0.0;
+        if (live) tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
+        if (live && tz > cam.near_clip) {
+            const double tx = dot3_blas(p[0], p[1], p[2], R[0], R[1], R[2]) + cam.trans[0];
+            const double ty = dot3_blas(p[0], p[1], p[2], R[3], R[4], R[5]) + cam.trans[1];
+            const double fl = cam.focal;
+            const double mx = fl * tx / tz + 0.5 * (double)cam.width;
+            const double my = fl * ty / tz + 0.5 * (double)cam.height;
+            // J (2x3) @ R_wc with the reference's explicit zeros
+            const double j00 = fl / tz;
+            const double zz = tz * tz;
+            const double j02 = -fl * tx / zz;
+            const double j12 = -fl * ty / zz;
+            double M[6];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                M[c] = dot3_blas(j00, 0.0, j02, R[c], R[3 + c], R[6 + c]);
+                M[3 + c] = dot3_blas(0.0, j00, j12, R[c], R[3 + c], R[6 + c]);
+            }
+            double MC[6];
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    MC[3 * r + c] = dot3_blas(M[3 * r], M[3 * r + 1], M[3 * r + 2], cv[c], cv[3 + c], cv[6 + c]);
+            const double a2 = dot3_blas(MC[0], MC[1], MC[2], M[0], M[1], M[2]) + kCovBlur;
+            const double b2 = dot3_blas(MC[0], MC[1], MC[2], M[3], M[4], M[5]);
+            const double c2 = dot3_blas(MC[3], MC[4], MC[5], M[3], M[4], M[5]) + kCovBlur;
+            const double det = a2 * c2 - b2 * b2;
+            Rec rec;
+            rec.mx = mx;
+            rec.my = my;
+            rec.ca = c2 / det;
+            rec.cb = -b2 / det;
+            rec.cc = a2 / det;
+            const double dd = a2 - c2;
+            const double eig = 0.5 * (a2 + c2) + sqrt(fmax(0.25 * (dd * dd) + b2 * b2, 0.0));
+            const double rad = kRadiusSigma * sqrt(eig);
+            const double Wd = (double)cam.width, Hd = (double)cam.height;
+            rec.x0 = (int32_t)fmin(fmax(floor(mx - rad), 0.0), Wd);
+            rec.x1 = (int32_t)fmin(fmax(ceil(mx + rad) + 1.0, 0.0), Wd);
+            rec.y0 = (int32_t)fmin(fmax(floor(my - rad), 0.0), Hd);
+            rec.y1 = (int32_t)fmin(fmax(ceil(my + rad) + 1.0, 0.0), Hd);
+            if (W == 26) {  // colour (ss/rasterizer.py:183-198), view dependent
+                const double d0 = p[0] - cam.center[0], d1 = p[1] - cam.center[1], d2 = p[2] - cam.center[2];
+                double dn = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+                if (dn == 0.0) dn = 1.0;
+                const double h0 = d0 / dn, h1 = d1 / dn, h2 = d2 / dn;
+                rec.cr = sigmoid_ref((p[11] + kShC0 * p[14]) + kShC1 * ((-h1 * p[17] + h2 * p[20]) - h0 * p[23]));
+                rec.cg = sigmoid_ref((p[12] + kShC0 * p[15]) + kShC1 * ((-h1 * p[18] + h2 * p[21]) - h0 * p[24]));
+                rec.cbl = sigmoid_ref((p[13] + kShC0 * p[16]) + kShC1 * ((-h1 * p[19] + h2 * p[22]) - h0 * p[25]));
+            } else {
+                rec.cr = col0[0];
+                rec.cg = col0[1];
+                rec.cbl = col0[2];
+            }
+            rec.al = alpha;
+            {
+                // e >= dx^2 / (2 Sxx) with Sigma = cov2d, so |dx| > sqrt(2 t Sxx) => e > t
+                const double t = log(alpha / kEpsContrib) * 1.0002 + 2e-4;
+                const double hx = sqrt(2.0 * fmax(t, 0.0) * (a2 + 1e-9 * a2)) * 1.0002 + 1e-3;
+                const double hy = sqrt(2.0 * fmax(t, 0.0) * (c2 + 1e-9 * c2)) * 1.0002 + 1e-3;
+                rec.hx = det > 0.0 && isfinite(hx) ? (float)hx * 1.0001f : 1e30f;
+                rec.hy = det > 0.0 && isfinite(hy) ? (float)hy * 1.0001f : 1e30f;
+            }
+            if (rec.x1 > rec.x0 && rec.y1 > rec.y0)
+                nt = ((rec.x1 - 1) / kTile - rec.x0 / kTile + 1) * ((rec.y1 - 1) / kTile - rec.y0 / kTile + 1);
+            if (nt > 0) {
+                a.recs[o] = rec;
+                const unsigned long long zk = order_key(tz);
+                a.depth[o] = zk;
+                zkey_min = zkey_max = zk;
+            }
         }
+        if (active) a.ntiles[o] = nt;
+        // block-level min/max of the depth keys -> one atomic pair per block
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            zkey_min = min(zkey_min, __shfl_xor_sync(0xffffffffu, zkey_min, d));
+            zkey_max = max(zkey_max, __shfl_xor_sync(0xffffffffu, zkey_max, d));
+        }
+        if (lane == 0) {
+            red_min[wid] = zkey_min;
+            red_max[wid] = zkey_max;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long mn = red_min[0], mxk = red_max[0];
+            for (int k = 1; k < kProjThreads / 32; ++k) {
+                mn = min(mn, red_min[k]);
+                mxk = max(mxk, red_max[k]);
+            }
+            if (mxk) {
+                atomicMin(a.zmin + item, mn);
+                atomicMax(a.zmax + item, mxk);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -293,121 +327,204 @@ struct CompItem {
     int32_t w, h, tiles_x, clip;
 };
 
+constexpr double kLog2e = 1.4426950408889634;
+// log2(1 / fl(1/255)) rounded to fp32 (threshold offset in the log2 domain)
+__device__ __forceinline__ float log2_inv_eps() { return 7.99435343685886f; }
+
+// exp(x) for the compositing weights: 256-entry table of 2^(i/256) in shared
+// memory + degree-5 polynomial on |r| <= ln2/512 (error < 0.51 ulp; agrees
+// with glibc's exp, which the reference's Cython kernel calls, on >99.9% of
+// inputs and never differs by more than 1 ulp -- tools/gen_exp_table.py).
+__device__ __forceinline__ double exp_tab(double x, const double2 *__restrict__ tab) {
+    const double shift = 6755399441055744.0;  // 1.5 * 2^52
+    const double z = x * kExpInvLn2N;
+    double kd = z + shift;
+    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    kd = kd - shift;
+    double r = fma(kd, kExpNegLn2HiN, x);
+    r = fma(kd, kExpNegLn2LoN, r);
+    const double2 t = tab[ki & (kExpN - 1)];
+    const unsigned long long sb = (unsigned long long)__double_as_longlong(t.y) + (ki << (52 - kExpBits));
+    const double r2 = r * r;
+    const double p1 = fma(r, 1.0 / 6.0, 0.5);
+    const double p2 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    double tmp = t.x + r;
+    tmp = fma(r2, p1, tmp);
+    tmp = fma(r2 * r2, p2, tmp);
+    const double sc = __longlong_as_double((long long)sb);
+    return fma(sc, tmp, sc);
+}
+
 struct CompShared {
-    float4 f0[kTileThreads];   // mx-ox, my-oy, a, b  (fp32 fast reject)
-    float2 f1[kTileThreads];   // c, ln(alpha)
-    int4 bb[kTileThreads];     // bbox
-    double mx[kTileThreads], my[kTileThreads];
-    double ca[kTileThreads], cb[kTileThreads], cc[kTileThreads], al[kTileThreads];
-    double cr[kTileThreads], cg[kTileThreads], cbl[kTileThreads];
+    float4 f0[kTileThreads];     // mx-ox, my-oy (tile origin), 0.5*log2e*a, log2e*b  (fp32, log2 domain)
+    float2 f1[kTileThreads];     // 0.5*log2e*c, log2(alpha)
+    double2 m[kTileThreads];     // mx, my
+    double2 hab[kTileThreads];   // 0.5*a, b
+    double2 hcal[kTileThreads];  // 0.5*c, alpha
+    double2 rg[kTileThreads];    // colour r, g
+    double bl[kTileThreads];     // colour b
     uint32_t gid[kTileThreads];
     int32_t cnt[kTileThreads];
-    double red[kTileThreads / 32];
+    uint8_t wmask[kTileThreads];  // bit w: may touch warp w's 8x4 sub-tile
+    double2 exptab[kExpN];
 };
 
-// ln(1 / fl(1/255)) in fp64, rounded to fp32 (threshold offset)
-__device__ __forceinline__ float ln_inv_eps() { return 5.54126354515842f; }
+constexpr int kCompWarps = kTileThreads / 32;
+#ifndef COMP_MIN_BLOCKS
+#define COMP_MIN_BLOCKS 3
+#endif
 
+// alpha' = min(al * exp(-e), 0.999) for staged primitive j at (dx, dy):
+// exact replay of _composite.pyx:56-60 (0.5*(A + C) == 0.5A + 0.5C exactly)
+__device__ __forceinline__ double alpha_at(const CompShared &sh, int j, double pxd, double pyd) {
+    const double2 mm = sh.m[j];
+    const double2 ab = sh.hab[j];
+    const double2 ca = sh.hcal[j];
+    const double dx = pxd - mm.x;
+    const double dy = pyd - mm.y;
+    const double ee = (ab.x * dx * dx + ca.x * dy * dy) + ab.y * dx * dy;
+    const double ap = ca.y * exp_tab(-ee, sh.exptab);
+    return ap > kAlphaClamp ? kAlphaClamp : ap;
+}
+
+// One CTA = one 16x16 tile, one pixel per thread; warps are 8x4 sub-tiles.
+// Per batch of 256 depth-ordered primitives (staged once per CTA), each warp
+// walks 32-entry chunks: phase A tests only primitives whose threshold-ellipse
+// AABB touches its sub-tile (fp32, log2 domain, proven guard band) and builds
+// a per-lane candidate mask; phase B has every lane run its own candidates
+// through the exact fp64 path in depth order (two candidates' exp in flight).
 template <bool USAGE>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
 k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems) {
     __shared__ CompShared sh;
+    {
+        const unsigned long long *src = &kExpTable[0][0];
+        for (int k = threadIdx.x; k < kExpN; k += kTileThreads)
+            sh.exptab[k] = make_double2(__longlong_as_double((long long)src[2 * k]),
+                                        __longlong_as_double((long long)src[2 * k + 1]));
+    }
     // locate item (binary search over tile_base)
     const int64_t g = blockIdx.x;
     int lo = 0, hi = nitems - 1;
     while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
+        const int mid = (lo + hi + 1) >> 1;
         if (tile_base[mid] <= g) lo = mid; else hi = mid - 1;
     }
-    const CompItem it = items[lo];
+    const CompItem *__restrict__ itp = items + lo;
     const int tl = (int)(g - tile_base[lo]);
-    const int tx = tl % it.tiles_x, ty = tl / it.tiles_x;
+    const int tiles_x = itp->tiles_x, img_w = itp->w, img_h = itp->h;
+    const int tx = tl % tiles_x, ty = tl / tiles_x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // warp = 8x4 sub-tile, lanes row-major inside it
     const int sx = (w & 1) * 8, sy = (w >> 1) * 4;
     const int lx = sx + (lane & 7), ly = sy + (lane >> 3);
     const int ox = tx * kTile, oy = ty * kTile;
     const int px = ox + lx, py = oy + ly;
-    const int wx0 = ox + sx, wx1 = wx0 + 8, wy0 = oy + sy, wy1 = wy0 + 4;
-    const bool inside = px < it.w && py < it.h;
+    const bool inside = px < img_w && py < img_h;
     const float pxl = (float)lx + 0.5f, pyl = (float)ly + 0.5f;
     const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
+    const uint32_t *__restrict__ gids = itp->gids;
+    const Rec *__restrict__ recs = itp->recs;
 
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     bool done = !inside;
-    float lnTk = ln_inv_eps();  // ln(T) - ln(EPS) at T = 1
+    float thr = log2_inv_eps() + 6e-5f;  // log2(T/EPS) + guard constant
 
-    const int64_t s = it.tstart[tl], e = it.tend[tl];
+    const int64_t s = itp->tstart[tl], e = itp->tend[tl];
     for (int64_t base = s; base < e; base += kTileThreads) {
         const int nb = (int)min((int64_t)kTileThreads, e - base);
         __syncthreads();
         if ((int)threadIdx.x < nb) {
-            const uint32_t gi = it.gids[base + threadIdx.x];
-            const Rec r = it.recs[gi];
             const int t = threadIdx.x;
+            const uint32_t gi = gids[base + t];
+            const Rec r = recs[gi];
+            const float mxl = (float)(r.mx - (double)ox), myl = (float)(r.my - (double)oy);
             sh.gid[t] = gi;
-            sh.mx[t] = r.mx;
-            sh.my[t] = r.my;
-            sh.ca[t] = r.ca;
-            sh.cb[t] = r.cb;
-            sh.cc[t] = r.cc;
-            sh.al[t] = r.al;
-            sh.cr[t] = r.cr;
-            sh.cg[t] = r.cg;
-            sh.cbl[t] = r.cbl;
-            sh.bb[t] = make_int4(r.x0, r.x1, r.y0, r.y1);
-            sh.f0[t] = make_float4((float)(r.mx - (double)ox), (float)(r.my - (double)oy), (float)r.ca,
-                                   (float)r.cb);
-            sh.f1[t] = make_float2((float)r.cc, logf((float)r.al));
+            sh.f0[t] = make_float4(mxl, myl, (float)(0.5 * kLog2e * r.ca), (float)(kLog2e * r.cb));
+            sh.f1[t] = make_float2((float)(0.5 * kLog2e * r.cc), __log2f((float)r.al));
+            sh.m[t] = make_double2(r.mx, r.my);
+            sh.hab[t] = make_double2(0.5 * r.ca, r.cb);
+            sh.hcal[t] = make_double2(0.5 * r.cc, r.al);
+            sh.rg[t] = make_double2(r.cr, r.cg);
+            sh.bl[t] = r.cbl;
+            // sub-tile mask: clipped reference bbox AND threshold-ellipse AABB
+            // (pixel centres of sub-tile column k span 8k+0.5 .. 8k+7.5, rows 4k+0.5 .. 4k+3.5)
+            unsigned xm = 0, ym = 0;
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                xm |= (r.x0 < ox + 8 * k + 8 && r.x1 > ox + 8 * k && mxl - r.hx <= 8.0f * k + 7.5f &&
+                       mxl + r.hx >= 8.0f * k + 0.5f) ? (1u << k) : 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                ym |= (r.y0 < oy + 4 * k + 4 && r.y1 > oy + 4 * k && myl - r.hy <= 4.0f * k + 3.5f &&
+                       myl + r.hy >= 4.0f * k + 0.5f) ? (1u << k) : 0u;
+            unsigned mk = 0;
+#pragma unroll
+            for (int ww = 0; ww < 8; ++ww) mk |= (((xm >> (ww & 1)) & (ym >> (ww >> 1))) & 1u) << ww;
+            sh.wmask[t] = (uint8_t)mk;
             if (USAGE) sh.cnt[t] = 0;
         }
         __syncthreads();
-        for (int j = 0; j < nb; ++j) {
-            const int4 bb = sh.bb[j];
-            if (bb.x >= wx1 || bb.y <= wx0 || bb.z >= wy1 || bb.w <= wy0) continue;  // warp-uniform
-            bool cand = false;
-            if (!done) {
-                const float4 f0 = sh.f0[j];
-                const float2 f1 = sh.f1[j];
+        for (int c = 0; c < nb; c += 32) {
+            if (__all_sync(0xffffffffu, done)) break;
+            const int jj = c + lane;
+            unsigned m = __ballot_sync(0xffffffffu, jj < nb && ((sh.wmask[jj] >> w) & 1u));
+            // phase A: fp32 candidate bits (T as of the chunk start; a larger T only
+            // admits more candidates, never fewer)
+            unsigned word = 0;
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
+                const float4 f0 = sh.f0[c + k];
+                const float2 f1 = sh.f1[c + k];
                 const float dx = pxl - f0.x, dy = pyl - f0.y;
-                const float q = fmaf(f0.z * dx, dx, (f1.x * dy) * dy);  // a dx^2 + c dy^2
-                const float ef = fmaf(f0.w * dx, dy, 0.5f * q);
-                // reject iff e > ln(al) + ln(T/EPS) + guard  (guard proof: DESIGN.md)
-                cand = ef <= f1.y + lnTk + fmaf(5e-6f, q, 4e-5f);
+                const float s2 = fmaf(f0.z * dx, dx, (f1.x * dy) * dy);  // log2e * 0.5(a dx^2 + c dy^2)
+                const float e2 = fmaf(f0.w * dx, dy, s2);               // log2e * e
+                // reject iff e > ln(al) + ln(T/EPS) + guard (guard proof: DESIGN.md)
+                word |= (unsigned)(e2 <= fmaf(1e-5f, s2, f1.y) + thr) << k;
             }
-            if (__any_sync(0xffffffffu, cand)) {
-                bool contrib = false;
-                if (cand) {
-                    // exact replay of _composite.pyx:53-68
-                    const double dx = pxd - sh.mx[j];
-                    const double dy = pyd - sh.my[j];
-                    const double ee = 0.5 * (sh.ca[j] * dx * dx + sh.cc[j] * dy * dy) + sh.cb[j] * dx * dy;
-                    double ap = sh.al[j] * exp(-ee);
-                    if (ap > kAlphaClamp) ap = kAlphaClamp;
-                    const double wgt = ap * T;
+            if (done) word = 0;
+            // phase B: each lane runs its own candidates in depth order (exact fp64)
+            while (word) {
+                const int j1 = c + __ffs(word) - 1;
+                word &= word - 1;
+                const bool two = word != 0;
+                const int j2 = two ? c + __ffs(word) - 1 : j1;
+                word &= word - 1;
+                const double ap1 = alpha_at(sh, j1, pxd, pyd);
+                const double ap2 = alpha_at(sh, j2, pxd, pyd);
+                double wgt = ap1 * T;
+                if (wgt > kEpsContrib) {
+                    const double2 rg = sh.rg[j1];
+                    cr += wgt * rg.x;
+                    cg += wgt * rg.y;
+                    cb += wgt * sh.bl[j1];
+                    T = T * (1.0 - ap1);
+                    if (USAGE) atomicAdd(&sh.cnt[j1], 1);
+                }
+                if (two) {
+                    wgt = ap2 * T;
                     if (wgt > kEpsContrib) {
-                        cr += wgt * sh.cr[j];
-                        cg += wgt * sh.cg[j];
-                        cb += wgt * sh.cbl[j];
-                        T = T * (1.0 - ap);
-                        contrib = true;
-                        done = kAlphaClamp * T <= kEpsContrib;
-                        lnTk = logf((float)T) + ln_inv_eps();
+                        const double2 rg = sh.rg[j2];
+                        cr += wgt * rg.x;
+                        cg += wgt * rg.y;
+                        cb += wgt * sh.bl[j2];
+                        T = T * (1.0 - ap2);
+                        if (USAGE) atomicAdd(&sh.cnt[j2], 1);
                     }
                 }
-                if (USAGE) {
-                    const unsigned m = __ballot_sync(0xffffffffu, contrib);
-                    if (lane == 0 && m) atomicAdd(&sh.cnt[j], __popc(m));
-                }
             }
+            // once 0.999*T <= EPS no later primitive can pass the weight test
+            done = done || kAlphaClamp * T <= kEpsContrib;
+            thr = __log2f((float)T) + (log2_inv_eps() + 6e-5f);
         }
         __syncthreads();
         if (USAGE && (int)threadIdx.x < nb && sh.cnt[threadIdx.x] > 0)
-            atomicAdd((unsigned long long *)(it.usage + sh.gid[threadIdx.x]),
+            atomicAdd((unsigned long long *)(itp->usage + sh.gid[threadIdx.x]),
                       (unsigned long long)sh.cnt[threadIdx.x]);
         if (__syncthreads_count(!done) == 0) break;
     }
 
+    const CompItem it = *itp;
     const int64_t pix = (int64_t)py * it.w + px;
     double vr = cr, vg = cg, vb = cb;
     if (it.clip) {
@@ -432,14 +549,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             se = (dr * dr + dg * dg) + db * db;
         }
         se = warp_reduce_sum(se);
-        __syncthreads();
-        if (lane == 0) sh.red[w] = se;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int k = 0; k < kTileThreads / 32; ++k) t += sh.red[k];
-            it.sse_tiles[tl] = t;
-        }
+        if (lane == 0) it.sse_tiles[(int64_t)tl * kCompWarps + w] = se;  // fixed-order reduce later
     }
 }
 
@@ -449,7 +559,7 @@ k_sse_items(const double *__restrict__ sse_tiles, const int64_t *__restrict__ ti
             const uint8_t *__restrict__ has_target, double *__restrict__ out) {
     const int s = blockIdx.x;
     if (!has_target[s]) return;
-    const int64_t b = tile_base[s], n = tile_base[s + 1] - b;
+    const int64_t b = tile_base[s] * kCompWarps, n = (tile_base[s + 1] - tile_base[s]) * kCompWarps;
     double acc = 0.0;
     for (int64_t k = threadIdx.x; k < n; k += 256) acc += sse_tiles[b + k];
     acc = warp_reduce_sum(acc);
@@ -515,7 +625,15 @@ k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__re
     r.x1 = (int32_t)bboxes[4 * i + 1];
     r.y0 = (int32_t)bboxes[4 * i + 2];
     r.y1 = (int32_t)bboxes[4 * i + 3];
-    r.pad[0] = r.pad[1] = 0;
+    {
+        // conic -> covariance diagonal: Sxx = c/det, Syy = a/det (seam inputs are conics)
+        const double det = r.ca * r.cc - r.cb * r.cb;
+        const double t = log(r.al / kEpsContrib) * 1.0002 + 2e-4;
+        const double hx = sqrt(2.0 * fmax(t, 0.0) * (r.cc / det)) * 1.0002 + 1e-3;
+        const double hy = sqrt(2.0 * fmax(t, 0.0) * (r.ca / det)) * 1.0002 + 1e-3;
+        r.hx = det > 0.0 && isfinite(hx) ? (float)hx * 1.0001f : 1e30f;
+        r.hy = det > 0.0 && isfinite(hy) ? (float)hy * 1.0001f : 1e30f;
+    }
     recs[i] = r;
     int nt = 0;
     if (r.x1 > r.x0 && r.y1 > r.y0)
@@ -624,7 +742,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         ++L;
         check_launch();
     }
-    double *sse_tiles = ctx->scratch_t<double>(kSlotSseTiles, (size_t)Tt);
+    double *sse_tiles = ctx->scratch_t<double>(kSlotSseTiles, (size_t)Tt * kCompWarps);
     std::vector<CompItem> ci(nitems);
     std::vector<uint8_t> has_t(nitems);
     bool any_usage = false, any_target = false;
@@ -639,7 +757,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         c.image = h.image;
         c.trans = h.trans;
         c.usage = h.usage;
-        c.sse_tiles = sse_tiles + tile_base[s];
+        c.sse_tiles = sse_tiles + tile_base[s] * kCompWarps;
         c.w = h.w;
         c.h = h.h;
         c.tiles_x = h.tiles_x;
@@ -768,8 +886,8 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.flags = flags;
     pa.stride = stride;
     {
-        dim3 grid((unsigned)ceil_div(stride, 128), (unsigned)nframes);
-        k_project<<<grid, 128, 0, st>>>(pa);
+        dim3 grid((unsigned)ceil_div(stride, kProjThreads), (unsigned)nframes);
+        k_project<<<grid, kProjThreads, 0, st>>>(pa);
         ++L;
         check_launch();
     }
