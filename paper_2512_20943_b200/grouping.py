@@ -173,6 +173,41 @@ class GroupPlan:
                          groups=tuple(GroupSpan(g["key"], g["start"], g["end"]) for g in obj["groups"]))
 
 
+class FrameRecord:
+    __slots__ = ("frame_index", "group_key", "is_keyframe", "step_delta", "cumulative_delta", "quality_db")
+
+    def __init__(self, frame_index, group_key, is_keyframe, step_delta, cumulative_delta, quality_db):
+        for k, v in (("frame_index", frame_index), ("group_key", group_key), ("is_keyframe", is_keyframe),
+                     ("step_delta", step_delta), ("cumulative_delta", cumulative_delta),
+                     ("quality_db", quality_db)):
+            object.__setattr__(self, k, v)
+
+    def __setattr__(self, k, v):
+        raise AttributeError("FrameRecord is immutable")
+
+
+class TrainedStream:
+    """Canonical spaces per group plus per-frame cumulative deltas
+    (ss/grouping.py:91-105)."""
+
+    __slots__ = ("plan", "spaces", "records")
+
+    def __init__(self, plan, spaces, records):
+        object.__setattr__(self, "plan", plan)
+        object.__setattr__(self, "spaces", dict(spaces))
+        object.__setattr__(self, "records", tuple(records))
+
+    def __setattr__(self, k, v):
+        raise AttributeError("TrainedStream is immutable")
+
+    def reconstruct(self, frame_index: int):
+        rec = self.records[frame_index]
+        return apply_delta(self.spaces[rec.group_key], rec.cumulative_delta, frame_index=frame_index)
+
+    def qualities(self):
+        return [r.quality_db for r in self.records]
+
+
 def plan_from_decisions(keyframe_flags, tau_db=DEFAULT_TAU_DB) -> GroupPlan:
     """Group spans from per-frame keyframe decisions (frame 0 always opens)."""
     spans = []

@@ -143,3 +143,23 @@ def test_probe_frames_batched_matches_oracle():
         ref.append(orc.frame_quality(b, cams, imgs))
     got = grouping.probe_frames(frames, cams, targets)
     assert np.max(np.abs(np.array(got) - np.array(ref))) <= DB_TOL
+
+
+def test_sharded_drivers_world1_equal_unsharded():
+    from paper_2512_20943_b200 import grouping, rasterizer, sharding
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+    from paper_2512_20943_b200.pruning import build_level_space
+
+    base_p, moved = _scene(31)
+    cams = _cams(3)
+    space = CanonicalSpace(GaussianFrame(params=base_p), capacity_U=base_p.shape[0])
+    gap = diff_frames(space.frame, GaussianFrame(params=moved))
+    _, usage = rasterizer.render_with_usage(GaussianFrame(params=moved), cams)
+    u2 = sharding.usage_sharded(GaussianFrame(params=moved), cams)
+    np.testing.assert_array_equal(u2.cpu().numpy(), usage.counts)
+    a = build_level_space(gap, space, cams, [0, 0.25, 0.5, 0.75], usage, 1e-4)
+    b = sharding.build_level_space_sharded(gap, space, cams, [0, 0.25, 0.5, 0.75], usage, 1e-4)
+    assert a.sizes() == b.sizes() and a.qualities() == b.qualities()
+    tg = grouping.GroundTruth(images=orc.render_with_usage(moved, cams)[0])
+    assert sharding.probe_frames_sharded([GaussianFrame(params=base_p)], cams, [tg]) == \
+        grouping.probe_frames([GaussianFrame(params=base_p)], cams, [tg])
