@@ -85,6 +85,7 @@ enum Slot : int {
     kSlotMisc1,
     kSlotMisc2,
     kSlotMisc3,
+    kSlotTileCount,
     kSlotCount
 };
 

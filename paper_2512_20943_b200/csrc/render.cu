@@ -4,18 +4,21 @@
 //   k_project       fp64 activation + EWA projection, op-for-op with
 //                   ss/rasterizer.py:100-212 (one thread per primitive, all
 //                   views of its frame in the inner loop so the parameter row
-//                   and the view-independent activation are read/computed once)
-//   compaction      stable per-item scan of visible primitives (warp scans)
-//   depth sort      stable LSD radix sort of (z bits - zmin) -> depth rank;
-//                   ties keep index order == np.argsort(kind="stable")
-//   binning         (tile) keys emitted in rank order, stable radix sort by
-//                   tile -> per-tile lists in depth order
-//   k_composite     16x16 tile per CTA, one pixel per thread, front-to-back
-//                   with exact early termination; fp32 log-domain fast reject
-//                   with a proven guard band, exact fp64 replay of
-//                   _composite.pyx:42-73 for every surviving (pixel, primitive)
-//                   pair; fused usage counts and per-tile SSE
+//                   and the view-independent activation are read/computed once);
+//                   emits a 96-byte record, an orderable depth key, and a
+//                   per-tile histogram (atomics)
+//   tile scan       exclusive scan of the histogram (warp scans) -> tile ranges
+//   k_emit          primitive ids into their tiles' ranges (atomic cursors, any order)
+//   k_composite     16x16 tile per CTA: the tile's list is sorted in shared memory
+//                   by (depth key, primitive index) -- exactly the reference's
+//                   stable argsort order restricted to the tile -- then
+//                   composited front to back with exact early termination; fp32
+//                   log2-domain candidate pass with a proven guard band, exact
+//                   fp64 replay of _composite.pyx:42-73 for candidates; fused
+//                   usage counts and per-warp SSE partials
 //   k_sse_items     deterministic per-item SSE reduction
+// Tiles whose list exceeds the in-shared-memory sort capacity are sorted
+// beforehand by a segmented radix sort over (index, then depth key).
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -35,11 +38,12 @@ struct ProjArgs {
     const int32_t *frame_item_ptr;  // CSR over frames
     const int32_t *frame_items;
     const int32_t *item_cam;
+    const int64_t *tile_base;  // [nitems] first global tile of each item
+    const int32_t *tiles_x;    // [nitems]
     Rec *recs;                 // [nitems][stride]
-    uint64_t *depth;           // [nitems][stride]
-    int32_t *ntiles;           // [nitems][stride]
-    unsigned long long *zmin;  // [nitems]
-    unsigned long long *zmax;  // [nitems]
+    uint64_t *depth;           // [nitems][stride] orderable depth keys
+    int32_t *ntiles;           // [nitems][stride] tiles touched (0 = not rendered)
+    uint32_t *tile_count;      // [total tiles] primitives per tile
     unsigned int *flags;
     int64_t stride;
 };
@@ -60,6 +64,27 @@ __device__ __forceinline__ unsigned long long order_key(double z) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// Tile range of a record: clipped bbox intersected with the pixel centres
+// inside the threshold-ellipse AABB (|dx| <= hx, |dy| <= hy); pixels outside
+// cannot pass the weight test, so tiles outside this range are never needed.
+__device__ __forceinline__ bool rec_tile_range(const Rec &r, int &u0, int &u1, int &v0, int &v1) {
+    int xa = r.x0, xb = r.x1 - 1, ya = r.y0, yb = r.y1 - 1;
+    if (r.hx < 1e29f) {
+        xa = max(xa, (int)ceilf((float)(r.mx - 0.5) - r.hx));
+        xb = min(xb, (int)floorf((float)(r.mx - 0.5) + r.hx));
+    }
+    if (r.hy < 1e29f) {
+        ya = max(ya, (int)ceilf((float)(r.my - 0.5) - r.hy));
+        yb = min(yb, (int)floorf((float)(r.my - 0.5) + r.hy));
+    }
+    if (xa > xb || ya > yb) return false;
+    u0 = xa / kTile;
+    u1 = xb / kTile;
+    v0 = ya / kTile;
+    v1 = yb / kTile;
+    return true;
+}
+
 constexpr int kProjThreads = 128;
 
 __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
@@ -67,8 +92,8 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
     const airgs_frame fr = a.frames[f];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int ib = a.frame_item_ptr[f], ie = a.frame_item_ptr[f + 1];
-    if (ib == ie || (int64_t)blockIdx.x * blockDim.x >= fr.count) return;  // block-uniform
-    const bool active = i < fr.count;
+    if (ib == ie || i >= fr.count) return;
+    const bool active = true;
     const int64_t ld = fr.ld;
     const int W = fr.width;
     double p[26];
@@ -112,15 +137,11 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
         col0[1] = sigmoid_ref(p[12] + kShC0 * p[15]);
         col0[2] = sigmoid_ref(p[13] + kShC0 * p[16]);
     }
-    __shared__ unsigned long long red_min[kProjThreads / 32], red_max[kProjThreads / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-
     for (int it = ib; it < ie; ++it) {
         const int item = a.frame_items[it];
         const int64_t o = (int64_t)item * a.stride + i;
         const airgs_camera &cam = a.cams[a.item_cam[item]];
         const double *R = cam.rot;
-        unsigned long long zkey_min = ~0ull, zkey_max = 0ull;
         int nt = 0;
         double tz = 0.0;
         if (live) tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
@@ -187,128 +208,121 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
                 rec.hx = det > 0.0 && isfinite(hx) ? (float)hx * 1.0001f : 1e30f;
                 rec.hy = det > 0.0 && isfinite(hy) ? (float)hy * 1.0001f : 1e30f;
             }
-            if (rec.x1 > rec.x0 && rec.y1 > rec.y0)
-                nt = ((rec.x1 - 1) / kTile - rec.x0 / kTile + 1) * ((rec.y1 - 1) / kTile - rec.y0 / kTile + 1);
+            int u0, u1, v0, v1;
+            if (rec.x1 > rec.x0 && rec.y1 > rec.y0 && rec_tile_range(rec, u0, u1, v0, v1))
+                nt = (u1 - u0 + 1) * (v1 - v0 + 1);
             if (nt > 0) {
                 a.recs[o] = rec;
-                const unsigned long long zk = order_key(tz);
-                a.depth[o] = zk;
-                zkey_min = zkey_max = zk;
+                a.depth[o] = order_key(tz);
+                // per-tile histogram for the binning scan
+                uint32_t *tc = a.tile_count + a.tile_base[item];
+                const int txn = a.tiles_x[item];
+                for (int v = v0; v <= v1; ++v)
+                    for (int u = u0; u <= u1; ++u) atomicAdd(tc + v * txn + u, 1u);
             }
         }
         if (active) a.ntiles[o] = nt;
-        // block-level min/max of the depth keys -> one atomic pair per block
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            zkey_min = min(zkey_min, __shfl_xor_sync(0xffffffffu, zkey_min, d));
-            zkey_max = max(zkey_max, __shfl_xor_sync(0xffffffffu, zkey_max, d));
-        }
-        if (lane == 0) {
-            red_min[wid] = zkey_min;
-            red_max[wid] = zkey_max;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long mn = red_min[0], mxk = red_max[0];
-            for (int k = 1; k < kProjThreads / 32; ++k) {
-                mn = min(mn, red_min[k]);
-                mxk = max(mxk, red_max[k]);
-            }
-            if (mxk) {
-                atomicMin(a.zmin + item, mn);
-                atomicMax(a.zmax + item, mxk);
-            }
-        }
-        __syncthreads();
     }
 }
-
-// ---------------------------------------------------------------------------
-// scan functors
-
-struct VisIn {
-    const int32_t *nt;
-    int64_t stride;
-    __device__ int64_t operator()(int s, int64_t i) const { return nt[(int64_t)s * stride + i] > 0 ? 1 : 0; }
-};
-struct VisOut {
-    const uint64_t *depth;
-    const unsigned long long *zmin;
-    uint64_t *keys;
-    uint32_t *vals;
-    int64_t stride;
-    __device__ void operator()(int s, int64_t i, int64_t ex, int64_t v) const {
-        if (v) {
-            const int64_t b = (int64_t)s * stride;
-            keys[b + ex] = depth[b + i] - zmin[s];
-            vals[b + ex] = (uint32_t)i;
-        }
-    }
-};
-struct TileCountIn {
-    const int32_t *nt;
-    const uint32_t *vals;
-    int64_t stride;
-    __device__ int64_t operator()(int s, int64_t r) const {
-        const int64_t b = (int64_t)s * stride;
-        return nt[b + vals[b + r]];
-    }
-};
-struct TileCountOut {
-    int64_t *off;
-    int64_t stride;
-    __device__ void operator()(int s, int64_t r, int64_t ex, int64_t) const {
-        off[(int64_t)s * stride + r] = ex;
-    }
-};
 
 // ---------------------------------------------------------------------------
 // binning
 
+struct TileScanIn {
+    const uint32_t *cnt;
+    __device__ int64_t operator()(int, int64_t g) const { return cnt[g]; }
+};
+struct TileScanOut {
+    int64_t *start;
+    uint32_t *big_list;  // tiles whose list exceeds the shared-memory sort
+    unsigned int *big_n;
+    uint32_t cap;
+    __device__ void operator()(int, int64_t g, int64_t ex, int64_t v) const {
+        start[g] = ex;
+        if (v > cap) big_list[atomicAdd(big_n, 1u)] = (uint32_t)g;
+    }
+};
+
 struct EmitArgs {
     const Rec *recs;
-    const uint32_t *vals;      // rank -> primitive per item
-    const int64_t *pair_off;   // rank -> offset within item's pairs
-    const int64_t *nvis;       // per item
-    const int64_t *pair_begin; // per item
-    const int32_t *tiles_x;    // per item
-    uint32_t *pkeys;
-    uint32_t *pvals;
+    const int32_t *ntiles;
+    const int64_t *tile_base;
+    const int32_t *tiles_x;
+    const int64_t *count;      // primitives per item
+    const int64_t *tstart;     // global tile -> first slot
+    uint32_t *cursor;          // global tile -> fill cursor
+    uint32_t *pairs;           // primitive ids
     int64_t stride;
 };
 
-__global__ void __launch_bounds__(256) k_emit_pairs(EmitArgs a) {
+__global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     const int s = blockIdx.y;
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= a.nvis[s]) return;
-    const int64_t b = (int64_t)s * a.stride;
-    const uint32_t i = a.vals[b + r];
-    const Rec &rec = a.recs[b + i];
-    const int tx = a.tiles_x[s];
-    int64_t o = a.pair_begin[s] + a.pair_off[b + r];
-    const int u0 = rec.x0 / kTile, u1 = (rec.x1 - 1) / kTile;
-    const int v0 = rec.y0 / kTile, v1 = (rec.y1 - 1) / kTile;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.count[s]) return;
+    const int64_t o = (int64_t)s * a.stride + i;
+    if (a.ntiles[o] <= 0) return;
+    const Rec &r = a.recs[o];
+    const int64_t tb = a.tile_base[s];
+    const int txn = a.tiles_x[s];
+    int u0, u1, v0, v1;
+    rec_tile_range(r, u0, u1, v0, v1);
     for (int v = v0; v <= v1; ++v)
         for (int u = u0; u <= u1; ++u) {
-            a.pkeys[o] = (uint32_t)(v * tx + u);
-            a.pvals[o] = i;
-            ++o;
+            const int64_t g = tb + v * txn + u;
+            a.pairs[a.tstart[g] + atomicAdd(a.cursor + g, 1u)] = (uint32_t)i;
         }
 }
 
-__global__ void __launch_bounds__(256)
-k_tile_ranges(const uint32_t *__restrict__ pkeys, const int64_t *__restrict__ pair_begin,
-              const int64_t *__restrict__ npairs, const int64_t *__restrict__ tile_base,
-              int64_t *__restrict__ tstart, int64_t *__restrict__ tend) {
-    const int s = blockIdx.y;
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n = npairs[s];
-    if (r >= n) return;
-    const uint32_t *k = pkeys + pair_begin[s];
-    const uint32_t key = k[r];
-    const int64_t g = tile_base[s] + key;
-    if (r == 0 || k[r - 1] != key) tstart[g] = r;
-    if (r == n - 1 || k[r + 1] != key) tend[g] = r + 1;
+// oversized tiles: gather (key, id) of their ranges for the radix fallback
+struct BigArgs {
+    const uint32_t *big_list;
+    const int64_t *tstart;
+    const uint32_t *tcount;
+    const int32_t *tile_item;   // global tile -> item
+    const uint64_t *depth;      // [nitems][stride]
+    const uint32_t *pairs;
+    int64_t stride;
+    const int64_t *seg_begin;   // per big tile: offset in the gathered arrays
+    uint64_t *keys;
+    uint32_t *vals;
+};
+
+__global__ void __launch_bounds__(256) k_big_gather(BigArgs a) {
+    const int b = blockIdx.y;
+    const uint32_t g = a.big_list[b];
+    const int64_t n = a.tcount[g], s0 = a.tstart[g], d0 = a.seg_begin[b];
+    const int64_t item = a.tile_item[g];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t id = a.pairs[s0 + k];
+        a.vals[d0 + k] = id;
+        a.keys[d0 + k] = a.depth[item * a.stride + id];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_big_scatter(BigArgs a, const uint32_t *__restrict__ sorted_vals) {
+    const int b = blockIdx.y;
+    const uint32_t g = a.big_list[b];
+    const int64_t n = a.tcount[g], s0 = a.tstart[g], d0 = a.seg_begin[b];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        const_cast<uint32_t *>(a.pairs)[s0 + k] = sorted_vals[d0 + k];
+}
+
+__global__ void __launch_bounds__(256) k_ids_as_keys(const uint32_t *__restrict__ vals, uint64_t *__restrict__ keys,
+                                                     int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = vals[i];
+}
+
+__global__ void __launch_bounds__(256) k_gather_keys(const uint32_t *__restrict__ vals, const int64_t *__restrict__ seg_begin,
+                                                     const uint32_t *__restrict__ big_list, const int32_t *__restrict__ tile_item,
+                                                     const uint32_t *__restrict__ tcount, const uint64_t *__restrict__ depth,
+                                                     int64_t stride, uint64_t *__restrict__ keys) {
+    const int b = blockIdx.y;
+    const uint32_t g = big_list[b];
+    const int64_t n = tcount[g], d0 = seg_begin[b];
+    const int64_t item = tile_item[g];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        keys[d0 + k] = depth[item * stride + vals[d0 + k]];
 }
 
 // ---------------------------------------------------------------------------
@@ -316,14 +330,12 @@ k_tile_ranges(const uint32_t *__restrict__ pkeys, const int64_t *__restrict__ pa
 
 struct CompItem {
     const Rec *recs;         // primitive records of this item
-    const uint32_t *gids;    // sorted pair values (primitive ids) of this item
-    const int64_t *tstart;   // per tile of this item
-    const int64_t *tend;
+    const uint64_t *depth;   // orderable depth keys of this item
     const double *target;    // (h,w,3) or null
     double *image;           // (h,w,3) or null
     double *trans;           // (h,w) or null
     int64_t *usage;          // [n] or null
-    double *sse_tiles;       // per tile of this item
+    double *sse_tiles;       // per (tile, warp) of this item
     int32_t w, h, tiles_x, clip;
 };
 
@@ -370,9 +382,11 @@ struct CompShared {
 };
 
 constexpr int kCompWarps = kTileThreads / 32;
+constexpr int kSortCap = 2048;  // tile lists up to this length are sorted in shared memory
 #ifndef COMP_MIN_BLOCKS
 #define COMP_MIN_BLOCKS 3
 #endif
+constexpr size_t kCompSmem = sizeof(CompShared) + (size_t)kSortCap * (sizeof(uint64_t) + sizeof(uint32_t));
 
 // alpha' = min(al * exp(-e), 0.999) for staged primitive j at (dx, dy):
 // exact replay of _composite.pyx:56-60 (0.5*(A + C) == 0.5A + 0.5C exactly)
@@ -387,16 +401,178 @@ __device__ __forceinline__ double alpha_at(const CompShared &sh, int j, double p
     return ap > kAlphaClamp ? kAlphaClamp : ap;
 }
 
+// ---- tile-list sort: ascending (depth key, primitive index) -----------------
+// Bitonic network over npad (power of 2) entries in shared memory.  Strides
+// below 64 run in registers on 64-entry warp segments (lane holds entries
+// lane and lane+32, partners via shuffles, no barriers); only strides >= 64
+// touch shared memory with block barriers.
+
+__device__ __forceinline__ bool kv_gt(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
+    return ka > kb || (ka == kb && va > vb);
+}
+
+// in-register steps for strides s = smax .. 1 (smax <= 32) of bitonic size `size`
+__device__ __forceinline__ void warp_bitonic_steps(uint64_t &k0, uint32_t &v0, uint64_t &k1, uint32_t &v1, int e0,
+                                                   int size, int smax) {
+    const int lane = threadIdx.x & 31;
+    if (smax >= 32) {  // stride 32: the lane's own pair (e0, e0 + 32)
+        const bool asc = (e0 & size) == 0;
+        if (kv_gt(k0, v0, k1, v1) == asc) {
+            const uint64_t tk = k0;
+            const uint32_t tv = v0;
+            k0 = k1;
+            v0 = v1;
+            k1 = tk;
+            v1 = tv;
+        }
+        smax = 16;
+    }
+    for (int st = smax; st > 0; st >>= 1) {
+        const bool lower = (lane & st) == 0;
+        {
+            const uint64_t pk = __shfl_xor_sync(0xffffffffu, k0, st);
+            const uint32_t pv = __shfl_xor_sync(0xffffffffu, v0, st);
+            const bool asc = (e0 & size) == 0;
+            const bool gt = kv_gt(k0, v0, pk, pv);
+            if ((lower == asc) ? gt : !gt && (pk != k0 || pv != v0)) {
+                k0 = pk;
+                v0 = pv;
+            }
+        }
+        {
+            const uint64_t pk = __shfl_xor_sync(0xffffffffu, k1, st);
+            const uint32_t pv = __shfl_xor_sync(0xffffffffu, v1, st);
+            const bool asc = ((e0 + 32) & size) == 0;
+            const bool gt = kv_gt(k1, v1, pk, pv);
+            if ((lower == asc) ? gt : !gt && (pk != k1 || pv != v1)) {
+                k1 = pk;
+                v1 = pv;
+            }
+        }
+    }
+}
+
+// Fast path: one 64-bit key per entry = (tile-local depth bucket << 32) | index.
+__device__ __forceinline__ void warp_bitonic_steps_u64(uint64_t &k0, uint64_t &k1, int e0, int size, int smax) {
+    const int lane = threadIdx.x & 31;
+    if (smax >= 32) {
+        const bool asc = (e0 & size) == 0;
+        if ((k0 > k1) == asc) {
+            const uint64_t t = k0;
+            k0 = k1;
+            k1 = t;
+        }
+        smax = 16;
+    }
+    for (int st = smax; st > 0; st >>= 1) {
+        const bool lower = (lane & st) == 0;
+        const uint64_t p0 = __shfl_xor_sync(0xffffffffu, k0, st);
+        const uint64_t p1 = __shfl_xor_sync(0xffffffffu, k1, st);
+        const bool a0 = (e0 & size) == 0, a1 = ((e0 + 32) & size) == 0;
+        k0 = (lower == a0) ? min(k0, p0) : max(k0, p0);
+        k1 = (lower == a1) ? min(k1, p1) : max(k1, p1);
+    }
+}
+
+__device__ __noinline__ void sort_tile_keys(uint64_t *k, int npad) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int seg = w; seg * 64 < npad; seg += kTileThreads / 32) {
+        const int e0 = seg * 64 + lane;
+        uint64_t k0 = k[e0], k1 = k[e0 + 32];
+        for (int size = 2; size <= 64; size <<= 1) warp_bitonic_steps_u64(k0, k1, e0, size, size >> 1);
+        k[e0] = k0;
+        k[e0 + 32] = k1;
+    }
+    __syncthreads();
+    for (int size = 128; size <= npad; size <<= 1) {
+        for (int st = size >> 1; st >= 64; st >>= 1) {
+            for (int i = threadIdx.x; i < (npad >> 1); i += kTileThreads) {
+                const int lo = ((i & ~(st - 1)) << 1) | (i & (st - 1));
+                const int hi = lo + st;
+                const bool asc = (lo & size) == 0;
+                const uint64_t ka = k[lo], kb = k[hi];
+                if ((ka > kb) == asc) {
+                    k[lo] = kb;
+                    k[hi] = ka;
+                }
+            }
+            __syncthreads();
+        }
+        for (int seg = w; seg * 64 < npad; seg += kTileThreads / 32) {
+            const int e0 = seg * 64 + lane;
+            uint64_t k0 = k[e0], k1 = k[e0 + 32];
+            warp_bitonic_steps_u64(k0, k1, e0, size, 32);
+            k[e0] = k0;
+            k[e0 + 32] = k1;
+        }
+        __syncthreads();
+    }
+}
+
+// Exact path: (64-bit depth key, index) pairs, used when two entries of a
+// tile share a 32-bit depth bucket.
+__device__ __noinline__ void sort_tile_list(uint64_t *k, uint32_t *v, int npad) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // sizes 2..64: each warp sorts whole 64-entry segments in registers
+    for (int seg = w; seg * 64 < npad; seg += kTileThreads / 32) {
+        const int e0 = seg * 64 + lane;
+        uint64_t k0 = k[e0], k1 = k[e0 + 32];
+        uint32_t v0 = v[e0], v1 = v[e0 + 32];
+        for (int size = 2; size <= 64; size <<= 1) warp_bitonic_steps(k0, v0, k1, v1, e0, size, size >> 1);
+        k[e0] = k0;
+        k[e0 + 32] = k1;
+        v[e0] = v0;
+        v[e0 + 32] = v1;
+    }
+    __syncthreads();
+    for (int size = 128; size <= npad; size <<= 1) {
+        for (int st = size >> 1; st >= 64; st >>= 1) {
+            for (int i = threadIdx.x; i < (npad >> 1); i += kTileThreads) {
+                const int lo = ((i & ~(st - 1)) << 1) | (i & (st - 1));
+                const int hi = lo + st;
+                const bool asc = (lo & size) == 0;
+                const uint64_t ka = k[lo], kb = k[hi];
+                const uint32_t va = v[lo], vb = v[hi];
+                if (kv_gt(ka, va, kb, vb) == asc) {
+                    k[lo] = kb;
+                    k[hi] = ka;
+                    v[lo] = vb;
+                    v[hi] = va;
+                }
+            }
+            __syncthreads();
+        }
+        for (int seg = w; seg * 64 < npad; seg += kTileThreads / 32) {
+            const int e0 = seg * 64 + lane;
+            uint64_t k0 = k[e0], k1 = k[e0 + 32];
+            uint32_t v0 = v[e0], v1 = v[e0 + 32];
+            warp_bitonic_steps(k0, v0, k1, v1, e0, size, 32);
+            k[e0] = k0;
+            k[e0 + 32] = k1;
+            v[e0] = v0;
+            v[e0 + 32] = v1;
+        }
+        __syncthreads();
+    }
+}
+
 // One CTA = one 16x16 tile, one pixel per thread; warps are 8x4 sub-tiles.
-// Per batch of 256 depth-ordered primitives (staged once per CTA), each warp
-// walks 32-entry chunks: phase A tests only primitives whose threshold-ellipse
+// The tile's primitive list is first put in depth order (shared-memory
+// bitonic sort on (depth key, index); oversized lists arrive presorted).
+// Per batch of 256 primitives (staged once per CTA), each warp walks
+// 32-entry chunks: phase A tests only primitives whose threshold-ellipse
 // AABB touches its sub-tile (fp32, log2 domain, proven guard band) and builds
 // a per-lane candidate mask; phase B has every lane run its own candidates
 // through the exact fp64 path in depth order (two candidates' exp in flight).
 template <bool USAGE>
 __global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
-k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems) {
-    __shared__ CompShared sh;
+k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
+            const int64_t *__restrict__ tstart, const uint32_t *__restrict__ tcount,
+            const uint32_t *__restrict__ pairs) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CompShared &sh = *reinterpret_cast<CompShared *>(smem_raw);
+    uint64_t *skey = reinterpret_cast<uint64_t *>(smem_raw + sizeof(CompShared));
+    uint32_t *sid = reinterpret_cast<uint32_t *>(skey + kSortCap);
     {
         const unsigned long long *src = &kExpTable[0][0];
         for (int k = threadIdx.x; k < kExpN; k += kTileThreads)
@@ -422,20 +598,86 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     const bool inside = px < img_w && py < img_h;
     const float pxl = (float)lx + 0.5f, pyl = (float)ly + 0.5f;
     const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
-    const uint32_t *__restrict__ gids = itp->gids;
     const Rec *__restrict__ recs = itp->recs;
+
+    const int64_t s0 = tstart[g];
+    const int n_all = (int)tcount[g];
+    const uint32_t *__restrict__ glist = pairs + s0;
+    const bool in_smem = n_all <= kSortCap;
+    if (in_smem && n_all > 1) {
+        const uint64_t *__restrict__ depth = itp->depth;
+        int npad = 64;
+        while (npad < n_all) npad <<= 1;
+        // tile-local depth range -> 32-bit buckets (monotone in depth)
+        unsigned long long kmin = ~0ull, kmax = 0ull;
+        for (int k = threadIdx.x; k < n_all; k += kTileThreads) {
+            const uint64_t zk = depth[glist[k]];
+            kmin = min(kmin, (unsigned long long)zk);
+            kmax = max(kmax, (unsigned long long)zk);
+        }
+        for (int d = 16; d > 0; d >>= 1) {
+            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, d));
+            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, d));
+        }
+        if (lane == 0) {
+            skey[2 * w] = kmin;
+            skey[2 * w + 1] = kmax;
+        }
+        __syncthreads();
+        kmin = skey[0];
+        kmax = skey[1];
+        for (int k = 1; k < kCompWarps; ++k) {
+            kmin = min(kmin, (unsigned long long)skey[2 * k]);
+            kmax = max(kmax, (unsigned long long)skey[2 * k + 1]);
+        }
+        const unsigned long long span = kmax - kmin;
+        const int sh = span >> 32 ? 64 - __clzll((long long)span) - 32 : 0;
+        __syncthreads();
+        for (int k = threadIdx.x; k < npad; k += kTileThreads) {
+            uint64_t key = ~0ull;
+            if (k < n_all) {
+                const uint32_t id = glist[k];
+                key = (((uint64_t)(depth[id] - kmin) >> sh) << 32) | id;
+            }
+            skey[k] = key;
+        }
+        __syncthreads();
+        sort_tile_keys(skey, npad);
+        // equal buckets need the exact (depth, index) comparison: redo exactly
+        int clash = 0;
+        for (int k = threadIdx.x; k + 1 < n_all; k += kTileThreads)
+            clash |= (skey[k] >> 32) == (skey[k + 1] >> 32);
+        if (__syncthreads_or(clash)) {
+            for (int k = threadIdx.x; k < npad; k += kTileThreads) {
+                if (k < n_all) {
+                    const uint32_t id = (uint32_t)skey[k];
+                    sid[k] = id;
+                } else {
+                    sid[k] = 0xffffffffu;
+                }
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < npad; k += kTileThreads)
+                skey[k] = sid[k] == 0xffffffffu ? ~0ull : depth[sid[k]];
+            __syncthreads();
+            sort_tile_list(skey, sid, npad);
+        } else {
+            for (int k = threadIdx.x; k < n_all; k += kTileThreads) sid[k] = (uint32_t)skey[k];
+        }
+    } else if (in_smem && n_all == 1) {
+        if (threadIdx.x == 0) sid[0] = glist[0];
+    }
 
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     bool done = !inside;
     float thr = log2_inv_eps() + 6e-5f;  // log2(T/EPS) + guard constant
 
-    const int64_t s = itp->tstart[tl], e = itp->tend[tl];
-    for (int64_t base = s; base < e; base += kTileThreads) {
-        const int nb = (int)min((int64_t)kTileThreads, e - base);
+    for (int base = 0; base < n_all; base += kTileThreads) {
+        const int nb = min(kTileThreads, n_all - base);
         __syncthreads();
         if ((int)threadIdx.x < nb) {
             const int t = threadIdx.x;
-            const uint32_t gi = gids[base + t];
+            const uint32_t gi = in_smem ? sid[base + t] : glist[base + t];
             const Rec r = recs[gi];
             const float mxl = (float)(r.mx - (double)ox), myl = (float)(r.my - (double)oy);
             sh.gid[t] = gi;
@@ -608,7 +850,7 @@ __global__ void __launch_bounds__(256)
 k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__restrict__ conics,
                const double *__restrict__ alphas, const double *__restrict__ colors,
                const int64_t *__restrict__ bboxes, Rec *__restrict__ recs, int32_t *__restrict__ ntiles,
-               uint32_t *__restrict__ vals) {
+               uint64_t *__restrict__ depth, uint32_t *__restrict__ tile_count, int tiles_x) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
     Rec r;
@@ -635,11 +877,13 @@ k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__re
         r.hy = det > 0.0 && isfinite(hy) ? (float)hy * 1.0001f : 1e30f;
     }
     recs[i] = r;
-    int nt = 0;
-    if (r.x1 > r.x0 && r.y1 > r.y0)
-        nt = ((r.x1 - 1) / kTile - r.x0 / kTile + 1) * ((r.y1 - 1) / kTile - r.y0 / kTile + 1);
+    int nt = 0, u0, u1, v0, v1;
+    if (r.x1 > r.x0 && r.y1 > r.y0 && rec_tile_range(r, u0, u1, v0, v1)) nt = (u1 - u0 + 1) * (v1 - v0 + 1);
     ntiles[i] = nt;
-    vals[i] = (uint32_t)i;
+    depth[i] = (uint64_t)i;  // the input order is the depth order
+    if (nt > 0)
+        for (int v = v0; v <= v1; ++v)
+            for (int u = u0; u <= u1; ++u) atomicAdd(tile_count + v * tiles_x + u, 1u);
 }
 
 __global__ void k_fill_i64(int64_t *p, int64_t n, int64_t v) {
@@ -661,86 +905,98 @@ struct ItemHost {
     int clip;
 };
 
-// Stage B: given per item records (recs + item*stride), the depth-sorted
-// primitive list vals (+ item*stride) of length nvis[item] (device), and
-// ntiles per primitive, bin into tiles, composite and reduce SSE.
-static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, int64_t stride,
-                              const Rec *recs, const uint32_t *vals, const int32_t *ntiles,
-                              const int64_t *d_nvis, int64_t max_nvis, double *sse, cudaStream_t st) {
-    const int nitems = (int)items.size();
-    int64_t &L = ctx->launches;
-    // rank-ordered tile counts -> per-rank pair offsets, per-item totals
-    int64_t *pair_off = ctx->scratch_t<int64_t>(kSlotPairOff, (size_t)nitems * stride);
-    int64_t *stats = ctx->scratch_t<int64_t>(kSlotItemStats, (size_t)8 * nitems + 8);
-    int64_t *d_npairs = stats + 4 * nitems;
-    const int bps = (int)std::max<int64_t>(1, ceil_div(std::max<int64_t>(max_nvis, 1), kScanTile));
-    int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, (size_t)nitems * bps);
-    if (max_nvis > 0) {
-        seg_scan<int64_t>(TileCountIn{ntiles, vals, stride}, TileCountOut{pair_off, stride}, d_nvis, nitems,
-                          max_nvis, blocks, d_npairs, st, &L);
-    } else {
-        AIRGS_CUDA_TRY(cudaMemsetAsync(d_npairs, 0, sizeof(int64_t) * nitems, st));
-    }
-    check_launch();
-    std::vector<int64_t> npairs(nitems);
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(npairs.data(), d_npairs, sizeof(int64_t) * nitems, cudaMemcpyDeviceToHost, st));
-    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+// Device layout of the per-call descriptors shared by project / emit / composite.
+struct Layout {
+    int nitems = 0;
+    int64_t stride = 0;
+    int64_t Tt = 0;                  // total tiles
+    std::vector<int64_t> tile_base;  // nitems + 1
+    const int64_t *d_tile_base = nullptr;
+    const int32_t *d_tiles_x = nullptr;
+    const int64_t *d_count = nullptr;
+    const int32_t *d_tile_item = nullptr;
+};
 
-    // host layout: pair segments and tile bases
-    std::vector<int64_t> hb(3 * nitems + 1);
-    int64_t *pair_begin = hb.data();
-    int64_t *tile_base = hb.data() + nitems;  // nitems + 1 entries
-    int64_t P = 0, maxp = 0, Tt = 0;
-    int max_tiles = 1;
-    for (int s = 0; s < nitems; ++s) {
-        pair_begin[s] = P;
-        P += npairs[s];
-        maxp = std::max(maxp, npairs[s]);
-        tile_base[s] = Tt;
-        Tt += (int64_t)items[s].tiles_x * items[s].tiles_y;
-        max_tiles = std::max(max_tiles, items[s].tiles_x * items[s].tiles_y);
-    }
-    tile_base[nitems] = Tt;
-    int64_t *d_pb = stats + 5 * nitems;  // pair_begin (nitems) then tile_base (nitems+1)
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(d_pb, hb.data(), sizeof(int64_t) * (2 * nitems + 1), cudaMemcpyHostToDevice, st));
-    const int64_t *d_pair_begin = d_pb;
-    const int64_t *d_tile_base = d_pb + nitems;
-
-    uint32_t *pk = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)P);
-    uint32_t *pv = ctx->scratch_t<uint32_t>(kSlotPairVals, (size_t)P);
-    uint32_t *pk2 = ctx->scratch_t<uint32_t>(kSlotPairKeysAlt, (size_t)P);
-    uint32_t *pv2 = ctx->scratch_t<uint32_t>(kSlotPairValsAlt, (size_t)P);
-    int32_t *d_tiles_x = (int32_t *)ctx->scratch_t<int32_t>(kSlotMisc0, (size_t)nitems);
+// Stage B: histogram (already accumulated in tile_count) -> ranges -> emit ->
+// oversized-tile fallback sort -> composite -> SSE.
+static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
+                              const Rec *recs, const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count,
+                              double *sse, cudaStream_t st) {
+    const int nitems = L.nitems;
+    int64_t &NL = ctx->launches;
+    const int64_t Tt = L.Tt;
+    int64_t *tstart = ctx->scratch_t<int64_t>(kSlotRanges, (size_t)Tt);
+    uint32_t *big_list = ctx->scratch_t<uint32_t>(kSlotPairValsAlt, (size_t)Tt);
+    int64_t *stats = ctx->scratch_t<int64_t>(kSlotItemStats, 8);
+    unsigned int *big_n = (unsigned int *)(stats + 2);
+    int64_t *d_total = stats;
+    int64_t *d_Tt = stats + 1;
+    AIRGS_CUDA_TRY(cudaMemsetAsync(big_n, 0, sizeof(unsigned int), st));
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(d_Tt, &Tt, sizeof(int64_t), cudaMemcpyHostToDevice, st));
     {
-        std::vector<int32_t> tx(nitems);
-        for (int s = 0; s < nitems; ++s) tx[s] = items[s].tiles_x;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(d_tiles_x, tx.data(), sizeof(int32_t) * nitems, cudaMemcpyHostToDevice, st));
-        // tx is destroyed at scope end: make the copy complete first
-        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-    }
-    if (P > 0 && max_nvis > 0) {
-        EmitArgs ea{recs, vals, pair_off, d_nvis, d_pair_begin, d_tiles_x, pk, pv, stride};
-        dim3 grid((unsigned)ceil_div(max_nvis, 256), (unsigned)nitems);
-        k_emit_pairs<<<grid, 256, 0, st>>>(ea);
-        ++L;
+        const int bps = (int)std::max<int64_t>(1, ceil_div(Tt, kScanTile));
+        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
+        seg_scan<int64_t>(TileScanIn{tile_count}, TileScanOut{tstart, big_list, big_n, (uint32_t)kSortCap}, d_Tt, 1,
+                          Tt, blocks, d_total, st, &NL);
         check_launch();
-        const int nbits = std::max(1, bit_length((uint64_t)(max_tiles - 1)));
-        uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)nitems * 256 * ceil_div(maxp, kSortTile));
-        bool alt = radix_sort<uint32_t>(pk, pv, pk2, pv2, d_pair_begin, d_npairs, nitems, maxp, nbits, hist, st, &L);
-        check_launch();
-        if (alt) {
-            std::swap(pk, pk2);
-            std::swap(pv, pv2);
-        }
     }
-    int64_t *ranges = ctx->scratch_t<int64_t>(kSlotRanges, (size_t)2 * Tt);
-    int64_t *tstart = ranges, *tend = ranges + Tt;
-    AIRGS_CUDA_TRY(cudaMemsetAsync(ranges, 0, sizeof(int64_t) * 2 * Tt, st));
+    int64_t hh[2];
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(hh, stats, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    unsigned int hbig = 0;
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbig, big_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t P = hh[0];
+    uint32_t *pairs = ctx->scratch_t<uint32_t>(kSlotPairVals, (size_t)std::max<int64_t>(P, 1));
+    uint32_t *cursor = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)Tt);
+    AIRGS_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * Tt, st));
+    int64_t maxc = 0;
+    for (const auto &h : items) maxc = std::max(maxc, h.count);
     if (P > 0) {
-        dim3 grid((unsigned)ceil_div(maxp, 256), (unsigned)nitems);
-        k_tile_ranges<<<grid, 256, 0, st>>>(pk, d_pair_begin, d_npairs, d_tile_base, tstart, tend);
-        ++L;
+        EmitArgs ea{recs, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tstart, cursor, pairs, L.stride};
+        k_emit<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ea);
+        ++NL;
         check_launch();
+    }
+    if (hbig > 0) {
+        // oversized tiles: stable radix sort of each range by index, then by depth key
+        std::vector<uint32_t> hlist(hbig);
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(hlist.data(), big_list, sizeof(uint32_t) * hbig, cudaMemcpyDeviceToHost, st));
+        std::vector<uint32_t> hcnt(hbig);
+        for (unsigned b = 0; b < hbig; ++b)
+            AIRGS_CUDA_TRY(cudaMemcpyAsync(&hcnt[b], tile_count + hlist[b], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        std::vector<int64_t> seg(2 * hbig);
+        int64_t tot = 0, mx = 0;
+        for (unsigned b = 0; b < hbig; ++b) {
+            seg[b] = tot;
+            seg[hbig + b] = hcnt[b];
+            tot += hcnt[b];
+            mx = std::max<int64_t>(mx, hcnt[b]);
+        }
+        int64_t *d_seg = ctx->scratch_t<int64_t>(kSlotMisc3, 2 * (size_t)hbig);
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(d_seg, seg.data(), sizeof(int64_t) * 2 * hbig, cudaMemcpyHostToDevice, st));
+        uint64_t *k1 = ctx->scratch_t<uint64_t>(kSlotKeys, (size_t)tot);
+        uint64_t *k2 = ctx->scratch_t<uint64_t>(kSlotKeysAlt, (size_t)tot);
+        uint32_t *v1 = ctx->scratch_t<uint32_t>(kSlotVals, (size_t)tot);
+        uint32_t *v2 = ctx->scratch_t<uint32_t>(kSlotValsAlt, (size_t)tot);
+        uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)hbig * 256 * ceil_div(mx, kSortTile));
+        BigArgs ba{big_list, tstart, tile_count, L.d_tile_item, depth, pairs, L.stride, d_seg, k1, v1};
+        const dim3 gg((unsigned)std::min<int64_t>(64, ceil_div(mx, 256)), hbig);
+        k_big_gather<<<gg, 256, 0, st>>>(ba);
+        k_ids_as_keys<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(v1, k1, tot);
+        NL += 2;
+        bool alt = radix_sort<uint64_t>(k1, v1, k2, v2, d_seg, d_seg + hbig, (int)hbig, mx, 32, hist, st, &NL);
+        uint32_t *vs = alt ? v2 : v1;
+        uint64_t *ks = alt ? k2 : k1;
+        uint64_t *ko = alt ? k1 : k2;
+        uint32_t *vo = alt ? v1 : v2;
+        k_gather_keys<<<gg, 256, 0, st>>>(vs, d_seg, big_list, L.d_tile_item, tile_count, depth, L.stride, ks);
+        ++NL;
+        bool alt2 = radix_sort<uint64_t>(ks, vs, ko, vo, d_seg, d_seg + hbig, (int)hbig, mx, 64, hist, st, &NL);
+        k_big_scatter<<<gg, 256, 0, st>>>(ba, alt2 ? vo : vs);
+        ++NL;
+        check_launch();
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
     }
     double *sse_tiles = ctx->scratch_t<double>(kSlotSseTiles, (size_t)Tt * kCompWarps);
     std::vector<CompItem> ci(nitems);
@@ -749,15 +1005,13 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     for (int s = 0; s < nitems; ++s) {
         const ItemHost &h = items[s];
         CompItem &c = ci[s];
-        c.recs = recs + (int64_t)s * stride;
-        c.gids = pv + pair_begin[s];
-        c.tstart = tstart + tile_base[s];
-        c.tend = tend + tile_base[s];
+        c.recs = recs + (int64_t)s * L.stride;
+        c.depth = depth + (int64_t)s * L.stride;
         c.target = h.target;
         c.image = h.image;
         c.trans = h.trans;
         c.usage = h.usage;
-        c.sse_tiles = sse_tiles + tile_base[s] * kCompWarps;
+        c.sse_tiles = sse_tiles + L.tile_base[s] * kCompWarps;
         c.w = h.w;
         c.h = h.h;
         c.tiles_x = h.tiles_x;
@@ -770,21 +1024,59 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     uint8_t *d_has = (uint8_t *)ctx->scratch(kSlotMisc2, nitems);
     AIRGS_CUDA_TRY(cudaMemcpyAsync(d_ci, ci.data(), sizeof(CompItem) * nitems, cudaMemcpyHostToDevice, st));
     AIRGS_CUDA_TRY(cudaMemcpyAsync(d_has, has_t.data(), nitems, cudaMemcpyHostToDevice, st));
+    static bool attr_set = false;
+    if (!attr_set) {
+        AIRGS_CUDA_TRY(cudaFuncSetAttribute(k_composite<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCompSmem));
+        AIRGS_CUDA_TRY(cudaFuncSetAttribute(k_composite<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCompSmem));
+        attr_set = true;
+    }
     if (Tt > 0) {
         if (any_usage)
-            k_composite<true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, d_tile_base, nitems);
+            k_composite<true><<<(unsigned)Tt, kTileThreads, kCompSmem, st>>>(d_ci, L.d_tile_base, nitems, tstart,
+                                                                               tile_count, pairs);
         else
-            k_composite<false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, d_tile_base, nitems);
-        ++L;
+            k_composite<false><<<(unsigned)Tt, kTileThreads, kCompSmem, st>>>(d_ci, L.d_tile_base, nitems, tstart,
+                                                                                tile_count, pairs);
+        ++NL;
         check_launch();
     }
     if (sse && any_target) {
-        k_sse_items<<<nitems, 256, 0, st>>>(sse_tiles, d_tile_base, d_has, sse);
-        ++L;
+        k_sse_items<<<nitems, 256, 0, st>>>(sse_tiles, L.d_tile_base, d_has, sse);
+        ++NL;
         check_launch();
     }
-    // host vectors (ci, has_t, hb) must outlive the async copies
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));  // host vectors outlive their async copies
+}
+
+// Upload per-item layout arrays (tile bases, tiles_x, counts, tile -> item map).
+static void upload_layout(airgs_ctx *ctx, const std::vector<ItemHost> &items, Layout &L, cudaStream_t st) {
+    const int nitems = (int)items.size();
+    L.nitems = nitems;
+    L.tile_base.assign(nitems + 1, 0);
+    for (int s = 0; s < nitems; ++s) L.tile_base[s + 1] = L.tile_base[s] + (int64_t)items[s].tiles_x * items[s].tiles_y;
+    L.Tt = L.tile_base[nitems];
+    size_t off = 0;
+    auto align = [](size_t x) { return (x + 15) & ~size_t(15); };
+    const size_t o_tb = off; off = align(off + sizeof(int64_t) * (nitems + 1));
+    const size_t o_tx = off; off = align(off + sizeof(int32_t) * nitems);
+    const size_t o_cnt = off; off = align(off + sizeof(int64_t) * nitems);
+    const size_t o_ti = off; off = align(off + sizeof(int32_t) * L.Tt);
+    std::vector<char> hbuf(off);
+    memcpy(hbuf.data() + o_tb, L.tile_base.data(), sizeof(int64_t) * (nitems + 1));
+    for (int s = 0; s < nitems; ++s) {
+        const int32_t tx = items[s].tiles_x;
+        memcpy(hbuf.data() + o_tx + sizeof(int32_t) * s, &tx, sizeof(int32_t));
+        memcpy(hbuf.data() + o_cnt + sizeof(int64_t) * s, &items[s].count, sizeof(int64_t));
+        int32_t *ti = reinterpret_cast<int32_t *>(hbuf.data() + o_ti);
+        for (int64_t g = L.tile_base[s]; g < L.tile_base[s + 1]; ++g) ti[g] = s;
+    }
+    char *d = (char *)ctx->scratch(kSlotMisc0, off);
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(d, hbuf.data(), off, cudaMemcpyHostToDevice, st));
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    L.d_tile_base = (const int64_t *)(d + o_tb);
+    L.d_tiles_x = (const int32_t *)(d + o_tx);
+    L.d_count = (const int64_t *)(d + o_cnt);
+    L.d_tile_item = (const int32_t *)(d + o_ti);
 }
 
 static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, const airgs_camera *cams,
@@ -821,7 +1113,10 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         per_frame[v.frame].push_back(s);
         stride = std::max(stride, f.count);
     }
-    int64_t &L = ctx->launches;
+    int64_t &NL = ctx->launches;
+    Layout L;
+    L.stride = stride;
+    upload_layout(ctx, ih, L, st);
     // descriptors -> device (one packed upload)
     std::vector<int32_t> fptr(nframes + 1), fitems, icam(nitems);
     fptr[0] = 0;
@@ -830,8 +1125,6 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         fptr[f + 1] = (int32_t)fitems.size();
     }
     for (int s = 0; s < nitems; ++s) icam[s] = ih[s].cam;
-    std::vector<int64_t> icount(nitems);
-    for (int s = 0; s < nitems; ++s) icount[s] = ih[s].count;
     size_t off = 0;
     auto align = [](size_t x) { return (x + 15) & ~size_t(15); };
     const size_t o_frames = off; off = align(off + sizeof(airgs_frame) * nframes);
@@ -839,38 +1132,23 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     const size_t o_fptr = off; off = align(off + sizeof(int32_t) * (nframes + 1));
     const size_t o_fitems = off; off = align(off + sizeof(int32_t) * nitems);
     const size_t o_icam = off; off = align(off + sizeof(int32_t) * nitems);
-    const size_t o_icount = off; off = align(off + sizeof(int64_t) * nitems);
     char *hs = (char *)ctx->staging(off);
     memcpy(hs + o_frames, frames, sizeof(airgs_frame) * nframes);
     memcpy(hs + o_cams, cams, sizeof(airgs_camera) * ncams);
     memcpy(hs + o_fptr, fptr.data(), sizeof(int32_t) * (nframes + 1));
     memcpy(hs + o_fitems, fitems.data(), sizeof(int32_t) * nitems);
     memcpy(hs + o_icam, icam.data(), sizeof(int32_t) * nitems);
-    memcpy(hs + o_icount, icount.data(), sizeof(int64_t) * nitems);
     char *dd = (char *)ctx->scratch(kSlotDesc, off);
     AIRGS_CUDA_TRY(cudaMemcpyAsync(dd, hs, off, cudaMemcpyHostToDevice, st));
 
-    // per-item stats: zmin, zmax, nvis, (npairs), ...
-    int64_t *stats = ctx->scratch_t<int64_t>(kSlotItemStats, (size_t)8 * nitems + 8);
-    unsigned long long *zmin = (unsigned long long *)stats;
-    unsigned long long *zmax = (unsigned long long *)(stats + nitems);
-    int64_t *nvis = stats + 2 * nitems;
     unsigned int *flags = ctx->scratch_t<unsigned int>(kSlotFlags, 4);
-    {
-        const int nb = (int)ceil_div(nitems, 256);
-        k_fill_i64<<<nb, 256, 0, st>>>((int64_t *)zmin, nitems, -1);  // all ones
-        k_fill_i64<<<nb, 256, 0, st>>>((int64_t *)zmax, 2 * nitems, 0);  // zmax + nvis
-        L += 2;
-        AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
-    }
+    AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
     const size_t per = (size_t)nitems * stride;
     Rec *recs = ctx->scratch_t<Rec>(kSlotRecs, per);
     uint64_t *depth = ctx->scratch_t<uint64_t>(kSlotDepth, per);
     int32_t *ntiles = ctx->scratch_t<int32_t>(kSlotNtiles, per);
-    uint64_t *keys = ctx->scratch_t<uint64_t>(kSlotKeys, per);
-    uint32_t *vals = ctx->scratch_t<uint32_t>(kSlotVals, per);
-    uint64_t *keys2 = ctx->scratch_t<uint64_t>(kSlotKeysAlt, per);
-    uint32_t *vals2 = ctx->scratch_t<uint32_t>(kSlotValsAlt, per);
+    uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
+    AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
 
     ProjArgs pa;
     pa.frames = (const airgs_frame *)(dd + o_frames);
@@ -878,56 +1156,26 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.frame_item_ptr = (const int32_t *)(dd + o_fptr);
     pa.frame_items = (const int32_t *)(dd + o_fitems);
     pa.item_cam = (const int32_t *)(dd + o_icam);
+    pa.tile_base = L.d_tile_base;
+    pa.tiles_x = L.d_tiles_x;
     pa.recs = recs;
     pa.depth = depth;
     pa.ntiles = ntiles;
-    pa.zmin = zmin;
-    pa.zmax = zmax;
+    pa.tile_count = tile_count;
     pa.flags = flags;
     pa.stride = stride;
     {
         dim3 grid((unsigned)ceil_div(stride, kProjThreads), (unsigned)nframes);
         k_project<<<grid, kProjThreads, 0, st>>>(pa);
-        ++L;
+        ++NL;
         check_launch();
     }
-    const int64_t *d_icount = (const int64_t *)(dd + o_icount);
-    {
-        const int bps = (int)std::max<int64_t>(1, ceil_div(stride, kScanTile));
-        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, (size_t)nitems * bps);
-        seg_scan<int64_t>(VisIn{ntiles, stride}, VisOut{depth, zmin, keys, vals, stride}, d_icount, nitems, stride,
-                          blocks, nvis, st, &L);
-        check_launch();
-    }
-    // readback: zmin, zmax, nvis, flags
-    int64_t *hst = (int64_t *)ctx->staging(sizeof(int64_t) * (3 * nitems + 1));
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(hst, stats, sizeof(int64_t) * 3 * nitems, cudaMemcpyDeviceToHost, st));
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(hst + 3 * nitems, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    unsigned int hflags = 0;
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-    unsigned int hflags = *(unsigned int *)(hst + 3 * nitems);
     if (hflags & kFlagInvalidParam)
         throw ApiFailure(AIRGS_E_VALIDATION, "frame contains invalid primitive parameters");
-    int64_t max_nvis = 0;
-    uint64_t span = 0;
-    for (int s = 0; s < nitems; ++s) {
-        const int64_t nv = hst[2 * nitems + s];
-        max_nvis = std::max(max_nvis, nv);
-        if (nv > 0) span = std::max(span, (uint64_t)hst[nitems + s] - (uint64_t)hst[s]);
-    }
-    if (max_nvis > 0 && span > 0) {
-        const int nbits = bit_length(span);
-        uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)nitems * 256 * ceil_div(max_nvis, kSortTile));
-        // segment begins = s*stride: reuse a small device array
-        int64_t *d_begin = ctx->scratch_t<int64_t>(kSlotMisc3, (size_t)nitems);
-        std::vector<int64_t> hb(nitems);
-        for (int s = 0; s < nitems; ++s) hb[s] = (int64_t)s * stride;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(d_begin, hb.data(), sizeof(int64_t) * nitems, cudaMemcpyHostToDevice, st));
-        bool alt = radix_sort<uint64_t>(keys, vals, keys2, vals2, d_begin, nvis, nitems, max_nvis, nbits, hist, st, &L);
-        check_launch();
-        if (alt) vals = vals2;
-        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));  // hb lifetime
-    }
-    bin_and_composite(ctx, ih, stride, recs, vals, ntiles, nvis, max_nvis, sse, st);
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, sse, st);
 }
 
 static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics, const double *alphas,
@@ -935,21 +1183,6 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
                       int64_t *usage, cudaStream_t st) {
     if (h < 1 || w < 1) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad image size");
     if (k > 0x7fffffffLL) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");
-    const int64_t stride = std::max<int64_t>(k, 1);
-    Rec *recs = ctx->scratch_t<Rec>(kSlotRecs, stride);
-    int32_t *ntiles = ctx->scratch_t<int32_t>(kSlotNtiles, stride);
-    uint32_t *vals = ctx->scratch_t<uint32_t>(kSlotVals, stride);
-    int64_t *stats = ctx->scratch_t<int64_t>(kSlotItemStats, 16);
-    int64_t *nvis = stats + 2;
-    if (usage && k > 0) AIRGS_CUDA_TRY(cudaMemsetAsync(usage, 0, sizeof(int64_t) * k, st));
-    if (k > 0) {
-        k_seam_records<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, means2d, conics, alphas, colors, bboxes, recs,
-                                                                  ntiles, vals);
-        ++ctx->launches;
-        check_launch();
-    }
-    k_fill_i64<<<1, 32, 0, st>>>(nvis, 1, k);
-    ++ctx->launches;
     std::vector<ItemHost> ih(1);
     ItemHost &it = ih[0];
     it.frame = 0;
@@ -964,9 +1197,23 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
     it.trans = tfinal;
     it.usage = usage;
     it.clip = 0;
-    // pixels never touched keep image 0 / T 1: the composite kernel writes
-    // every in-image pixel of every tile, so no pre-fill is needed.
-    bin_and_composite(ctx, ih, stride, recs, vals, ntiles, nvis, k, nullptr, st);
+    Layout L;
+    L.stride = std::max<int64_t>(k, 1);
+    upload_layout(ctx, ih, L, st);
+    Rec *recs = ctx->scratch_t<Rec>(kSlotRecs, L.stride);
+    int32_t *ntiles = ctx->scratch_t<int32_t>(kSlotNtiles, L.stride);
+    uint64_t *depth = ctx->scratch_t<uint64_t>(kSlotDepth, L.stride);
+    uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
+    AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
+    if (usage && k > 0) AIRGS_CUDA_TRY(cudaMemsetAsync(usage, 0, sizeof(int64_t) * k, st));
+    if (k > 0) {
+        k_seam_records<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, means2d, conics, alphas, colors, bboxes, recs,
+                                                                  ntiles, depth, tile_count, it.tiles_x);
+        ++ctx->launches;
+        check_launch();
+    }
+    // every in-image pixel of every tile is written by the composite kernel
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, nullptr, st);
 }
 
 static void sse_impl(airgs_ctx *ctx, const double *a, const double *b, int64_t n, double *out, cudaStream_t st) {

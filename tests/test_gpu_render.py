@@ -185,3 +185,44 @@ def test_psnr_device(rng):
 
     with pytest.raises(StructuralError):
         metrics.psnr(np.zeros((8, 8, 3)), np.zeros((9, 8, 3)))
+
+
+def test_seam_oversized_tile_list_fallback(rng):
+    """> 2048 primitives on one tile exercise the radix-sort fallback for
+    lists too long for the shared-memory sort."""
+    from paper_2512_20943_b200 import rasterizer
+
+    n, side = 3000, 40
+    means2d = rng.uniform(16, 32, (n, 2))
+    conics = np.zeros((n, 3))
+    conics[:, 0] = rng.uniform(0.2, 1.5, n)
+    conics[:, 2] = rng.uniform(0.2, 1.5, n)
+    alphas = rng.uniform(0.02, 0.3, n)
+    colors = rng.uniform(0, 1, (n, 3))
+    bboxes = np.zeros((n, 4), dtype=np.int64)
+    bboxes[:, 0] = np.clip(np.floor(means2d[:, 0] - 6), 0, side)
+    bboxes[:, 1] = np.clip(np.ceil(means2d[:, 0] + 6) + 1, 0, side)
+    bboxes[:, 2] = np.clip(np.floor(means2d[:, 1] - 6), 0, side)
+    bboxes[:, 3] = np.clip(np.ceil(means2d[:, 1] + 6) + 1, 0, side)
+    img, tr, us, _ = rasterizer.forward(means2d, conics, alphas, colors, bboxes, side, side)
+    ri, rt, ru = orc.composite(means2d, conics, alphas, colors, bboxes, side, side)
+    np.testing.assert_array_equal(us, ru)
+    assert np.max(np.abs(img - ri)) <= PIX_TOL
+    assert np.max(np.abs(tr - rt)) <= PIX_TOL
+
+
+def test_depth_ties_resolved_by_index(rng):
+    """Primitives at identical depth composite in index order (stable
+    argsort, ss/rasterizer.py:127)."""
+    from paper_2512_20943_b200 import rasterizer
+    from paper_2512_20943_b200.model import GaussianFrame
+
+    p = random_params(rng, 400, 0, spread=0.5)
+    p[:, 2] = 0.1  # every primitive at the same depth for a camera looking along z
+    from paper_2512_20943_b200.camera import look_at
+
+    cam = look_at((0.0, 0.0, -2.5), (0.0, 0.0, 0.0), focal=60.0, resolution=(64, 48))
+    imgs, usage = rasterizer.render_with_usage(GaussianFrame(params=p), [cam])
+    ri, ru = orc.render_with_usage(p, [cam])
+    np.testing.assert_array_equal(usage.counts, ru)
+    assert np.max(np.abs(imgs[0].pixels - ri[0])) <= PIX_TOL
