@@ -84,6 +84,14 @@ AIRGS_API const char *airgs_last_error(const airgs_ctx *ctx);
 /* Number of kernel launches issued by this context since creation. */
 AIRGS_API int64_t airgs_launch_count(const airgs_ctx *ctx);
 
+/* Per-kernel device timing with CUDA events on the launching stream around
+ * the compositing and projection kernels (for roofline reporting).  Reads
+ * the accumulated totals, then if enable >= 0 arms (1) or disarms (0) timing
+ * and resets the counters; enable < 0 only reads. */
+AIRGS_API int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms,
+                           int64_t *composite_launches, double *project_ms,
+                           int64_t *project_launches);
+
 /* ---- rasterizer --------------------------------------------------------- */
 
 /* Batched render: replaces ss/rasterizer.py:113-240 (_activate, _prepare,

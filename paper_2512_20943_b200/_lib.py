@@ -62,6 +62,7 @@ SIGNATURES = {
     "airgs_ctx_destroy": (ctypes.c_int, [vp]),
     "airgs_last_error": (ctypes.c_char_p, [vp]),
     "airgs_launch_count": (i64, [vp]),
+    "airgs_timing": (ctypes.c_int, [vp, i32, c_double_p, c_i64_p, c_double_p, c_i64_p]),
     "airgs_render": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), i32, ctypes.POINTER(CameraC), i32,
                                     ctypes.POINTER(ItemC), i32, vp, vp]),
     "airgs_composite_forward": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp]),
@@ -141,6 +142,16 @@ class Engine:
                 raise RuntimeError(f"{name} failed (status {rc}): {msg}")
             raise exc(msg)
         return rc
+
+    def timing(self, enable=-1):
+        """Read (and optionally re-arm/reset) the per-kernel event timers:
+        returns dict(composite_ms, composite_launches, project_ms, project_launches)."""
+        cm, pm = ctypes.c_double(0), ctypes.c_double(0)
+        cl, pl = ctypes.c_int64(0), ctypes.c_int64(0)
+        self.lib.airgs_timing(self.ctx, int(enable), ctypes.byref(cm), ctypes.byref(cl), ctypes.byref(pm),
+                              ctypes.byref(pl))
+        return {"composite_ms": cm.value, "composite_launches": cl.value, "project_ms": pm.value,
+                "project_launches": pl.value}
 
     @property
     def launches(self) -> int:

@@ -30,3 +30,18 @@ extern "C" int airgs_ctx_destroy(airgs_ctx *ctx) {
 extern "C" const char *airgs_last_error(const airgs_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 extern "C" int64_t airgs_launch_count(const airgs_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms, int64_t *composite_launches,
+                            double *project_ms, int64_t *project_launches) {
+    if (!ctx) return AIRGS_E_INTERNAL;
+    if (composite_ms) *composite_ms = ctx->composite_ms;
+    if (composite_launches) *composite_launches = ctx->composite_launches;
+    if (project_ms) *project_ms = ctx->project_ms;
+    if (project_launches) *project_launches = ctx->project_launches;
+    if (enable >= 0) {  // (re)arm or disarm and reset the counters
+        ctx->timing = enable != 0;
+        ctx->composite_ms = ctx->project_ms = 0.0;
+        ctx->composite_launches = ctx->project_launches = 0;
+    }
+    return AIRGS_OK;
+}

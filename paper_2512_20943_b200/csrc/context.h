@@ -17,6 +17,15 @@ struct airgs_ctx {
     std::vector<Buf> bufs;
     void *host = nullptr;
     size_t host_cap = 0;
+    // optional per-kernel timing (CUDA events around the dominant kernels)
+    bool timing = false;
+    double composite_ms = 0.0, project_ms = 0.0;
+    int64_t composite_launches = 0, project_launches = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    void ensure_events() {
+        for (auto &e : ev)
+            if (!e) AIRGS_CUDA_TRY(cudaEventCreate(&e));
+    }
 
     // Device scratch slot `id`, at least `bytes` long.  Growing synchronises
     // the device first (rare: capacity only grows).
@@ -56,6 +65,8 @@ struct airgs_ctx {
         for (auto &b : bufs)
             if (b.p) cudaFree(b.p);
         if (host) cudaFreeHost(host);
+        for (auto &e : ev)
+            if (e) cudaEventDestroy(e);
     }
 };
 

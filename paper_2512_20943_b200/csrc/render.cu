@@ -1030,6 +1030,10 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         AIRGS_CUDA_TRY(cudaFuncSetAttribute(k_composite<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCompSmem));
         attr_set = true;
     }
+    if (ctx->timing) {
+        ctx->ensure_events();
+        AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
+    }
     if (Tt > 0) {
         if (any_usage)
             k_composite<true><<<(unsigned)Tt, kTileThreads, kCompSmem, st>>>(d_ci, L.d_tile_base, nitems, tstart,
@@ -1040,12 +1044,19 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         ++NL;
         check_launch();
     }
+    if (ctx->timing) AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
     if (sse && any_target) {
         k_sse_items<<<nitems, 256, 0, st>>>(sse_tiles, L.d_tile_base, d_has, sse);
         ++NL;
         check_launch();
     }
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));  // host vectors outlive their async copies
+    if (ctx->timing && Tt > 0) {
+        float ms = 0.f;
+        AIRGS_CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+        ctx->composite_ms += ms;
+        ++ctx->composite_launches;
+    }
 }
 
 // Upload per-item layout arrays (tile bases, tiles_x, counts, tile -> item map).
@@ -1164,15 +1175,26 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.tile_count = tile_count;
     pa.flags = flags;
     pa.stride = stride;
+    if (ctx->timing) {
+        ctx->ensure_events();
+        AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
+    }
     {
         dim3 grid((unsigned)ceil_div(stride, kProjThreads), (unsigned)nframes);
         k_project<<<grid, kProjThreads, 0, st>>>(pa);
         ++NL;
         check_launch();
     }
+    if (ctx->timing) AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
     unsigned int hflags = 0;
     AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    if (ctx->timing) {
+        float ms = 0.f;
+        AIRGS_CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+        ctx->project_ms += ms;
+        ++ctx->project_launches;
+    }
     if (hflags & kFlagInvalidParam)
         throw ApiFailure(AIRGS_E_VALIDATION, "frame contains invalid primitive parameters");
     bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, sse, st);
