@@ -23,7 +23,7 @@ import numpy as np
 
 from . import device as dv
 from .errors import CapacityError, DecodeError, StructuralError
-from .model import DeltaTensor, GaussianFrame, degree_from_param_dim
+from .model import DeltaTensor, GaussianFrame, as_delta, as_frame, degree_from_param_dim
 
 IMAGE_MAGIC = b"GSAI"
 IMAGE_VERSION = 1
@@ -195,6 +195,7 @@ def encode_frame(frame: GaussianFrame, width: int = None, height: int = None) ->
     (ss/codec.py:124-158)."""
     import torch
 
+    frame = as_frame(frame)
     n, m = frame.count, frame.width
     if width is None or height is None:
         side = math.ceil(math.sqrt(n))
@@ -229,6 +230,8 @@ def decode_frame(image_set: AttributeImageSet, device=None) -> GaussianFrame:
     """Attribute planes -> device-resident frame (ss/codec.py:161-169)."""
     import torch
 
+    if not isinstance(image_set, AttributeImageSet):  # a reference AttributeImageSet
+        image_set = AttributeImageSet.from_bytes(image_set.to_bytes())
     m = image_set.num_attributes
     degree_from_param_dim(m)
     n = image_set.count
@@ -292,6 +295,7 @@ def encode_delta(delta: DeltaTensor, quant_step: float, frame_index: int = 0, ba
     zeros are dropped (ss/codec.py:187-214)."""
     if quant_step <= 0:
         raise StructuralError("quant_step must be positive")
+    delta = as_delta(delta)
     if delta.base_count == 0 or delta.is_empty():
         hdr = _DELTA_HEADER.pack(DELTA_MAGIC, frame_index, base_key, 0, quant_step)
         return DeltaPayload(hdr, frame_index, base_key, 0, quant_step)

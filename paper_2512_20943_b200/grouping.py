@@ -20,7 +20,7 @@ import numpy as np
 from . import device as dv
 from .errors import StructuralError, ValidationError
 from .metrics import psnr_from_sse
-from .model import CanonicalSpace, DeltaTensor, apply_delta
+from .model import CanonicalSpace, DeltaTensor, apply_delta, as_frame
 
 DEFAULT_TAU_DB = 30.0
 
@@ -93,7 +93,7 @@ def probe_frames(frames, cams, targets, device=None) -> list:
 
     dev = dv.device_of(device)
     cams = list(cams)
-    frames = list(frames)
+    frames = [as_frame(f) for f in frames]
     if not cams:
         raise ValidationError("at least one camera required")
     tgts = [_device_targets(t, cams, dev) for t in targets]

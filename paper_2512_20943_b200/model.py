@@ -284,6 +284,29 @@ class DeltaTensor:
 
 
 # ---------------------------------------------------------------------------
+# coercion of reference objects (duck typing) for the drop-in
+
+
+def as_frame(x) -> GaussianFrame:
+    if isinstance(x, GaussianFrame):
+        return x
+    return GaussianFrame(params=x.params, frame_index=getattr(x, "frame_index", 0),
+                         group_key=getattr(x, "group_key", 0))
+
+
+def as_delta(x) -> DeltaTensor:
+    if isinstance(x, DeltaTensor):
+        return x
+    return DeltaTensor(x.base_count, x.param_width, dict(x.entries))
+
+
+def as_space(x) -> CanonicalSpace:
+    if isinstance(x, CanonicalSpace):
+        return x
+    return CanonicalSpace(as_frame(x.frame), x.capacity_U)
+
+
+# ---------------------------------------------------------------------------
 # device-backed algebra
 
 
@@ -335,7 +358,7 @@ def _compose_overlays(items, apply_eps=True, eps=EPS_SPARSE) -> DeltaTensor:
 def compose_deltas(deltas, eps: float = EPS_SPARSE) -> DeltaTensor:
     """Componentwise sum over the union of indices, in list order, with one
     |.|max > eps filter at the end (ss/model.py:294-311)."""
-    deltas = list(deltas)
+    deltas = [as_delta(d) for d in deltas]
     if not deltas:
         return DeltaTensor.empty(0, param_dim(0))
     base, width = deltas[0].base_count, deltas[0].param_width
@@ -349,6 +372,7 @@ def compose_deltas(deltas, eps: float = EPS_SPARSE) -> DeltaTensor:
 
 def apply_delta(space: CanonicalSpace, delta: DeltaTensor, frame_index=None) -> GaussianFrame:
     """canonical + delta rows (ss/model.py:269-284), on device."""
+    space, delta = as_space(space), as_delta(delta)
     fr = space.frame
     if delta.base_count != fr.count:
         raise StructuralError(f"delta base_count {delta.base_count} != space count {fr.count}")
@@ -380,6 +404,7 @@ def apply_overlay(canon, n, ov_a, sel=None, rank=None, keep_min=0, ov_b=None):
 
 def diff_frames(a: GaussianFrame, b: GaussianFrame, eps: float = EPS_SPARSE) -> DeltaTensor:
     """Delta with apply_delta(a) == b exactly where kept (ss/model.py:287-291)."""
+    a, b = as_frame(a), as_frame(b)
     if a.count != b.count or a.width != b.width:
         raise StructuralError("frames must share primitive count and layout")
     n, w = a.count, a.width

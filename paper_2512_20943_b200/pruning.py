@@ -24,7 +24,7 @@ from . import device as dv
 from .codec import quantize_overlay
 from .errors import StructuralError, ValidationError
 from .metrics import psnr_from_sse
-from .model import EPS_SPARSE, CanonicalSpace, DeltaTensor, _compose_call, apply_overlay
+from .model import EPS_SPARSE, CanonicalSpace, DeltaTensor, _compose_call, apply_overlay, as_delta, as_space
 
 MIN_DROP = 1e-12
 
@@ -175,6 +175,7 @@ def _k_of(ratio, entries):
 def prune_order(delta: DeltaTensor, usage_counts) -> list:
     """Entry indices, lowest usage first, ties prune the higher index first
     (ss/pruning.py:72-76)."""
+    delta = as_delta(delta)
     ov = delta.overlay()
     if ov.n == 0:
         return []
@@ -187,6 +188,7 @@ def prune_order(delta: DeltaTensor, usage_counts) -> list:
 def prune_delta(delta: DeltaTensor, usage_counts, ratio: float):
     """Remove the ``ratio`` fraction of lowest-usage entries
     (ss/pruning.py:79-90).  Returns (kept DeltaTensor, sorted removed tuple)."""
+    delta = as_delta(delta)
     ov = delta.overlay()
     if ov.n == 0:
         return DeltaTensor(delta.base_count, delta.param_width, {}), ()
@@ -263,6 +265,8 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
     from .model import GaussianFrame
     from .rasterizer import render_views
 
+    delta, space = as_delta(delta), as_space(space)
+    base = None if base is None else as_delta(base)
     ratios = sorted(set(float(r) for r in ratios))
     if not ratios or ratios[0] != 0.0:
         raise StructuralError("ratios must include 0")

@@ -211,3 +211,38 @@ def test_synthetic_generator_is_seeded():
     np.testing.assert_array_equal(a.frame(7), b.frame(7))
     assert a.frame(4).shape[0] == 1000 and a.frame(7).shape[0] == 1010
     assert synth.CONFIGS["C2"].count == 300_000 and synth.CONFIGS["C2"].resolution == (1352, 1014)
+
+
+def test_dropin_installs_into_the_reference_package():
+    """The reference package itself (read in this container only) gets its
+    seam and entry points replaced; no GPU call is made."""
+    import importlib.util
+    import glob
+    import sys
+
+    if not os.path.exists("/root/reference/pkg/src/splatstream"):
+        pytest.skip("reference tree not present")
+    hits = glob.glob(os.path.join(ROOT, "oracle", "_ref", "_composite*.so"))
+    if hits and "splatstream._composite" not in sys.modules:
+        spec = importlib.util.spec_from_file_location("splatstream._composite", hits[0])
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        sys.modules["splatstream._composite"] = mod
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        import splatstream
+        from splatstream import pruning as ref_pruning, rasterizer as ref_ras, streamsim as ref_sim  # noqa: F401
+
+        from paper_2512_20943_b200 import dropin, pruning, rasterizer
+
+        done = dropin.install(splatstream)
+        assert ("rasterizer", "_kernels") in done and ("pruning", "build_level_space") in done
+        assert ref_ras.render is rasterizer.render
+        assert ref_pruning.build_level_space is pruning.build_level_space
+        assert ref_ras._kernels.forward.__func__ if hasattr(ref_ras._kernels.forward, "__func__") else True
+        assert ref_ras.KERNEL_BACKEND == rasterizer.KERNEL_BACKEND
+    finally:
+        sys.path.remove("/root/reference/pkg/src")
+        for k in [k for k in sys.modules if k == "splatstream" or k.startswith("splatstream.")]:
+            del sys.modules[k]
