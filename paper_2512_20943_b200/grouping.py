@@ -109,6 +109,77 @@ def probe_frames(frames, cams, targets, device=None) -> list:
     return [float(np.mean([psnr_from_sse(sse[f * V + v], px[v]) for v in range(V)])) for f in range(len(frames))]
 
 
+def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_DB, device=None):
+    """Keyframe detection over a sequence of frames of one group, streamed
+    from host memory: for frame t, decode its GSDP delta payload against the
+    group's canonical space, apply it, render every camera with SSE against
+    the frame's ground-truth images, and decide ``q < tau``.
+
+    ``payloads``: per frame GSDP bytes / DeltaPayload; ``targets``: per frame
+    a sequence of (h, w, 3) float64 host images (pinned torch tensors give
+    asynchronous copies).  Host->device copies of frame t+1 run on a copy
+    stream while frame t is evaluated (double buffering).  Returns a list of
+    (quality_db, is_keyframe) per frame."""
+    import torch
+
+    from . import codec
+    from .model import GaussianFrame, apply_overlay, as_space
+    from .rasterizer import render_views
+
+    space = as_space(space)
+    dev = dv.device_of(device)
+    cams = list(cams)
+    V = len(cams)
+    n, w = space.frame.count, space.frame.width
+    canon = space.frame.planes(dev)
+    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    bufs = [None, None]
+    used = [None, None]
+
+    def host_tensor(im):
+        t = im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im, dtype=np.float64))
+        return t
+
+    def stage(t):
+        b = t % 2
+        data = payloads[t].data if hasattr(payloads[t], "data") else bytes(payloads[t])
+        with torch.cuda.stream(copy):
+            if used[b] is not None:
+                copy.wait_event(used[b])
+            host = [host_tensor(im) for im in targets[t]]
+            check_targets(host, cams)
+            tg = [h.to(dev, non_blocking=True) for h in host]
+            pd = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+            pd = (pd.pin_memory() if pd.numel() else pd).to(dev, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+        bufs[b] = (tg, pd, data, ev)
+
+    out = []
+    if len(payloads) != len(targets):
+        raise StructuralError("one target set per payload required")
+    if payloads:
+        stage(0)
+    for t in range(len(payloads)):
+        tg, pd, data, ev = bufs[t % 2]
+        comp.wait_event(ev)
+        if t + 1 < len(payloads):
+            stage(t + 1)
+        delta, _ = codec.decode_delta_device(data, n, w, device=dev, payload_dev=pd)
+        planes = apply_overlay(canon, n, delta.overlay(dev))
+        vb = render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for v in range(V)],
+                          targets=tg, device=dev)
+        u = torch.cuda.Event()
+        u.record(comp)
+        used[t % 2] = u
+        sse = vb.sse.cpu().numpy()
+        q = float(np.mean([psnr_from_sse(sse[v], px[v]) for v in range(V)]))
+        out.append((q, is_keyframe(q, tau_db)))
+    return out
+
+
 def is_keyframe(quality_db: float, tau_db: float = DEFAULT_TAU_DB) -> bool:
     """The grouping decision: re-anchor when the probe misses tau
     (ss/grouping.py:213)."""

@@ -163,3 +163,30 @@ def test_sharded_drivers_world1_equal_unsharded():
     tg = grouping.GroundTruth(images=orc.render_with_usage(moved, cams)[0])
     assert sharding.probe_frames_sharded([GaussianFrame(params=base_p)], cams, [tg]) == \
         grouping.probe_frames([GaussianFrame(params=base_p)], cams, [tg])
+
+
+def test_probe_sequence_streams_from_host():
+    import torch
+
+    from paper_2512_20943_b200 import codec, grouping
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+
+    base_p, _ = _scene(41, n=1500)
+    cams = _cams(3, (64, 48))
+    space = CanonicalSpace(GaussianFrame(params=base_p), capacity_U=base_p.shape[0])
+    payloads, targets, ref = [], [], []
+    for s in range(4):
+        _, moved = _scene(50 + s, n=1500)
+        moved = base_p.copy()
+        rng = np.random.default_rng(s)
+        moved[::4, 0:3] += rng.normal(0, 0.01 * (s + 1), (moved[::4].shape[0], 3))
+        d = diff_frames(space.frame, GaussianFrame(params=moved))
+        pay = codec.encode_delta(d, 1e-4)
+        payloads.append(pay)
+        imgs = orc.render_with_usage(moved, cams)[0]
+        targets.append([torch.from_numpy(im).pin_memory() for im in imgs])
+        dec = codec.decode_delta(pay, base_p.shape[0], 17)
+        ref.append(grouping.quality_probe(space, dec, grouping.GroundTruth(images=imgs), cams))
+    got = grouping.probe_sequence(space, cams, payloads, targets, tau_db=60.0)
+    assert [q for q, _ in got] == ref
+    assert [k for _, k in got] == [not q >= 60.0 for q in ref]
