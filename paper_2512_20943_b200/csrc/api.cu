@@ -1,5 +1,39 @@
 // Context lifecycle of the airgs_b200 C-ABI.
+#include <algorithm>
+#include <cstring>
+
 #include "context.h"
+
+namespace airgs {
+
+constexpr int kParamChunk = 3968;
+struct ParamChunk {
+    unsigned char b[kParamChunk];
+};
+
+__global__ void k_param_copy(unsigned char *__restrict__ dst, const ParamChunk c, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = c.b[i];
+}
+
+void h2d_small(airgs_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return;
+    if (bytes > 16 * (size_t)kParamChunk) {
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    const unsigned char *s = static_cast<const unsigned char *>(src);
+    unsigned char *d = static_cast<unsigned char *>(dst);
+    for (size_t off = 0; off < bytes; off += kParamChunk) {
+        const int n = (int)std::min<size_t>(kParamChunk, bytes - off);
+        ParamChunk c;
+        memcpy(c.b, s + off, n);
+        k_param_copy<<<1, 256, 0, st>>>(d + off, c, n);
+        ++ctx->launches;
+    }
+    check_launch();
+}
+
+}  // namespace airgs
 
 using namespace airgs;
 

@@ -306,7 +306,7 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
     if (ok && E > 0) {
         // terminators in the section must be exactly E and the section must end on one
         int64_t *dV = misc;  // count for the scan driver
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(dV, &V, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, dV, &V, sizeof(int64_t), st);
         const int bps = (int)std::max<int64_t>(1, ceil_div(V, kScanTile));
         int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
         // gaps[] is written only for ex < E; protect against over-count by sizing V
@@ -337,14 +337,14 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
     }
     if (E == 0) {
         int64_t z = 0;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(entries_out, &z, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, entries_out, &z, sizeof(int64_t), st);
         AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
         return;
     }
     // indices = inclusive prefix sum of gaps
     {
         int64_t *dE = misc + 2;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(dE, &E, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, dE, &E, sizeof(int64_t), st);
         const int bps = (int)std::max<int64_t>(1, ceil_div(E, kScanTile));
         int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
         seg_scan<int64_t>(GapIn{gaps}, GapOut{idx_out}, dE, 1, E, blocks, (int64_t *)nullptr, st, &L);
@@ -357,7 +357,7 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
     }
     {
         const unsigned long long mx = ~0ull;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(bad, &mx, sizeof(mx), cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, bad, &mx, sizeof(mx), st);
         AIRGS_CUDA_TRY(cudaMemsetAsync(entries_out, 0, sizeof(int64_t), st));
         k_gsdp_rows<<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(payload + 24 + V, idx_out, E, W, step, base_count, rows,
                                                               ld, present, flags, bad,
@@ -428,7 +428,7 @@ extern "C" int airgs_gsdp_encode(airgs_ctx *ctx, const double *rows, const uint8
         if (n <= 0) return;
         int64_t *misc = ctx->scratch_t<int64_t>(kSlotMisc3, 8);
         int64_t *cidx = ctx->scratch_t<int64_t>(kSlotKeys, n);
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(misc, &n, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, misc, &n, sizeof(int64_t), st);
         const int bps = (int)std::max<int64_t>(1, ceil_div(n, kScanTile));
         int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
         seg_scan<int64_t>(NzIn{nz}, NzOut{cidx}, misc, 1, n, blocks, misc + 1, st, &L);

@@ -97,6 +97,7 @@ enum Slot : int {
     kSlotMisc2,
     kSlotMisc3,
     kSlotTileCount,
+    kSlotTileItem,
     kSlotCount
 };
 
@@ -125,5 +126,11 @@ int guarded(airgs_ctx *ctx, F &&fn) {
 }
 
 inline void check_launch() { AIRGS_CUDA_TRY(cudaGetLastError()); }
+
+// Host->device copy of a small block through kernel parameters instead of a
+// DMA transfer, so it never queues behind a large H2D copy another stream
+// has in flight on the copy engine (api.cu).  Larger blocks use
+// cudaMemcpyAsync.
+void h2d_small(airgs_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t st);
 
 }  // namespace airgs

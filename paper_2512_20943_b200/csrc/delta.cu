@@ -313,7 +313,7 @@ extern "C" int airgs_quantize(airgs_ctx *ctx, const double *rows, const uint8_t 
         cudaStream_t st = (cudaStream_t)stream;
         unsigned long long *bad = ctx->scratch_t<unsigned long long>(kSlotFlags, 2);
         const unsigned long long mx = ~0ull;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(bad, &mx, sizeof(mx), cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, bad, &mx, sizeof(mx), st);
         launch_w<QuantK>(width, dim3((unsigned)ceil_div(n, 256)), dim3(256), st, rows, present, n, ld, step, nz_out,
                          deq_out, bad);
         ++ctx->launches;
@@ -344,7 +344,7 @@ extern "C" int airgs_prune_rank(airgs_ctx *ctx, const uint8_t *present, const in
         int64_t *misc = ctx->scratch_t<int64_t>(kSlotMisc3, 8);
         int64_t *d_n = misc, *d_cnt = misc + 1;
         unsigned long long *umax = (unsigned long long *)(misc + 2);
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(d_n, &n, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, d_n, &n, sizeof(int64_t), st);
         AIRGS_CUDA_TRY(cudaMemsetAsync(umax, 0, sizeof(unsigned long long), st));
         const int bps = (int)std::max<int64_t>(1, ceil_div(n, kScanTile));
         int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
@@ -390,7 +390,7 @@ extern "C" int airgs_level_sizes(airgs_ctx *ctx, const uint8_t *nz, const int32_
         int64_t *d_k = ctx->scratch_t<int64_t>(kSlotMisc2, (size_t)2 * nlevels);
         int64_t *d_sizes = d_k + nlevels;
         ChunkSummary *ch = (ChunkSummary *)ctx->scratch(kSlotMisc1, sizeof(ChunkSummary) * (size_t)nchunks * nlevels);
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(d_k, kmin, sizeof(int64_t) * nlevels, cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, d_k, kmin, sizeof(int64_t) * nlevels, st);
         k_level_chunks<<<dim3((unsigned)nchunks, (unsigned)nlevels), kLvlThreads, 0, st>>>(nz, rank, n, d_k, nchunks, ch);
         k_level_finish<<<nlevels, 32, 0, st>>>(ch, nchunks, width, d_sizes);
         ctx->launches += 2;

@@ -894,6 +894,17 @@ __global__ void k_fill_i64(int64_t *p, int64_t n, int64_t v) {
 // ---------------------------------------------------------------------------
 // host orchestration
 
+__global__ void k_tile_item(const int64_t *__restrict__ tile_base, int nitems, int64_t Tt, int32_t *__restrict__ out) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Tt) return;
+    int lo = 0, hi = nitems - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tile_base[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    out[g] = lo;
+}
+
 struct ItemHost {
     int frame, cam;
     int64_t count;  // primitives of its frame
@@ -932,7 +943,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     int64_t *d_total = stats;
     int64_t *d_Tt = stats + 1;
     AIRGS_CUDA_TRY(cudaMemsetAsync(big_n, 0, sizeof(unsigned int), st));
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(d_Tt, &Tt, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    h2d_small(ctx, d_Tt, &Tt, sizeof(int64_t), st);
     {
         const int bps = (int)std::max<int64_t>(1, ceil_div(Tt, kScanTile));
         int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
@@ -973,14 +984,20 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
             tot += hcnt[b];
             mx = std::max<int64_t>(mx, hcnt[b]);
         }
+        int32_t *d_tile_item = nullptr;
+        {
+            d_tile_item = ctx->scratch_t<int32_t>(kSlotTileItem, (size_t)Tt);
+            k_tile_item<<<(unsigned)ceil_div(Tt, 256), 256, 0, st>>>(L.d_tile_base, nitems, Tt, d_tile_item);
+            ++NL;
+        }
         int64_t *d_seg = ctx->scratch_t<int64_t>(kSlotMisc3, 2 * (size_t)hbig);
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(d_seg, seg.data(), sizeof(int64_t) * 2 * hbig, cudaMemcpyHostToDevice, st));
+        h2d_small(ctx, d_seg, seg.data(), sizeof(int64_t) * 2 * hbig, st);
         uint64_t *k1 = ctx->scratch_t<uint64_t>(kSlotKeys, (size_t)tot);
         uint64_t *k2 = ctx->scratch_t<uint64_t>(kSlotKeysAlt, (size_t)tot);
         uint32_t *v1 = ctx->scratch_t<uint32_t>(kSlotVals, (size_t)tot);
         uint32_t *v2 = ctx->scratch_t<uint32_t>(kSlotValsAlt, (size_t)tot);
         uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)hbig * 256 * ceil_div(mx, kSortTile));
-        BigArgs ba{big_list, tstart, tile_count, L.d_tile_item, depth, pairs, L.stride, d_seg, k1, v1};
+        BigArgs ba{big_list, tstart, tile_count, d_tile_item, depth, pairs, L.stride, d_seg, k1, v1};
         const dim3 gg((unsigned)std::min<int64_t>(64, ceil_div(mx, 256)), hbig);
         k_big_gather<<<gg, 256, 0, st>>>(ba);
         k_ids_as_keys<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(v1, k1, tot);
@@ -990,7 +1007,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         uint64_t *ks = alt ? k2 : k1;
         uint64_t *ko = alt ? k1 : k2;
         uint32_t *vo = alt ? v1 : v2;
-        k_gather_keys<<<gg, 256, 0, st>>>(vs, d_seg, big_list, L.d_tile_item, tile_count, depth, L.stride, ks);
+        k_gather_keys<<<gg, 256, 0, st>>>(vs, d_seg, big_list, d_tile_item, tile_count, depth, L.stride, ks);
         ++NL;
         bool alt2 = radix_sort<uint64_t>(ks, vs, ko, vo, d_seg, d_seg + hbig, (int)hbig, mx, 64, hist, st, &NL);
         k_big_scatter<<<gg, 256, 0, st>>>(ba, alt2 ? vo : vs);
@@ -1022,8 +1039,8 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     }
     CompItem *d_ci = (CompItem *)ctx->scratch(kSlotMisc1, sizeof(CompItem) * nitems);
     uint8_t *d_has = (uint8_t *)ctx->scratch(kSlotMisc2, nitems);
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(d_ci, ci.data(), sizeof(CompItem) * nitems, cudaMemcpyHostToDevice, st));
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(d_has, has_t.data(), nitems, cudaMemcpyHostToDevice, st));
+    h2d_small(ctx, d_ci, ci.data(), sizeof(CompItem) * nitems, st);
+    h2d_small(ctx, d_has, has_t.data(), nitems, st);
     static bool attr_set = false;
     if (!attr_set) {
         AIRGS_CUDA_TRY(cudaFuncSetAttribute(k_composite<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCompSmem));
@@ -1071,24 +1088,21 @@ static void upload_layout(airgs_ctx *ctx, const std::vector<ItemHost> &items, La
     const size_t o_tb = off; off = align(off + sizeof(int64_t) * (nitems + 1));
     const size_t o_tx = off; off = align(off + sizeof(int32_t) * nitems);
     const size_t o_cnt = off; off = align(off + sizeof(int64_t) * nitems);
-    const size_t o_ti = off; off = align(off + sizeof(int32_t) * L.Tt);
     std::vector<char> hbuf(off);
     memcpy(hbuf.data() + o_tb, L.tile_base.data(), sizeof(int64_t) * (nitems + 1));
     for (int s = 0; s < nitems; ++s) {
         const int32_t tx = items[s].tiles_x;
         memcpy(hbuf.data() + o_tx + sizeof(int32_t) * s, &tx, sizeof(int32_t));
         memcpy(hbuf.data() + o_cnt + sizeof(int64_t) * s, &items[s].count, sizeof(int64_t));
-        int32_t *ti = reinterpret_cast<int32_t *>(hbuf.data() + o_ti);
-        for (int64_t g = L.tile_base[s]; g < L.tile_base[s + 1]; ++g) ti[g] = s;
     }
     char *d = (char *)ctx->scratch(kSlotMisc0, off);
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(d, hbuf.data(), off, cudaMemcpyHostToDevice, st));
-    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    h2d_small(ctx, d, hbuf.data(), off, st);
     L.d_tile_base = (const int64_t *)(d + o_tb);
     L.d_tiles_x = (const int32_t *)(d + o_tx);
     L.d_count = (const int64_t *)(d + o_cnt);
-    L.d_tile_item = (const int32_t *)(d + o_ti);
+    L.d_tile_item = nullptr;  // built on device when the oversized-tile path needs it
 }
+
 
 static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, const airgs_camera *cams,
                         int ncams, const airgs_view_item *items, int nitems, double *sse, cudaStream_t st) {
@@ -1150,7 +1164,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     memcpy(hs + o_fitems, fitems.data(), sizeof(int32_t) * nitems);
     memcpy(hs + o_icam, icam.data(), sizeof(int32_t) * nitems);
     char *dd = (char *)ctx->scratch(kSlotDesc, off);
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(dd, hs, off, cudaMemcpyHostToDevice, st));
+    h2d_small(ctx, dd, hs, off, st);
 
     unsigned int *flags = ctx->scratch_t<unsigned int>(kSlotFlags, 4);
     AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));

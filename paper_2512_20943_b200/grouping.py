@@ -137,24 +137,31 @@ def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_D
     copy = torch.cuda.Stream(dev)
     bufs = [None, None]
     used = [None, None]
+    # persistent pinned staging for payload bytes (no per-frame cudaHostAlloc,
+    # which would synchronise the device and serialise the pipeline)
+    datas = [payloads[t].data if hasattr(payloads[t], "data") else bytes(payloads[t]) for t in range(len(payloads))]
+    cap = max((len(d) for d in datas), default=1)
+    pinned = [torch.empty((cap,), dtype=torch.uint8).pin_memory() for _ in range(2)]
 
     def host_tensor(im):
-        t = im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im, dtype=np.float64))
-        return t
+        return im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im, dtype=np.float64))
 
     def stage(t):
         b = t % 2
-        data = payloads[t].data if hasattr(payloads[t], "data") else bytes(payloads[t])
+        data = datas[t]
         with torch.cuda.stream(copy):
             if used[b] is not None:
-                copy.wait_event(used[b])
+                copy.wait_event(used[b])  # buffer b's previous frame is done
             host = [host_tensor(im) for im in targets[t]]
             check_targets(host, cams)
             tg = [h.to(dev, non_blocking=True) for h in host]
-            pd = torch.frombuffer(bytearray(data), dtype=torch.uint8)
-            pd = (pd.pin_memory() if pd.numel() else pd).to(dev, non_blocking=True)
+            if data:
+                pinned[b][: len(data)].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
+            pd = pinned[b][: len(data)].to(dev, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(copy)
+        for x in tg + [pd]:
+            x.record_stream(comp)
         bufs[b] = (tg, pd, data, ev)
 
     out = []
