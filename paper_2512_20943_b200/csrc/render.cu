@@ -384,7 +384,7 @@ struct CompShared {
 constexpr int kCompWarps = kTileThreads / 32;
 constexpr int kSortCap = 2048;  // tile lists up to this length are sorted in shared memory
 #ifndef COMP_MIN_BLOCKS
-#define COMP_MIN_BLOCKS 3
+#define COMP_MIN_BLOCKS 4
 #endif
 constexpr size_t kCompSmem = sizeof(CompShared) + (size_t)kSortCap * (sizeof(uint64_t) + sizeof(uint32_t));
 
@@ -713,16 +713,25 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             // phase A: fp32 candidate bits (T as of the chunk start; a larger T only
             // admits more candidates, never fewer)
             unsigned word = 0;
+            // two primitives per iteration: both loads issued before the math
             while (m) {
-                const int k = __ffs(m) - 1;
+                const int k1 = __ffs(m) - 1;
                 m &= m - 1;
-                const float4 f0 = sh.f0[c + k];
-                const float2 f1 = sh.f1[c + k];
-                const float dx = pxl - f0.x, dy = pyl - f0.y;
-                const float s2 = fmaf(f0.z * dx, dx, (f1.x * dy) * dy);  // log2e * 0.5(a dx^2 + c dy^2)
-                const float e2 = fmaf(f0.w * dx, dy, s2);               // log2e * e
+                const int k2 = m ? __ffs(m) - 1 : k1;
+                m &= m - 1;
+                const float4 a0 = sh.f0[c + k1];
+                const float2 a1 = sh.f1[c + k1];
+                const float4 b0 = sh.f0[c + k2];
+                const float2 b1 = sh.f1[c + k2];
+                const float dxa = pxl - a0.x, dya = pyl - a0.y;
+                const float dxb = pxl - b0.x, dyb = pyl - b0.y;
+                const float sa = fmaf(a0.z * dxa, dxa, (a1.x * dya) * dya);  // log2e * 0.5(a dx^2 + c dy^2)
+                const float sb = fmaf(b0.z * dxb, dxb, (b1.x * dyb) * dyb);
+                const float ea = fmaf(a0.w * dxa, dya, sa);  // log2e * e
+                const float eb = fmaf(b0.w * dxb, dyb, sb);
                 // reject iff e > ln(al) + ln(T/EPS) + guard (guard proof: DESIGN.md)
-                word |= (unsigned)(e2 <= fmaf(1e-5f, s2, f1.y) + thr) << k;
+                word |= (unsigned)(ea <= fmaf(1e-5f, sa, a1.y) + thr) << k1;
+                word |= (unsigned)(eb <= fmaf(1e-5f, sb, b1.y) + thr) << k2;
             }
             if (done) word = 0;
             // phase B: each lane runs its own candidates in depth order (exact fp64)
