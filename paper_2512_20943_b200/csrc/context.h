@@ -98,6 +98,8 @@ enum Slot : int {
     kSlotMisc3,
     kSlotTileCount,
     kSlotTileItem,
+    kSlotSlowTiles,
+    kSlotZRange,
     kSlotCount
 };
 

@@ -44,6 +44,7 @@ struct ProjArgs {
     uint64_t *depth;           // [nitems][stride] orderable depth keys
     int32_t *ntiles;           // [nitems][stride] tiles touched (0 = not rendered)
     uint32_t *tile_count;      // [total tiles] primitives per tile
+    unsigned long long *zrange;  // [nitems][2] min/max orderable depth key
     unsigned int *flags;
     int64_t stride;
 };
@@ -92,8 +93,8 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
     const airgs_frame fr = a.frames[f];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int ib = a.frame_item_ptr[f], ie = a.frame_item_ptr[f + 1];
-    if (ib == ie || i >= fr.count) return;
-    const bool active = true;
+    if (ib == ie || (int64_t)blockIdx.x * blockDim.x >= fr.count) return;  // block-uniform
+    const bool active = i < fr.count;
     const int64_t ld = fr.ld;
     const int W = fr.width;
     double p[26];
@@ -137,11 +138,14 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
         col0[1] = sigmoid_ref(p[12] + kShC0 * p[15]);
         col0[2] = sigmoid_ref(p[13] + kShC0 * p[16]);
     }
+    __shared__ unsigned long long red_mn[kProjThreads / 32], red_mx[kProjThreads / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int it = ib; it < ie; ++it) {
         const int item = a.frame_items[it];
         const int64_t o = (int64_t)item * a.stride + i;
         const airgs_camera &cam = a.cams[a.item_cam[item]];
         const double *R = cam.rot;
+        unsigned long long zmn = ~0ull, zmx = 0ull;
         int nt = 0;
         double tz = 0.0;
         if (live) tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
@@ -213,7 +217,9 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
                 nt = (u1 - u0 + 1) * (v1 - v0 + 1);
             if (nt > 0) {
                 a.recs[o] = rec;
-                a.depth[o] = order_key(tz);
+                const unsigned long long zk = order_key(tz);
+                a.depth[o] = zk;
+                zmn = zmx = zk;
                 // per-tile histogram for the binning scan
                 uint32_t *tc = a.tile_count + a.tile_base[item];
                 const int txn = a.tiles_x[item];
@@ -222,6 +228,29 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
             }
         }
         if (active) a.ntiles[o] = nt;
+        // block min/max of the depth keys -> one atomic pair per block and item
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            zmn = min(zmn, __shfl_xor_sync(0xffffffffu, zmn, d));
+            zmx = max(zmx, __shfl_xor_sync(0xffffffffu, zmx, d));
+        }
+        if (lane == 0) {
+            red_mn[wid] = zmn;
+            red_mx[wid] = zmx;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long mn = red_mn[0], mx = red_mx[0];
+            for (int k = 1; k < kProjThreads / 32; ++k) {
+                mn = min(mn, red_mn[k]);
+                mx = max(mx, red_mx[k]);
+            }
+            if (mx) {
+                atomicMin(a.zrange + 2 * item, mn);
+                atomicMax(a.zrange + 2 * item + 1, mx);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -245,15 +274,24 @@ struct TileScanOut {
 
 struct EmitArgs {
     const Rec *recs;
+    const uint64_t *depth;
+    const unsigned long long *zrange;
     const int32_t *ntiles;
     const int64_t *tile_base;
     const int32_t *tiles_x;
     const int64_t *count;      // primitives per item
     const int64_t *tstart;     // global tile -> first slot
     uint32_t *cursor;          // global tile -> fill cursor
-    uint32_t *pairs;           // primitive ids
+    uint64_t *pairs;           // (view-level depth bucket << 32) | primitive id
     int64_t stride;
 };
+
+// 32-bit depth bucket of an orderable key within the view's depth range
+__device__ __forceinline__ uint32_t depth_bucket(uint64_t zk, const unsigned long long *zr) {
+    const unsigned long long span = zr[1] - zr[0];
+    const int sh = span >> 32 ? 64 - __clzll((long long)span) - 32 : 0;
+    return (uint32_t)((zk - zr[0]) >> sh);
+}
 
 __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     const int s = blockIdx.y;
@@ -264,12 +302,13 @@ __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     const Rec &r = a.recs[o];
     const int64_t tb = a.tile_base[s];
     const int txn = a.tiles_x[s];
+    const uint64_t key = ((uint64_t)depth_bucket(a.depth[o], a.zrange + 2 * s) << 32) | (uint32_t)i;
     int u0, u1, v0, v1;
     rec_tile_range(r, u0, u1, v0, v1);
     for (int v = v0; v <= v1; ++v)
         for (int u = u0; u <= u1; ++u) {
             const int64_t g = tb + v * txn + u;
-            a.pairs[a.tstart[g] + atomicAdd(a.cursor + g, 1u)] = (uint32_t)i;
+            a.pairs[a.tstart[g] + atomicAdd(a.cursor + g, 1u)] = key;
         }
 }
 
@@ -280,7 +319,7 @@ struct BigArgs {
     const uint32_t *tcount;
     const int32_t *tile_item;   // global tile -> item
     const uint64_t *depth;      // [nitems][stride]
-    const uint32_t *pairs;
+    const uint64_t *pairs;
     int64_t stride;
     const int64_t *seg_begin;   // per big tile: offset in the gathered arrays
     uint64_t *keys;
@@ -293,7 +332,7 @@ __global__ void __launch_bounds__(256) k_big_gather(BigArgs a) {
     const int64_t n = a.tcount[g], s0 = a.tstart[g], d0 = a.seg_begin[b];
     const int64_t item = a.tile_item[g];
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t id = a.pairs[s0 + k];
+        const uint32_t id = (uint32_t)a.pairs[s0 + k];
         a.vals[d0 + k] = id;
         a.keys[d0 + k] = a.depth[item * a.stride + id];
     }
@@ -304,7 +343,7 @@ __global__ void __launch_bounds__(256) k_big_scatter(BigArgs a, const uint32_t *
     const uint32_t g = a.big_list[b];
     const int64_t n = a.tcount[g], s0 = a.tstart[g], d0 = a.seg_begin[b];
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-        const_cast<uint32_t *>(a.pairs)[s0 + k] = sorted_vals[d0 + k];
+        const_cast<uint64_t *>(a.pairs)[s0 + k] = sorted_vals[d0 + k];
 }
 
 __global__ void __launch_bounds__(256) k_ids_as_keys(const uint32_t *__restrict__ vals, uint64_t *__restrict__ keys,
@@ -386,7 +425,6 @@ constexpr int kSortCap = 2048;  // tile lists up to this length are sorted in sh
 #ifndef COMP_MIN_BLOCKS
 #define COMP_MIN_BLOCKS 4
 #endif
-constexpr size_t kCompSmem = sizeof(CompShared) + (size_t)kSortCap * (sizeof(uint64_t) + sizeof(uint32_t));
 
 // alpha' = min(al * exp(-e), 0.999) for staged primitive j at (dx, dy):
 // exact replay of _composite.pyx:56-60 (0.5*(A + C) == 0.5A + 0.5C exactly)
@@ -556,6 +594,136 @@ __device__ __noinline__ void sort_tile_list(uint64_t *k, uint32_t *v, int npad) 
     }
 }
 
+// ---- per-tile list sort kernels ------------------------------------------------
+// One warp per tile, entries e = lane + 32 r held in registers (R per lane);
+// the full bitonic network runs with in-lane swaps for strides >= 32 and
+// shuffles below -- no shared memory, no barriers.
+template <int R>
+__device__ __forceinline__ void warp_reg_bitonic(uint64_t (&k)[R]) {
+    const int lane = threadIdx.x & 31;
+    constexpr int N = 32 * R;
+#pragma unroll
+    for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+        for (int st = size >> 1; st > 0; st >>= 1) {
+            if (st >= 32) {
+                const int rs = st >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r & rs) continue;
+                    const int r2 = r | rs;
+                    const bool asc = ((lane + 32 * r) & size) == 0;
+                    const uint64_t a = k[r], b = k[r2];
+                    const bool sw = (a > b) == asc;
+                    k[r] = sw ? b : a;
+                    k[r2] = sw ? a : b;
+                }
+            } else {
+                const bool lower = (lane & st) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint64_t p = __shfl_xor_sync(0xffffffffu, k[r], st);
+                    const bool asc = ((lane + 32 * r) & size) == 0;
+                    k[r] = (lower == asc) ? min(k[r], p) : max(k[r], p);
+                }
+            }
+        }
+    }
+}
+
+struct TileSortArgs {
+    const int64_t *tstart;
+    const uint32_t *tcount;
+    const int64_t *tile_base;  // per item
+    int nitems;
+    const uint64_t *depth;     // [nitems][stride]
+    int64_t stride;
+    uint64_t *pairs;
+    uint32_t *slow_list;       // tiles needing the block-level exact sort
+    unsigned int *slow_n;
+    int64_t Tt;
+};
+
+template <int R>
+__device__ __forceinline__ void warp_sort_tile(const TileSortArgs &a, int64_t g, int n) {
+    const int lane = threadIdx.x & 31;
+    uint64_t *lst = a.pairs + a.tstart[g];
+    uint64_t key[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = lane + 32 * r;
+        key[r] = e < n ? lst[e] : ~0ull;
+    }
+    warp_reg_bitonic<R>(key);
+    // adjacent entries in one 32-bit depth bucket need the exact comparison
+    bool clash = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = lane + 32 * r;
+        const uint64_t nxt_same = __shfl_down_sync(0xffffffffu, key[r], 1);
+        const uint64_t nxt_row = __shfl_sync(0xffffffffu, key[r + 1 < R ? r + 1 : r], 0);
+        const uint64_t nx = lane < 31 ? nxt_same : nxt_row;
+        if (e + 1 < n) clash |= (key[r] >> 32) == (nx >> 32);
+    }
+    if (__any_sync(0xffffffffu, clash)) {
+        if (lane == 0) a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
+        return;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = lane + 32 * r;
+        if (e < n) lst[e] = key[r];
+    }
+}
+
+constexpr int kWarpSortMax = 512;
+
+__global__ void __launch_bounds__(128) k_sort_tiles_warp(TileSortArgs a) {
+    const int64_t g = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (g >= a.Tt) return;
+    const int n = (int)a.tcount[g];
+    if (n <= 1 || n > kSortCap) return;  // > kSortCap: radix fallback already sorted it
+    if (n > kWarpSortMax) {
+        if ((threadIdx.x & 31) == 0) a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
+        return;
+    }
+    if (n <= 32) warp_sort_tile<1>(a, g, n);
+    else if (n <= 64) warp_sort_tile<2>(a, g, n);
+    else if (n <= 128) warp_sort_tile<4>(a, g, n);
+    else if (n <= 256) warp_sort_tile<8>(a, g, n);
+    else warp_sort_tile<16>(a, g, n);
+}
+
+// Exact block-level sort on (64-bit depth key, id) for the slow tiles.
+__global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs a) {
+    __shared__ uint64_t skey[kSortCap];
+    __shared__ uint32_t sid[kSortCap];
+    const int64_t g = a.slow_list[blockIdx.x];
+    const int n = (int)a.tcount[g];
+    int lo = 0, hi = a.nitems - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.tile_base[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const uint64_t *depth = a.depth + (int64_t)lo * a.stride;
+    uint64_t *lst = a.pairs + a.tstart[g];
+    int npad = 64;
+    while (npad < n) npad <<= 1;
+    for (int k = threadIdx.x; k < npad; k += kTileThreads) {
+        if (k < n) {
+            const uint32_t id = (uint32_t)lst[k];
+            sid[k] = id;
+            skey[k] = depth[id];
+        } else {
+            sid[k] = 0xffffffffu;
+            skey[k] = ~0ull;
+        }
+    }
+    __syncthreads();
+    sort_tile_list(skey, sid, npad);
+    for (int k = threadIdx.x; k < n; k += kTileThreads) lst[k] = sid[k];
+}
+
 // One CTA = one 16x16 tile, one pixel per thread; warps are 8x4 sub-tiles.
 // The tile's primitive list is first put in depth order (shared-memory
 // bitonic sort on (depth key, index); oversized lists arrive presorted).
@@ -568,11 +736,8 @@ template <bool USAGE>
 __global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
 k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
             const int64_t *__restrict__ tstart, const uint32_t *__restrict__ tcount,
-            const uint32_t *__restrict__ pairs) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    CompShared &sh = *reinterpret_cast<CompShared *>(smem_raw);
-    uint64_t *skey = reinterpret_cast<uint64_t *>(smem_raw + sizeof(CompShared));
-    uint32_t *sid = reinterpret_cast<uint32_t *>(skey + kSortCap);
+            const uint64_t *__restrict__ pairs) {
+    __shared__ CompShared sh;
     {
         const unsigned long long *src = &kExpTable[0][0];
         for (int k = threadIdx.x; k < kExpN; k += kTileThreads)
@@ -602,72 +767,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 
     const int64_t s0 = tstart[g];
     const int n_all = (int)tcount[g];
-    const uint32_t *__restrict__ glist = pairs + s0;
-    const bool in_smem = n_all <= kSortCap;
-    if (in_smem && n_all > 1) {
-        const uint64_t *__restrict__ depth = itp->depth;
-        int npad = 64;
-        while (npad < n_all) npad <<= 1;
-        // tile-local depth range -> 32-bit buckets (monotone in depth)
-        unsigned long long kmin = ~0ull, kmax = 0ull;
-        for (int k = threadIdx.x; k < n_all; k += kTileThreads) {
-            const uint64_t zk = depth[glist[k]];
-            kmin = min(kmin, (unsigned long long)zk);
-            kmax = max(kmax, (unsigned long long)zk);
-        }
-        for (int d = 16; d > 0; d >>= 1) {
-            kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, d));
-            kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, d));
-        }
-        if (lane == 0) {
-            skey[2 * w] = kmin;
-            skey[2 * w + 1] = kmax;
-        }
-        __syncthreads();
-        kmin = skey[0];
-        kmax = skey[1];
-        for (int k = 1; k < kCompWarps; ++k) {
-            kmin = min(kmin, (unsigned long long)skey[2 * k]);
-            kmax = max(kmax, (unsigned long long)skey[2 * k + 1]);
-        }
-        const unsigned long long span = kmax - kmin;
-        const int sh = span >> 32 ? 64 - __clzll((long long)span) - 32 : 0;
-        __syncthreads();
-        for (int k = threadIdx.x; k < npad; k += kTileThreads) {
-            uint64_t key = ~0ull;
-            if (k < n_all) {
-                const uint32_t id = glist[k];
-                key = (((uint64_t)(depth[id] - kmin) >> sh) << 32) | id;
-            }
-            skey[k] = key;
-        }
-        __syncthreads();
-        sort_tile_keys(skey, npad);
-        // equal buckets need the exact (depth, index) comparison: redo exactly
-        int clash = 0;
-        for (int k = threadIdx.x; k + 1 < n_all; k += kTileThreads)
-            clash |= (skey[k] >> 32) == (skey[k + 1] >> 32);
-        if (__syncthreads_or(clash)) {
-            for (int k = threadIdx.x; k < npad; k += kTileThreads) {
-                if (k < n_all) {
-                    const uint32_t id = (uint32_t)skey[k];
-                    sid[k] = id;
-                } else {
-                    sid[k] = 0xffffffffu;
-                }
-            }
-            __syncthreads();
-            for (int k = threadIdx.x; k < npad; k += kTileThreads)
-                skey[k] = sid[k] == 0xffffffffu ? ~0ull : depth[sid[k]];
-            __syncthreads();
-            sort_tile_list(skey, sid, npad);
-        } else {
-            for (int k = threadIdx.x; k < n_all; k += kTileThreads) sid[k] = (uint32_t)skey[k];
-        }
-    } else if (in_smem && n_all == 1) {
-        if (threadIdx.x == 0) sid[0] = glist[0];
-    }
-
+    const uint64_t *__restrict__ glist = pairs + s0;
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     bool done = !inside;
     float thr = log2_inv_eps() + 6e-5f;  // log2(T/EPS) + guard constant
@@ -677,7 +777,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
         __syncthreads();
         if ((int)threadIdx.x < nb) {
             const int t = threadIdx.x;
-            const uint32_t gi = in_smem ? sid[base + t] : glist[base + t];
+            const uint32_t gi = (uint32_t)glist[base + t];
             const Rec r = recs[gi];
             const float mxl = (float)(r.mx - (double)ox), myl = (float)(r.my - (double)oy);
             sh.gid[t] = gi;
@@ -895,6 +995,14 @@ k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__re
             for (int u = u0; u <= u1; ++u) atomicAdd(tile_count + v * tiles_x + u, 1u);
 }
 
+__global__ void k_init_zrange(unsigned long long *zr, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        zr[2 * i] = ~0ull;
+        zr[2 * i + 1] = 0ull;
+    }
+}
+
 __global__ void k_fill_i64(int64_t *p, int64_t n, int64_t v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -940,8 +1048,8 @@ struct Layout {
 // Stage B: histogram (already accumulated in tile_count) -> ranges -> emit ->
 // oversized-tile fallback sort -> composite -> SSE.
 static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
-                              const Rec *recs, const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count,
-                              double *sse, cudaStream_t st) {
+                              const Rec *recs, const uint64_t *depth, const unsigned long long *zrange,
+                              const int32_t *ntiles, uint32_t *tile_count, double *sse, cudaStream_t st) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
@@ -966,13 +1074,13 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbig, big_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
     const int64_t P = hh[0];
-    uint32_t *pairs = ctx->scratch_t<uint32_t>(kSlotPairVals, (size_t)std::max<int64_t>(P, 1));
+    uint64_t *pairs = ctx->scratch_t<uint64_t>(kSlotPairVals, (size_t)std::max<int64_t>(P, 1));
     uint32_t *cursor = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * Tt, st));
     int64_t maxc = 0;
     for (const auto &h : items) maxc = std::max(maxc, h.count);
     if (P > 0) {
-        EmitArgs ea{recs, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tstart, cursor, pairs, L.stride};
+        EmitArgs ea{recs, depth, zrange, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tstart, cursor, pairs, L.stride};
         k_emit<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ea);
         ++NL;
         check_launch();
@@ -1024,6 +1132,24 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         check_launch();
         AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
     }
+    if (P > 0) {
+        // depth-order every tile list: warp-level register sort, block-level exact sort for the rest
+        unsigned int *slow_n = (unsigned int *)(stats + 3);
+        uint32_t *slow_list = ctx->scratch_t<uint32_t>(kSlotSlowTiles, (size_t)Tt);
+        AIRGS_CUDA_TRY(cudaMemsetAsync(slow_n, 0, sizeof(unsigned int), st));
+        TileSortArgs ta{tstart, tile_count, L.d_tile_base, nitems, depth, L.stride, pairs, slow_list, slow_n, Tt};
+        k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
+        ++NL;
+        check_launch();
+        unsigned int hslow = 0;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&hslow, slow_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        if (hslow > 0) {
+            k_sort_tiles_block<<<hslow, kTileThreads, 0, st>>>(ta);
+            ++NL;
+            check_launch();
+        }
+    }
     double *sse_tiles = ctx->scratch_t<double>(kSlotSseTiles, (size_t)Tt * kCompWarps);
     std::vector<CompItem> ci(nitems);
     std::vector<uint8_t> has_t(nitems);
@@ -1050,22 +1176,16 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     uint8_t *d_has = (uint8_t *)ctx->scratch(kSlotMisc2, nitems);
     h2d_small(ctx, d_ci, ci.data(), sizeof(CompItem) * nitems, st);
     h2d_small(ctx, d_has, has_t.data(), nitems, st);
-    static bool attr_set = false;
-    if (!attr_set) {
-        AIRGS_CUDA_TRY(cudaFuncSetAttribute(k_composite<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCompSmem));
-        AIRGS_CUDA_TRY(cudaFuncSetAttribute(k_composite<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCompSmem));
-        attr_set = true;
-    }
     if (ctx->timing) {
         ctx->ensure_events();
         AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
     }
     if (Tt > 0) {
         if (any_usage)
-            k_composite<true><<<(unsigned)Tt, kTileThreads, kCompSmem, st>>>(d_ci, L.d_tile_base, nitems, tstart,
+            k_composite<true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
                                                                                tile_count, pairs);
         else
-            k_composite<false><<<(unsigned)Tt, kTileThreads, kCompSmem, st>>>(d_ci, L.d_tile_base, nitems, tstart,
+            k_composite<false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
                                                                                 tile_count, pairs);
         ++NL;
         check_launch();
@@ -1183,6 +1303,9 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     int32_t *ntiles = ctx->scratch_t<int32_t>(kSlotNtiles, per);
     uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
+    unsigned long long *zrange = ctx->scratch_t<unsigned long long>(kSlotZRange, 2 * (size_t)nitems);
+    k_init_zrange<<<(unsigned)ceil_div(nitems, 256), 256, 0, st>>>(zrange, nitems);
+    ++NL;
 
     ProjArgs pa;
     pa.frames = (const airgs_frame *)(dd + o_frames);
@@ -1196,6 +1319,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.depth = depth;
     pa.ntiles = ntiles;
     pa.tile_count = tile_count;
+    pa.zrange = zrange;
     pa.flags = flags;
     pa.stride = stride;
     if (ctx->timing) {
@@ -1220,7 +1344,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     }
     if (hflags & kFlagInvalidParam)
         throw ApiFailure(AIRGS_E_VALIDATION, "frame contains invalid primitive parameters");
-    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, sse, st);
+    bin_and_composite(ctx, ih, L, recs, depth, zrange, ntiles, tile_count, sse, st);
 }
 
 static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics, const double *alphas,
@@ -1250,6 +1374,11 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
     uint64_t *depth = ctx->scratch_t<uint64_t>(kSlotDepth, L.stride);
     uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
+    unsigned long long *zrange = ctx->scratch_t<unsigned long long>(kSlotZRange, 2);
+    {
+        const unsigned long long zr[2] = {0ull, (unsigned long long)std::max<int64_t>(k, 1)};
+        h2d_small(ctx, zrange, zr, sizeof(zr), st);
+    }
     if (usage && k > 0) AIRGS_CUDA_TRY(cudaMemsetAsync(usage, 0, sizeof(int64_t) * k, st));
     if (k > 0) {
         k_seam_records<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, means2d, conics, alphas, colors, bboxes, recs,
@@ -1258,7 +1387,7 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
         check_launch();
     }
     // every in-image pixel of every tile is written by the composite kernel
-    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, nullptr, st);
+    bin_and_composite(ctx, ih, L, recs, depth, zrange, ntiles, tile_count, nullptr, st);
 }
 
 static void sse_impl(airgs_ctx *ctx, const double *a, const double *b, int64_t n, double *out, cudaStream_t st) {
