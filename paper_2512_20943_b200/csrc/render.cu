@@ -770,7 +770,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     const uint64_t *__restrict__ glist = pairs + s0;
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     bool done = !inside;
-    float thr = log2_inv_eps() + 6e-5f;  // log2(T/EPS) + guard constant
+    float thr = log2_inv_eps();  // log2(T/EPS); the guard lives in the staged coefficients
 
     for (int base = 0; base < n_all; base += kTileThreads) {
         const int nb = min(kTileThreads, n_all - base);
@@ -781,8 +781,12 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             const Rec r = recs[gi];
             const float mxl = (float)(r.mx - (double)ox), myl = (float)(r.my - (double)oy);
             sh.gid[t] = gi;
-            sh.f0[t] = make_float4(mxl, myl, (float)(0.5 * kLog2e * r.ca), (float)(kLog2e * r.cb));
-            sh.f1[t] = make_float2((float)(0.5 * kLog2e * r.cc), __log2f((float)r.al));
+            // fast-reject coefficients: log2e * (a/2, b, c/2) with a/2, c/2 scaled by (1 - kappa) so
+            // e' = e - kappa*s absorbs the s-proportional guard; the constant guard
+            // is folded into log2(alpha) (fp32 fast reject)
+            const double kap = 1.0 - 2e-5;
+            sh.f0[t] = make_float4(mxl, myl, (float)(0.5 * kLog2e * kap * r.ca), (float)(kLog2e * r.cb));
+            sh.f1[t] = make_float2((float)(0.5 * kLog2e * kap * r.cc), __log2f((float)r.al) + 6e-5f);
             sh.m[t] = make_double2(r.mx, r.my);
             sh.hab[t] = make_double2(0.5 * r.ca, r.cb);
             sh.hcal[t] = make_double2(0.5 * r.cc, r.al);
@@ -825,13 +829,14 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                 const float2 b1 = sh.f1[c + k2];
                 const float dxa = pxl - a0.x, dya = pyl - a0.y;
                 const float dxb = pxl - b0.x, dyb = pyl - b0.y;
-                const float sa = fmaf(a0.z * dxa, dxa, (a1.x * dya) * dya);  // log2e * 0.5(a dx^2 + c dy^2)
-                const float sb = fmaf(b0.z * dxb, dxb, (b1.x * dyb) * dyb);
-                const float ea = fmaf(a0.w * dxa, dya, sa);  // log2e * e
-                const float eb = fmaf(b0.w * dxb, dyb, sb);
+                // e' = dx*(A dx + B dy) + C dy^2   (log2 units, guard-scaled)
+                const float ua = fmaf(a0.z, dxa, a0.w * dya);
+                const float ub = fmaf(b0.z, dxb, b0.w * dyb);
+                const float ea = fmaf(ua, dxa, (a1.x * dya) * dya);
+                const float eb = fmaf(ub, dxb, (b1.x * dyb) * dyb);
                 // reject iff e > ln(al) + ln(T/EPS) + guard (guard proof: DESIGN.md)
-                word |= (unsigned)(ea <= fmaf(1e-5f, sa, a1.y) + thr) << k1;
-                word |= (unsigned)(eb <= fmaf(1e-5f, sb, b1.y) + thr) << k2;
+                word |= (unsigned)(ea <= a1.y + thr) << k1;
+                word |= (unsigned)(eb <= b1.y + thr) << k2;
             }
             if (done) word = 0;
             // phase B: each lane runs its own candidates in depth order (exact fp64)
@@ -866,7 +871,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             }
             // once 0.999*T <= EPS no later primitive can pass the weight test
             done = done || kAlphaClamp * T <= kEpsContrib;
-            thr = __log2f((float)T) + (log2_inv_eps() + 6e-5f);
+            thr = __log2f((float)T) + log2_inv_eps();
         }
         __syncthreads();
         if (USAGE && (int)threadIdx.x < nb && sh.cnt[threadIdx.x] > 0)
