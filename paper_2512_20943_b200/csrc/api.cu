@@ -18,7 +18,9 @@ __global__ void k_param_copy(unsigned char *__restrict__ dst, const ParamChunk c
 void h2d_small(airgs_ctx *ctx, void *dst, const void *src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return;
     if (bytes > 16 * (size_t)kParamChunk) {
+        // large block: DMA, and drain so the (reusable) host source may change afterwards
         AIRGS_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
         return;
     }
     const unsigned char *s = static_cast<const unsigned char *>(src);
@@ -68,6 +70,12 @@ extern "C" int64_t airgs_launch_count(const airgs_ctx *ctx) { return ctx ? ctx->
 extern "C" int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms, int64_t *composite_launches,
                             double *project_ms, int64_t *project_launches) {
     if (!ctx) return AIRGS_E_INTERNAL;
+    try {
+        cudaSetDevice(ctx->device);
+        ctx->resolve_timing();
+    } catch (...) {
+        return AIRGS_E_CUDA;
+    }
     if (composite_ms) *composite_ms = ctx->composite_ms;
     if (composite_launches) *composite_launches = ctx->composite_launches;
     if (project_ms) *project_ms = ctx->project_ms;

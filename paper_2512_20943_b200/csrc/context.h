@@ -17,14 +17,57 @@ struct airgs_ctx {
     std::vector<Buf> bufs;
     void *host = nullptr;
     size_t host_cap = 0;
-    // optional per-kernel timing (CUDA events around the dominant kernels)
+    // optional per-kernel timing: event pairs recorded around the dominant
+    // kernels on their stream, resolved lazily (no synchronisation in the hot path)
     bool timing = false;
     double composite_ms = 0.0, project_ms = 0.0;
     int64_t composite_launches = 0, project_launches = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    void ensure_events() {
-        for (auto &e : ev)
-            if (!e) AIRGS_CUDA_TRY(cudaEventCreate(&e));
+    struct Pending {
+        cudaEvent_t a, b;
+        int kind;  // 0 composite, 1 project
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    cudaEvent_t take_event() {
+        if (event_pool.empty()) {
+            cudaEvent_t e;
+            AIRGS_CUDA_TRY(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    // record the start of a timed kernel; returns the start event (or null)
+    cudaEvent_t time_begin(cudaStream_t st) {
+        if (!timing) return nullptr;
+        cudaEvent_t e = take_event();
+        AIRGS_CUDA_TRY(cudaEventRecord(e, st));
+        return e;
+    }
+    void time_end(cudaEvent_t a, cudaStream_t st, int kind) {
+        if (!a) return;
+        cudaEvent_t b = take_event();
+        AIRGS_CUDA_TRY(cudaEventRecord(b, st));
+        pending.push_back({a, b, kind});
+        if (pending.size() > 256) resolve_timing();
+    }
+    void resolve_timing() {
+        for (auto &p : pending) {
+            AIRGS_CUDA_TRY(cudaEventSynchronize(p.b));
+            float ms = 0.f;
+            AIRGS_CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
+            if (p.kind == 0) {
+                composite_ms += ms;
+                ++composite_launches;
+            } else {
+                project_ms += ms;
+                ++project_launches;
+            }
+            event_pool.push_back(p.a);
+            event_pool.push_back(p.b);
+        }
+        pending.clear();
     }
 
     // Device scratch slot `id`, at least `bytes` long.  Growing synchronises
@@ -65,8 +108,11 @@ struct airgs_ctx {
         for (auto &b : bufs)
             if (b.p) cudaFree(b.p);
         if (host) cudaFreeHost(host);
-        for (auto &e : ev)
-            if (e) cudaEventDestroy(e);
+        for (auto &p : pending) {
+            cudaEventDestroy(p.a);
+            cudaEventDestroy(p.b);
+        }
+        for (auto &e : event_pool) cudaEventDestroy(e);
     }
 };
 

@@ -694,11 +694,8 @@ __global__ void __launch_bounds__(128) k_sort_tiles_warp(TileSortArgs a) {
     else warp_sort_tile<16>(a, g, n);
 }
 
-// Exact block-level sort on (64-bit depth key, id) for the slow tiles.
-__global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs a) {
-    __shared__ uint64_t skey[kSortCap];
-    __shared__ uint32_t sid[kSortCap];
-    const int64_t g = a.slow_list[blockIdx.x];
+// Exact block-level sort of one slow tile on (64-bit depth key, id).
+__device__ __noinline__ void sort_one_slow_tile(const TileSortArgs &a, int64_t g, uint64_t *skey, uint32_t *sid) {
     const int n = (int)a.tcount[g];
     int lo = 0, hi = a.nitems - 1;
     while (lo < hi) {
@@ -724,9 +721,20 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs 
     for (int k = threadIdx.x; k < n; k += kTileThreads) lst[k] = sid[k];
 }
 
+// Exact block-level sort on (64-bit depth key, id) for the slow tiles; a
+// fixed grid strides over the device-side slow list.
+__global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs a) {
+    __shared__ uint64_t skey[kSortCap];
+    __shared__ uint32_t sid[kSortCap];
+    const unsigned int nslow = *a.slow_n;
+    for (unsigned int b = blockIdx.x; b < nslow; b += gridDim.x) {
+        __syncthreads();
+        sort_one_slow_tile(a, a.slow_list[b], skey, sid);
+    }
+}
+
 // One CTA = one 16x16 tile, one pixel per thread; warps are 8x4 sub-tiles.
-// The tile's primitive list is first put in depth order (shared-memory
-// bitonic sort on (depth key, index); oversized lists arrive presorted).
+// The tile's primitive list arrives in depth order (k_sort_tiles_*).
 // Per batch of 256 primitives (staged once per CTA), each warp walks
 // 32-entry chunks: phase A tests only primitives whose threshold-ellipse
 // AABB touches its sub-tile (fp32, log2 domain, proven guard band) and builds
@@ -1054,7 +1062,8 @@ struct Layout {
 // oversized-tile fallback sort -> composite -> SSE.
 static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
                               const Rec *recs, const uint64_t *depth, const unsigned long long *zrange,
-                              const int32_t *ntiles, uint32_t *tile_count, double *sse, cudaStream_t st) {
+                              const int32_t *ntiles, uint32_t *tile_count, double *sse, cudaStream_t st,
+                              const unsigned int *flags = nullptr) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
@@ -1075,9 +1084,12 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     }
     int64_t hh[2];
     AIRGS_CUDA_TRY(cudaMemcpyAsync(hh, stats, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    unsigned int hbig = 0;
+    unsigned int hbig = 0, hflags = 0;
     AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbig, big_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    if (flags) AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hflags & kFlagInvalidParam)
+        throw ApiFailure(AIRGS_E_VALIDATION, "frame contains invalid primitive parameters");
     const int64_t P = hh[0];
     uint64_t *pairs = ctx->scratch_t<uint64_t>(kSlotPairVals, (size_t)std::max<int64_t>(P, 1));
     uint32_t *cursor = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)Tt);
@@ -1144,16 +1156,10 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         AIRGS_CUDA_TRY(cudaMemsetAsync(slow_n, 0, sizeof(unsigned int), st));
         TileSortArgs ta{tstart, tile_count, L.d_tile_base, nitems, depth, L.stride, pairs, slow_list, slow_n, Tt};
         k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
-        ++NL;
+        // the exact block sort walks the device-side slow list (no host readback)
+        k_sort_tiles_block<<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
+        NL += 2;
         check_launch();
-        unsigned int hslow = 0;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(&hslow, slow_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-        if (hslow > 0) {
-            k_sort_tiles_block<<<hslow, kTileThreads, 0, st>>>(ta);
-            ++NL;
-            check_launch();
-        }
     }
     double *sse_tiles = ctx->scratch_t<double>(kSlotSseTiles, (size_t)Tt * kCompWarps);
     std::vector<CompItem> ci(nitems);
@@ -1181,10 +1187,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     uint8_t *d_has = (uint8_t *)ctx->scratch(kSlotMisc2, nitems);
     h2d_small(ctx, d_ci, ci.data(), sizeof(CompItem) * nitems, st);
     h2d_small(ctx, d_has, has_t.data(), nitems, st);
-    if (ctx->timing) {
-        ctx->ensure_events();
-        AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[0], st));
-    }
+    cudaEvent_t t_comp = Tt > 0 ? ctx->time_begin(st) : nullptr;
     if (Tt > 0) {
         if (any_usage)
             k_composite<true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
@@ -1195,19 +1198,13 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         ++NL;
         check_launch();
     }
-    if (ctx->timing) AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[1], st));
+    ctx->time_end(t_comp, st, 0);
     if (sse && any_target) {
         k_sse_items<<<nitems, 256, 0, st>>>(sse_tiles, L.d_tile_base, d_has, sse);
         ++NL;
         check_launch();
     }
-    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));  // host vectors outlive their async copies
-    if (ctx->timing && Tt > 0) {
-        float ms = 0.f;
-        AIRGS_CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
-        ctx->composite_ms += ms;
-        ++ctx->composite_launches;
-    }
+    // small uploads travel as kernel parameters: nothing host-side must outlive the launches
 }
 
 // Upload per-item layout arrays (tile bases, tiles_x, counts, tile -> item map).
@@ -1327,29 +1324,15 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.zrange = zrange;
     pa.flags = flags;
     pa.stride = stride;
-    if (ctx->timing) {
-        ctx->ensure_events();
-        AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[2], st));
-    }
+    cudaEvent_t t_proj = ctx->time_begin(st);
     {
         dim3 grid((unsigned)ceil_div(stride, kProjThreads), (unsigned)nframes);
         k_project<<<grid, kProjThreads, 0, st>>>(pa);
         ++NL;
         check_launch();
     }
-    if (ctx->timing) AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev[3], st));
-    unsigned int hflags = 0;
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-    if (ctx->timing) {
-        float ms = 0.f;
-        AIRGS_CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
-        ctx->project_ms += ms;
-        ++ctx->project_launches;
-    }
-    if (hflags & kFlagInvalidParam)
-        throw ApiFailure(AIRGS_E_VALIDATION, "frame contains invalid primitive parameters");
-    bin_and_composite(ctx, ih, L, recs, depth, zrange, ntiles, tile_count, sse, st);
+    ctx->time_end(t_proj, st, 1);
+    bin_and_composite(ctx, ih, L, recs, depth, zrange, ntiles, tile_count, sse, st, flags);
 }
 
 static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics, const double *alphas,

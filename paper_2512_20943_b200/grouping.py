@@ -135,13 +135,18 @@ def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_D
     px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
-    bufs = [None, None]
     used = [None, None]
-    # persistent pinned staging for payload bytes (no per-frame cudaHostAlloc,
-    # which would synchronise the device and serialise the pipeline)
+    ready = [None, None]
+    if len(payloads) != len(targets):
+        raise StructuralError("one target set per payload required")
     datas = [payloads[t].data if hasattr(payloads[t], "data") else bytes(payloads[t]) for t in range(len(payloads))]
     cap = max((len(d) for d in datas), default=1)
+    # double buffers allocated once: pinned payload staging (no per-frame cudaHostAlloc,
+    # which synchronises the device) and device targets / payloads (no allocator churn)
     pinned = [torch.empty((cap,), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    dpay = [torch.empty((cap,), dtype=torch.uint8, device=dev) for _ in range(2)]
+    dtg = [[torch.empty((c.resolution[1], c.resolution[0], 3), dtype=torch.float64, device=dev) for c in cams]
+           for _ in range(2)]
 
     def host_tensor(im):
         return im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im, dtype=np.float64))
@@ -149,38 +154,36 @@ def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_D
     def stage(t):
         b = t % 2
         data = datas[t]
+        host = [host_tensor(im) for im in targets[t]]
+        check_targets(host, cams)
         with torch.cuda.stream(copy):
             if used[b] is not None:
                 copy.wait_event(used[b])  # buffer b's previous frame is done
-            host = [host_tensor(im) for im in targets[t]]
-            check_targets(host, cams)
-            tg = [h.to(dev, non_blocking=True) for h in host]
+            for d, h in zip(dtg[b], host):
+                d.copy_(h, non_blocking=True)
             if data:
                 pinned[b][: len(data)].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
-            pd = pinned[b][: len(data)].to(dev, non_blocking=True)
+                dpay[b][: len(data)].copy_(pinned[b][: len(data)], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(copy)
-        for x in tg + [pd]:
-            x.record_stream(comp)
-        bufs[b] = (tg, pd, data, ev)
+        ready[b] = ev
 
     out = []
-    if len(payloads) != len(targets):
-        raise StructuralError("one target set per payload required")
     if payloads:
         stage(0)
     for t in range(len(payloads)):
-        tg, pd, data, ev = bufs[t % 2]
-        comp.wait_event(ev)
+        b = t % 2
+        comp.wait_event(ready[b])
         if t + 1 < len(payloads):
             stage(t + 1)
+        data, pd, tg = datas[t], dpay[b][: len(datas[t])], dtg[b]
         delta, _ = codec.decode_delta_device(data, n, w, device=dev, payload_dev=pd)
         planes = apply_overlay(canon, n, delta.overlay(dev))
         vb = render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for v in range(V)],
                           targets=tg, device=dev)
         u = torch.cuda.Event()
         u.record(comp)
-        used[t % 2] = u
+        used[b] = u
         sse = vb.sse.cpu().numpy()
         q = float(np.mean([psnr_from_sse(sse[v], px[v]) for v in range(V)]))
         out.append((q, is_keyframe(q, tau_db)))
