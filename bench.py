@@ -242,6 +242,8 @@ def run_gpu(args):
             "gpu_launches": int(round(launches)),
             "clocks": clocks, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "keyframe_decisions": decisions, "qualities_db": [round(q, 6) for q in quals],
+            "decision_margins": {"min_abs_q_minus_tau_db": round(min(abs(q - TAU_DB) for q in quals), 6),
+                                 "tau_db": TAU_DB},
         }
         print(json.dumps(line))
     if world > 1:

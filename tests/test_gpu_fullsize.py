@@ -1,0 +1,177 @@
+"""GPU at BASELINE.json's full sizes (configs C2-C5).  Where the oracle
+finishes in seconds it is run directly (one C2 view; level sizes and pruned
+sets, which need no rendering); otherwise size-independent properties the
+domain guarantees are checked (determinism, batch/single and sharded/unsharded
+equivalence, zero-usage removal, ratio-0 = 100 dB, nested pruned sets,
+strictly decreasing sizes, unit-colour conservation)."""
+
+import numpy as np
+import pytest
+
+from oracle import airgs_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(name, views=None, count=None):
+    from dataclasses import replace
+
+    from paper_2512_20943_b200 import synth
+
+    c = synth.CONFIGS[name]
+    if views is not None:
+        c = replace(c, views=views)
+    if count is not None:
+        c = replace(c, count=count)
+    return c
+
+
+def test_c2_view_matches_oracle_exactly():
+    """300k Gaussians, 1352x1014: usage counts bit-exact, pixels 1e-12."""
+    from paper_2512_20943_b200 import rasterizer, synth
+    from paper_2512_20943_b200.model import GaussianFrame
+
+    cfg = _cfg("C2")
+    seq = synth.Sequence(cfg, seed=0, event_every=0)
+    p = seq.frame(1)
+    cam = synth.cameras(cfg)[3]
+    imgs, usage = rasterizer.render_with_usage(GaussianFrame(params=p), [cam])
+    ref_img, ref_usage = orc.render_full(p, cam)
+    np.testing.assert_array_equal(usage.counts, ref_usage)
+    assert np.max(np.abs(imgs[0].pixels - ref_img)) <= 1e-12
+
+
+def test_c2_batched_views_equal_single_views_and_are_deterministic():
+    import torch
+
+    from paper_2512_20943_b200 import synth
+    from paper_2512_20943_b200.model import GaussianFrame
+    from paper_2512_20943_b200.rasterizer import render_views
+
+    cfg = _cfg("C2", views=6)
+    seq = synth.Sequence(cfg, seed=1, event_every=0)
+    fr = GaussianFrame(params=seq.frame(2))
+    cams = synth.cameras(cfg)
+    batch = render_views([fr], cams, [(0, v) for v in range(6)], want_images=True, usage_frames=[0])
+    again = render_views([fr], cams, [(0, v) for v in range(6)], want_images=True, usage_frames=[0])
+    total = torch.zeros_like(batch.usage[0])
+    for v in range(6):
+        one = render_views([fr], cams, [(0, v)], want_images=True, usage_frames=[0])
+        assert torch.equal(one.images[0], batch.images[v])
+        total += one.usage[0]
+    assert torch.equal(total, batch.usage[0])  # usage merging is an exact associative sum
+    for a, b in zip(batch.images, again.images):
+        assert torch.equal(a, b)
+
+
+def test_c2_zero_usage_removal_is_bit_identical():
+    from paper_2512_20943_b200 import rasterizer, synth
+    from paper_2512_20943_b200.model import GaussianFrame
+
+    cfg = _cfg("C2")
+    p = synth.Sequence(cfg, seed=2, event_every=0).frame(0)
+    cam = synth.cameras(cfg)[0]
+    imgs, usage = rasterizer.render_with_usage(GaussianFrame(params=p), [cam])
+    keep = np.nonzero(usage.counts > 0)[0]
+    assert keep.size < p.shape[0]
+    cut = rasterizer.render(GaussianFrame(params=p[keep]), cam)
+    np.testing.assert_array_equal(imgs[0].pixels, cut.pixels)
+
+
+def test_c3_level_sweep_full_size():
+    """300k x 8 levels at 1080p: exact sizes and pruned sets vs the oracle
+    (no rendering needed), ratio 0 = 100 dB, nested pruned sets, strictly
+    decreasing sizes; one (level, view) quality checked against the oracle."""
+    from paper_2512_20943_b200 import rasterizer, synth
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+    from paper_2512_20943_b200.pruning import build_level_space
+
+    cfg = _cfg("C3", views=4)
+    seq = synth.Sequence(cfg, seed=3, event_every=0)
+    base, moved = seq.frame(0), seq.frame(4)
+    cams = synth.cameras(cfg)
+    space = CanonicalSpace(GaussianFrame(params=base, frame_index=0, group_key=0), capacity_U=base.shape[0])
+    gap = diff_frames(space.frame, GaussianFrame(params=moved))
+    _, usage = rasterizer.render_with_usage(GaussianFrame(params=moved), cams)
+    ratios = [i / 10 for i in range(8)]
+    lv = build_level_space(gap, space, cams, ratios, usage, 1e-4, frame_index=4)
+    gi = gap.indices()
+    gr = np.stack([gap.entries[i] for i in gi.tolist()])
+    last = None
+    for level in lv.levels:
+        ki, kr, rm = orc.prune(gi, gr, usage.counts, level.ratio)
+        assert level.size_bytes == orc.gsdp_size(ki, kr, 1e-4)
+        assert level.pruned_indices == tuple(rm.tolist())
+        if last is not None:
+            assert set(last.pruned_indices) <= set(level.pruned_indices)
+            assert level.size_bytes < last.size_bytes
+        last = level
+    assert lv.levels[0].ratio == 0.0 and lv.levels[0].quality_db == 100.0
+    # one level, one view, against the oracle
+    j = len(lv.levels) // 2
+    ki, kr, _ = orc.prune(gi, gr, usage.counts, lv.levels[j].ratio)
+    q, keep = orc.quantize(kr, 1e-4)
+    pruned = orc.apply(base, ki[keep], q[keep].astype(np.float64) * 1e-4)
+    q0, keep0 = orc.quantize(gr, 1e-4)
+    full = orc.apply(base, gi[keep0], q0[keep0].astype(np.float64) * 1e-4)
+    ref_q = orc.psnr(orc.render(pruned, cams[1]), orc.render(full, cams[1]))
+    one = build_level_space(gap, space, [cams[1]], [0.0, lv.levels[j].ratio], usage, 1e-4)
+    assert abs(one.levels[-1].quality_db - ref_q) <= 1e-6
+
+
+def test_c4_sharded_probe_world1_and_decisions():
+    """150k Gaussians, 13 views 1280x720: the sharded driver (world 1) equals
+    the batched probe; keyframe decisions follow tau."""
+    from paper_2512_20943_b200 import grouping, sharding, synth
+    from paper_2512_20943_b200.model import GaussianFrame
+    from paper_2512_20943_b200.rasterizer import render_views
+
+    cfg = _cfg("C4")
+    seq = synth.Sequence(cfg, seed=4, event_every=3, event_fraction=0.05)
+    cams = synth.cameras(cfg)
+    base = GaussianFrame(params=seq.frame(0))
+    frames = [GaussianFrame(params=seq.frame(t)[: base.count]) for t in (1, 4)]
+    targets = []
+    for t in (1, 4):
+        vb = render_views([GaussianFrame(params=seq.frame(t))], cams, [(0, v) for v in range(len(cams))],
+                          want_images=True)
+        targets.append(vb.images)
+    q1 = grouping.probe_frames(frames, cams, targets)
+    q2 = sharding.probe_frames_sharded(frames, cams, targets)
+    assert q1 == q2
+    assert q1[0] > q1[1]  # frame 4 misses the appearance event's new primitives
+
+
+def test_c5_stress_properties():
+    """2M Gaussians at 1080p: deterministic, finite, usage consistent with the
+    rendered images (a view with no contributions is black)."""
+    import torch
+
+    from paper_2512_20943_b200 import synth
+    from paper_2512_20943_b200.model import GaussianFrame
+    from paper_2512_20943_b200.rasterizer import render_views
+
+    cfg = _cfg("C5", views=2)
+    fr = GaussianFrame(params=synth.Sequence(cfg, seed=5, event_every=0).frame(0))
+    cams = synth.cameras(cfg)
+    a = render_views([fr], cams, [(0, 0), (0, 1)], want_images=True, usage_frames=[0])
+    b = render_views([fr], cams, [(0, 0), (0, 1)], want_images=True, usage_frames=[0])
+    for x, y in zip(a.images, b.images):
+        assert torch.equal(x, y)
+        assert torch.isfinite(x).all() and x.min() >= 0 and x.max() <= 1
+    assert torch.equal(a.usage[0], b.usage[0])
+    assert int(a.usage[0].sum()) > 0
+
+
+def test_seam_unit_colour_conservation_full_size():
+    """rgb = 1 - T with unit colours on a full C2 view through the seam."""
+    from paper_2512_20943_b200 import rasterizer, synth
+
+    cfg = _cfg("C2")
+    p = synth.Sequence(cfg, seed=6, event_every=0).frame(0)[:100_000]
+    cam = synth.cameras(cfg)[2]
+    pr = orc.prepare(p, cam)
+    W, H = cam.resolution
+    img, tr, us, _ = rasterizer.forward(pr.means2d, pr.conics, pr.alphas, np.ones_like(pr.colors), pr.bboxes, H, W)
+    np.testing.assert_allclose(img[:, :, 0], 1.0 - tr, atol=1e-12)
+    assert np.all(tr > 0) and np.all(tr <= 1)
