@@ -220,6 +220,10 @@ def run_gpu(args):
 
     # ---- roofline of the dominant kernel (k_composite), timed live above
     roof = roofline(space, cams, payloads, ktime, ms_max / args.steps)
+    # ---- its compute-side roofline: algorithmic fp64 work of the reference loop
+    # (diagnostic counting pass over the timed frames, untimed)
+    roof_sm = roofline_sm(eng, space, cams, payload_dev, payloads, targets, device,
+                          [i % nf for i in range(args.warmup, total)], roof["kernel_ms_per_launch"])
 
     # ---- e2e through the public API from pinned host buffers
     e2e = run_e2e(space, cams, payloads, targets, device, args, world)
@@ -240,7 +244,7 @@ def run_gpu(args):
                        "l2": "inputs larger than L2 (18 float64 targets = 592 MB per step)",
                        "parallelism": f"frame-sharded x{world}"},
             "gpu_launches": int(round(launches)),
-            "clocks": clocks, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_sm": roof_sm, "cpu_baseline": cpu,
             "keyframe_decisions": decisions, "qualities_db": [round(q, 6) for q in quals],
             "decision_margins": {"min_abs_q_minus_tau_db": round(min(abs(q - TAU_DB) for q in quals), 6),
                                  "tau_db": TAU_DB},
@@ -285,6 +289,50 @@ def roofline(space, cams, payloads, ktime, step_ms):
     if sm:
         out["sm"] = sm
     return out
+
+
+# fp64 pipe operations per (pixel, primitive) evaluation of the reference loop
+# (_composite.pyx:42-73) as executed exactly: dx, dy (2) + e (9, the
+# reference's expression) + exp (13: table exp, tools/gen_exp_table.py) +
+# al*g, clamp, w = ap*T, w > 1/255 (4); a contribution adds 3 colour
+# multiply-adds (6), 1 - ap and T*(1 - ap) (2).
+OPS_PER_LIVE_EVAL = 28
+OPS_PER_CONTRIB = 8
+
+
+def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames_used, k_ms):
+    """k_composite against the fp64 pipe (compositing is SM
+    bound).  Algorithmic work per launch = live evaluations x 28 + contributions
+    x 8 fp64 ops, with live / contributing (pixel, primitive) pairs counted
+    exactly on the timed frames (airgs_eval_stats, verified against the CPU
+    restatement of the reference loop in tests/test_gpu_render.py).  The
+    kernel skips most of this work (fp32 candidate pass), so `frac` is the
+    rate at which it disposes of the reference's work, not pipe utilisation;
+    the measured pipe utilisation is roofline.sm.fp64_pipe_active_pct."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            pk = json.load(fh)
+        peak = float(pk["fp64_fma_tflops"]) / 2.0  # DFMA lane-ops / s (an FMA = 1 op here)
+        src = "profiles/fp64_peak.json (DFMA microbenchmark, tools/fp64_peak.cu)"
+    except Exception:
+        peak, src = 148 * 64 * 1.965e9 / 1e12, "fallback: 148 SMs x 64 DFMA/clk x 1.965 GHz"
+    counts = {}
+    eng.eval_stats(1)
+    try:
+        for f in sorted(set(frames_used)):
+            evaluate_frame(space, cams, payload_dev[f], payloads[f].data, targets[f], device)
+            counts[f] = eng.eval_stats(1)
+    finally:
+        eng.eval_stats(0)
+    V = len(cams)
+    tot = {k: sum(counts[f][k] for f in frames_used) / len(frames_used) for k in ("bbox", "live", "contrib")}
+    ops = tot["live"] * OPS_PER_LIVE_EVAL + tot["contrib"] * OPS_PER_CONTRIB
+    achieved = ops / (k_ms / 1e3) / 1e12 if k_ms else None
+    return {"bound": "fp64", "kernel": "k_composite", "achieved": round(achieved, 3) if achieved else None,
+            "peak": round(peak, 3), "unit": "T fp64 ops/s", "frac": round(achieved / peak, 4) if achieved else None,
+            "peak_source": src, "ops_per_live_eval": OPS_PER_LIVE_EVAL, "ops_per_contribution": OPS_PER_CONTRIB,
+            "per_view": {k: int(round(v / V)) for k, v in tot.items()},
+            "algorithmic_ops_per_launch": int(ops)}
 
 
 def run_e2e(space, cams, payloads, targets, device, args, world):

@@ -92,6 +92,16 @@ AIRGS_API int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms,
                            int64_t *composite_launches, double *project_ms,
                            int64_t *project_launches);
 
+/* Diagnostic evaluation counters (no reference equivalent; used by bench.py
+ * for the algorithmic-work roofline).  While armed, renders
+ * use a counting variant of the compositing kernel that also accumulates, over
+ * all (pixel, primitive) pairs of the reference's Gaussian-major loop
+ * (ss/_composite.pyx:42-73): counts[0] = pairs inside the clipped bbox,
+ * counts[1] = those evaluated before the pixel terminated (0.999*T <= 1/255),
+ * counts[2] = contributing pairs (= summed usage).  Returns the counts since
+ * the last (re)arm; enable = 1 arms, 0 disarms, -1 only reads.  Synchronises. */
+AIRGS_API int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts);
+
 /* ---- rasterizer --------------------------------------------------------- */
 
 /* Batched render: replaces ss/rasterizer.py:113-240 (_activate, _prepare,

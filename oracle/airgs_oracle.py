@@ -234,6 +234,9 @@ def _load():
         fn = lib.oracle_fma
         fn.restype = None
         fn.argtypes = [ctypes.c_int64, dp, dp, dp, dp]
+        fn = lib.oracle_eval_counts
+        fn.restype = None
+        fn.argtypes = [ctypes.c_int64, dp, dp, dp, dp, ip, ctypes.c_int, ctypes.c_int, ip]
         fn = lib.oracle_composite_tiles
         fn.restype = None
         fn.argtypes = [ctypes.c_int64, dp, dp, dp, dp, ip, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, ip]
@@ -264,6 +267,23 @@ def composite(means2d, conics, alphas, colors, bboxes, height, width, pixel_majo
     else:
         lib.oracle_composite_gmajor(*args, _ptr(img, D), _ptr(tr, D), _ptr(us, I))
     return img, tr, us[:k]
+
+
+def eval_counts(params, cam):
+    """(bbox, live, contrib) pair counts of the reference loop for one view
+    (_composite.pyx:42-73; live = pixel not yet terminated, 0.999*T > 1/255)."""
+    lib = _load()
+    pr = prepare(params, cam)
+    ct = CamTerms(cam)
+    D, I = ctypes.c_double, ctypes.c_int64
+    m2 = np.ascontiguousarray(pr.means2d, dtype=np.float64)
+    co = np.ascontiguousarray(pr.conics, dtype=np.float64)
+    al = np.ascontiguousarray(pr.alphas, dtype=np.float64)
+    bb = np.ascontiguousarray(pr.bboxes, dtype=np.int64)
+    out = np.zeros(3, dtype=np.int64)
+    lib.oracle_eval_counts(m2.shape[0], _ptr(m2, D), _ptr(co, D), _ptr(al, D), _ptr(al, D), _ptr(bb, I),
+                           int(ct.H), int(ct.W), _ptr(out, I))
+    return tuple(int(v) for v in out)
 
 
 def tile_keys(bboxes, width, height, tile=TILE):

@@ -142,3 +142,44 @@ void oracle_fma(int64_t n, const double *a, const double *b, const double *c, do
 {
     for (int64_t i = 0; i < n; ++i) out[i] = fma(a[i], b[i], c[i]);
 }
+
+/* Evaluation counts of the reference loop:
+ * counts[0] = (pixel, primitive) pairs inside clipped bboxes, counts[1] =
+ * those whose pixel was still live (0.999*T > 1/255 before the evaluation),
+ * counts[2] = contributing pairs.  Same arithmetic as the gmajor loop. */
+void oracle_eval_counts(int64_t k, const double *means2d, const double *conics,
+                        const double *alphas, const double *bboxes_unused, const int64_t *bboxes,
+                        int height, int width, int64_t *counts)
+{
+    (void)bboxes_unused;
+    int64_t npx = (int64_t)height * width;
+    double *trans = (double *)malloc(sizeof(double) * (size_t)(npx > 0 ? npx : 1));
+    for (int64_t p = 0; p < npx; ++p) trans[p] = 1.0;
+    counts[0] = counts[1] = counts[2] = 0;
+    for (int64_t i = 0; i < k; ++i) {
+        int x0 = (int)bboxes[4 * i], x1 = (int)bboxes[4 * i + 1];
+        int y0 = (int)bboxes[4 * i + 2], y1 = (int)bboxes[4 * i + 3];
+        if (x1 <= x0 || y1 <= y0) continue;
+        double mx = means2d[2 * i], my = means2d[2 * i + 1];
+        double a = conics[3 * i], b = conics[3 * i + 1], c = conics[3 * i + 2];
+        double al = alphas[i];
+        for (int iy = y0; iy < y1; ++iy) {
+            double dy = ((double)iy + 0.5) - my;
+            for (int ix = x0; ix < x1; ++ix) {
+                int64_t p = (int64_t)iy * width + ix;
+                double t = trans[p];
+                counts[0] += 1;
+                if (K_CLAMP * t > K_EPS) counts[1] += 1;
+                double dx = ((double)ix + 0.5) - mx;
+                double e = 0.5 * (a * dx * dx + c * dy * dy) + b * dx * dy;
+                double ap = al * exp(-e);
+                if (ap > K_CLAMP) ap = K_CLAMP;
+                if (ap * t > K_EPS) {
+                    trans[p] = t * (1.0 - ap);
+                    counts[2] += 1;
+                }
+            }
+        }
+    }
+    free(trans);
+}

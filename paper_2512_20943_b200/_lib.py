@@ -63,6 +63,7 @@ SIGNATURES = {
     "airgs_last_error": (ctypes.c_char_p, [vp]),
     "airgs_launch_count": (i64, [vp]),
     "airgs_timing": (ctypes.c_int, [vp, i32, c_double_p, c_i64_p, c_double_p, c_i64_p]),
+    "airgs_eval_stats": (ctypes.c_int, [vp, i32, c_i64_p]),
     "airgs_render": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), i32, ctypes.POINTER(CameraC), i32,
                                     ctypes.POINTER(ItemC), i32, vp, vp]),
     "airgs_composite_forward": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp]),
@@ -152,6 +153,13 @@ class Engine:
                               ctypes.byref(pl))
         return {"composite_ms": cm.value, "composite_launches": cl.value, "project_ms": pm.value,
                 "project_launches": pl.value}
+
+    def eval_stats(self, enable=-1):
+        """Read (and optionally re-arm/reset) the diagnostic evaluation counters:
+        returns dict(bbox, live, contrib) (pairs of the reference's loop)."""
+        c = (ctypes.c_int64 * 3)()
+        self.call("airgs_eval_stats", int(enable), c)
+        return {"bbox": c[0], "live": c[1], "contrib": c[2]}
 
     @property
     def launches(self) -> int:

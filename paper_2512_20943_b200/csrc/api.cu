@@ -59,6 +59,7 @@ extern "C" int airgs_ctx_destroy(airgs_ctx *ctx) {
     if (!ctx) return AIRGS_OK;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
+    if (ctx->d_stats) cudaFree(ctx->d_stats);
     delete ctx;
     return AIRGS_OK;
 }
@@ -84,6 +85,30 @@ extern "C" int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms
         ctx->timing = enable != 0;
         ctx->composite_ms = ctx->project_ms = 0.0;
         ctx->composite_launches = ctx->project_launches = 0;
+    }
+    return AIRGS_OK;
+}
+
+extern "C" int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts) {
+    if (!ctx) return AIRGS_E_INTERNAL;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return AIRGS_E_CUDA;
+    unsigned long long h[3] = {0, 0, 0};
+    if (ctx->d_stats) {
+        if (cudaDeviceSynchronize() != cudaSuccess ||
+            cudaMemcpy(h, ctx->d_stats, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            ctx->err = "eval stats readback failed";
+            return AIRGS_E_CUDA;
+        }
+    }
+    if (counts)
+        for (int k = 0; k < 3; ++k) counts[k] = (int64_t)h[k];
+    if (enable >= 0) {  // (re)arm or disarm and reset the counters
+        if (enable && !ctx->d_stats && cudaMalloc(&ctx->d_stats, sizeof(h)) != cudaSuccess) {
+            ctx->err = "eval stats allocation failed";
+            return AIRGS_E_CUDA;
+        }
+        if (ctx->d_stats && cudaMemset(ctx->d_stats, 0, sizeof(h)) != cudaSuccess) return AIRGS_E_CUDA;
+        ctx->stats = enable != 0;
     }
     return AIRGS_OK;
 }

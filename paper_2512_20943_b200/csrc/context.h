@@ -27,6 +27,10 @@ struct airgs_ctx {
         int kind;  // 0 composite, 1 project
     };
     std::vector<Pending> pending;
+    // optional evaluation counters (diagnostic compositing kernel): bbox, live
+    // and contributing (pixel, primitive) evaluations, accumulated on device
+    bool stats = false;
+    unsigned long long *d_stats = nullptr;
     std::vector<cudaEvent_t> event_pool;
     cudaEvent_t take_event() {
         if (event_pool.empty()) {
@@ -146,6 +150,7 @@ enum Slot : int {
     kSlotTileItem,
     kSlotSlowTiles,
     kSlotZRange,
+    kSlotTerm,
     kSlotCount
 };
 

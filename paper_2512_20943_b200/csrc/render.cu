@@ -42,7 +42,7 @@ struct ProjArgs {
     const int32_t *tiles_x;    // [nitems]
     Rec *recs;                 // [nitems][stride]
     uint64_t *depth;           // [nitems][stride] orderable depth keys
-    int32_t *ntiles;           // [nitems][stride] tiles touched (0 = not rendered)
+    int32_t *ntiles;           // [nitems][stride] tiles touched (0 = empty bbox, -1 = no tile)
     uint32_t *tile_count;      // [total tiles] primitives per tile
     unsigned long long *zrange;  // [nitems][2] min/max orderable depth key
     unsigned int *flags;
@@ -213,18 +213,22 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
                 rec.hy = det > 0.0 && isfinite(hy) ? (float)hy * 1.0001f : 1e30f;
             }
             int u0, u1, v0, v1;
-            if (rec.x1 > rec.x0 && rec.y1 > rec.y0 && rec_tile_range(rec, u0, u1, v0, v1))
-                nt = (u1 - u0 + 1) * (v1 - v0 + 1);
-            if (nt > 0) {
+            const bool has_bbox = rec.x1 > rec.x0 && rec.y1 > rec.y0;
+            if (has_bbox && rec_tile_range(rec, u0, u1, v0, v1)) nt = (u1 - u0 + 1) * (v1 - v0 + 1);
+            const unsigned long long zk = order_key(tz);
+            if (has_bbox) {  // (bbox-only records are read by the diagnostic counters alone)
                 a.recs[o] = rec;
-                const unsigned long long zk = order_key(tz);
                 a.depth[o] = zk;
+            }
+            if (nt > 0) {
                 zmn = zmx = zk;
                 // per-tile histogram for the binning scan
                 uint32_t *tc = a.tile_count + a.tile_base[item];
                 const int txn = a.tiles_x[item];
                 for (int v = v0; v <= v1; ++v)
                     for (int u = u0; u <= u1; ++u) atomicAdd(tc + v * txn + u, 1u);
+            } else if (has_bbox) {
+                nt = -1;  // evaluated by the reference, but no pixel can pass the weight test
             }
         }
         if (active) a.ntiles[o] = nt;
@@ -375,6 +379,7 @@ struct CompItem {
     double *trans;           // (h,w) or null
     int64_t *usage;          // [n] or null
     double *sse_tiles;       // per (tile, warp) of this item
+    int32_t *term;           // (h,w) terminating primitive or -1 (diagnostic counters only)
     int32_t w, h, tiles_x, clip;
 };
 
@@ -740,11 +745,11 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs 
 // AABB touches its sub-tile (fp32, log2 domain, proven guard band) and builds
 // a per-lane candidate mask; phase B has every lane run its own candidates
 // through the exact fp64 path in depth order (two candidates' exp in flight).
-template <bool USAGE>
+template <bool USAGE, bool STATS>
 __global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
 k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
             const int64_t *__restrict__ tstart, const uint32_t *__restrict__ tcount,
-            const uint64_t *__restrict__ pairs) {
+            const uint64_t *__restrict__ pairs, unsigned long long *__restrict__ stats) {
     __shared__ CompShared sh;
     {
         const unsigned long long *src = &kExpTable[0][0];
@@ -778,6 +783,8 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     const uint64_t *__restrict__ glist = pairs + s0;
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     bool done = !inside;
+    int term_id = -1;          // STATS: primitive whose contribution terminated the pixel
+    unsigned long long ncon = 0;  // STATS: contributions of this pixel
     float thr = log2_inv_eps();  // log2(T/EPS); the guard lives in the staged coefficients
 
     for (int base = 0; base < n_all; base += kTileThreads) {
@@ -864,6 +871,10 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                     cb += wgt * sh.bl[j1];
                     T = T * (1.0 - ap1);
                     if (USAGE) atomicAdd(&sh.cnt[j1], 1);
+                    if (STATS) {
+                        ++ncon;
+                        if (term_id < 0 && kAlphaClamp * T <= kEpsContrib) term_id = (int)sh.gid[j1];
+                    }
                 }
                 if (two) {
                     wgt = ap2 * T;
@@ -872,8 +883,12 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                         cr += wgt * rg.x;
                         cg += wgt * rg.y;
                         cb += wgt * sh.bl[j2];
-                        T = T * (1.0 - ap2);
+                    T = T * (1.0 - ap2);
                         if (USAGE) atomicAdd(&sh.cnt[j2], 1);
+                        if (STATS) {
+                            ++ncon;
+                            if (term_id < 0 && kAlphaClamp * T <= kEpsContrib) term_id = (int)sh.gid[j2];
+                        }
                     }
                 }
             }
@@ -903,6 +918,11 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             it.image[3 * pix + 2] = vb;
         }
         if (it.trans) it.trans[pix] = T;
+        if (STATS) it.term[pix] = term_id;
+    }
+    if (STATS) {
+        ncon = warp_reduce_sum(ncon);
+        if (lane == 0 && ncon) atomicAdd(stats + 2, ncon);
     }
     if (it.target) {
         double se = 0.0;
@@ -914,6 +934,35 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
         }
         se = warp_reduce_sum(se);
         if (lane == 0) it.sse_tiles[(int64_t)tl * kCompWarps + w] = se;  // fixed-order reduce later
+    }
+}
+
+// Diagnostic counters: for every (primitive, pixel of its clipped bbox) pair of
+// the reference's loop, count it (bbox) and whether the pixel was still live
+// there, i.e. the primitive is not behind the pixel's terminating primitive in
+// (depth key, index) order.  One thread per primitive; not on the hot path.
+__global__ void __launch_bounds__(128)
+k_count_pairs(const CompItem *__restrict__ items, const int32_t *__restrict__ ntiles,
+              const int64_t *__restrict__ count, int64_t stride, unsigned long long *__restrict__ stats) {
+    const int s = blockIdx.y;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long nb = 0, nl = 0;
+    if (i < count[s] && ntiles[(int64_t)s * stride + i] != 0) {
+        const CompItem it = items[s];
+        const Rec &r = it.recs[i];
+        const uint64_t key = it.depth[i];
+        for (int y = r.y0; y < r.y1; ++y)
+            for (int x = r.x0; x < r.x1; ++x) {
+                const int t = it.term[(int64_t)y * it.w + x];
+                ++nb;
+                if (t < 0 || key < it.depth[t] || (key == it.depth[t] && i <= t)) ++nl;
+            }
+    }
+    nb = warp_reduce_sum(nb);
+    nl = warp_reduce_sum(nl);
+    if ((threadIdx.x & 31) == 0 && nb) {
+        atomicAdd(stats, nb);
+        atomicAdd(stats + 1, nl);
     }
 }
 
@@ -1001,7 +1050,7 @@ k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__re
     recs[i] = r;
     int nt = 0, u0, u1, v0, v1;
     if (r.x1 > r.x0 && r.y1 > r.y0 && rec_tile_range(r, u0, u1, v0, v1)) nt = (u1 - u0 + 1) * (v1 - v0 + 1);
-    ntiles[i] = nt;
+    ntiles[i] = nt > 0 ? nt : (r.x1 > r.x0 && r.y1 > r.y0 ? -1 : 0);
     depth[i] = (uint64_t)i;  // the input order is the depth order
     if (nt > 0)
         for (int v = v0; v <= v1; ++v)
@@ -1165,6 +1214,18 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     std::vector<CompItem> ci(nitems);
     std::vector<uint8_t> has_t(nitems);
     bool any_usage = false, any_target = false;
+    const bool stats_on = ctx->stats && ctx->d_stats;
+    int32_t *term = nullptr;
+    int64_t maxcount = 0;
+    if (stats_on) {
+        int64_t px = 0;
+        for (const ItemHost &h : items) {
+            px += (int64_t)h.w * h.h;
+            maxcount = std::max(maxcount, h.count);
+        }
+        term = ctx->scratch_t<int32_t>(kSlotTerm, (size_t)std::max<int64_t>(px, 1));
+    }
+    int64_t term_off = 0;
     for (int s = 0; s < nitems; ++s) {
         const ItemHost &h = items[s];
         CompItem &c = ci[s];
@@ -1175,6 +1236,8 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         c.trans = h.trans;
         c.usage = h.usage;
         c.sse_tiles = sse_tiles + L.tile_base[s] * kCompWarps;
+        c.term = term ? term + term_off : nullptr;
+        term_off += (int64_t)h.w * h.h;
         c.w = h.w;
         c.h = h.h;
         c.tiles_x = h.tiles_x;
@@ -1189,12 +1252,28 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     h2d_small(ctx, d_has, has_t.data(), nitems, st);
     cudaEvent_t t_comp = Tt > 0 ? ctx->time_begin(st) : nullptr;
     if (Tt > 0) {
-        if (any_usage)
-            k_composite<true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
-                                                                               tile_count, pairs);
-        else
-            k_composite<false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
-                                                                                tile_count, pairs);
+        unsigned long long *cs = ctx->d_stats;
+        if (stats_on) {
+            if (any_usage)
+                k_composite<true, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
+                                                                               tile_count, pairs, cs);
+            else
+                k_composite<false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
+                                                                                tile_count, pairs, cs);
+        } else if (any_usage) {
+            k_composite<true, false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
+                                                                            tile_count, pairs, cs);
+        } else {
+            k_composite<false, false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
+                                                                             tile_count, pairs, cs);
+        }
+        ++NL;
+        check_launch();
+    }
+    if (stats_on && maxcount > 0) {
+        // bbox / live pair counts of the reference's Gaussian-major loop
+        k_count_pairs<<<dim3((unsigned)ceil_div(maxcount, 128), nitems), 128, 0, st>>>(d_ci, ntiles, L.d_count,
+                                                                                       L.stride, ctx->d_stats);
         ++NL;
         check_launch();
     }

@@ -226,3 +226,31 @@ def test_depth_ties_resolved_by_index(rng):
     ri, ru = orc.render_with_usage(p, [cam])
     np.testing.assert_array_equal(usage.counts, ru)
     assert np.max(np.abs(imgs[0].pixels - ri[0])) <= PIX_TOL
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_eval_stats_match_reference_loop_counts(cfg):
+    """The diagnostic counters behind bench.py's algorithmic-work roofline:
+    bbox / live / contributing pair counts equal the reference loop's, per
+    view, exactly (C1: 4 views; C2: one full view)."""
+    from dataclasses import replace
+
+    from paper_2512_20943_b200 import _lib, synth
+    from paper_2512_20943_b200.model import GaussianFrame
+    from paper_2512_20943_b200.rasterizer import render_views
+
+    c = synth.CONFIGS[cfg]
+    if cfg == "C2":
+        c = replace(c, views=1)
+    p = synth.Sequence(c, seed=7, event_every=0).frame(0)
+    cams = synth.cameras(c)
+    eng = _lib.engine()
+    fr = GaussianFrame(params=p)
+    eng.eval_stats(1)
+    try:
+        for v, cam in enumerate(cams):
+            render_views([fr], cams, [(0, v)], want_images=True, usage_frames=[0])
+            got = eng.eval_stats(1)  # read + reset
+            assert (got["bbox"], got["live"], got["contrib"]) == orc.eval_counts(p, cam)
+    finally:
+        eng.eval_stats(0)
