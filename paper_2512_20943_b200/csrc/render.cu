@@ -387,23 +387,29 @@ constexpr double kLog2e = 1.4426950408889634;
 // log2(1 / fl(1/255)) rounded to fp32 (threshold offset in the log2 domain)
 __device__ __forceinline__ float log2_inv_eps() { return 7.99435343685886f; }
 
+// fp64 constants of the exact path, read as constant-bank operands (no
+// per-iteration immediate materialisation)
+__constant__ double kCompC[8] = {kExpInvLn2N, kExpNegLn2HiN, kExpNegLn2LoN, 1.0 / 6.0,
+                                 1.0 / 120.0, 1.0 / 24.0, kAlphaClamp, kEpsContrib};
+
 // exp(x) for the compositing weights: 256-entry table of 2^(i/256) in shared
 // memory + degree-5 polynomial on |r| <= ln2/512 (error < 0.51 ulp; agrees
 // with glibc's exp, which the reference's Cython kernel calls, on >99.9% of
 // inputs and never differs by more than 1 ulp -- tools/gen_exp_table.py).
+
 __device__ __forceinline__ double exp_tab(double x, const double2 *__restrict__ tab) {
     const double shift = 6755399441055744.0;  // 1.5 * 2^52
-    const double z = x * kExpInvLn2N;
+    const double z = x * kCompC[0];
     double kd = z + shift;
     const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
     kd = kd - shift;
-    double r = fma(kd, kExpNegLn2HiN, x);
-    r = fma(kd, kExpNegLn2LoN, r);
+    double r = fma(kd, kCompC[1], x);
+    r = fma(kd, kCompC[2], r);
     const double2 t = tab[ki & (kExpN - 1)];
     const unsigned long long sb = (unsigned long long)__double_as_longlong(t.y) + (ki << (52 - kExpBits));
     const double r2 = r * r;
-    const double p1 = fma(r, 1.0 / 6.0, 0.5);
-    const double p2 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    const double p1 = fma(r, kCompC[3], 0.5);
+    const double p2 = fma(r, kCompC[4], kCompC[5]);
     double tmp = t.x + r;
     tmp = fma(r2, p1, tmp);
     tmp = fma(r2 * r2, p2, tmp);
@@ -411,22 +417,37 @@ __device__ __forceinline__ double exp_tab(double x, const double2 *__restrict__ 
     return fma(sc, tmp, sc);
 }
 
+constexpr int kCompWarps = kTileThreads / 32;
+constexpr int kBatch = 128;             // primitives staged per CTA batch
+constexpr int kWarpList = kBatch + 8;   // per-warp compacted list, padded to a multiple of 8
+
+// Per CTA: one staged batch of the tile's depth-ordered list (fp64 fields for
+// the exact path, indexed by staged position) and, per warp, the compacted
+// sub-list of the batch entries that may touch the warp's 8x4 sub-tile, with
+// the fp32 fast-reject fields pair-interleaved for packed f32x2 arithmetic.
 struct CompShared {
-    float4 f0[kTileThreads];     // mx-ox, my-oy (tile origin), 0.5*log2e*a, log2e*b  (fp32, log2 domain)
-    float2 f1[kTileThreads];     // 0.5*log2e*c, log2(alpha)
-    double2 m[kTileThreads];     // mx, my
-    double2 hab[kTileThreads];   // 0.5*a, b
-    double2 hcal[kTileThreads];  // 0.5*c, alpha
-    double2 rg[kTileThreads];    // colour r, g
-    double bl[kTileThreads];     // colour b
-    uint32_t gid[kTileThreads];
-    int32_t cnt[kTileThreads];
-    uint8_t wmask[kTileThreads];  // bit w: may touch warp w's 8x4 sub-tile
+    double2 m[kBatch];     // mx, my
+    double2 hab[kBatch];   // 0.5*a, b
+    double2 hcal[kBatch];  // 0.5*c, alpha
+    double2 rg[kBatch];    // colour r, g
+    double bl[kBatch];     // colour b
+    float4 f0[kBatch];     // -(mx-ox), -(my-oy), A, B   (fp32, log2 domain, staged order)
+    float2 f1[kBatch];     // C, -L
+    uint32_t gid[kBatch];
+    int32_t cnt[kBatch];
+    uint8_t wmask[kBatch];  // bit w: may touch warp w's 8x4 sub-tile
+    // per warp, entry pairs (a, b): {-mx_a,-mx_b,-my_a,-my_b}, {A_a,A_b,B_a,B_b}, {C_a,C_b,-L_a,-L_b}
+    float4 pl[kCompWarps][kWarpList / 2][3];
+    uint8_t sidx[kCompWarps][kWarpList];  // compacted position -> staged position
     double2 exptab[kExpN];
 };
 
-constexpr int kCompWarps = kTileThreads / 32;
 constexpr int kSortCap = 2048;  // tile lists up to this length are sorted in shared memory
+#ifndef COMP_CHUNK
+#define COMP_CHUNK 16
+#endif
+constexpr int kChunk = COMP_CHUNK;  // compacted entries per phase A / phase B round (T refreshed after each)
+static_assert(kChunk % 8 == 0 && kChunk <= 32, "chunk");
 #ifndef COMP_MIN_BLOCKS
 #define COMP_MIN_BLOCKS 4
 #endif
@@ -441,7 +462,7 @@ __device__ __forceinline__ double alpha_at(const CompShared &sh, int j, double p
     const double dy = pyd - mm.y;
     const double ee = (ab.x * dx * dx + ca.x * dy * dy) + ab.y * dx * dy;
     const double ap = ca.y * exp_tab(-ee, sh.exptab);
-    return ap > kAlphaClamp ? kAlphaClamp : ap;
+    return ap > kCompC[6] ? kCompC[6] : ap;
 }
 
 // ---- tile-list sort: ascending (depth key, primitive index) -----------------
@@ -740,11 +761,13 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs 
 
 // One CTA = one 16x16 tile, one pixel per thread; warps are 8x4 sub-tiles.
 // The tile's primitive list arrives in depth order (k_sort_tiles_*).
-// Per batch of 256 primitives (staged once per CTA), each warp walks
-// 32-entry chunks: phase A tests only primitives whose threshold-ellipse
-// AABB touches its sub-tile (fp32, log2 domain, proven guard band) and builds
-// a per-lane candidate mask; phase B has every lane run its own candidates
-// through the exact fp64 path in depth order (two candidates' exp in flight).
+// Per batch of kBatch primitives (staged once per CTA), every warp compacts
+// the entries whose threshold-ellipse AABB touches its sub-tile into its own
+// list, then walks that list in 32-entry chunks: phase A tests the lane's
+// pixel against two entries per packed f32x2 instruction sequence (fp32, log2
+// domain, proven guard band) and builds a per-lane candidate mask; phase B has
+// every lane run its own candidates through the exact fp64 path in depth
+// order (two candidates' exp in flight).
 template <bool USAGE, bool STATS>
 __global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
 k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
@@ -774,9 +797,11 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     const int ox = tx * kTile, oy = ty * kTile;
     const int px = ox + lx, py = oy + ly;
     const bool inside = px < img_w && py < img_h;
-    const float pxl = (float)lx + 0.5f, pyl = (float)ly + 0.5f;
+    const float2 px2 = make_float2((float)lx + 0.5f, (float)lx + 0.5f);
+    const float2 py2 = make_float2((float)ly + 0.5f, (float)ly + 0.5f);
     const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
     const Rec *__restrict__ recs = itp->recs;
+    const unsigned lt_mask = (1u << lane) - 1u;
 
     const int64_t s0 = tstart[g];
     const int n_all = (int)tcount[g];
@@ -787,8 +812,8 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     unsigned long long ncon = 0;  // STATS: contributions of this pixel
     float thr = log2_inv_eps();  // log2(T/EPS); the guard lives in the staged coefficients
 
-    for (int base = 0; base < n_all; base += kTileThreads) {
-        const int nb = min(kTileThreads, n_all - base);
+    for (int base = 0; base < n_all; base += kBatch) {
+        const int nb = min(kBatch, n_all - base);
         __syncthreads();
         if ((int)threadIdx.x < nb) {
             const int t = threadIdx.x;
@@ -798,10 +823,10 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             sh.gid[t] = gi;
             // fast-reject coefficients: log2e * (a/2, b, c/2) with a/2, c/2 scaled by (1 - kappa) so
             // e' = e - kappa*s absorbs the s-proportional guard; the constant guard
-            // is folded into log2(alpha) (fp32 fast reject)
+            // is folded into L = log2(alpha) + 6e-5 (fp32 fast reject)
             const double kap = 1.0 - 2e-5;
-            sh.f0[t] = make_float4(mxl, myl, (float)(0.5 * kLog2e * kap * r.ca), (float)(kLog2e * r.cb));
-            sh.f1[t] = make_float2((float)(0.5 * kLog2e * kap * r.cc), __log2f((float)r.al) + 6e-5f);
+            sh.f0[t] = make_float4(-mxl, -myl, (float)(0.5 * kLog2e * kap * r.ca), (float)(kLog2e * r.cb));
+            sh.f1[t] = make_float2((float)(0.5 * kLog2e * kap * r.cc), -(__log2f((float)r.al) + 6e-5f));
             sh.m[t] = make_double2(r.mx, r.my);
             sh.hab[t] = make_double2(0.5 * r.ca, r.cb);
             sh.hcal[t] = make_double2(0.5 * r.cc, r.al);
@@ -825,46 +850,78 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             if (USAGE) sh.cnt[t] = 0;
         }
         __syncthreads();
-        for (int c = 0; c < nb; c += 32) {
+        // compaction: this warp's entries of the batch, in depth order, pair-interleaved
+        int ncomp = 0;  // warp-uniform
+        if (!__all_sync(0xffffffffu, done)) {
+            for (int c0 = 0; c0 < nb; c0 += 32) {
+                const int j = c0 + lane;
+                const bool hit = j < nb && ((sh.wmask[j] >> w) & 1u);
+                const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                if (hit) {
+                    const int p = ncomp + __popc(bal & lt_mask);
+                    const float4 a0 = sh.f0[j];
+                    const float2 a1 = sh.f1[j];
+                    float *d = reinterpret_cast<float *>(&sh.pl[w][p >> 1][0]) + (p & 1);
+                    d[0] = a0.x;
+                    d[2] = a0.y;
+                    d[4] = a0.z;
+                    d[6] = a0.w;
+                    d[8] = a1.x;
+                    d[10] = a1.y;
+                    sh.sidx[w][p] = (uint8_t)j;
+                }
+                ncomp += __popc(bal);
+            }
+            // pad to a multiple of 8 with entries that always reject (-L = +inf)
+            if (lane < ((8 - (ncomp & 7)) & 7)) {
+                const int p = ncomp + lane;
+                float *d = reinterpret_cast<float *>(&sh.pl[w][p >> 1][0]) + (p & 1);
+                d[0] = 0.0f;
+                d[2] = 0.0f;
+                d[4] = 0.0f;
+                d[6] = 0.0f;
+                d[8] = 0.0f;
+                d[10] = __int_as_float(0x7f800000);
+            }
+            __syncwarp();
+        }
+        for (int c = 0; c < ncomp; c += kChunk) {
             if (__all_sync(0xffffffffu, done)) break;
-            const int jj = c + lane;
-            unsigned m = __ballot_sync(0xffffffffu, jj < nb && ((sh.wmask[jj] >> w) & 1u));
-            // phase A: fp32 candidate bits (T as of the chunk start; a larger T only
-            // admits more candidates, never fewer)
+            // phase A: fp32 candidate bits, two entries per f32x2 op (T as of the
+            // chunk start; a larger T only admits more candidates, never fewer)
             unsigned word = 0;
-            // two primitives per iteration: both loads issued before the math
-            while (m) {
-                const int k1 = __ffs(m) - 1;
-                m &= m - 1;
-                const int k2 = m ? __ffs(m) - 1 : k1;
-                m &= m - 1;
-                const float4 a0 = sh.f0[c + k1];
-                const float2 a1 = sh.f1[c + k1];
-                const float4 b0 = sh.f0[c + k2];
-                const float2 b1 = sh.f1[c + k2];
-                const float dxa = pxl - a0.x, dya = pyl - a0.y;
-                const float dxb = pxl - b0.x, dyb = pyl - b0.y;
-                // e' = dx*(A dx + B dy) + C dy^2   (log2 units, guard-scaled)
-                const float ua = fmaf(a0.z, dxa, a0.w * dya);
-                const float ub = fmaf(b0.z, dxb, b0.w * dyb);
-                const float ea = fmaf(ua, dxa, (a1.x * dya) * dya);
-                const float eb = fmaf(ub, dxb, (b1.x * dyb) * dyb);
-                // reject iff e > ln(al) + ln(T/EPS) + guard (guard proof: DESIGN.md)
-                word |= (unsigned)(ea <= a1.y + thr) << k1;
-                word |= (unsigned)(eb <= b1.y + thr) << k2;
+            const float4 *pl = &sh.pl[w][c >> 1][0];
+#pragma unroll
+            for (int gq = 0; gq < kChunk / 8; ++gq) {
+                if (c + 8 * gq >= ncomp) break;  // warp-uniform; the list is padded to 8
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int pr = 4 * gq + q;
+                    const float4 p0 = pl[3 * pr], p1 = pl[3 * pr + 1], p2 = pl[3 * pr + 2];
+                    const float2 dx = __fadd2_rn(px2, make_float2(p0.x, p0.y));
+                    const float2 dy = __fadd2_rn(py2, make_float2(p0.z, p0.w));
+                    // e' - L = dx*(A dx + B dy) + (C dy^2 - L)   (log2 units, guard-scaled)
+                    const float2 u = __ffma2_rn(make_float2(p1.x, p1.y), dx, __fmul2_rn(make_float2(p1.z, p1.w), dy));
+                    const float2 qv = __ffma2_rn(__fmul2_rn(make_float2(p2.x, p2.y), dy), dy, make_float2(p2.z, p2.w));
+                    const float2 e = __ffma2_rn(u, dx, qv);
+                    // reject iff e' - L > log2(T/EPS) (guard proof: DESIGN.md)
+                    word |= (e.x <= thr ? 1u : 0u) << (2 * pr);
+                    word |= (e.y <= thr ? 1u : 0u) << (2 * pr + 1);
+                }
             }
             if (done) word = 0;
             // phase B: each lane runs its own candidates in depth order (exact fp64)
+            const uint8_t *sid = &sh.sidx[w][c];
             while (word) {
-                const int j1 = c + __ffs(word) - 1;
+                const int j1 = sid[__ffs(word) - 1];
                 word &= word - 1;
                 const bool two = word != 0;
-                const int j2 = two ? c + __ffs(word) - 1 : j1;
+                const int j2 = two ? sid[__ffs(word) - 1] : j1;
                 word &= word - 1;
                 const double ap1 = alpha_at(sh, j1, pxd, pyd);
                 const double ap2 = alpha_at(sh, j2, pxd, pyd);
                 double wgt = ap1 * T;
-                if (wgt > kEpsContrib) {
+                if (wgt > kCompC[7]) {
                     const double2 rg = sh.rg[j1];
                     cr += wgt * rg.x;
                     cg += wgt * rg.y;
@@ -878,12 +935,12 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                 }
                 if (two) {
                     wgt = ap2 * T;
-                    if (wgt > kEpsContrib) {
+                    if (wgt > kCompC[7]) {
                         const double2 rg = sh.rg[j2];
                         cr += wgt * rg.x;
                         cg += wgt * rg.y;
                         cb += wgt * sh.bl[j2];
-                    T = T * (1.0 - ap2);
+                        T = T * (1.0 - ap2);
                         if (USAGE) atomicAdd(&sh.cnt[j2], 1);
                         if (STATS) {
                             ++ncon;
