@@ -624,8 +624,8 @@ __device__ __noinline__ void sort_tile_list(uint64_t *k, uint32_t *v, int npad) 
 // One warp per tile, entries e = lane + 32 r held in registers (R per lane);
 // the full bitonic network runs with in-lane swaps for strides >= 32 and
 // shuffles below -- no shared memory, no barriers.
-template <int R>
-__device__ __forceinline__ void warp_reg_bitonic(uint64_t (&k)[R]) {
+template <int R, typename K>
+__device__ __forceinline__ void warp_reg_bitonic(K (&k)[R]) {
     const int lane = threadIdx.x & 31;
     constexpr int N = 32 * R;
 #pragma unroll
@@ -639,7 +639,7 @@ __device__ __forceinline__ void warp_reg_bitonic(uint64_t (&k)[R]) {
                     if (r & rs) continue;
                     const int r2 = r | rs;
                     const bool asc = ((lane + 32 * r) & size) == 0;
-                    const uint64_t a = k[r], b = k[r2];
+                    const K a = k[r], b = k[r2];
                     const bool sw = (a > b) == asc;
                     k[r] = sw ? b : a;
                     k[r2] = sw ? a : b;
@@ -648,7 +648,7 @@ __device__ __forceinline__ void warp_reg_bitonic(uint64_t (&k)[R]) {
                 const bool lower = (lane & st) == 0;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const uint64_t p = __shfl_xor_sync(0xffffffffu, k[r], st);
+                    const K p = __shfl_xor_sync(0xffffffffu, k[r], st);
                     const bool asc = ((lane + 32 * r) & size) == 0;
                     k[r] = (lower == asc) ? min(k[r], p) : max(k[r], p);
                 }
@@ -670,35 +670,62 @@ struct TileSortArgs {
     int64_t Tt;
 };
 
+// Sort one tile list (n <= 32 R) in registers on 32-bit keys: the entries'
+// view-level depth buckets are re-bucketed to 22 bits over the tile's own
+// bucket range, with the entry's list position in the low 10 bits.  Distinct
+// 22-bit buckets are strictly depth ordered; adjacent equal buckets send the
+// tile to the exact (64-bit depth key, index) block sort.
 template <int R>
 __device__ __forceinline__ void warp_sort_tile(const TileSortArgs &a, int64_t g, int n) {
     const int lane = threadIdx.x & 31;
     uint64_t *lst = a.pairs + a.tstart[g];
-    uint64_t key[R];
+    uint32_t key[R];
+    uint32_t bmin = 0xffffffffu, bmax = 0u;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = lane + 32 * r;
-        key[r] = e < n ? lst[e] : ~0ull;
+        const uint32_t b = e < n ? (uint32_t)(lst[e] >> 32) : 0u;
+        key[r] = b;
+        if (e < n) {
+            bmin = min(bmin, b);
+            bmax = max(bmax, b);
+        }
+    }
+    bmin = __reduce_min_sync(0xffffffffu, bmin);
+    bmax = __reduce_max_sync(0xffffffffu, bmax);
+    const uint32_t span = bmax - bmin;
+    const int sh = max(0, (32 - __clz((int)span)) - 22);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = lane + 32 * r;
+        key[r] = e < n ? (((key[r] - bmin) >> sh) << 10) | (uint32_t)e : 0xffffffffu;
     }
     warp_reg_bitonic<R>(key);
-    // adjacent entries in one 32-bit depth bucket need the exact comparison
+    // adjacent entries in one 22-bit bucket need the exact comparison
     bool clash = false;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = lane + 32 * r;
-        const uint64_t nxt_same = __shfl_down_sync(0xffffffffu, key[r], 1);
-        const uint64_t nxt_row = __shfl_sync(0xffffffffu, key[r + 1 < R ? r + 1 : r], 0);
-        const uint64_t nx = lane < 31 ? nxt_same : nxt_row;
-        if (e + 1 < n) clash |= (key[r] >> 32) == (nx >> 32);
+        const uint32_t nxt_same = __shfl_down_sync(0xffffffffu, key[r], 1);
+        const uint32_t nxt_row = __shfl_sync(0xffffffffu, key[r + 1 < R ? r + 1 : r], 0);
+        const uint32_t nx = lane < 31 ? nxt_same : nxt_row;
+        if (e + 1 < n) clash |= (key[r] >> 10) == (nx >> 10);
     }
     if (__any_sync(0xffffffffu, clash)) {
         if (lane == 0) a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
         return;
     }
+    uint64_t out[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = lane + 32 * r;
-        if (e < n) lst[e] = key[r];
+        out[r] = e < n ? lst[key[r] & 1023u] : 0ull;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e = lane + 32 * r;
+        if (e < n) lst[e] = out[r];
     }
 }
 
