@@ -52,6 +52,7 @@ enum DevFlag : unsigned int {
     kFlagVarintLong = 4u,     // varint longer than 10 bytes
     kFlagIndexRange = 8u,     // delta index >= base_count
     kFlagQuantOverflow = 16u, // |q| > 2^31-1
+    kFlagBucketOverflow = 32u, // a tile received more primitives than its bucket holds
 };
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -30,6 +30,7 @@ struct airgs_ctx {
     // optional evaluation counters (diagnostic compositing kernel): bbox, live
     // and contributing (pixel, primitive) evaluations, accumulated on device
     bool stats = false;
+    uint32_t bucket_cap = 512;  // tile bucket capacity (doubled after an overflow, up to the sort cap)
     unsigned long long *d_stats = nullptr;
     std::vector<cudaEvent_t> event_pool;
     cudaEvent_t take_event() {

@@ -43,8 +43,6 @@ struct ProjArgs {
     Rec *recs;                 // [nitems][stride]
     uint64_t *depth;           // [nitems][stride] orderable depth keys
     int32_t *ntiles;           // [nitems][stride] tiles touched (0 = empty bbox, -1 = no tile)
-    uint32_t *tile_count;      // [total tiles] primitives per tile
-    unsigned long long *zrange;  // [nitems][2] min/max orderable depth key
     unsigned int *flags;
     int64_t stride;
 };
@@ -88,6 +86,9 @@ __device__ __forceinline__ bool rec_tile_range(const Rec &r, int &u0, int &u1, i
 
 constexpr int kProjThreads = 128;
 
+// WMAX = 17 when every frame of the launch is SH degree 0 (fewer live registers),
+// 26 otherwise (handles both widths).
+template <int WMAX>
 __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
     const int f = blockIdx.y;
     const airgs_frame fr = a.frames[f];
@@ -99,13 +100,13 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
     const int W = fr.width;
     double p[26];
 #pragma unroll
-    for (int c = 0; c < 26; ++c) p[c] = (active && c < W) ? fr.params[i + c * ld] : 0.0;
+    for (int c = 0; c < 26; ++c) p[c] = (active && c < W && c < WMAX) ? fr.params[i + c * ld] : 0.0;
 
     // _activate (ss/rasterizer.py:100-110)
     const double qn = sqrt(((p[3] * p[3] + p[4] * p[4]) + p[5] * p[5]) + p[6] * p[6]);
     bool finite = true;
 #pragma unroll
-    for (int c = 0; c < 26; ++c) finite &= isfinite(p[c]);
+    for (int c = 0; c < WMAX; ++c) finite &= isfinite(p[c]);
     const bool valid = active && qn != 0.0 && finite;
     if (active && !valid) atomicOr(a.flags, (unsigned)kFlagInvalidParam);
     const double w_ = p[3] / qn, x_ = p[4] / qn, y_ = p[5] / qn, z_ = p[6] / qn;
@@ -138,14 +139,11 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
         col0[1] = sigmoid_ref(p[12] + kShC0 * p[15]);
         col0[2] = sigmoid_ref(p[13] + kShC0 * p[16]);
     }
-    __shared__ unsigned long long red_mn[kProjThreads / 32], red_mx[kProjThreads / 32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int it = ib; it < ie; ++it) {
         const int item = a.frame_items[it];
         const int64_t o = (int64_t)item * a.stride + i;
         const airgs_camera &cam = a.cams[a.item_cam[item]];
         const double *R = cam.rot;
-        unsigned long long zmn = ~0ull, zmx = 0ull;
         int nt = 0;
         double tz = 0.0;
         if (live) tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
@@ -190,7 +188,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
             rec.x1 = (int32_t)fmin(fmax(ceil(mx + rad) + 1.0, 0.0), Wd);
             rec.y0 = (int32_t)fmin(fmax(floor(my - rad), 0.0), Hd);
             rec.y1 = (int32_t)fmin(fmax(ceil(my + rad) + 1.0, 0.0), Hd);
-            if (W == 26) {  // colour (ss/rasterizer.py:183-198), view dependent
+            if (WMAX == 26 && W == 26) {  // colour (ss/rasterizer.py:183-198), view dependent
                 const double d0 = p[0] - cam.center[0], d1 = p[1] - cam.center[1], d2 = p[2] - cam.center[2];
                 double dn = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
                 if (dn == 0.0) dn = 1.0;
@@ -220,46 +218,88 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
                 a.recs[o] = rec;
                 a.depth[o] = zk;
             }
-            if (nt > 0) {
-                zmn = zmx = zk;
-                // per-tile histogram for the binning scan
-                uint32_t *tc = a.tile_count + a.tile_base[item];
-                const int txn = a.tiles_x[item];
-                for (int v = v0; v <= v1; ++v)
-                    for (int u = u0; u <= u1; ++u) atomicAdd(tc + v * txn + u, 1u);
-            } else if (has_bbox) {
-                nt = -1;  // evaluated by the reference, but no pixel can pass the weight test
-            }
+            if (nt <= 0 && has_bbox) nt = -1;  // evaluated by the reference, but no pixel can pass the weight test
         }
         if (active) a.ntiles[o] = nt;
-        // block min/max of the depth keys -> one atomic pair per block and item
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            zmn = min(zmn, __shfl_xor_sync(0xffffffffu, zmn, d));
-            zmx = max(zmx, __shfl_xor_sync(0xffffffffu, zmx, d));
-        }
-        if (lane == 0) {
-            red_mn[wid] = zmn;
-            red_mx[wid] = zmx;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned long long mn = red_mn[0], mx = red_mx[0];
-            for (int k = 1; k < kProjThreads / 32; ++k) {
-                mn = min(mn, red_mn[k]);
-                mx = max(mx, red_mx[k]);
-            }
-            if (mx) {
-                atomicMin(a.zrange + 2 * item, mn);
-                atomicMax(a.zrange + 2 * item + 1, mx);
-            }
-        }
-        __syncthreads();
     }
 }
 
 // ---------------------------------------------------------------------------
 // binning
+
+// Binning straight into fixed-capacity tile buckets: the tile counter's old
+// value is the entry's slot (any order; k_sort_tiles_* restores depth order).
+// Entry = fp32 depth bits (monotone for z > 0; or the input index for the
+// composite seam) << 32 | primitive id.  Warp-cooperative: the warp's
+// (primitive, tile) pairs are spread over its lanes so that 32 counter
+// atomics are in flight per round instead of one serial chain per thread.
+struct BinArgs {
+    const Rec *recs;
+    const uint64_t *depth;
+    const int32_t *ntiles;
+    const int64_t *tile_base;
+    const int32_t *tiles_x;
+    const int64_t *count;
+    uint32_t *tile_count;
+    uint64_t *bucket;
+    uint32_t cap;
+    unsigned int *flags;
+    int64_t stride;
+    int index_order;
+};
+
+__global__ void __launch_bounds__(256) k_bin(BinArgs a) {
+    const int s = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t o = (int64_t)s * a.stride + i;
+    const int nt = i < a.count[s] ? max(a.ntiles[o], 0) : 0;
+    if (__all_sync(0xffffffffu, nt == 0)) return;
+    int u0 = 0, u1 = 0, v0 = 0, v1 = 0;
+    uint64_t entry = 0;
+    if (nt > 0) {
+        const Rec &r = a.recs[o];
+        rec_tile_range(r, u0, u1, v0, v1);
+        const uint64_t zk = a.depth[o];
+        const double z = __longlong_as_double((long long)(zk & 0x7fffffffffffffffull));
+        const uint32_t hi = a.index_order ? (uint32_t)zk : __float_as_uint((float)z);
+        entry = ((uint64_t)hi << 32) | (uint32_t)i;
+    }
+    const int nu = u1 - u0 + 1;
+    int incl = nt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+    }
+    const int excl = incl - nt;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int64_t tb = a.tile_base[s];
+    const int txn = a.tiles_x[s];
+    for (int k0 = 0; k0 < total; k0 += 32) {
+        const int k = k0 + lane;
+        // owner lane: the last lane whose first pair index is <= k
+        int L = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int e = __shfl_sync(0xffffffffu, excl, L + step);
+            if (e <= k) L += step;
+        }
+        const int j = k - __shfl_sync(0xffffffffu, excl, L);
+        const int ou0 = __shfl_sync(0xffffffffu, u0, L), onu = __shfl_sync(0xffffffffu, nu, L);
+        const int ov0 = __shfl_sync(0xffffffffu, v0, L);
+        const uint64_t oent = __shfl_sync(0xffffffffu, entry, L);
+        if (k < total) {
+            const int dv = j / onu;
+            const int64_t g = tb + (int64_t)(ov0 + dv) * txn + ou0 + (j - dv * onu);
+            const uint32_t pos = atomicAdd(a.tile_count + g, 1u);
+            if (pos < a.cap) a.bucket[g * a.cap + pos] = oent;
+            else atomicOr(a.flags, (unsigned)kFlagBucketOverflow);
+        }
+    }
+}
+
+
 
 struct TileScanIn {
     const uint32_t *cnt;
@@ -269,33 +309,28 @@ struct TileScanOut {
     int64_t *start;
     uint32_t *big_list;  // tiles whose list exceeds the shared-memory sort
     unsigned int *big_n;
+    unsigned int *vmax;  // longest list above 256 (bucket capacity adaptation)
     uint32_t cap;
     __device__ void operator()(int, int64_t g, int64_t ex, int64_t v) const {
         start[g] = ex;
         if (v > cap) big_list[atomicAdd(big_n, 1u)] = (uint32_t)g;
+        if (v > 256) atomicMax(vmax, (unsigned int)v);
     }
 };
 
 struct EmitArgs {
     const Rec *recs;
     const uint64_t *depth;
-    const unsigned long long *zrange;
     const int32_t *ntiles;
     const int64_t *tile_base;
     const int32_t *tiles_x;
     const int64_t *count;      // primitives per item
     const int64_t *tstart;     // global tile -> first slot
     uint32_t *cursor;          // global tile -> fill cursor
-    uint64_t *pairs;           // (view-level depth bucket << 32) | primitive id
+    uint64_t *ids;             // list entries (fp32 depth bits << 32 | id) in tile ranges
     int64_t stride;
+    int index_order;           // seam: the depth keys are the input order itself
 };
-
-// 32-bit depth bucket of an orderable key within the view's depth range
-__device__ __forceinline__ uint32_t depth_bucket(uint64_t zk, const unsigned long long *zr) {
-    const unsigned long long span = zr[1] - zr[0];
-    const int sh = span >> 32 ? 64 - __clzll((long long)span) - 32 : 0;
-    return (uint32_t)((zk - zr[0]) >> sh);
-}
 
 __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     const int s = blockIdx.y;
@@ -305,14 +340,17 @@ __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     if (a.ntiles[o] <= 0) return;
     const Rec &r = a.recs[o];
     const int64_t tb = a.tile_base[s];
+    // fp32 depth from the orderable key (z > 0: key = bits | sign bit)
+    const double z = __longlong_as_double((long long)(a.depth[o] & 0x7fffffffffffffffull));
+    const uint32_t hi = a.index_order ? (uint32_t)a.depth[o] : __float_as_uint((float)z);
+    const uint64_t entry = ((uint64_t)hi << 32) | (uint32_t)i;
     const int txn = a.tiles_x[s];
-    const uint64_t key = ((uint64_t)depth_bucket(a.depth[o], a.zrange + 2 * s) << 32) | (uint32_t)i;
     int u0, u1, v0, v1;
     rec_tile_range(r, u0, u1, v0, v1);
     for (int v = v0; v <= v1; ++v)
         for (int u = u0; u <= u1; ++u) {
             const int64_t g = tb + v * txn + u;
-            a.pairs[a.tstart[g] + atomicAdd(a.cursor + g, 1u)] = key;
+            a.ids[a.tstart[g] + atomicAdd(a.cursor + g, 1u)] = entry;
         }
 }
 
@@ -323,7 +361,7 @@ struct BigArgs {
     const uint32_t *tcount;
     const int32_t *tile_item;   // global tile -> item
     const uint64_t *depth;      // [nitems][stride]
-    const uint64_t *pairs;
+    uint64_t *ids;
     int64_t stride;
     const int64_t *seg_begin;   // per big tile: offset in the gathered arrays
     uint64_t *keys;
@@ -336,7 +374,7 @@ __global__ void __launch_bounds__(256) k_big_gather(BigArgs a) {
     const int64_t n = a.tcount[g], s0 = a.tstart[g], d0 = a.seg_begin[b];
     const int64_t item = a.tile_item[g];
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t id = (uint32_t)a.pairs[s0 + k];
+        const uint32_t id = (uint32_t)a.ids[s0 + k];
         a.vals[d0 + k] = id;
         a.keys[d0 + k] = a.depth[item * a.stride + id];
     }
@@ -347,7 +385,7 @@ __global__ void __launch_bounds__(256) k_big_scatter(BigArgs a, const uint32_t *
     const uint32_t g = a.big_list[b];
     const int64_t n = a.tcount[g], s0 = a.tstart[g], d0 = a.seg_begin[b];
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-        const_cast<uint64_t *>(a.pairs)[s0 + k] = sorted_vals[d0 + k];
+        a.ids[s0 + k] = sorted_vals[d0 + k];
 }
 
 __global__ void __launch_bounds__(256) k_ids_as_keys(const uint32_t *__restrict__ vals, uint64_t *__restrict__ keys,
@@ -657,28 +695,45 @@ __device__ __forceinline__ void warp_reg_bitonic(K (&k)[R]) {
     }
 }
 
+// Tile lists: primitive ids, either in fixed-capacity buckets (list of tile g
+// at g * cap) or in scanned ranges (at tstart[g]).
+struct TileLists {
+    uint64_t *ids;          // entries: fp32 depth bits << 32 | primitive id
+    const int64_t *tstart;  // null: buckets
+    uint32_t cap;
+    __device__ __forceinline__ uint64_t *list(int64_t g) const { return ids + (tstart ? tstart[g] : g * (int64_t)cap); }
+};
+
 struct TileSortArgs {
-    const int64_t *tstart;
+    TileLists tl;
     const uint32_t *tcount;
     const int64_t *tile_base;  // per item
     int nitems;
-    const uint64_t *depth;     // [nitems][stride]
+    const uint64_t *depth;     // [nitems][stride] orderable depth keys
     int64_t stride;
-    uint64_t *pairs;
     uint32_t *slow_list;       // tiles needing the block-level exact sort
     unsigned int *slow_n;
     int64_t Tt;
 };
 
-// Sort one tile list (n <= 32 R) in registers on 32-bit keys: the entries'
-// view-level depth buckets are re-bucketed to 22 bits over the tile's own
-// bucket range, with the entry's list position in the low 10 bits.  Distinct
-// 22-bit buckets are strictly depth ordered; adjacent equal buckets send the
-// tile to the exact (64-bit depth key, index) block sort.
+__device__ __forceinline__ int item_of_tile(const int64_t *__restrict__ tile_base, int nitems, int64_t g) {
+    int lo = 0, hi = nitems - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tile_base[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Sort one tile list (n <= 32 R) in registers on 32-bit keys: each entry's
+// fp32 depth bits are re-bucketed to 22 bits over the tile's own range, with
+// the entry's list position in the low 10 bits.  Distinct 22-bit buckets are
+// strictly depth ordered (fp32 rounding and bucketing are monotone); adjacent
+// equal buckets send the tile to the exact (64-bit depth key, index) block sort.
 template <int R>
 __device__ __forceinline__ void warp_sort_tile(const TileSortArgs &a, int64_t g, int n) {
     const int lane = threadIdx.x & 31;
-    uint64_t *lst = a.pairs + a.tstart[g];
+    uint64_t *lst = a.tl.list(g);
     uint32_t key[R];
     uint32_t bmin = 0xffffffffu, bmax = 0u;
 #pragma unroll
@@ -750,13 +805,8 @@ __global__ void __launch_bounds__(128) k_sort_tiles_warp(TileSortArgs a) {
 // Exact block-level sort of one slow tile on (64-bit depth key, id).
 __device__ __noinline__ void sort_one_slow_tile(const TileSortArgs &a, int64_t g, uint64_t *skey, uint32_t *sid) {
     const int n = (int)a.tcount[g];
-    int lo = 0, hi = a.nitems - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (a.tile_base[mid] <= g) lo = mid; else hi = mid - 1;
-    }
-    const uint64_t *depth = a.depth + (int64_t)lo * a.stride;
-    uint64_t *lst = a.pairs + a.tstart[g];
+    const uint64_t *depth = a.depth + (int64_t)item_of_tile(a.tile_base, a.nitems, g) * a.stride;
+    uint64_t *lst = a.tl.list(g);
     int npad = 64;
     while (npad < n) npad <<= 1;
     for (int k = threadIdx.x; k < npad; k += kTileThreads) {
@@ -798,8 +848,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs 
 template <bool USAGE, bool STATS>
 __global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
 k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
-            const int64_t *__restrict__ tstart, const uint32_t *__restrict__ tcount,
-            const uint64_t *__restrict__ pairs, unsigned long long *__restrict__ stats) {
+            const TileLists tls, const uint32_t *__restrict__ tcount, unsigned long long *__restrict__ stats) {
     __shared__ CompShared sh;
     {
         const unsigned long long *src = &kExpTable[0][0];
@@ -830,9 +879,8 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     const Rec *__restrict__ recs = itp->recs;
     const unsigned lt_mask = (1u << lane) - 1u;
 
-    const int64_t s0 = tstart[g];
     const int n_all = (int)tcount[g];
-    const uint64_t *__restrict__ glist = pairs + s0;
+    const uint64_t *__restrict__ glist = tls.list(g);
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     bool done = !inside;
     int term_id = -1;          // STATS: primitive whose contribution terminated the pixel
@@ -1105,7 +1153,7 @@ __global__ void __launch_bounds__(256)
 k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__restrict__ conics,
                const double *__restrict__ alphas, const double *__restrict__ colors,
                const int64_t *__restrict__ bboxes, Rec *__restrict__ recs, int32_t *__restrict__ ntiles,
-               uint64_t *__restrict__ depth, uint32_t *__restrict__ tile_count, int tiles_x) {
+               uint64_t *__restrict__ depth) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
     Rec r;
@@ -1136,18 +1184,8 @@ k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__re
     if (r.x1 > r.x0 && r.y1 > r.y0 && rec_tile_range(r, u0, u1, v0, v1)) nt = (u1 - u0 + 1) * (v1 - v0 + 1);
     ntiles[i] = nt > 0 ? nt : (r.x1 > r.x0 && r.y1 > r.y0 ? -1 : 0);
     depth[i] = (uint64_t)i;  // the input order is the depth order
-    if (nt > 0)
-        for (int v = v0; v <= v1; ++v)
-            for (int u = u0; u <= u1; ++u) atomicAdd(tile_count + v * tiles_x + u, 1u);
 }
 
-__global__ void k_init_zrange(unsigned long long *zr, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
-        zr[2 * i] = ~0ull;
-        zr[2 * i + 1] = 0ull;
-    }
-}
 
 __global__ void k_fill_i64(int64_t *p, int64_t n, int64_t v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1194,100 +1232,123 @@ struct Layout {
 // Stage B: histogram (already accumulated in tile_count) -> ranges -> emit ->
 // oversized-tile fallback sort -> composite -> SSE.
 static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
-                              const Rec *recs, const uint64_t *depth, const unsigned long long *zrange,
-                              const int32_t *ntiles, uint32_t *tile_count, double *sse, cudaStream_t st,
-                              const unsigned int *flags = nullptr) {
+                              const Rec *recs, const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count,
+                              int index_order, double *sse, cudaStream_t st, unsigned int *flags) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
-    int64_t *tstart = ctx->scratch_t<int64_t>(kSlotRanges, (size_t)Tt);
-    uint32_t *big_list = ctx->scratch_t<uint32_t>(kSlotPairValsAlt, (size_t)Tt);
     int64_t *stats = ctx->scratch_t<int64_t>(kSlotItemStats, 8);
-    unsigned int *big_n = (unsigned int *)(stats + 2);
-    int64_t *d_total = stats;
-    int64_t *d_Tt = stats + 1;
-    AIRGS_CUDA_TRY(cudaMemsetAsync(big_n, 0, sizeof(unsigned int), st));
-    h2d_small(ctx, d_Tt, &Tt, sizeof(int64_t), st);
-    {
-        const int bps = (int)std::max<int64_t>(1, ceil_div(Tt, kScanTile));
-        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
-        seg_scan<int64_t>(TileScanIn{tile_count}, TileScanOut{tstart, big_list, big_n, (uint32_t)kSortCap}, d_Tt, 1,
-                          Tt, blocks, d_total, st, &NL);
+    int64_t maxc = 0;
+    for (const auto &h : items) maxc = std::max(maxc, h.count);
+    // binning straight into fixed-capacity tile buckets (capacity adapted after an overflow)
+    const uint32_t cap = ctx->bucket_cap;
+    uint64_t *bucket = ctx->scratch_t<uint64_t>(kSlotPairKeysAlt, (size_t)std::max<int64_t>(Tt, 1) * cap);
+    if (maxc > 0 && Tt > 0) {
+        BinArgs ba{recs, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tile_count, bucket, cap, flags, L.stride,
+                   index_order};
+        k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
+        ++NL;
         check_launch();
     }
-    int64_t hh[2];
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(hh, stats, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    unsigned int hbig = 0, hflags = 0;
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbig, big_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-    if (flags) AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    unsigned int hflags = 0;
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
     if (hflags & kFlagInvalidParam)
         throw ApiFailure(AIRGS_E_VALIDATION, "frame contains invalid primitive parameters");
-    const int64_t P = hh[0];
-    uint64_t *pairs = ctx->scratch_t<uint64_t>(kSlotPairVals, (size_t)std::max<int64_t>(P, 1));
-    uint32_t *cursor = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)Tt);
-    AIRGS_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * Tt, st));
-    int64_t maxc = 0;
-    for (const auto &h : items) maxc = std::max(maxc, h.count);
-    if (P > 0) {
-        EmitArgs ea{recs, depth, zrange, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tstart, cursor, pairs, L.stride};
-        k_emit<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ea);
-        ++NL;
-        check_launch();
-    }
-    if (hbig > 0) {
-        // oversized tiles: stable radix sort of each range by index, then by depth key
-        std::vector<uint32_t> hlist(hbig);
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(hlist.data(), big_list, sizeof(uint32_t) * hbig, cudaMemcpyDeviceToHost, st));
-        std::vector<uint32_t> hcnt(hbig);
-        for (unsigned b = 0; b < hbig; ++b)
-            AIRGS_CUDA_TRY(cudaMemcpyAsync(&hcnt[b], tile_count + hlist[b], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-        std::vector<int64_t> seg(2 * hbig);
-        int64_t tot = 0, mx = 0;
-        for (unsigned b = 0; b < hbig; ++b) {
-            seg[b] = tot;
-            seg[hbig + b] = hcnt[b];
-            tot += hcnt[b];
-            mx = std::max<int64_t>(mx, hcnt[b]);
-        }
-        int32_t *d_tile_item = nullptr;
+    TileLists tl{bucket, nullptr, cap};
+    if (hflags & kFlagBucketOverflow) {
+        // scanned ranges: exclusive scan of the (complete) tile counts, ids emitted
+        // into the ranges, oversized tiles presorted by a segmented radix sort
+        int64_t *tstart = ctx->scratch_t<int64_t>(kSlotRanges, (size_t)Tt);
+        uint32_t *big_list = ctx->scratch_t<uint32_t>(kSlotPairValsAlt, (size_t)Tt);
+        unsigned int *big_n = (unsigned int *)(stats + 2);
+        unsigned int *vmax = (unsigned int *)(stats + 4);
+        int64_t *d_total = stats;
+        int64_t *d_Tt = stats + 1;
+        AIRGS_CUDA_TRY(cudaMemsetAsync(big_n, 0, sizeof(unsigned int), st));
+        AIRGS_CUDA_TRY(cudaMemsetAsync(vmax, 0, sizeof(unsigned int), st));
+        h2d_small(ctx, d_Tt, &Tt, sizeof(int64_t), st);
         {
-            d_tile_item = ctx->scratch_t<int32_t>(kSlotTileItem, (size_t)Tt);
+            const int bps = (int)std::max<int64_t>(1, ceil_div(Tt, kScanTile));
+            int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
+            seg_scan<int64_t>(TileScanIn{tile_count}, TileScanOut{tstart, big_list, big_n, vmax, (uint32_t)kSortCap},
+                              d_Tt, 1, Tt, blocks, d_total, st, &NL);
+            check_launch();
+        }
+        int64_t P = 0;
+        unsigned int hbig = 0, hmax = 0;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&P, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbig, big_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&hmax, vmax, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        {  // adapt the bucket capacity for the next call
+            uint32_t c = cap;
+            while (c < hmax && c < (uint32_t)kSortCap) c <<= 1;
+            ctx->bucket_cap = c;
+        }
+        uint64_t *ids = ctx->scratch_t<uint64_t>(kSlotPairVals, (size_t)std::max<int64_t>(P, 1));
+        uint32_t *cursor = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)Tt);
+        AIRGS_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * Tt, st));
+        if (P > 0) {
+            EmitArgs ea{recs, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tstart, cursor, ids, L.stride,
+                        index_order};
+            k_emit<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ea);
+            ++NL;
+            check_launch();
+        }
+        if (hbig > 0) {
+            // oversized tiles: stable radix sort of each range by index, then by depth key
+            std::vector<uint32_t> hlist(hbig);
+            AIRGS_CUDA_TRY(cudaMemcpyAsync(hlist.data(), big_list, sizeof(uint32_t) * hbig, cudaMemcpyDeviceToHost, st));
+            std::vector<uint32_t> hcnt(hbig);
+            for (unsigned b = 0; b < hbig; ++b)
+                AIRGS_CUDA_TRY(
+                    cudaMemcpyAsync(&hcnt[b], tile_count + hlist[b], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+            AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+            std::vector<int64_t> seg(2 * hbig);
+            int64_t tot = 0, mx = 0;
+            for (unsigned b = 0; b < hbig; ++b) {
+                seg[b] = tot;
+                seg[hbig + b] = hcnt[b];
+                tot += hcnt[b];
+                mx = std::max<int64_t>(mx, hcnt[b]);
+            }
+            int32_t *d_tile_item = ctx->scratch_t<int32_t>(kSlotTileItem, (size_t)Tt);
             k_tile_item<<<(unsigned)ceil_div(Tt, 256), 256, 0, st>>>(L.d_tile_base, nitems, Tt, d_tile_item);
             ++NL;
+            int64_t *d_seg = ctx->scratch_t<int64_t>(kSlotMisc3, 2 * (size_t)hbig);
+            h2d_small(ctx, d_seg, seg.data(), sizeof(int64_t) * 2 * hbig, st);
+            uint64_t *k1 = ctx->scratch_t<uint64_t>(kSlotKeys, (size_t)tot);
+            uint64_t *k2 = ctx->scratch_t<uint64_t>(kSlotKeysAlt, (size_t)tot);
+            uint32_t *v1 = ctx->scratch_t<uint32_t>(kSlotVals, (size_t)tot);
+            uint32_t *v2 = ctx->scratch_t<uint32_t>(kSlotValsAlt, (size_t)tot);
+            uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)hbig * 256 * ceil_div(mx, kSortTile));
+            BigArgs ba{big_list, tstart, tile_count, d_tile_item, depth, ids, L.stride, d_seg, k1, v1};
+            const dim3 gg((unsigned)std::min<int64_t>(64, ceil_div(mx, 256)), hbig);
+            k_big_gather<<<gg, 256, 0, st>>>(ba);
+            k_ids_as_keys<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(v1, k1, tot);
+            NL += 2;
+            bool alt = radix_sort<uint64_t>(k1, v1, k2, v2, d_seg, d_seg + hbig, (int)hbig, mx, 32, hist, st, &NL);
+            uint32_t *vs = alt ? v2 : v1;
+            uint64_t *ks = alt ? k2 : k1;
+            uint64_t *ko = alt ? k1 : k2;
+            uint32_t *vo = alt ? v1 : v2;
+            k_gather_keys<<<gg, 256, 0, st>>>(vs, d_seg, big_list, d_tile_item, tile_count, depth, L.stride, ks);
+            ++NL;
+            bool alt2 = radix_sort<uint64_t>(ks, vs, ko, vo, d_seg, d_seg + hbig, (int)hbig, mx, 64, hist, st, &NL);
+            k_big_scatter<<<gg, 256, 0, st>>>(ba, alt2 ? vo : vs);
+            ++NL;
+            check_launch();
+            AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
         }
-        int64_t *d_seg = ctx->scratch_t<int64_t>(kSlotMisc3, 2 * (size_t)hbig);
-        h2d_small(ctx, d_seg, seg.data(), sizeof(int64_t) * 2 * hbig, st);
-        uint64_t *k1 = ctx->scratch_t<uint64_t>(kSlotKeys, (size_t)tot);
-        uint64_t *k2 = ctx->scratch_t<uint64_t>(kSlotKeysAlt, (size_t)tot);
-        uint32_t *v1 = ctx->scratch_t<uint32_t>(kSlotVals, (size_t)tot);
-        uint32_t *v2 = ctx->scratch_t<uint32_t>(kSlotValsAlt, (size_t)tot);
-        uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)hbig * 256 * ceil_div(mx, kSortTile));
-        BigArgs ba{big_list, tstart, tile_count, d_tile_item, depth, pairs, L.stride, d_seg, k1, v1};
-        const dim3 gg((unsigned)std::min<int64_t>(64, ceil_div(mx, 256)), hbig);
-        k_big_gather<<<gg, 256, 0, st>>>(ba);
-        k_ids_as_keys<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(v1, k1, tot);
-        NL += 2;
-        bool alt = radix_sort<uint64_t>(k1, v1, k2, v2, d_seg, d_seg + hbig, (int)hbig, mx, 32, hist, st, &NL);
-        uint32_t *vs = alt ? v2 : v1;
-        uint64_t *ks = alt ? k2 : k1;
-        uint64_t *ko = alt ? k1 : k2;
-        uint32_t *vo = alt ? v1 : v2;
-        k_gather_keys<<<gg, 256, 0, st>>>(vs, d_seg, big_list, d_tile_item, tile_count, depth, L.stride, ks);
-        ++NL;
-        bool alt2 = radix_sort<uint64_t>(ks, vs, ko, vo, d_seg, d_seg + hbig, (int)hbig, mx, 64, hist, st, &NL);
-        k_big_scatter<<<gg, 256, 0, st>>>(ba, alt2 ? vo : vs);
-        ++NL;
-        check_launch();
-        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        tl = TileLists{ids, tstart, 0u};
     }
-    if (P > 0) {
+    if (Tt > 0) {
         // depth-order every tile list: warp-level register sort, block-level exact sort for the rest
         unsigned int *slow_n = (unsigned int *)(stats + 3);
         uint32_t *slow_list = ctx->scratch_t<uint32_t>(kSlotSlowTiles, (size_t)Tt);
         AIRGS_CUDA_TRY(cudaMemsetAsync(slow_n, 0, sizeof(unsigned int), st));
-        TileSortArgs ta{tstart, tile_count, L.d_tile_base, nitems, depth, L.stride, pairs, slow_list, slow_n, Tt};
+        TileSortArgs ta{tl, tile_count, L.d_tile_base, nitems, depth, L.stride, slow_list, slow_n, Tt};
         k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
         // the exact block sort walks the device-side slow list (no host readback)
         k_sort_tiles_block<<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
@@ -1339,17 +1400,17 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         unsigned long long *cs = ctx->d_stats;
         if (stats_on) {
             if (any_usage)
-                k_composite<true, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
-                                                                               tile_count, pairs, cs);
+                k_composite<true, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                               tile_count, cs);
             else
-                k_composite<false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
-                                                                                tile_count, pairs, cs);
+                k_composite<false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                                tile_count, cs);
         } else if (any_usage) {
-            k_composite<true, false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
-                                                                            tile_count, pairs, cs);
+            k_composite<true, false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                            tile_count, cs);
         } else {
-            k_composite<false, false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tstart,
-                                                                             tile_count, pairs, cs);
+            k_composite<false, false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                             tile_count, cs);
         }
         ++NL;
         check_launch();
@@ -1468,9 +1529,6 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     int32_t *ntiles = ctx->scratch_t<int32_t>(kSlotNtiles, per);
     uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
-    unsigned long long *zrange = ctx->scratch_t<unsigned long long>(kSlotZRange, 2 * (size_t)nitems);
-    k_init_zrange<<<(unsigned)ceil_div(nitems, 256), 256, 0, st>>>(zrange, nitems);
-    ++NL;
 
     ProjArgs pa;
     pa.frames = (const airgs_frame *)(dd + o_frames);
@@ -1483,19 +1541,22 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.recs = recs;
     pa.depth = depth;
     pa.ntiles = ntiles;
-    pa.tile_count = tile_count;
-    pa.zrange = zrange;
     pa.flags = flags;
     pa.stride = stride;
     cudaEvent_t t_proj = ctx->time_begin(st);
     {
         dim3 grid((unsigned)ceil_div(stride, kProjThreads), (unsigned)nframes);
-        k_project<<<grid, kProjThreads, 0, st>>>(pa);
+        bool all17 = true;
+        for (int f = 0; f < nframes; ++f) all17 &= frames[f].width == 17;
+        if (all17)
+            k_project<17><<<grid, kProjThreads, 0, st>>>(pa);
+        else
+            k_project<26><<<grid, kProjThreads, 0, st>>>(pa);
         ++NL;
         check_launch();
     }
     ctx->time_end(t_proj, st, 1);
-    bin_and_composite(ctx, ih, L, recs, depth, zrange, ntiles, tile_count, sse, st, flags);
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags);
 }
 
 static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics, const double *alphas,
@@ -1525,20 +1586,17 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
     uint64_t *depth = ctx->scratch_t<uint64_t>(kSlotDepth, L.stride);
     uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
-    unsigned long long *zrange = ctx->scratch_t<unsigned long long>(kSlotZRange, 2);
-    {
-        const unsigned long long zr[2] = {0ull, (unsigned long long)std::max<int64_t>(k, 1)};
-        h2d_small(ctx, zrange, zr, sizeof(zr), st);
-    }
+    unsigned int *flags = ctx->scratch_t<unsigned int>(kSlotFlags, 4);
+    AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
     if (usage && k > 0) AIRGS_CUDA_TRY(cudaMemsetAsync(usage, 0, sizeof(int64_t) * k, st));
     if (k > 0) {
         k_seam_records<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, means2d, conics, alphas, colors, bboxes, recs,
-                                                                  ntiles, depth, tile_count, it.tiles_x);
+                                                                  ntiles, depth);
         ++ctx->launches;
         check_launch();
     }
     // every in-image pixel of every tile is written by the composite kernel
-    bin_and_composite(ctx, ih, L, recs, depth, zrange, ntiles, tile_count, nullptr, st);
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 1, nullptr, st, flags);
 }
 
 static void sse_impl(airgs_ctx *ctx, const double *a, const double *b, int64_t n, double *out, cudaStream_t st) {
