@@ -246,8 +246,8 @@ def run_gpu(args):
             "gpu_launches": int(round(launches)),
             "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_sm": roof_sm, "cpu_baseline": cpu,
             "keyframe_decisions": decisions, "qualities_db": [round(q, 6) for q in quals],
-            "decision_margins": {"min_abs_q_minus_tau_db": round(min(abs(q - TAU_DB) for q in quals), 6),
-                                 "tau_db": TAU_DB},
+            "decision_margins": dict({"min_abs_q_minus_tau_db": round(min(abs(q - TAU_DB) for q in quals), 6),
+                                      "tau_db": TAU_DB}, **roof_sm.pop("decision_margins", {})),
         }
         print(json.dumps(line))
     if world > 1:
@@ -316,11 +316,13 @@ def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames
         src = "profiles/fp64_peak.json (DFMA microbenchmark, tools/fp64_peak.cu)"
     except Exception:
         peak, src = 148 * 64 * 1.965e9 / 1e12, "fallback: 148 SMs x 64 DFMA/clk x 1.965 GHz"
-    counts = {}
+    counts, margins = {}, {}
     eng.eval_stats(1)
     try:
         for f in sorted(set(frames_used)):
             evaluate_frame(space, cams, payload_dev[f], payloads[f].data, targets[f], device)
+            for k, v in eng.eval_margins().items():
+                margins[k] = v + margins.get(k, 0.0) if k == "depth_ties" else min(v, margins.get(k, float("inf")))
             counts[f] = eng.eval_stats(1)
     finally:
         eng.eval_stats(0)
@@ -332,7 +334,7 @@ def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames
             "peak": round(peak, 3), "unit": "T fp64 ops/s", "frac": round(achieved / peak, 4) if achieved else None,
             "peak_source": src, "ops_per_live_eval": OPS_PER_LIVE_EVAL, "ops_per_contribution": OPS_PER_CONTRIB,
             "per_view": {k: int(round(v / V)) for k, v in tot.items()},
-            "algorithmic_ops_per_launch": int(ops)}
+            "algorithmic_ops_per_launch": int(ops), "decision_margins": margins}
 
 
 def run_e2e(space, cams, payloads, targets, device, args, world):

@@ -102,6 +102,23 @@ AIRGS_API int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms,
  * the last (re)arm; enable = 1 arms, 0 disarms, -1 only reads.  Synchronises. */
 AIRGS_API int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts);
 
+/* Decision margins of the renders since the counters were armed (SURVEY.md
+ * s8(a) numerics contract: "the harness must report decision margins"):
+ * margins[0] = min |w - 1/255| / (1/255) over the exactly evaluated weight
+ *              tests (pairs the fp32 pass rejects have margin >= ~4e-5 by
+ *              its guard band), ss/_composite.pyx:62;
+ * margins[1] = min |0.999 T - 1/255| / (1/255) after any contribution
+ *              (early-termination test);
+ * margins[2] = min gap in ulps between adjacent distinct depth keys of a
+ *              tile list (ss/rasterizer.py:127 stable argsort);
+ * margins[3] = number of adjacent exact depth ties (ordered by index);
+ * margins[4] = min distance of a bbox floor/ceil argument to an integer (px),
+ *              ss/rasterizer.py:177-180;
+ * margins[5] = min |z - near_clip| (cull), ss/rasterizer.py:124;
+ * margins[6] = min |alpha - 1/255| / (1/255) (opacity cull), ss/rasterizer.py:124.
+ * Synchronises. */
+AIRGS_API int airgs_eval_margins(airgs_ctx *ctx, double *margins);
+
 /* ---- rasterizer --------------------------------------------------------- */
 
 /* Batched render: replaces ss/rasterizer.py:113-240 (_activate, _prepare,

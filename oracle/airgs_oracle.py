@@ -114,7 +114,8 @@ def sh_degree_of(width):
 
 
 class Prepared:
-    __slots__ = ("order", "means2d", "conics", "alphas", "colors", "bboxes", "depth")
+    __slots__ = ("order", "means2d", "conics", "alphas", "colors", "bboxes", "depth",
+                 "radius", "z_all", "alpha_all")
 
 
 def prepare(params, cam):
@@ -195,6 +196,7 @@ def prepare(params, cam):
     bb[:, 2] = np.clip(np.floor(my - rad), 0, H)
     bb[:, 3] = np.clip(np.ceil(my + rad) + 1, 0, H)
     out.bboxes = bb
+    out.radius, out.z_all, out.alpha_all = rad, tc[:, 2], alpha  # (decision-margin checks)
     # colour (ss/rasterizer.py:183-198)
     dirs = mu[order] - ct.center
     sd = dirs * dirs

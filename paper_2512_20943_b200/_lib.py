@@ -64,6 +64,7 @@ SIGNATURES = {
     "airgs_launch_count": (i64, [vp]),
     "airgs_timing": (ctypes.c_int, [vp, i32, c_double_p, c_i64_p, c_double_p, c_i64_p]),
     "airgs_eval_stats": (ctypes.c_int, [vp, i32, c_i64_p]),
+    "airgs_eval_margins": (ctypes.c_int, [vp, c_double_p]),
     "airgs_render": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), i32, ctypes.POINTER(CameraC), i32,
                                     ctypes.POINTER(ItemC), i32, vp, vp]),
     "airgs_composite_forward": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp]),
@@ -160,6 +161,16 @@ class Engine:
         c = (ctypes.c_int64 * 3)()
         self.call("airgs_eval_stats", int(enable), c)
         return {"bbox": c[0], "live": c[1], "contrib": c[2]}
+
+    MARGIN_KEYS = ("min_rel_weight_margin", "min_rel_termination_margin", "min_depth_gap_ulps", "depth_ties",
+                   "min_bbox_floor_margin_px", "min_near_clip_margin", "min_rel_alpha_cull_margin")
+
+    def eval_margins(self):
+        """Decision margins accumulated since the counters were armed (see
+        airgs_eval_margins); +inf where no such decision was taken."""
+        m = (ctypes.c_double * 7)()
+        self.call("airgs_eval_margins", m)
+        return {k: float(v) for k, v in zip(self.MARGIN_KEYS, m)}
 
     @property
     def launches(self) -> int:

@@ -89,26 +89,57 @@ extern "C" int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms
     return AIRGS_OK;
 }
 
+static int stats_reset(airgs_ctx *ctx) {
+    unsigned long long h[airgs::kStatSlots];
+    for (int k = 0; k < airgs::kStatSlots; ++k) h[k] = 0ull;
+    const unsigned long long inf = 0x7ff0000000000000ull;  // +inf bits: min slots start empty
+    h[airgs::kMarginWeight] = h[airgs::kMarginTerm] = h[airgs::kMarginDepthGap] = inf;
+    h[airgs::kMarginBBox] = h[airgs::kMarginNear] = h[airgs::kMarginAlpha] = inf;
+    return cudaMemcpy(ctx->d_stats, h, sizeof(h), cudaMemcpyHostToDevice) == cudaSuccess ? AIRGS_OK : AIRGS_E_CUDA;
+}
+
+static int stats_read(airgs_ctx *ctx, unsigned long long *h) {
+    for (int k = 0; k < airgs::kStatSlots; ++k) h[k] = 0ull;
+    if (!ctx->d_stats) return AIRGS_OK;
+    if (cudaDeviceSynchronize() != cudaSuccess ||
+        cudaMemcpy(h, ctx->d_stats, sizeof(unsigned long long) * airgs::kStatSlots, cudaMemcpyDeviceToHost) !=
+            cudaSuccess) {
+        ctx->err = "eval stats readback failed";
+        return AIRGS_E_CUDA;
+    }
+    return AIRGS_OK;
+}
+
 extern "C" int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts) {
     if (!ctx) return AIRGS_E_INTERNAL;
     if (cudaSetDevice(ctx->device) != cudaSuccess) return AIRGS_E_CUDA;
-    unsigned long long h[3] = {0, 0, 0};
-    if (ctx->d_stats) {
-        if (cudaDeviceSynchronize() != cudaSuccess ||
-            cudaMemcpy(h, ctx->d_stats, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) {
-            ctx->err = "eval stats readback failed";
-            return AIRGS_E_CUDA;
-        }
-    }
+    unsigned long long h[airgs::kStatSlots];
+    if (int rc = stats_read(ctx, h)) return rc;
     if (counts)
         for (int k = 0; k < 3; ++k) counts[k] = (int64_t)h[k];
     if (enable >= 0) {  // (re)arm or disarm and reset the counters
-        if (enable && !ctx->d_stats && cudaMalloc(&ctx->d_stats, sizeof(h)) != cudaSuccess) {
+        if (enable && !ctx->d_stats &&
+            cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * airgs::kStatSlots) != cudaSuccess) {
             ctx->err = "eval stats allocation failed";
             return AIRGS_E_CUDA;
         }
-        if (ctx->d_stats && cudaMemset(ctx->d_stats, 0, sizeof(h)) != cudaSuccess) return AIRGS_E_CUDA;
+        if (ctx->d_stats)
+            if (int rc = stats_reset(ctx)) return rc;
         ctx->stats = enable != 0;
+    }
+    return AIRGS_OK;
+}
+
+extern "C" int airgs_eval_margins(airgs_ctx *ctx, double *margins) {
+    if (!ctx || !margins) return AIRGS_E_INTERNAL;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return AIRGS_E_CUDA;
+    unsigned long long h[airgs::kStatSlots];
+    if (int rc = stats_read(ctx, h)) return rc;
+    for (int k = 0; k < 7; ++k) {
+        const int slot = airgs::kMarginWeight + k;
+        double v;
+        std::memcpy(&v, &h[slot], sizeof(v));
+        margins[k] = slot == airgs::kMarginDepthTies ? (double)h[slot] : v;
     }
     return AIRGS_OK;
 }

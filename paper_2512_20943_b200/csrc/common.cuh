@@ -46,6 +46,20 @@ struct Status {
 };
 
 // device-side error flags (bitmask) written by kernels
+// Diagnostic decision margins (airgs_eval_margins): non-negative doubles kept
+// as their bit patterns (integer order = value order), min-reduced per warp
+// then one atomicMin per warp.
+enum MarginSlot {
+    kMarginWeight = 3,       // min |w - 1/255| / (1/255) over every weight test
+    kMarginTerm = 4,         // min |0.999 T - 1/255| / (1/255) after every contribution
+    kMarginDepthGap = 5,     // min gap (ulps) between adjacent distinct depth keys of a tile list
+    kMarginDepthTies = 6,    // adjacent equal depth keys (resolved by index)
+    kMarginBBox = 7,         // min distance of a bbox floor/ceil argument to an integer (px)
+    kMarginNear = 8,         // min |z - near_clip|
+    kMarginAlpha = 9,        // min |alpha - 1/255| / (1/255) (opacity cull)
+    kStatSlots = 10
+};
+
 enum DevFlag : unsigned int {
     kFlagInvalidParam = 1u,   // zero quaternion / non-finite parameter
     kFlagDecodeTrunc = 2u,    // varint section inconsistent

@@ -45,7 +45,18 @@ struct ProjArgs {
     int32_t *ntiles;           // [nitems][stride] tiles touched (0 = empty bbox, -1 = no tile)
     unsigned int *flags;
     int64_t stride;
+    unsigned long long *stats;  // diagnostic decision margins (null: off)
 };
+
+
+__device__ __forceinline__ double dist_to_int(double x) { return fabs(x - rint(x)); }
+
+__device__ __forceinline__ void margin_min(unsigned long long *stats, int slot, double v) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v));
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) b = min(b, __shfl_xor_sync(0xffffffffu, b, d));
+    if ((threadIdx.x & 31) == 0) atomicMin(stats + slot, b);
+}
 
 __device__ __forceinline__ double dot3_blas(double x0, double x1, double x2, double y0, double y1,
                                             double y2) {
@@ -146,7 +157,9 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
         const double *R = cam.rot;
         int nt = 0;
         double tz = 0.0;
+        double bbm = 1.0;  // stats: bbox floor/ceil argument margin
         if (live) tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
+        if (a.stats) margin_min(a.stats, kMarginNear, live ? fabs(tz - cam.near_clip) : 1e300);
         if (live && tz > cam.near_clip) {
             const double tx = dot3_blas(p[0], p[1], p[2], R[0], R[1], R[2]) + cam.trans[0];
             const double ty = dot3_blas(p[0], p[1], p[2], R[3], R[4], R[5]) + cam.trans[1];
@@ -184,6 +197,9 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
             const double eig = 0.5 * (a2 + c2) + sqrt(fmax(0.25 * (dd * dd) + b2 * b2, 0.0));
             const double rad = kRadiusSigma * sqrt(eig);
             const double Wd = (double)cam.width, Hd = (double)cam.height;
+            if (a.stats)
+                bbm = fmin(bbm, fmin(fmin(dist_to_int(mx - rad), dist_to_int(mx + rad)),
+                                     fmin(dist_to_int(my - rad), dist_to_int(my + rad))));
             rec.x0 = (int32_t)fmin(fmax(floor(mx - rad), 0.0), Wd);
             rec.x1 = (int32_t)fmin(fmax(ceil(mx + rad) + 1.0, 0.0), Wd);
             rec.y0 = (int32_t)fmin(fmax(floor(my - rad), 0.0), Hd);
@@ -221,7 +237,10 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
             if (nt <= 0 && has_bbox) nt = -1;  // evaluated by the reference, but no pixel can pass the weight test
         }
         if (active) a.ntiles[o] = nt;
+        if (a.stats) margin_min(a.stats, kMarginBBox, bbm);
     }
+    if (a.stats)
+        margin_min(a.stats, kMarginAlpha, valid ? fabs(alpha - kEpsContrib) / kEpsContrib : 1e300);
 }
 
 // ---------------------------------------------------------------------------
@@ -836,6 +855,29 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs 
     }
 }
 
+// Diagnostic: depth-order margins of the sorted tile lists -- the smallest
+// gap (in ulps of the orderable 64-bit depth keys) between adjacent entries
+// with distinct depths, and the number of adjacent exact ties (ordered by
+// primitive index).  One warp per tile.
+__global__ void __launch_bounds__(128) k_depth_gaps(TileSortArgs a, unsigned long long *stats) {
+    const int64_t g = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    unsigned long long gmin = ~0ull, ties = 0;
+    if (g < a.Tt) {
+        const int n = (int)a.tcount[g];
+        const uint64_t *lst = a.tl.list(g);
+        const uint64_t *depth = a.depth + (int64_t)item_of_tile(a.tile_base, a.nitems, g) * a.stride;
+        for (int k = lane; k + 1 < n; k += 32) {
+            const uint64_t z0 = depth[(uint32_t)lst[k]], z1 = depth[(uint32_t)lst[k + 1]];
+            if (z1 == z0) ++ties;
+            else gmin = min(gmin, (unsigned long long)(z1 - z0));
+        }
+    }
+    ties = warp_reduce_sum(ties);
+    margin_min(stats, kMarginDepthGap, gmin == ~0ull ? 1e300 : (double)gmin);
+    if (lane == 0 && ties) atomicAdd(stats + kMarginDepthTies, ties);
+}
+
 // One CTA = one 16x16 tile, one pixel per thread; warps are 8x4 sub-tiles.
 // The tile's primitive list arrives in depth order (k_sort_tiles_*).
 // Per batch of kBatch primitives (staged once per CTA), every warp compacts
@@ -885,6 +927,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     bool done = !inside;
     int term_id = -1;          // STATS: primitive whose contribution terminated the pixel
     unsigned long long ncon = 0;  // STATS: contributions of this pixel
+    double wmar = 1e300, tmar = 1e300;  // STATS: weight / termination test margins (absolute)
     float thr = log2_inv_eps();  // log2(T/EPS); the guard lives in the staged coefficients
 
     for (int base = 0; base < n_all; base += kBatch) {
@@ -996,6 +1039,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                 const double ap1 = alpha_at(sh, j1, pxd, pyd);
                 const double ap2 = alpha_at(sh, j2, pxd, pyd);
                 double wgt = ap1 * T;
+                if (STATS) wmar = fmin(wmar, fabs(wgt - kEpsContrib));
                 if (wgt > kCompC[7]) {
                     const double2 rg = sh.rg[j1];
                     cr += wgt * rg.x;
@@ -1006,10 +1050,12 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                     if (STATS) {
                         ++ncon;
                         if (term_id < 0 && kAlphaClamp * T <= kEpsContrib) term_id = (int)sh.gid[j1];
+                        tmar = fmin(tmar, fabs(kAlphaClamp * T - kEpsContrib));
                     }
                 }
                 if (two) {
                     wgt = ap2 * T;
+                    if (STATS) wmar = fmin(wmar, fabs(wgt - kEpsContrib));
                     if (wgt > kCompC[7]) {
                         const double2 rg = sh.rg[j2];
                         cr += wgt * rg.x;
@@ -1020,6 +1066,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                         if (STATS) {
                             ++ncon;
                             if (term_id < 0 && kAlphaClamp * T <= kEpsContrib) term_id = (int)sh.gid[j2];
+                            tmar = fmin(tmar, fabs(kAlphaClamp * T - kEpsContrib));
                         }
                     }
                 }
@@ -1055,6 +1102,8 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     if (STATS) {
         ncon = warp_reduce_sum(ncon);
         if (lane == 0 && ncon) atomicAdd(stats + 2, ncon);
+        margin_min(stats, kMarginWeight, wmar / kEpsContrib);
+        margin_min(stats, kMarginTerm, tmar / kEpsContrib);
     }
     if (it.target) {
         double se = 0.0;
@@ -1354,6 +1403,11 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         k_sort_tiles_block<<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
         NL += 2;
         check_launch();
+        if (ctx->stats && ctx->d_stats) {  // diagnostic depth-order margins
+            k_depth_gaps<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta, ctx->d_stats);
+            ++NL;
+            check_launch();
+        }
     }
     double *sse_tiles = ctx->scratch_t<double>(kSlotSseTiles, (size_t)Tt * kCompWarps);
     std::vector<CompItem> ci(nitems);
@@ -1543,6 +1597,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.ntiles = ntiles;
     pa.flags = flags;
     pa.stride = stride;
+    pa.stats = (ctx->stats && ctx->d_stats) ? ctx->d_stats : nullptr;
     cudaEvent_t t_proj = ctx->time_begin(st);
     {
         dim3 grid((unsigned)ceil_div(stride, kProjThreads), (unsigned)nframes);

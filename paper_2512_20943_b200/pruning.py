@@ -338,6 +338,31 @@ def select_pruning_level(space: PruningLevelSpace, ctx: SelectionContext) -> int
     return len(lv) - 1 if best is None else best
 
 
+def selection_margins(space: PruningLevelSpace, ctx: SelectionContext, entries: int = None) -> dict:
+    """Decision margins of ``select_pruning_level`` and the prune counts
+    (SURVEY.md s8(a) numerics contract): min |drop/prev - beta| over the
+    cliff tests actually evaluated, min |size - budget| over the budget tests,
+    and, when ``entries`` is given, min distance of ``ratio * E + 0.5`` to an
+    integer over the levels (the floor in ss/pruning.py:83)."""
+    lv = space.levels
+    out = {"min_abs_cliff_ratio_minus_beta": float("inf"), "min_abs_size_minus_budget_bytes": float("inf")}
+    if len(lv) > 1:
+        q = [x.quality_db for x in lv]
+        prev = q[0] - q[1]
+        for i in range(1, len(lv)):
+            drop = q[i - 1] - q[i]
+            r = drop / max(prev, MIN_DROP)
+            out["min_abs_cliff_ratio_minus_beta"] = min(out["min_abs_cliff_ratio_minus_beta"], abs(r - ctx.cliff_beta))
+            if r > ctx.cliff_beta:
+                break
+            prev = drop
+        out["min_abs_size_minus_budget_bytes"] = float(min(abs(x.size_bytes - ctx.budget_bytes) for x in lv))
+    if entries is not None:
+        fr = [x.ratio * entries + 0.5 for x in lv]
+        out["min_k_floor_margin"] = float(min((abs(v - round(v)) for v in fr), default=float("inf")))
+    return out
+
+
 def ilp_optimal(level_spaces, budgets_bytes) -> list:
     """Exact optimum of the separable selection program: per frame, the
     highest-quality level within budget (first index wins ties)."""

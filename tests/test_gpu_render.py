@@ -274,3 +274,66 @@ def test_eval_stats_match_reference_loop_counts(cfg):
             assert (got["bbox"], got["live"], got["contrib"]) == orc.eval_counts(p, cam)
     finally:
         eng.eval_stats(0)
+
+
+def test_decision_margins_match_reference_quantities(rng):
+    """airgs_eval_margins against the same quantities computed from the
+    oracle's projection and a direct replay of the reference loop: bbox
+    floor/ceil, near-clip and opacity-cull margins exactly; the termination
+    margin to 1e-9; the weight margin exactly where it is below the fp32
+    guard band (every such pair is evaluated in fp64), else a lower bound;
+    the tile-list depth gap is bounded below by the view's global one."""
+    from paper_2512_20943_b200 import _lib, rasterizer
+    from paper_2512_20943_b200.model import GaussianFrame
+
+    p = random_params(rng, 300, 0, spread=0.5)
+    cam = _cams(1, (40, 32))[0]
+    eng = _lib.engine()
+    eng.eval_stats(1)
+    try:
+        rasterizer.render_with_usage(GaussianFrame(params=p), [cam])
+        m = eng.eval_margins()
+    finally:
+        eng.eval_stats(0)
+    pr = orc.prepare(p, cam)
+    eps = 1.0 / 255.0
+    live = pr.alpha_all > eps
+    mx, my, r = pr.means2d[:, 0], pr.means2d[:, 1], pr.radius
+    dist = lambda x: np.abs(x - np.rint(x))  # noqa: E731
+    bbm = min(dist(mx - r).min(), dist(mx + r).min(), dist(my - r).min(), dist(my + r).min())
+    assert m["min_bbox_floor_margin_px"] == bbm
+    assert m["min_near_clip_margin"] == np.abs(pr.z_all[live] - cam.near_clip).min()
+    assert m["min_rel_alpha_cull_margin"] == (np.abs(pr.alpha_all - eps) / eps).min()
+    z = np.sort(pr.depth)
+    gaps = np.diff(z.view(np.int64))
+    gaps = gaps[gaps > 0]
+    if gaps.size:
+        assert m["min_depth_gap_ulps"] >= gaps.min()
+    # the reference loop, pixel-major, weight and termination margins
+    H, W = cam.resolution[1], cam.resolution[0]
+    wmin, wlive, tmin = np.inf, np.inf, np.inf
+    a, b, c = pr.conics[:, 0], pr.conics[:, 1], pr.conics[:, 2]
+    for y in range(H):
+        for x in range(W):
+            sel = np.nonzero((pr.bboxes[:, 0] <= x) & (x < pr.bboxes[:, 1]) & (pr.bboxes[:, 2] <= y)
+                             & (y < pr.bboxes[:, 3]))[0]
+            T = 1.0
+            for k in sel:  # every pair, as the reference (no early exit)
+                dx, dy = x + 0.5 - mx[k], y + 0.5 - my[k]
+                e = 0.5 * (a[k] * dx * dx + c[k] * dy * dy) + b[k] * dx * dy
+                ap = min(pr.alphas[k] * np.exp(-e), 0.999)
+                w = ap * T
+                if 0.999 * T > eps:
+                    wlive = min(wlive, abs(w - eps) / eps)
+                wmin = min(wmin, abs(w - eps) / eps)
+                if w > eps:
+                    T = T * (1.0 - ap)
+                    tmin = min(tmin, abs(0.999 * T - eps) / eps)
+    assert np.isfinite(tmin)
+    assert abs(m["min_rel_termination_margin"] - tmin) <= 1e-9 * tmin
+    # the device evaluates a subset of the weight tests in fp64 (the fp32 pass
+    # rejects the rest with margin >= ~4e-5): never below the true minimum, and
+    # equal to it when the minimum is a live test inside the guard band
+    assert m["min_rel_weight_margin"] >= wmin * (1 - 1e-9)
+    if wlive < 4e-5 and wlive < tmin:
+        assert abs(m["min_rel_weight_margin"] - wlive) <= 1e-9 * wlive

@@ -32,7 +32,8 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2512_20943_b200 import synth  # noqa: E402
 from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames  # noqa: E402
-from paper_2512_20943_b200.pruning import build_level_space  # noqa: E402
+from paper_2512_20943_b200.pruning import (SelectionContext, build_level_space, select_pruning_level,  # noqa: E402
+                                           selection_margins)
 
 
 def cuda_time(fn, steps, warmup):
@@ -74,14 +75,25 @@ def sweep(cfg, dev, steps, warmup, ratios=tuple(i / 10 for i in range(8))):
 
     from paper_2512_20943_b200.streamsim import _usage_only
 
+    out = {}
+
     def step():
         usage = _usage_only(mv, cams)  # the session's usage pass (counts only, ss/streamsim.py:223-225)
-        build_level_space(gap, space, cams, list(ratios), usage, 1e-4, frame_index=4)
+        out["space"] = build_level_space(gap, space, cams, list(ratios), usage, 1e-4, frame_index=4)
 
     ms = cuda_time(step, steps, warmup)
     evals = len(cams) * (len(ratios) + 1)  # usage pass + one render per (level, view)
+    lv = out["space"]
+    # selection at a budget between the middle levels' sizes (beta = 2, R = 1 frame/s)
+    mid = len(lv.levels) // 2
+    budget = 0.5 * (lv.levels[mid - 1].size_bytes + lv.levels[mid].size_bytes)
+    ctx = SelectionContext(bandwidth_B=budget * 8.0, target_rate_R=1.0, cliff_beta=2.0)
     return {"levels": len(ratios), "views": len(cams), "ms_per_frame": round(ms, 2),
-            "level_view_evals_per_s": round(evals / ms * 1e3, 1)}
+            "level_view_evals_per_s": round(evals / ms * 1e3, 1),
+            "quality_table_db": [round(x.quality_db, 4) for x in lv.levels],
+            "sizes_bytes": [x.size_bytes for x in lv.levels],
+            "selected_level": select_pruning_level(lv, ctx),
+            "decision_margins": selection_margins(lv, ctx, entries=len(gap.indices()))}
 
 
 def cpu(cfg, views):
