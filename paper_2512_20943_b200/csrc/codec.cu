@@ -301,28 +301,55 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
     int64_t *misc = ctx->scratch_t<int64_t>(kSlotMisc3, 8);
     AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
     bool ok = V >= 0 && V >= E && V <= 10 * E;
+    if (ok && E == 0) ok = V == 0;
     int64_t nterm = -1;
-    int64_t *gaps = ctx->scratch_t<int64_t>(kSlotKeys, (size_t)std::max<int64_t>(E, 1));
+    // Optimistic single-synchronisation decode: the varint scan, the gap prefix
+    // sum and the row scatter are enqueued back to back; the section's validity
+    // (exactly E terminators, the last byte one of them) is read back once at
+    // the end together with the error flags.  A malformed payload only ever
+    // writes inside [0, base_count) (the row kernel range-checks every index)
+    // and is then re-walked sequentially for the reference's exact error.
+    unsigned long long *bad = (unsigned long long *)(misc + 4);
+    int64_t hh[2] = {0, 0};
+    uint8_t last = 0;
     if (ok && E > 0) {
-        // terminators in the section must be exactly E and the section must end on one
         int64_t *dV = misc;  // count for the scan driver
         h2d_small(ctx, dV, &V, sizeof(int64_t), st);
         const int bps = (int)std::max<int64_t>(1, ceil_div(V, kScanTile));
         int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
-        // gaps[] is written only for ex < E; protect against over-count by sizing V
+        // gaps[] has one slot per byte of the section, so any terminator count fits
         int64_t *gbuf = ctx->scratch_t<int64_t>(kSlotKeysAlt, (size_t)V + 1);
         seg_scan<int64_t>(TermIn{payload + 24}, TermOut{payload + 24, gbuf, flags}, dV, 1, V, blocks, misc + 1, st, &L);
         check_launch();
-        int64_t h[2];
-        uint8_t last = 0;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(h, misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        // indices = inclusive prefix sum of gaps
+        int64_t *dE = misc + 2;
+        h2d_small(ctx, dE, &E, sizeof(int64_t), st);
+        const int bpe = (int)std::max<int64_t>(1, ceil_div(E, kScanTile));
+        int64_t *eblocks = ctx->scratch_t<int64_t>(kSlotPairOff, bpe);
+        seg_scan<int64_t>(GapIn{gbuf}, GapOut{idx_out}, dE, 1, E, eblocks, (int64_t *)nullptr, st, &L);
+        check_launch();
+        if (rows != nullptr) {
+            const unsigned long long mx = ~0ull;
+            h2d_small(ctx, bad, &mx, sizeof(mx), st);
+            AIRGS_CUDA_TRY(cudaMemsetAsync(entries_out, 0, sizeof(int64_t), st));
+            k_gsdp_rows<<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(payload + 24 + V, idx_out, E, W, step,
+                                                                  base_count, rows, ld, present, flags, bad,
+                                                                  (unsigned long long *)entries_out);
+            ++L;
+            check_launch();
+        }
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(hh, misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         AIRGS_CUDA_TRY(cudaMemcpyAsync(&last, payload + 24 + V - 1, 1, cudaMemcpyDeviceToHost, st));
+        nterm = -2;  // resolved after the synchronisation below
+    }
+    unsigned int hf = 0;
+    unsigned long long hbad = 0;
+    if (ok && E > 0) {
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
+        if (rows != nullptr) AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, st));
         AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-        nterm = h[0];
+        nterm = hh[0];
         ok = nterm == E && !(last & 0x80);
-        if (ok) gaps = gbuf;
-    } else if (ok && E == 0) {
-        ok = V == 0;
     }
     if (!ok) {
         // exact reference error path
@@ -341,35 +368,7 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
         AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
         return;
     }
-    // indices = inclusive prefix sum of gaps
-    {
-        int64_t *dE = misc + 2;
-        h2d_small(ctx, dE, &E, sizeof(int64_t), st);
-        const int bps = (int)std::max<int64_t>(1, ceil_div(E, kScanTile));
-        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
-        seg_scan<int64_t>(GapIn{gaps}, GapOut{idx_out}, dE, 1, E, blocks, (int64_t *)nullptr, st, &L);
-        check_launch();
-    }
-    unsigned long long *bad = (unsigned long long *)(misc + 4);
-    if (rows == nullptr) {  // indices only (caller infers base_count)
-        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-        return;
-    }
-    {
-        const unsigned long long mx = ~0ull;
-        h2d_small(ctx, bad, &mx, sizeof(mx), st);
-        AIRGS_CUDA_TRY(cudaMemsetAsync(entries_out, 0, sizeof(int64_t), st));
-        k_gsdp_rows<<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(payload + 24 + V, idx_out, E, W, step, base_count, rows,
-                                                              ld, present, flags, bad,
-                                                              (unsigned long long *)entries_out);
-        ++L;
-        check_launch();
-    }
-    unsigned int hf = 0;
-    unsigned long long hbad = 0;
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(hbad), cudaMemcpyDeviceToHost, st));
-    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    if (rows == nullptr) return;  // indices only (caller infers base_count)
     if (hf & kFlagVarintLong) throw ApiFailure(AIRGS_E_DECODE, "varint too long");
     if (hf & kFlagIndexRange)
         throw ApiFailure(AIRGS_E_STRUCTURAL, "delta index " + std::to_string((long long)hbad) + " out of range");

@@ -152,6 +152,7 @@ enum Slot : int {
     kSlotSlowTiles,
     kSlotZRange,
     kSlotTerm,
+    kSlotUsage,
     kSlotCount
 };
 

@@ -721,6 +721,12 @@ struct TileLists {
     const int64_t *tstart;  // null: buckets
     uint32_t cap;
     __device__ __forceinline__ uint64_t *list(int64_t g) const { return ids + (tstart ? tstart[g] : g * (int64_t)cap); }
+    // entries of tile g's list (an overflowed bucket holds only cap of them; such a
+    // call is redone through scanned ranges, see bin_and_composite)
+    __device__ __forceinline__ int count(const uint32_t *tcount, int64_t g) const {
+        const uint32_t n = tcount[g];
+        return (int)(tstart ? n : min(n, cap));
+    }
 };
 
 struct TileSortArgs {
@@ -808,7 +814,7 @@ constexpr int kWarpSortMax = 512;
 __global__ void __launch_bounds__(128) k_sort_tiles_warp(TileSortArgs a) {
     const int64_t g = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     if (g >= a.Tt) return;
-    const int n = (int)a.tcount[g];
+    const int n = a.tl.count(a.tcount, g);
     if (n <= 1 || n > kSortCap) return;  // > kSortCap: radix fallback already sorted it
     if (n > kWarpSortMax) {
         if ((threadIdx.x & 31) == 0) a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
@@ -823,7 +829,7 @@ __global__ void __launch_bounds__(128) k_sort_tiles_warp(TileSortArgs a) {
 
 // Exact block-level sort of one slow tile on (64-bit depth key, id).
 __device__ __noinline__ void sort_one_slow_tile(const TileSortArgs &a, int64_t g, uint64_t *skey, uint32_t *sid) {
-    const int n = (int)a.tcount[g];
+    const int n = a.tl.count(a.tcount, g);
     const uint64_t *depth = a.depth + (int64_t)item_of_tile(a.tile_base, a.nitems, g) * a.stride;
     uint64_t *lst = a.tl.list(g);
     int npad = 64;
@@ -864,7 +870,7 @@ __global__ void __launch_bounds__(128) k_depth_gaps(TileSortArgs a, unsigned lon
     const int lane = threadIdx.x & 31;
     unsigned long long gmin = ~0ull, ties = 0;
     if (g < a.Tt) {
-        const int n = (int)a.tcount[g];
+        const int n = a.tl.count(a.tcount, g);
         const uint64_t *lst = a.tl.list(g);
         const uint64_t *depth = a.depth + (int64_t)item_of_tile(a.tile_base, a.nitems, g) * a.stride;
         for (int k = lane; k + 1 < n; k += 32) {
@@ -921,7 +927,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     const Rec *__restrict__ recs = itp->recs;
     const unsigned lt_mask = (1u << lane) - 1u;
 
-    const int n_all = (int)tcount[g];
+    const int n_all = tls.count(tcount, g);
     const uint64_t *__restrict__ glist = tls.list(g);
     double T = 1.0, cr = 0.0, cg = 0.0, cb = 0.0;
     bool done = !inside;
@@ -1236,6 +1242,11 @@ k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__re
 }
 
 
+__global__ void k_add_i64(int64_t *__restrict__ dst, const int64_t *__restrict__ src, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] += src[i];
+}
+
 __global__ void k_fill_i64(int64_t *p, int64_t n, int64_t v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -1280,118 +1291,113 @@ struct Layout {
 
 // Stage B: histogram (already accumulated in tile_count) -> ranges -> emit ->
 // oversized-tile fallback sort -> composite -> SSE.
-static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
-                              const Rec *recs, const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count,
-                              int index_order, double *sse, cudaStream_t st, unsigned int *flags) {
+// Fallback binning into scanned ranges: exclusive scan of the (complete) tile
+// counts, entries emitted into the ranges, oversized lists presorted by a
+// segmented radix sort.  Also adapts the bucket capacity for the next call.
+static TileLists scanned_lists(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L, const Rec *recs,
+                               const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count, int index_order,
+                               uint32_t cap, cudaStream_t st) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
     int64_t *stats = ctx->scratch_t<int64_t>(kSlotItemStats, 8);
     int64_t maxc = 0;
     for (const auto &h : items) maxc = std::max(maxc, h.count);
-    // binning straight into fixed-capacity tile buckets (capacity adapted after an overflow)
-    const uint32_t cap = ctx->bucket_cap;
-    uint64_t *bucket = ctx->scratch_t<uint64_t>(kSlotPairKeysAlt, (size_t)std::max<int64_t>(Tt, 1) * cap);
-    if (maxc > 0 && Tt > 0) {
-        BinArgs ba{recs, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tile_count, bucket, cap, flags, L.stride,
-                   index_order};
-        k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
+    // scanned ranges: exclusive scan of the (complete) tile counts, ids emitted
+    // into the ranges, oversized tiles presorted by a segmented radix sort
+    int64_t *tstart = ctx->scratch_t<int64_t>(kSlotRanges, (size_t)Tt);
+    uint32_t *big_list = ctx->scratch_t<uint32_t>(kSlotPairValsAlt, (size_t)Tt);
+    unsigned int *big_n = (unsigned int *)(stats + 2);
+    unsigned int *vmax = (unsigned int *)(stats + 4);
+    int64_t *d_total = stats;
+    int64_t *d_Tt = stats + 1;
+    AIRGS_CUDA_TRY(cudaMemsetAsync(big_n, 0, sizeof(unsigned int), st));
+    AIRGS_CUDA_TRY(cudaMemsetAsync(vmax, 0, sizeof(unsigned int), st));
+    h2d_small(ctx, d_Tt, &Tt, sizeof(int64_t), st);
+    {
+        const int bps = (int)std::max<int64_t>(1, ceil_div(Tt, kScanTile));
+        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
+        seg_scan<int64_t>(TileScanIn{tile_count}, TileScanOut{tstart, big_list, big_n, vmax, (uint32_t)kSortCap},
+                          d_Tt, 1, Tt, blocks, d_total, st, &NL);
+        check_launch();
+    }
+    int64_t P = 0;
+    unsigned int hbig = 0, hmax = 0;
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&P, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbig, big_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hmax, vmax, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    {  // adapt the bucket capacity for the next call
+        uint32_t c = cap;
+        while (c < hmax && c < (uint32_t)kSortCap) c <<= 1;
+        ctx->bucket_cap = c;
+    }
+    uint64_t *ids = ctx->scratch_t<uint64_t>(kSlotPairVals, (size_t)std::max<int64_t>(P, 1));
+    uint32_t *cursor = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)Tt);
+    AIRGS_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * Tt, st));
+    if (P > 0) {
+        EmitArgs ea{recs, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tstart, cursor, ids, L.stride,
+                    index_order};
+        k_emit<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ea);
         ++NL;
         check_launch();
     }
-    unsigned int hflags = 0;
-    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-    if (hflags & kFlagInvalidParam)
-        throw ApiFailure(AIRGS_E_VALIDATION, "frame contains invalid primitive parameters");
-    TileLists tl{bucket, nullptr, cap};
-    if (hflags & kFlagBucketOverflow) {
-        // scanned ranges: exclusive scan of the (complete) tile counts, ids emitted
-        // into the ranges, oversized tiles presorted by a segmented radix sort
-        int64_t *tstart = ctx->scratch_t<int64_t>(kSlotRanges, (size_t)Tt);
-        uint32_t *big_list = ctx->scratch_t<uint32_t>(kSlotPairValsAlt, (size_t)Tt);
-        unsigned int *big_n = (unsigned int *)(stats + 2);
-        unsigned int *vmax = (unsigned int *)(stats + 4);
-        int64_t *d_total = stats;
-        int64_t *d_Tt = stats + 1;
-        AIRGS_CUDA_TRY(cudaMemsetAsync(big_n, 0, sizeof(unsigned int), st));
-        AIRGS_CUDA_TRY(cudaMemsetAsync(vmax, 0, sizeof(unsigned int), st));
-        h2d_small(ctx, d_Tt, &Tt, sizeof(int64_t), st);
-        {
-            const int bps = (int)std::max<int64_t>(1, ceil_div(Tt, kScanTile));
-            int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, bps);
-            seg_scan<int64_t>(TileScanIn{tile_count}, TileScanOut{tstart, big_list, big_n, vmax, (uint32_t)kSortCap},
-                              d_Tt, 1, Tt, blocks, d_total, st, &NL);
-            check_launch();
-        }
-        int64_t P = 0;
-        unsigned int hbig = 0, hmax = 0;
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(&P, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(&hbig, big_n, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-        AIRGS_CUDA_TRY(cudaMemcpyAsync(&hmax, vmax, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    if (hbig > 0) {
+        // oversized tiles: stable radix sort of each range by index, then by depth key
+        std::vector<uint32_t> hlist(hbig);
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(hlist.data(), big_list, sizeof(uint32_t) * hbig, cudaMemcpyDeviceToHost, st));
+        std::vector<uint32_t> hcnt(hbig);
+        for (unsigned b = 0; b < hbig; ++b)
+            AIRGS_CUDA_TRY(
+                cudaMemcpyAsync(&hcnt[b], tile_count + hlist[b], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-        {  // adapt the bucket capacity for the next call
-            uint32_t c = cap;
-            while (c < hmax && c < (uint32_t)kSortCap) c <<= 1;
-            ctx->bucket_cap = c;
+        std::vector<int64_t> seg(2 * hbig);
+        int64_t tot = 0, mx = 0;
+        for (unsigned b = 0; b < hbig; ++b) {
+            seg[b] = tot;
+            seg[hbig + b] = hcnt[b];
+            tot += hcnt[b];
+            mx = std::max<int64_t>(mx, hcnt[b]);
         }
-        uint64_t *ids = ctx->scratch_t<uint64_t>(kSlotPairVals, (size_t)std::max<int64_t>(P, 1));
-        uint32_t *cursor = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)Tt);
-        AIRGS_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * Tt, st));
-        if (P > 0) {
-            EmitArgs ea{recs, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tstart, cursor, ids, L.stride,
-                        index_order};
-            k_emit<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ea);
-            ++NL;
-            check_launch();
-        }
-        if (hbig > 0) {
-            // oversized tiles: stable radix sort of each range by index, then by depth key
-            std::vector<uint32_t> hlist(hbig);
-            AIRGS_CUDA_TRY(cudaMemcpyAsync(hlist.data(), big_list, sizeof(uint32_t) * hbig, cudaMemcpyDeviceToHost, st));
-            std::vector<uint32_t> hcnt(hbig);
-            for (unsigned b = 0; b < hbig; ++b)
-                AIRGS_CUDA_TRY(
-                    cudaMemcpyAsync(&hcnt[b], tile_count + hlist[b], sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-            AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-            std::vector<int64_t> seg(2 * hbig);
-            int64_t tot = 0, mx = 0;
-            for (unsigned b = 0; b < hbig; ++b) {
-                seg[b] = tot;
-                seg[hbig + b] = hcnt[b];
-                tot += hcnt[b];
-                mx = std::max<int64_t>(mx, hcnt[b]);
-            }
-            int32_t *d_tile_item = ctx->scratch_t<int32_t>(kSlotTileItem, (size_t)Tt);
-            k_tile_item<<<(unsigned)ceil_div(Tt, 256), 256, 0, st>>>(L.d_tile_base, nitems, Tt, d_tile_item);
-            ++NL;
-            int64_t *d_seg = ctx->scratch_t<int64_t>(kSlotMisc3, 2 * (size_t)hbig);
-            h2d_small(ctx, d_seg, seg.data(), sizeof(int64_t) * 2 * hbig, st);
-            uint64_t *k1 = ctx->scratch_t<uint64_t>(kSlotKeys, (size_t)tot);
-            uint64_t *k2 = ctx->scratch_t<uint64_t>(kSlotKeysAlt, (size_t)tot);
-            uint32_t *v1 = ctx->scratch_t<uint32_t>(kSlotVals, (size_t)tot);
-            uint32_t *v2 = ctx->scratch_t<uint32_t>(kSlotValsAlt, (size_t)tot);
-            uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)hbig * 256 * ceil_div(mx, kSortTile));
-            BigArgs ba{big_list, tstart, tile_count, d_tile_item, depth, ids, L.stride, d_seg, k1, v1};
-            const dim3 gg((unsigned)std::min<int64_t>(64, ceil_div(mx, 256)), hbig);
-            k_big_gather<<<gg, 256, 0, st>>>(ba);
-            k_ids_as_keys<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(v1, k1, tot);
-            NL += 2;
-            bool alt = radix_sort<uint64_t>(k1, v1, k2, v2, d_seg, d_seg + hbig, (int)hbig, mx, 32, hist, st, &NL);
-            uint32_t *vs = alt ? v2 : v1;
-            uint64_t *ks = alt ? k2 : k1;
-            uint64_t *ko = alt ? k1 : k2;
-            uint32_t *vo = alt ? v1 : v2;
-            k_gather_keys<<<gg, 256, 0, st>>>(vs, d_seg, big_list, d_tile_item, tile_count, depth, L.stride, ks);
-            ++NL;
-            bool alt2 = radix_sort<uint64_t>(ks, vs, ko, vo, d_seg, d_seg + hbig, (int)hbig, mx, 64, hist, st, &NL);
-            k_big_scatter<<<gg, 256, 0, st>>>(ba, alt2 ? vo : vs);
-            ++NL;
-            check_launch();
-            AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
-        }
-        tl = TileLists{ids, tstart, 0u};
+        int32_t *d_tile_item = ctx->scratch_t<int32_t>(kSlotTileItem, (size_t)Tt);
+        k_tile_item<<<(unsigned)ceil_div(Tt, 256), 256, 0, st>>>(L.d_tile_base, nitems, Tt, d_tile_item);
+        ++NL;
+        int64_t *d_seg = ctx->scratch_t<int64_t>(kSlotMisc3, 2 * (size_t)hbig);
+        h2d_small(ctx, d_seg, seg.data(), sizeof(int64_t) * 2 * hbig, st);
+        uint64_t *k1 = ctx->scratch_t<uint64_t>(kSlotKeys, (size_t)tot);
+        uint64_t *k2 = ctx->scratch_t<uint64_t>(kSlotKeysAlt, (size_t)tot);
+        uint32_t *v1 = ctx->scratch_t<uint32_t>(kSlotVals, (size_t)tot);
+        uint32_t *v2 = ctx->scratch_t<uint32_t>(kSlotValsAlt, (size_t)tot);
+        uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)hbig * 256 * ceil_div(mx, kSortTile));
+        BigArgs ba{big_list, tstart, tile_count, d_tile_item, depth, ids, L.stride, d_seg, k1, v1};
+        const dim3 gg((unsigned)std::min<int64_t>(64, ceil_div(mx, 256)), hbig);
+        k_big_gather<<<gg, 256, 0, st>>>(ba);
+        k_ids_as_keys<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(v1, k1, tot);
+        NL += 2;
+        bool alt = radix_sort<uint64_t>(k1, v1, k2, v2, d_seg, d_seg + hbig, (int)hbig, mx, 32, hist, st, &NL);
+        uint32_t *vs = alt ? v2 : v1;
+        uint64_t *ks = alt ? k2 : k1;
+        uint64_t *ko = alt ? k1 : k2;
+        uint32_t *vo = alt ? v1 : v2;
+        k_gather_keys<<<gg, 256, 0, st>>>(vs, d_seg, big_list, d_tile_item, tile_count, depth, L.stride, ks);
+        ++NL;
+        bool alt2 = radix_sort<uint64_t>(ks, vs, ko, vo, d_seg, d_seg + hbig, (int)hbig, mx, 64, hist, st, &NL);
+        k_big_scatter<<<gg, 256, 0, st>>>(ba, alt2 ? vo : vs);
+        ++NL;
+        check_launch();
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
     }
+    return TileLists{ids, tstart, 0u};
+}
+
+// Depth-order every tile list, composite, reduce the per-item SSE.
+static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
+                               const TileLists &tl, const Rec *recs, const uint64_t *depth, const int32_t *ntiles,
+                               uint32_t *tile_count, double *sse, cudaStream_t st) {
+    const int nitems = L.nitems;
+    int64_t &NL = ctx->launches;
+    const int64_t Tt = L.Tt;
+    int64_t *stats = ctx->scratch_t<int64_t>(kSlotItemStats, 8);
     if (Tt > 0) {
         // depth-order every tile list: warp-level register sort, block-level exact sort for the rest
         unsigned int *slow_n = (unsigned int *)(stats + 3);
@@ -1483,6 +1489,86 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         check_launch();
     }
     // small uploads travel as kernel parameters: nothing host-side must outlive the launches
+}
+
+static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
+                              const Rec *recs, const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count,
+                              int index_order, double *sse, cudaStream_t st, unsigned int *flags) {
+    const int nitems = L.nitems;
+    int64_t &NL = ctx->launches;
+    const int64_t Tt = L.Tt;
+    int64_t *stats = ctx->scratch_t<int64_t>(kSlotItemStats, 8);
+    int64_t maxc = 0;
+    for (const auto &h : items) maxc = std::max(maxc, h.count);
+    // binning straight into fixed-capacity tile buckets (capacity adapted after an overflow)
+    const uint32_t cap = ctx->bucket_cap;
+    uint64_t *bucket = ctx->scratch_t<uint64_t>(kSlotPairKeysAlt, (size_t)std::max<int64_t>(Tt, 1) * cap);
+    if (maxc > 0 && Tt > 0) {
+        BinArgs ba{recs, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tile_count, bucket, cap, flags, L.stride,
+                   index_order};
+        k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
+        ++NL;
+        check_launch();
+    }
+    // usage counts are ADDED to the caller's arrays (airgs_b200.h): accumulate
+    // this call's counts in zeroed scratch first, so that a redone call cannot
+    // count twice, and add them once at the end
+    std::vector<ItemHost> work(items);
+    std::vector<std::pair<int64_t *, int64_t *>> usage_map;  // (caller array, scratch)
+    {
+        int64_t total = 0;
+        std::vector<std::pair<int64_t *, int64_t>> uniq;
+        for (const ItemHost &h : items)
+            if (h.usage && std::find_if(uniq.begin(), uniq.end(), [&](const std::pair<int64_t *, int64_t> &u) {
+                               return u.first == h.usage;
+                           }) == uniq.end()) {
+                uniq.push_back({h.usage, h.count});
+                total += h.count;
+            }
+        if (total > 0) {
+            int64_t *scratch = ctx->scratch_t<int64_t>(kSlotUsage, (size_t)total);
+            AIRGS_CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(int64_t) * total, st));
+            int64_t off = 0;
+            for (const auto &u : uniq) {
+                usage_map.push_back({u.first, scratch + off});
+                off += u.second;
+            }
+            for (ItemHost &h : work)
+                if (h.usage)
+                    for (const auto &m : usage_map)
+                        if (m.first == h.usage) h.usage = m.second;
+        }
+    }
+    TileLists tl{bucket, nullptr, cap};
+    sort_composite_sse(ctx, work, L, tl, recs, depth, ntiles, tile_count, sse, st);
+    // one host synchronisation per render: parameter validity and bucket overflow
+    unsigned int hflags = 0;
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hflags & kFlagInvalidParam)
+        throw ApiFailure(AIRGS_E_VALIDATION, "frame contains invalid primitive parameters");
+    if (hflags & kFlagBucketOverflow) {
+        // some tile outgrew its bucket: redo this call through scanned ranges
+        // (images and SSE are overwritten, the usage scratch is reset)
+        for (size_t k = 0; k < usage_map.size(); ++k) {
+            int64_t n = 0;
+            for (const ItemHost &h : items)
+                if (h.usage == usage_map[k].first) n = h.count;
+            AIRGS_CUDA_TRY(cudaMemsetAsync(usage_map[k].second, 0, sizeof(int64_t) * n, st));
+        }
+        const TileLists tl2 = scanned_lists(ctx, items, L, recs, depth, ntiles, tile_count, index_order, cap, st);
+        sort_composite_sse(ctx, work, L, tl2, recs, depth, ntiles, tile_count, sse, st);
+    }
+    for (const auto &m : usage_map) {
+        int64_t n = 0;
+        for (const ItemHost &h : items)
+            if (h.usage == m.first) n = h.count;
+        if (n > 0) {
+            k_add_i64<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(m.first, m.second, n);
+            ++NL;
+            check_launch();
+        }
+    }
 }
 
 // Upload per-item layout arrays (tile bases, tiles_x, counts, tile -> item map).
