@@ -119,6 +119,22 @@ AIRGS_API int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts);
  * Synchronises. */
 AIRGS_API int airgs_eval_margins(airgs_ctx *ctx, double *margins);
 
+/* ---- image metrics of the trainer's loss ---------------------------------- */
+
+/* Mean windowed SSIM of the luminance of a vs b (device float64, (h, w) when
+ * channels == 1 or (h, w, 3)), ss/metrics.py:77-86, and optionally its
+ * gradient w.r.t. a (same shape as a), ss/metrics.py:89-113.  window = the
+ * reference's 11-tap Gaussian g (sigma 1.5) normalised to sum 1 (host
+ * float64[11]).  ssim_out: device float64[1].  grad may be NULL.  Fails with
+ * AIRGS_E_STRUCTURAL when the image is smaller than the window. */
+AIRGS_API int airgs_ssim(airgs_ctx *ctx, const double *a, const double *b, int32_t height, int32_t width,
+                         int32_t channels, const double *window, double *ssim_out, double *grad, void *stream);
+
+/* mean |a - b| over n values (ss/metrics.py:116-118) into l1_out (device
+ * float64[1]) and optionally its gradient sign(a - b) / n (ss/metrics.py:121). */
+AIRGS_API int airgs_l1(airgs_ctx *ctx, const double *a, const double *b, int64_t n, double *l1_out, double *grad,
+                       void *stream);
+
 /* ---- rasterizer --------------------------------------------------------- */
 
 /* Batched render: replaces ss/rasterizer.py:113-240 (_activate, _prepare,

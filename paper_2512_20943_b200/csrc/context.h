@@ -153,6 +153,9 @@ enum Slot : int {
     kSlotZRange,
     kSlotTerm,
     kSlotUsage,
+    kSlotMetric0,
+    kSlotMetric1,
+    kSlotMetric2,
     kSlotCount
 };
 

@@ -280,11 +280,68 @@ def gen_session(ss):
     np.savez_compressed(os.path.join(HERE, "session.npz"), **out)
 
 
+def gen_metrics(ss):
+    """SSIM / SSIM gradient / L1 / L1 gradient (ss/metrics.py:77-121) on
+    colour and grey image pairs."""
+    from splatstream import metrics
+
+    out = {}
+    cases = [(0, (24, 31, 3)), (1, (16, 16)), (2, (40, 57, 3)), (3, (11, 11, 3))]
+    for cid, shape in cases:
+        rng = np.random.default_rng(700 + cid)
+        a = rng.uniform(0, 1, shape)
+        b = np.clip(a + rng.normal(0, 0.1, shape), 0, 1)
+        out[f"c{cid}_a"], out[f"c{cid}_b"] = a, b
+        out[f"c{cid}_ssim"] = np.array(metrics.ssim(a, b))
+        out[f"c{cid}_ssim_grad"] = metrics.ssim_grad(a, b)
+        out[f"c{cid}_l1"] = np.array(metrics.l1(a, b))
+        out[f"c{cid}_l1_grad"] = metrics.l1_grad(a, b)
+        out[f"c{cid}_ssim_self"] = np.array(metrics.ssim(a, a))
+    np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
+
+
+def gen_backward(ss):
+    """render_forward / render_backward (ss/rasterizer.py:248-369, the
+    compiled _composite.backward): per-parameter gradients of a random
+    image-space loss gradient, SH degrees 0 and 1."""
+    from splatstream import camera, model, rasterizer
+
+    out = {}
+    cases = [(0, 300, 0, (40, 32), 0.4), (1, 250, 1, (33, 29), 0.4), (2, 1200, 0, (72, 56), 0.6)]
+    for cid, n, deg, res, spread in cases:
+        rng = np.random.default_rng(800 + cid)
+        p = random_params(rng, n, deg, spread)
+        cam = camera.ring_rig(2, radius=3.0, height=0.3, focal=res[0] * 40.0 / 48.0, resolution=res)[1]
+        f = model.GaussianFrame(params=p)
+        image, state = rasterizer.render_forward(f, cam)
+        d_image = rng.normal(0, 1.0, image.shape)
+        grads = rasterizer.render_backward(state, d_image)
+        out[f"c{cid}_params"] = p
+        for k, v in cam_arrays([cam]).items():
+            out[f"c{cid}_{k}"] = v
+        out[f"c{cid}_image"] = image
+        out[f"c{cid}_d_image"] = d_image
+        out[f"c{cid}_grads"] = grads
+        prep, t_final, masks = state
+        out[f"c{cid}_t_final"] = t_final
+        d2 = rasterizer._kernels.backward(prep.means2d, prep.conics, prep.alphas, prep.colors, prep.bboxes,
+                                          res[1], res[0], masks, t_final, np.ascontiguousarray(d_image))
+        for name, v in zip(("d_means2d", "d_conics", "d_alphas", "d_colors"), d2):
+            out[f"c{cid}_{name}"] = v
+        out[f"c{cid}_order"] = prep.order
+    np.savez_compressed(os.path.join(HERE, "backward.npz"), **out)
+
+
+GENERATORS = ("gen_render", "gen_composite", "gen_codec", "gen_delta", "gen_pruning", "gen_grouping", "gen_session",
+              "gen_metrics", "gen_backward")
+
+
 def main():
     ss = import_reference()
-    for fn in (gen_render, gen_composite, gen_codec, gen_delta, gen_pruning, gen_grouping, gen_session):
-        fn(ss)
-        print("ok", fn.__name__)
+    only = sys.argv[1:] or GENERATORS  # e.g. `make_golden.py gen_metrics`
+    for name in only:
+        globals()[name](ss)
+        print("ok", name)
     total = sum(os.path.getsize(p) for p in glob.glob(os.path.join(HERE, "*.npz")))
     print(f"fixtures: {total / 1e6:.2f} MB")
 
