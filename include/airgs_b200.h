@@ -119,6 +119,17 @@ AIRGS_API int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts);
  * Synchronises. */
 AIRGS_API int airgs_eval_margins(airgs_ctx *ctx, double *margins);
 
+/* Backward pass of one view (training; ss/rasterizer.py:248-369 render_forward
+ * + render_backward with the compiled _composite.backward, ss/_composite.pyx:
+ * 77-152): recomputes the forward with its contribution record, back-
+ * propagates d_image (device float64 (h, w, 3), dLoss/dpixel of the
+ * unclipped forward image) through compositing and projection, and writes
+ * the pre-activation parameter gradients grads (device float64 row-major
+ * [count][width], every row written).  Depth order is the forward's (the
+ * reference's frozen_order option is not supported). */
+AIRGS_API int airgs_render_backward(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
+                                    const double *d_image, double *grads, void *stream);
+
 /* ---- image metrics of the trainer's loss ---------------------------------- */
 
 /* Mean windowed SSIM of the luminance of a vs b (device float64, (h, w) when

@@ -67,6 +67,7 @@ SIGNATURES = {
     "airgs_eval_margins": (ctypes.c_int, [vp, c_double_p]),
     "airgs_render": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), i32, ctypes.POINTER(CameraC), i32,
                                     ctypes.POINTER(ItemC), i32, vp, vp]),
+    "airgs_render_backward": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), ctypes.POINTER(CameraC), vp, vp, vp]),
     "airgs_composite_forward": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp]),
     "airgs_sse": (ctypes.c_int, [vp, vp, vp, i64, vp, vp]),
     "airgs_ssim": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, c_double_p, vp, vp, vp]),

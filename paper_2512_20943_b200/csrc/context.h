@@ -156,6 +156,10 @@ enum Slot : int {
     kSlotMetric0,
     kSlotMetric1,
     kSlotMetric2,
+    kSlotRecBase,
+    kSlotRecBits,
+    kSlotBwdGrad,
+    kSlotTFinal,
     kSlotCount
 };
 

@@ -437,6 +437,8 @@ struct CompItem {
     int64_t *usage;          // [n] or null
     double *sse_tiles;       // per (tile, warp) of this item
     int32_t *term;           // (h,w) terminating primitive or -1 (diagnostic counters only)
+    uint32_t *cbits;         // RECORD: contribution bit per (pixel, tile-list entry), or null
+    const int64_t *cbase;    // RECORD: first word of each (global) tile's bit block
     int32_t w, h, tiles_x, clip;
 };
 
@@ -893,7 +895,7 @@ __global__ void __launch_bounds__(128) k_depth_gaps(TileSortArgs a, unsigned lon
 // domain, proven guard band) and builds a per-lane candidate mask; phase B has
 // every lane run its own candidates through the exact fp64 path in depth
 // order (two candidates' exp in flight).
-template <bool USAGE, bool STATS>
+template <bool USAGE, bool STATS, bool RECORD = false>
 __global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
 k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
             const TileLists tls, const uint32_t *__restrict__ tcount, unsigned long long *__restrict__ stats) {
@@ -1053,6 +1055,11 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                     cb += wgt * sh.bl[j1];
                     T = T * (1.0 - ap1);
                     if (USAGE) atomicAdd(&sh.cnt[j1], 1);
+                    if (RECORD) {  // the reference's record=True mask (_composite.pyx:69-71)
+                        const int e = base + j1;
+                        atomicOr(itp->cbits + itp->cbase[g] + (e >> 5) * kTileThreads + (ly * kTile + lx),
+                                 1u << (e & 31));
+                    }
                     if (STATS) {
                         ++ncon;
                         if (term_id < 0 && kAlphaClamp * T <= kEpsContrib) term_id = (int)sh.gid[j1];
@@ -1069,6 +1076,11 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                         cb += wgt * sh.bl[j2];
                         T = T * (1.0 - ap2);
                         if (USAGE) atomicAdd(&sh.cnt[j2], 1);
+                        if (RECORD) {
+                            const int e = base + j2;
+                            atomicOr(itp->cbits + itp->cbase[g] + (e >> 5) * kTileThreads + (ly * kTile + lx),
+                                     1u << (e & 31));
+                        }
                         if (STATS) {
                             ++ncon;
                             if (term_id < 0 && kAlphaClamp * T <= kEpsContrib) term_id = (int)sh.gid[j2];
@@ -1391,9 +1403,28 @@ static TileLists scanned_lists(airgs_ctx *ctx, const std::vector<ItemHost> &item
 }
 
 // Depth-order every tile list, composite, reduce the per-item SSE.
+// Contribution record of a forward pass (the reference's record=True masks,
+// _composite.pyx:33-35,69-71) for the backward pass: one bit per (pixel,
+// tile-list entry), tile g's block of ceil(n_g / 32) x 256 words at cbase[g].
+struct RecordOut {
+    TileLists tl{};          // the depth-ordered lists the forward composited
+    uint32_t *cbits = nullptr;
+    int64_t *cbase = nullptr;
+};
+
+struct RecWordsIn {
+    const uint32_t *tcount;
+    TileLists tl;
+    __device__ int64_t operator()(int, int64_t g) const { return (int64_t)((tl.count(tcount, g) + 31) >> 5) * kTileThreads; }
+};
+struct RecWordsOut {
+    int64_t *base;
+    __device__ void operator()(int, int64_t g, int64_t ex, int64_t) const { base[g] = ex; }
+};
+
 static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
                                const TileLists &tl, const Rec *recs, const uint64_t *depth, const int32_t *ntiles,
-                               uint32_t *tile_count, double *sse, cudaStream_t st) {
+                               uint32_t *tile_count, double *sse, cudaStream_t st, RecordOut *rec = nullptr) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
@@ -1451,6 +1482,26 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         any_target |= h.target != nullptr;
         has_t[s] = h.target != nullptr;
     }
+    if (rec && Tt > 0) {  // record layout: exclusive scan of the per-tile bit-block sizes
+        int64_t *cbase = ctx->scratch_t<int64_t>(kSlotRecBase, (size_t)Tt + 1);
+        int64_t *d_Tt = stats + 5, *d_total = stats + 6;
+        h2d_small(ctx, d_Tt, &Tt, sizeof(int64_t), st);
+        int64_t *blocks = ctx->scratch_t<int64_t>(kSlotScanBlocks, (size_t)std::max<int64_t>(1, ceil_div(Tt, kScanTile)));
+        seg_scan<int64_t>(RecWordsIn{tile_count, tl}, RecWordsOut{cbase}, d_Tt, 1, Tt, blocks, d_total, st, &NL);
+        check_launch();
+        int64_t words = 0;
+        AIRGS_CUDA_TRY(cudaMemcpyAsync(&words, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        uint32_t *cbits = ctx->scratch_t<uint32_t>(kSlotRecBits, (size_t)std::max<int64_t>(words, 1));
+        AIRGS_CUDA_TRY(cudaMemsetAsync(cbits, 0, sizeof(uint32_t) * std::max<int64_t>(words, 1), st));
+        for (CompItem &c : ci) {
+            c.cbits = cbits;
+            c.cbase = cbase;
+        }
+        rec->tl = tl;
+        rec->cbits = cbits;
+        rec->cbase = cbase;
+    }
     CompItem *d_ci = (CompItem *)ctx->scratch(kSlotMisc1, sizeof(CompItem) * nitems);
     uint8_t *d_has = (uint8_t *)ctx->scratch(kSlotMisc2, nitems);
     h2d_small(ctx, d_ci, ci.data(), sizeof(CompItem) * nitems, st);
@@ -1458,7 +1509,10 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
     cudaEvent_t t_comp = Tt > 0 ? ctx->time_begin(st) : nullptr;
     if (Tt > 0) {
         unsigned long long *cs = ctx->d_stats;
-        if (stats_on) {
+        if (rec) {
+            k_composite<false, false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                                   tile_count, cs);
+        } else if (stats_on) {
             if (any_usage)
                 k_composite<true, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
                                                                                tile_count, cs);
@@ -1493,7 +1547,8 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
 
 static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
                               const Rec *recs, const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count,
-                              int index_order, double *sse, cudaStream_t st, unsigned int *flags) {
+                              int index_order, double *sse, cudaStream_t st, unsigned int *flags,
+                              RecordOut *rec = nullptr) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
@@ -1540,7 +1595,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         }
     }
     TileLists tl{bucket, nullptr, cap};
-    sort_composite_sse(ctx, work, L, tl, recs, depth, ntiles, tile_count, sse, st);
+    sort_composite_sse(ctx, work, L, tl, recs, depth, ntiles, tile_count, sse, st, rec);
     // one host synchronisation per render: parameter validity and bucket overflow
     unsigned int hflags = 0;
     AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
@@ -1557,7 +1612,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
             AIRGS_CUDA_TRY(cudaMemsetAsync(usage_map[k].second, 0, sizeof(int64_t) * n, st));
         }
         const TileLists tl2 = scanned_lists(ctx, items, L, recs, depth, ntiles, tile_count, index_order, cap, st);
-        sort_composite_sse(ctx, work, L, tl2, recs, depth, ntiles, tile_count, sse, st);
+        sort_composite_sse(ctx, work, L, tl2, recs, depth, ntiles, tile_count, sse, st, rec);
     }
     for (const auto &m : usage_map) {
         int64_t n = 0;
@@ -1599,8 +1654,19 @@ static void upload_layout(airgs_ctx *ctx, const std::vector<ItemHost> &items, La
 }
 
 
+// What a backward pass needs from its (recomputed) forward pass.
+struct BwdState {
+    RecordOut rec;
+    const Rec *recs = nullptr;
+    double *t_final = nullptr;  // set by the caller: forward writes (h, w)
+    int64_t Tt = 0;
+    const int64_t *tile_base = nullptr;
+    uint32_t *tile_count = nullptr;
+};
+
 static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, const airgs_camera *cams,
-                        int ncams, const airgs_view_item *items, int nitems, double *sse, cudaStream_t st) {
+                        int ncams, const airgs_view_item *items, int nitems, double *sse, cudaStream_t st,
+                        BwdState *bwd = nullptr) {
     if (nitems <= 0) return;
     if (nframes <= 0 || ncams <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "no frames or cameras");
     std::vector<ItemHost> ih(nitems);
@@ -1627,9 +1693,9 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         h.tiles_y = (c.height + kTile - 1) / kTile;
         h.target = v.target;
         h.image = v.image;
-        h.trans = nullptr;
+        h.trans = bwd ? bwd->t_final : nullptr;
         h.usage = v.usage;
-        h.clip = 1;
+        h.clip = bwd ? 0 : 1;  // the forward of render_forward returns the unclipped image
         per_frame[v.frame].push_back(s);
         stride = std::max(stride, f.count);
     }
@@ -1697,7 +1763,343 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         check_launch();
     }
     ctx->time_end(t_proj, st, 1);
-    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags);
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags, bwd ? &bwd->rec : nullptr);
+    if (bwd) {
+        bwd->recs = recs;
+        bwd->Tt = L.Tt;
+        bwd->tile_base = L.d_tile_base;
+        bwd->tile_count = tile_count;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// backward (training): _composite.backward
+// (ss/_composite.pyx:77-152) and the projection chain rule of render_backward
+// (ss/rasterizer.py:270-369).
+
+constexpr int kBwdBatch = 128;
+struct BwdShared {
+    double f[9][kBwdBatch];    // mx, my, a, b, c, al, cr, cg, cb of the staged entries
+    double acc[9][kBwdBatch];  // d_means2d (2), d_conics (3), d_alphas, d_colors (3)
+    uint32_t gid[kBwdBatch];
+    double2 exptab[kExpN];
+};
+
+// One CTA per tile, one pixel per thread: the pixel's recorded contributors in
+// reverse depth order with the reference's per-pixel recurrences (t_before =
+// T / (1 - ap), the running colour accumulator, d_ap with the clamp rule);
+// per-entry gradients are summed in shared memory then added to the per
+// primitive totals G[id][9] (fp64 atomics: the cross-pixel summation order
+// differs from the reference's row-major loop, the per-pixel terms do not).
+__global__ void __launch_bounds__(kTileThreads) k_composite_bwd(const Rec *__restrict__ recs, const TileLists tls,
+                                                               const uint32_t *__restrict__ tcount,
+                                                               const uint32_t *__restrict__ cbits,
+                                                               const int64_t *__restrict__ cbase, int tiles_x, int w,
+                                                               int h, const double *__restrict__ t_final,
+                                                               const double *__restrict__ d_image,
+                                                               double *__restrict__ G) {
+    __shared__ BwdShared sh;
+    {
+        const unsigned long long *src = &kExpTable[0][0];
+        for (int k = threadIdx.x; k < kExpN; k += kTileThreads)
+            sh.exptab[k] = make_double2(__longlong_as_double((long long)src[2 * k]),
+                                        __longlong_as_double((long long)src[2 * k + 1]));
+    }
+    const int64_t g = blockIdx.x;
+    const int tx = (int)(g % tiles_x), ty = (int)(g / tiles_x);
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int px = tx * kTile + lx, py = ty * kTile + ly;
+    const bool inside = px < w && py < h;
+    const int64_t pix = (int64_t)py * w + px;
+    double T = inside ? t_final[pix] : 1.0;
+    double dc0 = 0.0, dc1 = 0.0, dc2 = 0.0;
+    if (inside) {
+        dc0 = d_image[3 * pix];
+        dc1 = d_image[3 * pix + 1];
+        dc2 = d_image[3 * pix + 2];
+    }
+    double ac0 = 0.0, ac1 = 0.0, ac2 = 0.0;
+    const double pxd = (double)px + 0.5, pyd = (double)py + 0.5;
+    const int n = tls.count(tcount, g);
+    const uint64_t *lst = tls.list(g);
+    const uint32_t *bits = cbits + cbase[g] + threadIdx.x;
+    for (int hi = n; hi > 0; hi -= kBwdBatch) {
+        const int lo = max(0, hi - kBwdBatch), nb = hi - lo;
+        __syncthreads();
+        if ((int)threadIdx.x < nb) {
+            const int t = threadIdx.x;
+            const uint32_t id = (uint32_t)lst[lo + t];
+            const Rec &r = recs[id];
+            sh.gid[t] = id;
+            sh.f[0][t] = r.mx;
+            sh.f[1][t] = r.my;
+            sh.f[2][t] = r.ca;
+            sh.f[3][t] = r.cb;
+            sh.f[4][t] = r.cc;
+            sh.f[5][t] = r.al;
+            sh.f[6][t] = r.cr;
+            sh.f[7][t] = r.cg;
+            sh.f[8][t] = r.cbl;
+#pragma unroll
+            for (int q = 0; q < 9; ++q) sh.acc[q][t] = 0.0;
+        }
+        __syncthreads();
+        if (inside) {
+            for (int wd = (hi - 1) >> 5; wd >= (lo >> 5); --wd) {
+                uint32_t m = bits[(int64_t)wd * kTileThreads];
+                // keep entries in [lo, hi) of this word
+                const int e0 = wd << 5;
+                if (e0 < lo) m &= ~0u << (lo - e0);
+                if (e0 + 32 > hi) m &= (hi - e0) >= 32 ? ~0u : ((1u << (hi - e0)) - 1u);
+                while (m) {
+                    const int b = 31 - __clz(m);
+                    m &= ~(1u << b);
+                    const int j = e0 + b - lo;
+                    const double mx = sh.f[0][j], my = sh.f[1][j], a = sh.f[2][j], bb = sh.f[3][j], c = sh.f[4][j];
+                    const double al = sh.f[5][j], cr = sh.f[6][j], cg = sh.f[7][j], cb = sh.f[8][j];
+                    // _composite.pyx:121-151, op for op
+                    const double dy = pyd - my;
+                    const double dx = pxd - mx;
+                    const double e = 0.5 * (a * dx * dx + c * dy * dy) + bb * dx * dy;
+                    const double gg = exp_tab(-e, sh.exptab);
+                    const double raw = al * gg;
+                    const double ap = raw > kAlphaClamp ? kAlphaClamp : raw;
+                    const double t_before = T / (1.0 - ap);
+                    const double wgt = ap * t_before;
+                    atomicAdd(&sh.acc[6][j], wgt * dc0);
+                    atomicAdd(&sh.acc[7][j], wgt * dc1);
+                    atomicAdd(&sh.acc[8][j], wgt * dc2);
+                    const double dc_dot_col = (dc0 * cr + dc1 * cg) + dc2 * cb;
+                    double d_ap = t_before * dc_dot_col - ((ac0 * dc0 + ac1 * dc1) + ac2 * dc2) / (1.0 - ap);
+                    if (raw >= kAlphaClamp) d_ap = 0.0;
+                    atomicAdd(&sh.acc[5][j], d_ap * gg);
+                    const double d_g = d_ap * al;
+                    const double d_e = -gg * d_g;
+                    atomicAdd(&sh.acc[0][j], -d_e * (a * dx + bb * dy));
+                    atomicAdd(&sh.acc[1][j], -d_e * (bb * dx + c * dy));
+                    atomicAdd(&sh.acc[2][j], d_e * 0.5 * dx * dx);
+                    atomicAdd(&sh.acc[3][j], d_e * dx * dy);
+                    atomicAdd(&sh.acc[4][j], d_e * 0.5 * dy * dy);
+                    ac0 += cr * wgt;
+                    ac1 += cg * wgt;
+                    ac2 += cb * wgt;
+                    T = t_before;
+                }
+            }
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < nb) {
+            const int t = threadIdx.x;
+            double *gp = G + (int64_t)sh.gid[t] * 9;
+#pragma unroll
+            for (int q = 0; q < 9; ++q)
+                if (sh.acc[q][t] != 0.0) atomicAdd(gp + q, sh.acc[q][t]);
+        }
+    }
+}
+
+struct ProjBwdArgs {
+    airgs_frame fr;
+    airgs_camera cam;
+    const double *G;    // [n][9] image-space gradients per primitive
+    double *grads;      // [n][W] row-major parameter gradients (written for every primitive)
+};
+
+// The chain rule of render_backward (ss/rasterizer.py:288-368), one thread per
+// primitive; the forward quantities are recomputed with k_project's exact
+// arithmetic.
+template <int WMAX>
+__global__ void __launch_bounds__(128) k_project_bwd(ProjBwdArgs a) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.fr.count) return;
+    const int W = a.fr.width;
+    const int64_t ld = a.fr.ld;
+    double *gr = a.grads + i * W;
+    for (int c = 0; c < W; ++c) gr[c] = 0.0;
+    double Gv[9];
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        Gv[q] = a.G[i * 9 + q];
+        any |= Gv[q] != 0.0;
+    }
+    if (!any) return;  // not kept, or no recorded contribution: every term is zero
+    double p[26];
+#pragma unroll
+    for (int c = 0; c < 26; ++c) p[c] = (c < W && c < WMAX) ? a.fr.params[i + c * ld] : 0.0;
+    const airgs_camera &cam = a.cam;
+    const double *R = cam.rot;
+    const double f = cam.focal;
+    // activation (ss/rasterizer.py:100-110)
+    const double qn = sqrt(((p[3] * p[3] + p[4] * p[4]) + p[5] * p[5]) + p[6] * p[6]);
+    const double qw = p[3] / qn, qx = p[4] / qn, qy = p[5] / qn, qz = p[6] / qn;
+    const double s2v[3] = {exp(2.0 * p[7]), exp(2.0 * p[8]), exp(2.0 * p[9])};
+    const double alpha = sigmoid_ref(p[10]);
+    double rq[9];
+    rq[0] = 1.0 - 2.0 * (qy * qy + qz * qz);
+    rq[1] = 2.0 * (qx * qy - qw * qz);
+    rq[2] = 2.0 * (qx * qz + qw * qy);
+    rq[3] = 2.0 * (qx * qy + qw * qz);
+    rq[4] = 1.0 - 2.0 * (qx * qx + qz * qz);
+    rq[5] = 2.0 * (qy * qz - qw * qx);
+    rq[6] = 2.0 * (qx * qz - qw * qy);
+    rq[7] = 2.0 * (qy * qz + qw * qx);
+    rq[8] = 1.0 - 2.0 * (qx * qx + qy * qy);
+    double cv[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+            cv[3 * r + c] = dot3_blas(rq[3 * r] * s2v[0], rq[3 * r + 1] * s2v[1], rq[3 * r + 2] * s2v[2], rq[3 * c],
+                                      rq[3 * c + 1], rq[3 * c + 2]);
+    const double tx = dot3_blas(p[0], p[1], p[2], R[0], R[1], R[2]) + cam.trans[0];
+    const double ty = dot3_blas(p[0], p[1], p[2], R[3], R[4], R[5]) + cam.trans[1];
+    const double tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
+    const double j00 = f / tz, zz = tz * tz, j02 = -f * tx / zz, j12 = -f * ty / zz;
+    double M[6];
+    for (int c = 0; c < 3; ++c) {
+        M[c] = dot3_blas(j00, 0.0, j02, R[c], R[3 + c], R[6 + c]);
+        M[3 + c] = dot3_blas(0.0, j00, j12, R[c], R[3 + c], R[6 + c]);
+    }
+    double MC[6];
+    for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 3; ++c)
+            MC[3 * r + c] = dot3_blas(M[3 * r], M[3 * r + 1], M[3 * r + 2], cv[c], cv[3 + c], cv[6 + c]);
+    const double a2 = dot3_blas(MC[0], MC[1], MC[2], M[0], M[1], M[2]) + kCovBlur;
+    const double b2 = dot3_blas(MC[0], MC[1], MC[2], M[3], M[4], M[5]);
+    const double c2 = dot3_blas(MC[3], MC[4], MC[5], M[3], M[4], M[5]) + kCovBlur;
+    const double det = a2 * c2 - b2 * b2;
+    const double ca = c2 / det, cbn = -b2 / det, cc = a2 / det;
+    // d_cov2d = -conic @ g_full @ conic
+    const double g00 = Gv[2], g01 = 0.5 * Gv[3], g11 = Gv[4];
+    const double t00 = ca * g00 + cbn * g01, t01 = ca * g01 + cbn * g11;
+    const double t10 = cbn * g00 + cc * g01, t11 = cbn * g01 + cc * g11;
+    const double dc00 = -(t00 * ca + t01 * cbn), dc01 = -(t00 * cbn + t01 * cc);
+    const double dc10 = -(t10 * ca + t11 * cbn), dc11 = -(t10 * cbn + t11 * cc);
+    // d_m = 2 d_cov2d @ m @ cov3d ; d_cov3d = m^T d_cov2d m
+    double DM[6], MCv[6];
+    for (int c = 0; c < 3; ++c) {
+        DM[c] = dc00 * M[c] + dc01 * M[3 + c];
+        DM[3 + c] = dc10 * M[c] + dc11 * M[3 + c];
+    }
+    for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 3; ++c)
+            MCv[3 * r + c] = 2.0 * ((DM[3 * r] * cv[c] + DM[3 * r + 1] * cv[3 + c]) + DM[3 * r + 2] * cv[6 + c]);
+    double dcv[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+            dcv[3 * r + c] = M[r] * DM[c] + M[3 + r] * DM[3 + c];
+    // d_jac = d_m @ rot_wc^T
+    double dj[6];
+    for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 3; ++c)
+            dj[3 * r + c] = (MCv[3 * r] * R[3 * c] + MCv[3 * r + 1] * R[3 * c + 1]) + MCv[3 * r + 2] * R[3 * c + 2];
+    const double inv_z = 1.0 / tz, inv_z2 = inv_z * inv_z;
+    double dt0 = dj[2] * (-f * inv_z2);
+    double dt1 = dj[5] * (-f * inv_z2);
+    double dt2 = ((dj[0] * (-f * inv_z2) + dj[4] * (-f * inv_z2)) + dj[2] * (2 * f * tx * inv_z2 * inv_z)) +
+                 dj[5] * (2 * f * ty * inv_z2 * inv_z);
+    const double du = Gv[0], dv = Gv[1];
+    dt0 += du * f * inv_z;
+    dt1 += dv * f * inv_z;
+    dt2 += -f * (du * tx + dv * ty) * inv_z2;
+    double gpos[3];
+    for (int k = 0; k < 3; ++k) gpos[k] = (R[k] * dt0 + R[3 + k] * dt1) + R[6 + k] * dt2;  // rot_wc^T d_t
+    // scales and rotation through the 3D covariance
+    double ps[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) ps[3 * r + c] = 0.5 * (dcv[3 * r + c] + dcv[3 * c + r]);
+    for (int k = 0; k < 3; ++k) {
+        const double r0 = rq[k], r1 = rq[3 + k], r2 = rq[6 + k];  // column k
+        const double v0 = ps[0] * r0 + ps[1] * r1 + ps[2] * r2;
+        const double v1 = ps[3] * r0 + ps[4] * r1 + ps[5] * r2;
+        const double v2 = ps[6] * r0 + ps[7] * r1 + ps[8] * r2;
+        gr[7 + k] += 2.0 * s2v[k] * ((r0 * v0 + r1 * v1) + r2 * v2);
+    }
+    double drot[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+            drot[3 * r + c] = 2.0 * ((ps[3 * r] * rq[c] + ps[3 * r + 1] * rq[3 + c]) + ps[3 * r + 2] * rq[6 + c]) *
+                              s2v[c];
+    // _rot_jacobians (ss/rasterizer.py:262-268)
+    const double Jw[9] = {0, -qz, qy, qz, 0, -qx, -qy, qx, 0};
+    const double Jx[9] = {0, qy, qz, qy, -2 * qx, -qw, qz, qw, -2 * qx};
+    const double Jy[9] = {-2 * qy, qx, qw, qx, 0, qz, -qw, qz, -2 * qy};
+    const double Jz[9] = {-2 * qz, -qw, qx, qw, -2 * qz, qy, qx, qy, 0};
+    double dq[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 9; ++k) {
+        dq[0] += drot[k] * (2.0 * Jw[k]);
+        dq[1] += drot[k] * (2.0 * Jx[k]);
+        dq[2] += drot[k] * (2.0 * Jy[k]);
+        dq[3] += drot[k] * (2.0 * Jz[k]);
+    }
+    const double qv[4] = {qw, qx, qy, qz};
+    const double dqq = ((dq[0] * qw + dq[1] * qx) + dq[2] * qy) + dq[3] * qz;
+    for (int k = 0; k < 4; ++k) gr[3 + k] += (dq[k] - dqq * qv[k]) / qn;
+    // opacity logit
+    gr[10] += Gv[5] * alpha * (1.0 - alpha);
+    // colour logit and SH
+    const double d0 = p[0] - cam.center[0], d1 = p[1] - cam.center[1], d2 = p[2] - cam.center[2];
+    double dn = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+    if (dn == 0.0) dn = 1.0;
+    const double h0 = d0 / dn, h1 = d1 / dn, h2 = d2 / dn;
+    double dl[3];
+    for (int ch = 0; ch < 3; ++ch) {
+        double lin = p[11 + ch] + kShC0 * p[14 + ch];
+        if (WMAX == 26 && W == 26)
+            lin = lin + kShC1 * ((-h1 * p[17 + ch] + h2 * p[20 + ch]) - h0 * p[23 + ch]);
+        const double col = sigmoid_ref(lin);
+        dl[ch] = Gv[6 + ch] * col * (1.0 - col);
+        gr[11 + ch] += dl[ch];
+        gr[14 + ch] += kShC0 * dl[ch];
+    }
+    if (WMAX == 26 && W == 26) {
+        double dd[3] = {0, 0, 0};
+        for (int ch = 0; ch < 3; ++ch) {
+            gr[17 + ch] += -kShC1 * h1 * dl[ch];
+            gr[20 + ch] += kShC1 * h2 * dl[ch];
+            gr[23 + ch] += -kShC1 * h0 * dl[ch];
+            // sh_block[coeff][ch] = params[17 + 3 coeff + ch]
+            dd[0] += dl[ch] * (-kShC1 * p[23 + ch]);
+            dd[1] += dl[ch] * (-kShC1 * p[17 + ch]);
+            dd[2] += dl[ch] * (kShC1 * p[20 + ch]);
+        }
+        const double ddh = (dd[0] * h0 + dd[1] * h1) + dd[2] * h2;
+        gpos[0] += (dd[0] - ddh * h0) / dn;
+        gpos[1] += (dd[1] - ddh * h1) / dn;
+        gpos[2] += (dd[2] - ddh * h2) / dn;
+    }
+    for (int k = 0; k < 3; ++k) gr[k] += gpos[k];
+}
+
+static void render_backward_impl(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
+                                 const double *d_image, double *grads, cudaStream_t st) {
+    if (frame->count <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "cannot render an empty frame");
+    BwdState bw;
+    bw.t_final = ctx->scratch_t<double>(kSlotTFinal, (size_t)cam->width * cam->height);
+    airgs_view_item it{};
+    it.frame = 0;
+    it.camera = 0;
+    // recompute the forward with its contribution record (deterministic: the same
+    // lists, masks and final transmittance as render_forward)
+    render_impl(ctx, frame, 1, cam, 1, &it, 1, nullptr, st, &bw);
+    const int64_t n = frame->count;
+    double *G = ctx->scratch_t<double>(kSlotBwdGrad, (size_t)n * 9);
+    AIRGS_CUDA_TRY(cudaMemsetAsync(G, 0, sizeof(double) * 9 * n, st));
+    if (bw.Tt > 0 && bw.rec.cbits) {
+        const int tiles_x = (cam->width + kTile - 1) / kTile;
+        k_composite_bwd<<<(unsigned)bw.Tt, kTileThreads, 0, st>>>(bw.recs, bw.rec.tl, bw.tile_count, bw.rec.cbits,
+                                                                 bw.rec.cbase, tiles_x, cam->width, cam->height,
+                                                                 bw.t_final, d_image, G);
+        ++ctx->launches;
+        check_launch();
+    }
+    ProjBwdArgs pa{*frame, *cam, G, grads};
+    if (frame->width == 17)
+        k_project_bwd<17><<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pa);
+    else
+        k_project_bwd<26><<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pa);
+    ++ctx->launches;
+    check_launch();
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
 }
 
 static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics, const double *alphas,
@@ -1770,6 +2172,11 @@ extern "C" int airgs_composite_forward(airgs_ctx *ctx, int64_t k, const double *
         seam_impl(ctx, k, means2d, conics, alphas, colors, bboxes, height, width, image, t_final, usage,
                   (cudaStream_t)stream);
     });
+}
+
+extern "C" int airgs_render_backward(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
+                                     const double *d_image, double *grads, void *stream) {
+    return guarded(ctx, [&] { render_backward_impl(ctx, frame, cam, d_image, grads, (cudaStream_t)stream); });
 }
 
 extern "C" int airgs_sse(airgs_ctx *ctx, const double *a, const double *b, int64_t n, double *out, void *stream) {

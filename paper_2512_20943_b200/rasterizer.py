@@ -173,6 +173,59 @@ def render_with_usage(frame, cams) -> tuple:
     return imgs, UsageFrequency(counts=vb.usage[0].cpu().numpy())
 
 
+class ForwardState:
+    """What ``render_backward`` needs from ``render_forward``: the frame (host
+    or device parameters) and the camera.  The backward recomputes the forward
+    on the device with its contribution record (deterministic: the same depth
+    order, masks and final transmittance)."""
+
+    __slots__ = ("frame", "cam")
+
+    def __init__(self, frame, cam):
+        self.frame = frame
+        self.cam = cam
+
+
+def render_forward(frame, cam, frozen_order=None):
+    """Forward pass that records what backward needs (ss/rasterizer.py:248-257).
+    Returns ``(image, state)``; ``image`` is the forward image (h, w, 3) (the
+    reference's unclipped kernel output; compositing keeps it in [0, 1))."""
+    if frozen_order is not None:
+        raise NotImplementedError("frozen compositing orders are not supported on the device path")
+    if frame.count == 0:
+        raise StructuralError("cannot render an empty frame")
+    vb = render_views([frame], [cam], [(0, 0)], want_images=True)
+    return vb.images[0].cpu().numpy(), ForwardState(frame, cam)
+
+
+def render_backward(state, d_image, as_numpy: bool = True):
+    """Backpropagate ``d_image`` (dLoss/dpixel, (h, w, 3)) to the
+    pre-activation parameters, depth order and contribution masks frozen to
+    the recorded forward (ss/rasterizer.py:270-369).  Returns an (n, width)
+    gradient array."""
+    import ctypes
+
+    import torch
+
+    dev = dv.device_of(None)
+    eng = engine(dev)
+    frame, cam = state.frame, state.cam
+    p, n, w = _frame_planes(frame, dev)
+    wpx, hpx = cam.resolution
+    if isinstance(d_image, torch.Tensor):
+        dimg = d_image.to(device=dev, dtype=torch.float64).contiguous()
+    else:
+        dimg = torch.from_numpy(np.ascontiguousarray(np.asarray(d_image, dtype=np.float64))).to(dev)
+    if tuple(dimg.shape) != (hpx, wpx, 3):
+        raise StructuralError(f"d_image shape {tuple(dimg.shape)} != ({hpx}, {wpx}, 3)")
+    fc = FrameC()
+    fc.params, fc.count, fc.ld, fc.width = p.data_ptr(), n, p.shape[1], w
+    cc = camera_struct(cam)
+    grads = torch.empty((n, w), dtype=torch.float64, device=dev)
+    eng.call("airgs_render_backward", ctypes.byref(fc), ctypes.byref(cc), ptr(dimg), ptr(grads), eng.stream())
+    return grads.cpu().numpy() if as_numpy else grads
+
+
 def forward(means2d, conics, alphas, colors, bboxes, height, width, record=False):
     """The reference kernel seam ``_composite.forward`` on the GPU.
 
@@ -207,10 +260,3 @@ def forward(means2d, conics, alphas, colors, bboxes, height, width, record=False
 def backward(*args, **kwargs):
     raise NotImplementedError("the backward compositing pass is training-only and outside the evaluation path")
 
-
-def render_forward(*args, **kwargs):
-    raise NotImplementedError("render_forward records training state; outside the evaluation path")
-
-
-def render_backward(*args, **kwargs):
-    raise NotImplementedError("render_backward is training-only; outside the evaluation path")
