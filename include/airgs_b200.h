@@ -146,6 +146,15 @@ AIRGS_API int airgs_ssim(airgs_ctx *ctx, const double *a, const double *b, int32
 AIRGS_API int airgs_l1(airgs_ctx *ctx, const double *a, const double *b, int64_t n, double *l1_out, double *grad,
                        void *stream);
 
+/* ---- parameter transfer / on-disk formats -------------------------------- */
+
+/* Row-major little-endian float64 rows (n x width) starting at
+ * bytes + byte_offset (device memory, any alignment) -> plane-major
+ * planes[c * ld + i].  The device side of GaussianFrame uploads and of the
+ * GSSC scene loader (ss/model.py:318-350, rows at byte 15 + ...). */
+AIRGS_API int airgs_rows_to_planes(airgs_ctx *ctx, const uint8_t *bytes, int64_t byte_offset, int64_t n,
+                                   int32_t width, double *planes, int64_t ld, void *stream);
+
 /* ---- rasterizer --------------------------------------------------------- */
 
 /* Batched render: replaces ss/rasterizer.py:113-240 (_activate, _prepare,

@@ -72,6 +72,7 @@ SIGNATURES = {
     "airgs_sse": (ctypes.c_int, [vp, vp, vp, i64, vp, vp]),
     "airgs_ssim": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, c_double_p, vp, vp, vp]),
     "airgs_l1": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
+    "airgs_rows_to_planes": (ctypes.c_int, [vp, vp, i64, i64, i32, vp, i64, vp]),
     "airgs_gsai_decode": (ctypes.c_int, [vp, vp, i64, i64, i32, i64, vp, i64, vp]),
     "airgs_gsdp_decode": (ctypes.c_int, [vp, vp, i64, i64, f64, i32, i64, vp, i64, vp, vp, vp, vp]),
     "airgs_gsdp_varint_end": (ctypes.c_int, [vp, vp, i64, i64, c_i64_p, ctypes.POINTER(i32), vp]),

@@ -43,8 +43,14 @@ def upload_params(params: np.ndarray, device=None):
     n, w = params.shape
     t = torch.zeros((w, ld_for(n)), dtype=torch.float64, device=dev)
     if n:
-        src = torch.from_numpy(np.ascontiguousarray(np.asarray(params, dtype=np.float64).T))
-        t[:, :n].copy_(src.pin_memory() if src.numel() > (1 << 16) else src, non_blocking=False)
+        # one copy of the row-major bytes, transposed to planes on the device
+        # (no host-side transpose: airgs_rows_to_planes)
+        from ._lib import engine, ptr
+
+        rows = np.ascontiguousarray(np.asarray(params, dtype=np.float64))
+        raw = torch.from_numpy(rows.view(np.uint8).reshape(-1)).to(dev)
+        eng = engine(dev)
+        eng.call("airgs_rows_to_planes", ptr(raw), 0, n, w, ptr(t), t.shape[1], eng.stream())
     return t
 
 

@@ -298,3 +298,49 @@ def plan_from_decisions(keyframe_flags, tau_db=DEFAULT_TAU_DB) -> GroupPlan:
         else:
             spans[-1][2] = t
     return GroupPlan(tau_db, tuple(GroupSpan(*s) for s in spans))
+
+
+# ---------------------------------------------------------------------------
+# Trained-stream persistence (ss/grouping.py:108-150): one .npz with the plan as
+# embedded JSON; the file format is the reference's.
+
+
+def save_stream(path, stream: TrainedStream) -> None:
+    arrays = {
+        "plan_json": np.frombuffer(stream.plan.to_json().encode(), dtype=np.uint8),
+        "group_keys": np.array(sorted(stream.spaces), dtype=np.int64),
+        "frame_group": np.array([r.group_key for r in stream.records], dtype=np.int64),
+        "frame_iskey": np.array([r.is_keyframe for r in stream.records], dtype=np.bool_),
+        "frame_quality": np.array([r.quality_db for r in stream.records]),
+    }
+    for k, sp in stream.spaces.items():
+        arrays[f"space_{k}"] = sp.frame.params
+        arrays[f"capacity_{k}"] = np.array(sp.capacity_U, dtype=np.int64)
+    for r in stream.records:
+        arrays[f"cumulative_{r.frame_index}"] = r.cumulative_delta.dense()
+        arrays[f"step_{r.frame_index}"] = r.step_delta.dense()
+    np.savez_compressed(path, **arrays)
+
+
+def load_stream(path, device=None) -> TrainedStream:
+    """Inverse of ``save_stream`` (ss/grouping.py:125-150).  Canonical spaces
+    are uploaded and every dense delta is filtered to its sparse rows on the
+    device (``DeltaTensor.from_dense``), so the stream is HBM-resident."""
+    from .model import GaussianFrame
+
+    with np.load(path) as z:
+        plan = GroupPlan.from_json(bytes(z["plan_json"]).decode())
+        spaces = {}
+        for k in z["group_keys"]:
+            k = int(k)
+            fr = GaussianFrame(params=z[f"space_{k}"], frame_index=k, group_key=k)
+            fr.planes(device)
+            spaces[k] = CanonicalSpace(frame=fr, capacity_U=int(z[f"capacity_{k}"]))
+        records = []
+        for t in range(len(z["frame_group"])):
+            records.append(FrameRecord(frame_index=t, group_key=int(z["frame_group"][t]),
+                                       is_keyframe=bool(z["frame_iskey"][t]),
+                                       step_delta=DeltaTensor.from_dense(z[f"step_{t}"]),
+                                       cumulative_delta=DeltaTensor.from_dense(z[f"cumulative_{t}"]),
+                                       quality_db=float(z["frame_quality"][t])))
+    return TrainedStream(plan=plan, spaces=spaces, records=tuple(records))

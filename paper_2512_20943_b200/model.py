@@ -27,6 +27,8 @@ OPACITY = 10
 COLOR = slice(11, 14)
 SH_START = 14
 EPS_SPARSE = 1e-9  # ss/model.py:35
+SCENE_MAGIC = b"GSSC"  # ss/model.py:42-43
+SCENE_VERSION = 1
 TOMBSTONE_LOGIT = -100.0
 LIVE_LOGIT_FLOOR = -50.0
 
@@ -428,3 +430,70 @@ def quat_to_matrix(q: np.ndarray) -> np.ndarray:
     m[..., 1, :] = np.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], -1)
     m[..., 2, :] = np.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], -1)
     return m
+
+
+# ---------------------------------------------------------------------------
+# Scene container I/O ("GSSC", ss/model.py:318-350): little-endian, header then
+# packed f64 rows.  The file format is the reference's, byte for byte.
+
+
+def save_scene(path, frames) -> None:
+    import struct
+
+    frames = list(frames)
+    if not frames:
+        raise StructuralError("cannot save an empty scene")
+    degree = frames[0].sh_degree
+    with open(path, "wb") as fh:
+        fh.write(SCENE_MAGIC)
+        fh.write(struct.pack("<HIB", SCENE_VERSION, len(frames), degree))
+        for fr in frames:
+            if fr.sh_degree != degree:
+                raise StructuralError("mixed sh degrees in one scene")
+            fh.write(struct.pack("<I", fr.count))
+            fh.write(fr.params.astype("<f8").tobytes())
+
+
+def load_scene(path, device=None, to_device: bool = False):
+    """Frames of a GSSC file (ss/model.py:332-350).  ``to_device=True``
+    streams the whole file into HBM with one copy and builds every frame's
+    plane-major parameters there (airgs_rows_to_planes: rows start at an odd
+    byte offset), so the frames are device-resident without a host transpose."""
+    import struct
+
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if data[:4] != SCENE_MAGIC:
+        raise ValidationError(f"bad scene magic {data[:4]!r}")
+    if len(data) < 11:
+        raise ValidationError("truncated scene file")
+    version, frame_count, degree = struct.unpack_from("<HIB", data, 4)
+    if version != SCENE_VERSION:
+        raise ValidationError(f"unsupported scene version {version}")
+    width = param_dim(degree)
+    spans = []
+    pos = 11
+    for _ in range(frame_count):
+        if pos + 4 > len(data):
+            raise ValidationError("truncated scene file")
+        (n,) = struct.unpack_from("<I", data, pos)
+        pos += 4
+        nbytes = 8 * n * width
+        if pos + nbytes > len(data):
+            raise ValidationError("truncated scene file")
+        spans.append((pos, n))
+        pos += nbytes
+    if not to_device:
+        return [GaussianFrame(params=np.frombuffer(data, dtype="<f8", count=n * width, offset=off).reshape(n, width),
+                              frame_index=t, group_key=0) for t, (off, n) in enumerate(spans)]
+    import torch
+
+    dev = dv.device_of(device)
+    eng = _engine(dev)
+    raw = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev)
+    frames = []
+    for t, (off, n) in enumerate(spans):
+        planes = torch.zeros((width, dv.ld_for(n)), dtype=torch.float64, device=dev)
+        eng.call("airgs_rows_to_planes", _ptr(raw), off, n, width, _ptr(planes), planes.shape[1], eng.stream())
+        frames.append(GaussianFrame(device_params=planes, count=n, frame_index=t, group_key=0))
+    return frames

@@ -332,8 +332,35 @@ def gen_backward(ss):
     np.savez_compressed(os.path.join(HERE, "backward.npz"), **out)
 
 
+def gen_io(ss):
+    """A GSSC scene (2 frames, SH degree 1) and a trained-stream .npz written
+    by the reference's own save_scene / save_stream (ss/model.py:318-329,
+    ss/grouping.py:108-122), plus the values they hold."""
+    from splatstream import grouping, model
+
+    rng = np.random.default_rng(900)
+    frames = [model.GaussianFrame(params=random_params(rng, n, 1, 0.5), frame_index=t)
+              for t, n in enumerate((37, 41))]
+    model.save_scene(os.path.join(HERE, "io_scene.gssc"), frames)
+    base = random_params(rng, 30, 0, 0.5)
+    space = model.CanonicalSpace(model.GaussianFrame(params=base, frame_index=0, group_key=0), capacity_U=32)
+    recs = []
+    cum = model.DeltaTensor.empty(30, 17)
+    for t in range(3):
+        step = model.DeltaTensor.from_dense(np.where(rng.uniform(0, 1, (30, 17)) < 0.2,
+                                                     rng.normal(0, 1e-3, (30, 17)), 0.0))
+        cum = model.compose_deltas([cum, step])
+        recs.append(grouping.FrameRecord(t, 0, t == 0, step, cum, 40.0 - t))
+    plan = grouping.GroupPlan(30.0, (grouping.GroupSpan(0, 0, 2),))
+    grouping.save_stream(os.path.join(HERE, "io_stream.npz"),
+                         grouping.TrainedStream(plan=plan, spaces={0: space}, records=recs))
+    np.savez_compressed(os.path.join(HERE, "io_values.npz"), f0=frames[0].params, f1=frames[1].params, base=base,
+                        **{f"cum{t}": r.cumulative_delta.dense() for t, r in enumerate(recs)},
+                        **{f"step{t}": r.step_delta.dense() for t, r in enumerate(recs)})
+
+
 GENERATORS = ("gen_render", "gen_composite", "gen_codec", "gen_delta", "gen_pruning", "gen_grouping", "gen_session",
-              "gen_metrics", "gen_backward")
+              "gen_metrics", "gen_backward", "gen_io")
 
 
 def main():

@@ -8,7 +8,7 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 SRC=$ROOT/paper_2512_20943_b200/csrc
 OUT=$ROOT/paper_2512_20943_b200/lib/variants/$NAME
 mkdir -p $OUT
-for f in api render codec delta metrics; do
+for f in api render codec delta metrics io; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -fmad=false \
     -Xcompiler -fPIC,-fvisibility=hidden --expt-relaxed-constexpr $DEFS -c $SRC/$f.cu -o $OUT/$f.o &
 done
