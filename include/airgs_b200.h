@@ -74,6 +74,10 @@ typedef struct airgs_view_item {
     const double *target;   /* (h,w,3) float64 reference image for SSE, or NULL */
     double *image;          /* (h,w,3) float64 clipped render out, or NULL */
     int64_t *usage;         /* int64[count], counts are ADDED (+=), or NULL */
+    const int64_t *frozen_pos; /* int64[count] or NULL: frozen compositing order
+                                * (ss/rasterizer.py:128-142): position of each primitive
+                                * in the frozen order, -1 if absent (kept primitives
+                                * absent from it are appended in depth order) */
 } airgs_view_item;
 
 /* ---- context ------------------------------------------------------------ */
@@ -125,10 +129,19 @@ AIRGS_API int airgs_eval_margins(airgs_ctx *ctx, double *margins);
  * propagates d_image (device float64 (h, w, 3), dLoss/dpixel of the
  * unclipped forward image) through compositing and projection, and writes
  * the pre-activation parameter gradients grads (device float64 row-major
- * [count][width], every row written).  Depth order is the forward's (the
- * reference's frozen_order option is not supported). */
+ * [count][width], every row written).  Depth order is the forward's,
+ * frozen through frozen_pos as in airgs_view_item (or NULL). */
 AIRGS_API int airgs_render_backward(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
-                                    const double *d_image, double *grads, void *stream);
+                                    const int64_t *frozen_pos, const double *d_image, double *grads,
+                                    void *stream);
+
+/* Compositing order of one view (ss/rasterizer.py:243-246 compositing_orders,
+ * _prepare's stable depth sort of the kept primitives, or the frozen order
+ * rule when frozen_pos != NULL): order_out (device int64[count]) receives the
+ * kept primitives' indices, *kept_out their number.  Synchronises. */
+AIRGS_API int airgs_compositing_order(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
+                                      const int64_t *frozen_pos, int64_t *order_out, int64_t *kept_out,
+                                      void *stream);
 
 /* ---- image metrics of the trainer's loss ---------------------------------- */
 

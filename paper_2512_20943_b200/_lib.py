@@ -53,6 +53,7 @@ class ItemC(ctypes.Structure):
         ("target", ctypes.c_void_p),
         ("image", ctypes.c_void_p),
         ("usage", ctypes.c_void_p),
+        ("frozen_pos", ctypes.c_void_p),
     ]
 
 
@@ -67,7 +68,9 @@ SIGNATURES = {
     "airgs_eval_margins": (ctypes.c_int, [vp, c_double_p]),
     "airgs_render": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), i32, ctypes.POINTER(CameraC), i32,
                                     ctypes.POINTER(ItemC), i32, vp, vp]),
-    "airgs_render_backward": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), ctypes.POINTER(CameraC), vp, vp, vp]),
+    "airgs_render_backward": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), ctypes.POINTER(CameraC), vp, vp, vp, vp]),
+    "airgs_compositing_order": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), ctypes.POINTER(CameraC), vp, vp, c_i64_p,
+                                               vp]),
     "airgs_composite_forward": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp]),
     "airgs_sse": (ctypes.c_int, [vp, vp, vp, i64, vp, vp]),
     "airgs_ssim": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, c_double_p, vp, vp, vp]),

@@ -46,7 +46,14 @@ struct ProjArgs {
     unsigned int *flags;
     int64_t stride;
     unsigned long long *stats;  // diagnostic decision margins (null: off)
+    const int64_t *const *item_frozen;  // per item: frozen order positions or null (null: none at all)
 };
+
+// Compositing-order key of a kept primitive: its position in a frozen order
+// (< 2^63, ahead of everything else) or, for primitives outside it and in the
+// unfrozen case, the orderable depth key (>= 2^63 for z > 0); ties in either
+// resolve by index (ss/rasterizer.py:127-142, stable argsorts).
+__device__ __forceinline__ unsigned long long order_key_of(const int64_t *frozen, int64_t i, double tz);
 
 
 __device__ __forceinline__ double dist_to_int(double x) { return fabs(x - rint(x)); }
@@ -72,6 +79,11 @@ __device__ __forceinline__ double sigmoid_ref(double x) {
 __device__ __forceinline__ unsigned long long order_key(double z) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(z);
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ unsigned long long order_key_of(const int64_t *frozen, int64_t i, double tz) {
+    if (frozen && frozen[i] >= 0) return (unsigned long long)frozen[i];
+    return order_key(tz);
 }
 
 // Tile range of a record: clipped bbox intersected with the pixel centres
@@ -229,7 +241,8 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
             int u0, u1, v0, v1;
             const bool has_bbox = rec.x1 > rec.x0 && rec.y1 > rec.y0;
             if (has_bbox && rec_tile_range(rec, u0, u1, v0, v1)) nt = (u1 - u0 + 1) * (v1 - v0 + 1);
-            const unsigned long long zk = order_key(tz);
+            const int64_t *fz = a.item_frozen ? a.item_frozen[item] : nullptr;
+            const unsigned long long zk = order_key_of(fz, i, tz);
             if (has_bbox) {  // (bbox-only records are read by the diagnostic counters alone)
                 a.recs[o] = rec;
                 a.depth[o] = zk;
@@ -280,8 +293,10 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
         const Rec &r = a.recs[o];
         rec_tile_range(r, u0, u1, v0, v1);
         const uint64_t zk = a.depth[o];
+        // 32-bit order key: small keys (frozen positions, the seam's input order)
+        // as they are; depth keys (z > 0) as their fp32 bits, monotone, behind them
         const double z = __longlong_as_double((long long)(zk & 0x7fffffffffffffffull));
-        const uint32_t hi = a.index_order ? (uint32_t)zk : __float_as_uint((float)z);
+        const uint32_t hi = (zk >> 63) ? (0x80000000u | (__float_as_uint((float)z) >> 1)) : (uint32_t)zk;
         entry = ((uint64_t)hi << 32) | (uint32_t)i;
     }
     const int nu = u1 - u0 + 1;
@@ -348,7 +363,7 @@ struct EmitArgs {
     uint32_t *cursor;          // global tile -> fill cursor
     uint64_t *ids;             // list entries (fp32 depth bits << 32 | id) in tile ranges
     int64_t stride;
-    int index_order;           // seam: the depth keys are the input order itself
+    int index_order;           // (informational: the keys themselves decide, see k_bin)
 };
 
 __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
@@ -361,7 +376,8 @@ __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     const int64_t tb = a.tile_base[s];
     // fp32 depth from the orderable key (z > 0: key = bits | sign bit)
     const double z = __longlong_as_double((long long)(a.depth[o] & 0x7fffffffffffffffull));
-    const uint32_t hi = a.index_order ? (uint32_t)a.depth[o] : __float_as_uint((float)z);
+    const uint64_t zk = a.depth[o];
+    const uint32_t hi = (zk >> 63) ? (0x80000000u | (__float_as_uint((float)z) >> 1)) : (uint32_t)zk;
     const uint64_t entry = ((uint64_t)hi << 32) | (uint32_t)i;
     const int txn = a.tiles_x[s];
     int u0, u1, v0, v1;
@@ -1287,6 +1303,7 @@ struct ItemHost {
     double *trans;
     int64_t *usage;
     int clip;
+    const int64_t *frozen = nullptr;  // frozen compositing order positions, or null
 };
 
 // Device layout of the per-call descriptors shared by project / emit / composite.
@@ -1695,6 +1712,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         h.image = v.image;
         h.trans = bwd ? bwd->t_final : nullptr;
         h.usage = v.usage;
+        h.frozen = v.frozen_pos;
         h.clip = bwd ? 0 : 1;  // the forward of render_forward returns the unclipped image
         per_frame[v.frame].push_back(s);
         stride = std::max(stride, f.count);
@@ -1718,12 +1736,17 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     const size_t o_fptr = off; off = align(off + sizeof(int32_t) * (nframes + 1));
     const size_t o_fitems = off; off = align(off + sizeof(int32_t) * nitems);
     const size_t o_icam = off; off = align(off + sizeof(int32_t) * nitems);
+    bool any_frozen = false;
+    for (int s = 0; s < nitems; ++s) any_frozen |= ih[s].frozen != nullptr;
+    const size_t o_frz = off; off = align(off + (any_frozen ? sizeof(const int64_t *) * nitems : 0));
     char *hs = (char *)ctx->staging(off);
     memcpy(hs + o_frames, frames, sizeof(airgs_frame) * nframes);
     memcpy(hs + o_cams, cams, sizeof(airgs_camera) * ncams);
     memcpy(hs + o_fptr, fptr.data(), sizeof(int32_t) * (nframes + 1));
     memcpy(hs + o_fitems, fitems.data(), sizeof(int32_t) * nitems);
     memcpy(hs + o_icam, icam.data(), sizeof(int32_t) * nitems);
+    if (any_frozen)
+        for (int s = 0; s < nitems; ++s) memcpy(hs + o_frz + sizeof(const int64_t *) * s, &ih[s].frozen, sizeof(void *));
     char *dd = (char *)ctx->scratch(kSlotDesc, off);
     h2d_small(ctx, dd, hs, off, st);
 
@@ -1742,6 +1765,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.frame_item_ptr = (const int32_t *)(dd + o_fptr);
     pa.frame_items = (const int32_t *)(dd + o_fitems);
     pa.item_cam = (const int32_t *)(dd + o_icam);
+    pa.item_frozen = any_frozen ? (const int64_t *const *)(dd + o_frz) : nullptr;
     pa.tile_base = L.d_tile_base;
     pa.tiles_x = L.d_tiles_x;
     pa.recs = recs;
@@ -2071,13 +2095,15 @@ __global__ void __launch_bounds__(128) k_project_bwd(ProjBwdArgs a) {
 }
 
 static void render_backward_impl(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
-                                 const double *d_image, double *grads, cudaStream_t st) {
+                                 const int64_t *frozen_pos, const double *d_image, double *grads,
+                                 cudaStream_t st) {
     if (frame->count <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "cannot render an empty frame");
     BwdState bw;
     bw.t_final = ctx->scratch_t<double>(kSlotTFinal, (size_t)cam->width * cam->height);
     airgs_view_item it{};
     it.frame = 0;
     it.camera = 0;
+    it.frozen_pos = frozen_pos;
     // recompute the forward with its contribution record (deterministic: the same
     // lists, masks and final transmittance as render_forward)
     render_impl(ctx, frame, 1, cam, 1, &it, 1, nullptr, st, &bw);
@@ -2099,6 +2125,66 @@ static void render_backward_impl(airgs_ctx *ctx, const airgs_frame *frame, const
         k_project_bwd<26><<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(pa);
     ++ctx->launches;
     check_launch();
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+}
+
+// Keep test and order key per primitive for one view, with k_project's exact
+// arithmetic (ss/rasterizer.py:116-142): kept = z > near_clip and alpha > 1/255;
+// key = order_key_of(frozen, i, z) for kept primitives, all ones otherwise.
+__global__ void __launch_bounds__(256) k_order_keys(airgs_frame fr, airgs_camera cam, const int64_t *frozen,
+                                                    uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
+                                                    unsigned long long *__restrict__ kept) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool keep = false;
+    uint64_t key = ~0ull;
+    if (i < fr.count) {
+        const int64_t ld = fr.ld;
+        double p[11];
+#pragma unroll
+        for (int c = 0; c < 11; ++c) p[c] = fr.params[i + c * ld];
+        const double alpha = sigmoid_ref(p[10]);
+        const double *R = cam.rot;
+        const double tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
+        keep = tz > cam.near_clip && alpha > kEpsContrib;
+        if (keep) key = order_key_of(frozen, i, tz);
+        keys[i] = key;
+        vals[i] = (uint32_t)i;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(kept, (unsigned long long)__popc(m));
+}
+
+__global__ void k_vals_to_order(const uint32_t *__restrict__ vals, int64_t n, int64_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = vals[i];
+}
+
+static void compositing_order_impl(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
+                                   const int64_t *frozen_pos, int64_t *order_out, int64_t *kept_out,
+                                   cudaStream_t st) {
+    const int64_t n = frame->count;
+    if (n <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "cannot render an empty frame");
+    if (n > (int64_t)0xffffffffLL) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");
+    int64_t &NL = ctx->launches;
+    uint64_t *k1 = ctx->scratch_t<uint64_t>(kSlotKeys, (size_t)n);
+    uint64_t *k2 = ctx->scratch_t<uint64_t>(kSlotKeysAlt, (size_t)n);
+    uint32_t *v1 = ctx->scratch_t<uint32_t>(kSlotVals, (size_t)n);
+    uint32_t *v2 = ctx->scratch_t<uint32_t>(kSlotValsAlt, (size_t)n);
+    int64_t *misc = ctx->scratch_t<int64_t>(kSlotMisc3, 4);
+    AIRGS_CUDA_TRY(cudaMemsetAsync(misc, 0, sizeof(int64_t) * 4, st));
+    k_order_keys<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(*frame, *cam, frozen_pos, k1, v1,
+                                                            (unsigned long long *)misc);
+    ++NL;
+    const int64_t seg[2] = {0, n};
+    int64_t *d_seg = misc + 2;
+    h2d_small(ctx, d_seg, seg, sizeof(seg), st);
+    uint32_t *hist = ctx->scratch_t<uint32_t>(kSlotHist, (size_t)256 * ceil_div(n, kSortTile));
+    // stable LSD radix sort on the 64-bit key; equal keys keep the index order
+    const bool alt = radix_sort<uint64_t>(k1, v1, k2, v2, d_seg, d_seg + 1, 1, n, 64, hist, st, &NL);
+    k_vals_to_order<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(alt ? v2 : v1, n, order_out);
+    ++NL;
+    check_launch();
+    AIRGS_CUDA_TRY(cudaMemcpyAsync(kept_out, misc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
 }
 
@@ -2175,8 +2261,19 @@ extern "C" int airgs_composite_forward(airgs_ctx *ctx, int64_t k, const double *
 }
 
 extern "C" int airgs_render_backward(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
-                                     const double *d_image, double *grads, void *stream) {
-    return guarded(ctx, [&] { render_backward_impl(ctx, frame, cam, d_image, grads, (cudaStream_t)stream); });
+                                     const int64_t *frozen_pos, const double *d_image, double *grads,
+                                     void *stream) {
+    return guarded(ctx, [&] {
+        render_backward_impl(ctx, frame, cam, frozen_pos, d_image, grads, (cudaStream_t)stream);
+    });
+}
+
+extern "C" int airgs_compositing_order(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
+                                       const int64_t *frozen_pos, int64_t *order_out, int64_t *kept_out,
+                                       void *stream) {
+    return guarded(ctx, [&] {
+        compositing_order_impl(ctx, frame, cam, frozen_pos, order_out, kept_out, (cudaStream_t)stream);
+    });
 }
 
 extern "C" int airgs_sse(airgs_ctx *ctx, const double *a, const double *b, int64_t n, double *out, void *stream) {

@@ -30,7 +30,7 @@ for _name, _code in _TABLE:
 
 
 class TrainingError(SplatStreamError):
-    """Carried for API parity only: training is outside this package."""
+    """A fit diverged (ss/errors.py; raised by train.py)."""
 
     code = "TRAINING"
 

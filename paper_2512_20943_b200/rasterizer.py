@@ -95,7 +95,8 @@ def _frame_planes(frame, dev):
     return dv.upload_params(p, dev), p.shape[0], p.shape[1]
 
 
-def render_views(frames, cams, items, targets=None, want_images=False, usage_frames=None, device=None):
+def render_views(frames, cams, items, targets=None, want_images=False, usage_frames=None, device=None,
+                 frozen=None):
     """Render ``items`` = [(frame_idx, cam_idx), ...] in one pipeline pass.
 
     targets: optional list (per item) of device (h, w, 3) float64 tensors;
@@ -103,6 +104,8 @@ def render_views(frames, cams, items, targets=None, want_images=False, usage_fra
     want_images: return clipped device images per item.
     usage_frames: iterable of frame indices whose items accumulate usage
       counts; ``.usage[f]`` is an int64 device tensor over the frame.
+    frozen: optional list (per item) of frozen-order position tensors
+      (``frozen_positions``) or None (ss/rasterizer.py:128-142).
     """
     import torch
 
@@ -142,6 +145,8 @@ def render_views(frames, cams, items, targets=None, want_images=False, usage_fra
             ic[s].image = img.data_ptr()
         if fi in usage:
             ic[s].usage = usage[fi].data_ptr()
+        if frozen is not None and frozen[s] is not None:
+            ic[s].frozen_pos = frozen[s].data_ptr()
     sse = torch.zeros((len(items),), dtype=torch.float64, device=dev)
     before = eng.launches
     eng.call("airgs_render", fc, len(frames), cc, len(cams), ic, len(items), ptr(sse), eng.stream())
@@ -175,27 +180,71 @@ def render_with_usage(frame, cams) -> tuple:
 
 class ForwardState:
     """What ``render_backward`` needs from ``render_forward``: the frame (host
-    or device parameters) and the camera.  The backward recomputes the forward
-    on the device with its contribution record (deterministic: the same depth
-    order, masks and final transmittance)."""
+    or device parameters), the camera and the frozen order, if any.  The
+    backward recomputes the forward on the device with its contribution
+    record (deterministic: the same order, masks and final transmittance)."""
 
-    __slots__ = ("frame", "cam")
+    __slots__ = ("frame", "cam", "frozen")
 
-    def __init__(self, frame, cam):
+    def __init__(self, frame, cam, frozen=None):
         self.frame = frame
         self.cam = cam
+        self.frozen = frozen
+
+
+def frozen_positions(frozen_order, n, device=None):
+    """Device int64[n]: position of each primitive in ``frozen_order``, -1 if
+    absent (the device form of _prepare's frozen_order argument)."""
+    import torch
+
+    dev = dv.device_of(device)
+    pos = torch.full((n,), -1, dtype=torch.int64, device=dev)
+    fo = torch.as_tensor(np.asarray(frozen_order, dtype=np.int64) if not isinstance(frozen_order, torch.Tensor)
+                         else frozen_order, dtype=torch.int64).to(dev)
+    if fo.numel():
+        if int(fo.min()) < 0 or int(fo.max()) >= n:
+            raise StructuralError("frozen order references a missing primitive")
+        pos[fo] = torch.arange(fo.numel(), dtype=torch.int64, device=dev)
+    return pos
+
+
+def compositing_orders(frame, cams, frozen_orders=None) -> list:
+    """Per-camera compositing orders of ``frame`` (ss/rasterizer.py:243-246):
+    the kept primitives (z > near, alpha > 1/255) in stable depth order, or in
+    the frozen order followed by the rest by depth."""
+    import ctypes
+
+    import torch
+
+    dev = dv.device_of(None)
+    eng = engine(dev)
+    p, n, w = _frame_planes(frame, dev)
+    fc = FrameC()
+    fc.params, fc.count, fc.ld, fc.width = p.data_ptr(), n, p.shape[1], w
+    out = []
+    for k, cam in enumerate(cams):
+        fz = None
+        if frozen_orders is not None and frozen_orders[k] is not None:
+            fz = frozen_positions(frozen_orders[k], n, dev)
+        order = torch.empty((max(n, 1),), dtype=torch.int64, device=dev)
+        kept = ctypes.c_int64(0)
+        cc = camera_struct(cam)
+        eng.call("airgs_compositing_order", ctypes.byref(fc), ctypes.byref(cc), ptr(fz), ptr(order),
+                 ctypes.byref(kept), eng.stream())
+        out.append(order[: kept.value].cpu().numpy())
+    return out
 
 
 def render_forward(frame, cam, frozen_order=None):
     """Forward pass that records what backward needs (ss/rasterizer.py:248-257).
     Returns ``(image, state)``; ``image`` is the forward image (h, w, 3) (the
-    reference's unclipped kernel output; compositing keeps it in [0, 1))."""
-    if frozen_order is not None:
-        raise NotImplementedError("frozen compositing orders are not supported on the device path")
+    reference's unclipped kernel output; compositing keeps it in [0, 1)).
+    ``frozen_order`` reuses a compositing order (see compositing_orders)."""
     if frame.count == 0:
         raise StructuralError("cannot render an empty frame")
-    vb = render_views([frame], [cam], [(0, 0)], want_images=True)
-    return vb.images[0].cpu().numpy(), ForwardState(frame, cam)
+    fz = None if frozen_order is None else frozen_positions(frozen_order, frame.count)
+    vb = render_views([frame], [cam], [(0, 0)], want_images=True, frozen=[fz])
+    return vb.images[0].cpu().numpy(), ForwardState(frame, cam, fz)
 
 
 def render_backward(state, d_image, as_numpy: bool = True):
@@ -222,7 +271,8 @@ def render_backward(state, d_image, as_numpy: bool = True):
     fc.params, fc.count, fc.ld, fc.width = p.data_ptr(), n, p.shape[1], w
     cc = camera_struct(cam)
     grads = torch.empty((n, w), dtype=torch.float64, device=dev)
-    eng.call("airgs_render_backward", ctypes.byref(fc), ctypes.byref(cc), ptr(dimg), ptr(grads), eng.stream())
+    eng.call("airgs_render_backward", ctypes.byref(fc), ctypes.byref(cc), ptr(state.frozen), ptr(dimg), ptr(grads),
+             eng.stream())
     return grads.cpu().numpy() if as_numpy else grads
 
 

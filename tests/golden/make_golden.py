@@ -359,8 +359,60 @@ def gen_io(ss):
                         **{f"step{t}": r.step_delta.dense() for t, r in enumerate(recs)})
 
 
+def gen_train(ss):
+    """Frozen compositing orders and short fits of the reference trainer
+    (ss/train.py:262-292, 370-486): compositing_orders, a frozen-order
+    forward/backward, fit_group_frame and fit_keyframe (with one
+    densification event) on a small scene."""
+    from splatstream import camera, model, rasterizer, train
+
+    out = {}
+    rng = np.random.default_rng(1000)
+    p = random_params(rng, 250, 0, 0.45)
+    cams = camera.ring_rig(2, radius=3.0, height=0.3, focal=40.0, resolution=(48, 40))
+    for k, v in cam_arrays(cams).items():
+        out[k] = v
+    out["params"] = p
+    moved = p.copy()
+    sel = rng.uniform(0, 1, p.shape[0]) < 0.3
+    moved[sel, 0:3] += rng.normal(0, 0.02, (int(sel.sum()), 3))
+    out["moved"] = moved
+    # targets = renders of the moved scene plus noise: an exact render would sit
+    # on L1's kink (sign(0)) wherever the fit's render equals it bit for bit,
+    # where a 1-ulp exp difference flips the subgradient
+    target = train.GroundTruth(images=tuple(
+        np.clip(rasterizer.render(model.GaussianFrame(params=moved), c).pixels + rng.normal(0, 0.01, (40, 48, 3)),
+                0, 1) for c in cams))
+    for k, im in enumerate(target.images):
+        out[f"target{k}"] = im
+    orders = rasterizer.compositing_orders(model.GaussianFrame(params=p), cams)
+    for k, o in enumerate(orders):
+        out[f"order{k}"] = o
+    # frozen forward / backward at the moved parameters (depths crossed, some primitives culled)
+    q = moved.copy()
+    q[:5, 10] = -8.0  # below the contribution quantum: absent from the frozen order's kept set
+    img, st = rasterizer.render_forward(model.GaussianFrame(params=q), cams[0], frozen_order=orders[0])
+    d_image = rng.normal(0, 1, img.shape)
+    out["frozen_q"] = q
+    out["frozen_image"] = img
+    out["frozen_d_image"] = d_image
+    out["frozen_grads"] = rasterizer.render_backward(st, d_image)
+    out["frozen_order_used"] = st[0].order
+    space = model.CanonicalSpace(model.GaussianFrame(params=p, frame_index=0, group_key=0), capacity_U=250)
+    weights = train.LossWeights()
+    d = train.fit_group_frame(space, model.DeltaTensor.empty(250, 17), target, cams, weights,
+                              train.TrainConfig(iterations=3, step_size=0.05))
+    out["group_delta"] = d.dense()
+    ks = train.fit_keyframe(model.GaussianFrame(params=p, frame_index=0, group_key=0), target, cams, weights,
+                            train.TrainConfig(iterations=4, step_size=0.05, densify_interval=2,
+                                              densify_grad_threshold=1e-5, capacity_U=260))
+    out["key_params"] = ks.frame.params
+    out["key_capacity"] = np.array(ks.capacity_U)
+    np.savez_compressed(os.path.join(HERE, "train.npz"), **out)
+
+
 GENERATORS = ("gen_render", "gen_composite", "gen_codec", "gen_delta", "gen_pruning", "gen_grouping", "gen_session",
-              "gen_metrics", "gen_backward", "gen_io")
+              "gen_metrics", "gen_backward", "gen_io", "gen_train")
 
 
 def main():
