@@ -47,8 +47,12 @@ def upload_params(params: np.ndarray, device=None):
         # (no host-side transpose: airgs_rows_to_planes)
         from ._lib import engine, ptr
 
+        import warnings
+
         rows = np.ascontiguousarray(np.asarray(params, dtype=np.float64))
-        raw = torch.from_numpy(rows.view(np.uint8).reshape(-1)).to(dev)
+        with warnings.catch_warnings():  # read-only frames: the tensor is only read by the copy
+            warnings.simplefilter("ignore", UserWarning)
+            raw = torch.from_numpy(rows.view(np.uint8).reshape(-1)).to(dev)
         eng = engine(dev)
         eng.call("airgs_rows_to_planes", ptr(raw), 0, n, w, ptr(t), t.shape[1], eng.stream())
     return t

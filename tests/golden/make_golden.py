@@ -408,6 +408,26 @@ def gen_train(ss):
                                               densify_grad_threshold=1e-5, capacity_U=260))
     out["key_params"] = ks.frame.params
     out["key_capacity"] = np.array(ks.capacity_U)
+    # the whole training-based grouping driver on a 3-frame toy sequence
+    from splatstream import grouping
+
+    seq = [moved.copy() for _ in range(3)]
+    seq[2][:, 0:3] += 0.05  # a jump the motion fit cannot follow
+    tgts = [train.GroundTruth(images=tuple(np.clip(rasterizer.render(model.GaussianFrame(params=f), c).pixels
+                                                   + rng.normal(0, 0.01, (40, 48, 3)), 0, 1) for c in cams))
+            for f in seq]
+    for t, tg in enumerate(tgts):
+        for k, im in enumerate(tg.images):
+            out[f"bg_t{t}_c{k}"] = im
+    stream = grouping.build_groups(tgts, cams, weights, train.TrainConfig(iterations=2, step_size=0.05),
+                                   train.TrainConfig(iterations=3, step_size=0.05, densify_interval=2),
+                                   (np.full(3, -0.5), np.full(3, 0.5)), 120, tau_db=18.9, seed=3)
+    out["bg_iskey"] = np.array([r.is_keyframe for r in stream.records])
+    out["bg_quality"] = np.array([r.quality_db for r in stream.records])
+    for k, sp in stream.spaces.items():
+        out[f"bg_space{k}"] = sp.frame.params
+    for r in stream.records:
+        out[f"bg_cum{r.frame_index}"] = r.cumulative_delta.dense()
     np.savez_compressed(os.path.join(HERE, "train.npz"), **out)
 
 

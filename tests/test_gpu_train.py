@@ -76,3 +76,26 @@ def test_fit_keyframe_matches_reference():
     assert ks.frame.params.shape == ref.shape
     assert ks.capacity_U == int(g["key_capacity"])
     assert np.max(np.abs(ks.frame.params - ref)) <= 1e-8 * max(np.max(np.abs(ref)), 1.0)
+
+
+def test_build_groups_matches_reference():
+    """The training-based grouping driver (ss/grouping.py:169-250) on a
+    3-frame toy sequence: the same keyframe decisions (frame 1 a delta, frame
+    2 a new group), qualities to 1e-6 dB, spaces and cumulative deltas 1e-8."""
+    from paper_2512_20943_b200 import grouping, train
+
+    g = load_golden("train.npz")
+    cams = _cams(g)
+    tgts = [train.GroundTruth(images=[g[f"bg_t{t}_c0"], g[f"bg_t{t}_c1"]]) for t in range(3)]
+    stream = grouping.build_groups(tgts, cams, train.LossWeights(), train.TrainConfig(iterations=2, step_size=0.05),
+                                   train.TrainConfig(iterations=3, step_size=0.05, densify_interval=2),
+                                   (np.full(3, -0.5), np.full(3, 0.5)), 120, tau_db=18.9, seed=3)
+    np.testing.assert_array_equal([r.is_keyframe for r in stream.records], g["bg_iskey"])
+    assert np.max(np.abs(np.array([r.quality_db for r in stream.records]) - g["bg_quality"])) <= 1e-6
+    for k, sp in stream.spaces.items():
+        ref = g[f"bg_space{k}"]
+        assert sp.frame.params.shape == ref.shape
+        assert np.max(np.abs(sp.frame.params - ref)) <= 1e-8 * max(np.max(np.abs(ref)), 1.0)
+    for r in stream.records:
+        ref = g[f"bg_cum{r.frame_index}"]
+        assert np.max(np.abs(r.cumulative_delta.dense() - ref)) <= 1e-8 * max(np.max(np.abs(ref)), 1e-12)
