@@ -956,7 +956,8 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 
     for (int base = 0; base < n_all; base += kBatch) {
         const int nb = min(kBatch, n_all - base);
-        __syncthreads();
+        // (the previous batch ended with a block-wide __syncthreads_count: every
+        // warp is done with the staging arrays this batch overwrites)
         if ((int)threadIdx.x < nb) {
             const int t = threadIdx.x;
             const uint32_t gi = (uint32_t)glist[base + t];
@@ -1109,10 +1110,12 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             done = done || kAlphaClamp * T <= kEpsContrib;
             thr = __log2f((float)T) + log2_inv_eps();
         }
-        __syncthreads();
-        if (USAGE && (int)threadIdx.x < nb && sh.cnt[threadIdx.x] > 0)
-            atomicAdd((unsigned long long *)(itp->usage + sh.gid[threadIdx.x]),
-                      (unsigned long long)sh.cnt[threadIdx.x]);
+        if (USAGE) {  // every warp's shared-memory counts of this batch are final
+            __syncthreads();
+            if ((int)threadIdx.x < nb && sh.cnt[threadIdx.x] > 0)
+                atomicAdd((unsigned long long *)(itp->usage + sh.gid[threadIdx.x]),
+                          (unsigned long long)sh.cnt[threadIdx.x]);
+        }
         if (__syncthreads_count(!done) == 0) break;
     }
 
