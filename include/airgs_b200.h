@@ -194,6 +194,26 @@ AIRGS_API int airgs_composite_forward(airgs_ctx *ctx, int64_t k, const double *m
                             int32_t height, int32_t width, double *image,
                             double *t_final, int64_t *usage, void *stream);
 
+/* forward(..., record=True) of the kernel seam (ss/_composite.pyx:18-74):
+ * airgs_composite_forward plus the reference's contribution masks, uint8
+ * [total bbox area], primitive i's clipped bbox row-major at mask_offsets[i]
+ * (device int64 [k], the prefix of the non-empty bbox areas). */
+AIRGS_API int airgs_composite_forward_record(airgs_ctx *ctx, int64_t k, const double *means2d,
+                                             const double *conics, const double *alphas, const double *colors,
+                                             const int64_t *bboxes, int32_t height, int32_t width, double *image,
+                                             double *t_final, int64_t *usage, const int64_t *mask_offsets,
+                                             uint8_t *masks, void *stream);
+
+/* backward(...) of the kernel seam (ss/_composite.pyx:77-152): masks and
+ * t_final as returned by the recorded forward, d_image (h, w, 3); grads9
+ * (device float64 [k][9]) receives d_means2d (2), d_conics (3), d_alphas,
+ * d_colors (3) per primitive. */
+AIRGS_API int airgs_composite_backward(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics,
+                                       const double *alphas, const double *colors, const int64_t *bboxes,
+                                       int32_t height, int32_t width, const int64_t *mask_offsets,
+                                       const uint8_t *masks, const double *t_final, const double *d_image,
+                                       double *grads9, void *stream);
+
 /* Sum of squared differences of two device float64 arrays of n values
  * (ss/metrics.py:40 numerator), deterministic order.  out: device double. */
 AIRGS_API int airgs_sse(airgs_ctx *ctx, const double *a, const double *b, int64_t n,

@@ -73,6 +73,9 @@ SIGNATURES = {
                                                vp]),
     "airgs_composite_forward": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp]),
     "airgs_sse": (ctypes.c_int, [vp, vp, vp, i64, vp, vp]),
+    "airgs_composite_forward_record": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp,
+                                                      vp]),
+    "airgs_composite_backward": (ctypes.c_int, [vp, i64, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
     "airgs_ssim": (ctypes.c_int, [vp, vp, vp, i32, i32, i32, c_double_p, vp, vp, vp]),
     "airgs_l1": (ctypes.c_int, [vp, vp, vp, i64, vp, vp, vp]),
     "airgs_rows_to_planes": (ctypes.c_int, [vp, vp, i64, i64, i32, vp, i64, vp]),

@@ -511,6 +511,7 @@ struct CompShared {
     uint32_t gid[kBatch];
     int32_t cnt[kBatch];
     uint8_t wmask[kBatch];  // bit w: may touch warp w's 8x4 sub-tile
+    int4 bbox[kBatch];      // BBOX mode: clipped bbox x0, x1, y0, y1
     // per warp, entry pairs (a, b): {-mx_a,-mx_b,-my_a,-my_b}, {A_a,A_b,B_a,B_b}, {C_a,C_b,-L_a,-L_b}
     float4 pl[kCompWarps][kWarpList / 2][3];
     uint8_t sidx[kCompWarps][kWarpList];  // compacted position -> staged position
@@ -911,7 +912,12 @@ __global__ void __launch_bounds__(128) k_depth_gaps(TileSortArgs a, unsigned lon
 // domain, proven guard band) and builds a per-lane candidate mask; phase B has
 // every lane run its own candidates through the exact fp64 path in depth
 // order (two candidates' exp in flight).
-template <bool USAGE, bool STATS, bool RECORD = false>
+// RECORD: write the contribution record (backward passes).  BBOX: test every
+// candidate pixel against the primitive's clipped bbox -- needed only for the
+// kernel seam, whose caller-supplied bboxes need not contain the primitive's
+// contributing pixels (bboxes from the projection always do: outside the
+// 3.5-sigma box alpha * g < 1/255).
+template <bool USAGE, bool STATS, bool RECORD = false, bool BBOX = false>
 __global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
 k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
             const TileLists tls, const uint32_t *__restrict__ tcount, unsigned long long *__restrict__ stats) {
@@ -990,6 +996,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #pragma unroll
             for (int ww = 0; ww < 8; ++ww) mk |= (((xm >> (ww & 1)) & (ym >> (ww >> 1))) & 1u) << ww;
             sh.wmask[t] = (uint8_t)mk;
+            if (BBOX) sh.bbox[t] = make_int4(r.x0, r.x1, r.y0, r.y1);
             if (USAGE) sh.cnt[t] = 0;
         }
         __syncthreads();
@@ -1061,8 +1068,13 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                 const bool two = word != 0;
                 const int j2 = two ? sid[__ffs(word) - 1] : j1;
                 word &= word - 1;
-                const double ap1 = alpha_at(sh, j1, pxd, pyd);
-                const double ap2 = alpha_at(sh, j2, pxd, pyd);
+                double ap1 = alpha_at(sh, j1, pxd, pyd);
+                double ap2 = alpha_at(sh, j2, pxd, pyd);
+                if (BBOX) {  // outside the caller's bbox the reference never evaluates the pair
+                    const int4 b1 = sh.bbox[j1], b2 = sh.bbox[j2];
+                    if (px < b1.x || px >= b1.y || py < b1.z || py >= b1.w) ap1 = 0.0;
+                    if (px < b2.x || px >= b2.y || py < b2.z || py >= b2.w) ap2 = 0.0;
+                }
                 double wgt = ap1 * T;
                 if (STATS) wmar = fmin(wmar, fabs(wgt - kEpsContrib));
                 if (wgt > kCompC[7]) {
@@ -1444,7 +1456,8 @@ struct RecWordsOut {
 
 static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
                                const TileLists &tl, const Rec *recs, const uint64_t *depth, const int32_t *ntiles,
-                               uint32_t *tile_count, double *sse, cudaStream_t st, RecordOut *rec = nullptr) {
+                               uint32_t *tile_count, double *sse, cudaStream_t st, RecordOut *rec = nullptr,
+                               bool bbox = false) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
@@ -1529,9 +1542,29 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
     cudaEvent_t t_comp = Tt > 0 ? ctx->time_begin(st) : nullptr;
     if (Tt > 0) {
         unsigned long long *cs = ctx->d_stats;
-        if (rec) {
-            k_composite<false, false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                                   tile_count, cs);
+        const dim3 grid((unsigned)Tt), block(kTileThreads);
+        if (bbox) {  // the kernel seam (caller-supplied bboxes)
+            if (rec) {
+                if (any_usage)
+                    k_composite<true, false, true, true><<<grid, block, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                                 tile_count, cs);
+                else
+                    k_composite<false, false, true, true><<<grid, block, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                                  tile_count, cs);
+            } else if (any_usage) {
+                k_composite<true, false, false, true><<<grid, block, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                              tile_count, cs);
+            } else {
+                k_composite<false, false, false, true><<<grid, block, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
+                                                                               tile_count, cs);
+            }
+        } else if (rec) {
+            if (any_usage)
+                k_composite<true, false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems,
+                                                                                      tl, tile_count, cs);
+            else
+                k_composite<false, false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems,
+                                                                                       tl, tile_count, cs);
         } else if (stats_on) {
             if (any_usage)
                 k_composite<true, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
@@ -1615,7 +1648,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         }
     }
     TileLists tl{bucket, nullptr, cap};
-    sort_composite_sse(ctx, work, L, tl, recs, depth, ntiles, tile_count, sse, st, rec);
+    sort_composite_sse(ctx, work, L, tl, recs, depth, ntiles, tile_count, sse, st, rec, index_order != 0);
     // one host synchronisation per render: parameter validity and bucket overflow
     unsigned int hflags = 0;
     AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
@@ -1632,7 +1665,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
             AIRGS_CUDA_TRY(cudaMemsetAsync(usage_map[k].second, 0, sizeof(int64_t) * n, st));
         }
         const TileLists tl2 = scanned_lists(ctx, items, L, recs, depth, ntiles, tile_count, index_order, cap, st);
-        sort_composite_sse(ctx, work, L, tl2, recs, depth, ntiles, tile_count, sse, st, rec);
+        sort_composite_sse(ctx, work, L, tl2, recs, depth, ntiles, tile_count, sse, st, rec, index_order != 0);
     }
     for (const auto &m : usage_map) {
         int64_t n = 0;
@@ -2191,9 +2224,79 @@ static void compositing_order_impl(airgs_ctx *ctx, const airgs_frame *frame, con
     AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
 }
 
+// ---- kernel seam record / backward: the reference's mask layout -----------
+// masks[off_i + (iy - y0) * (x1 - x0) + (ix - x0)] for primitive i's clipped
+// bbox, off_i = prefix of the non-empty bbox areas (ss/_composite.pyx:29-35,
+// 67-73); tile bits <-> reference masks through the primitive's position in the
+// tile list (sorted by input index on the seam).
+
+__device__ __forceinline__ int list_find(const uint64_t *lst, int n, uint32_t id) {
+    int lo = 0, hi = n - 1;
+    while (lo <= hi) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t v = (uint32_t)lst[mid];
+        if (v == id) return mid;
+        if (v < id) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+// one block per primitive: its bbox pixels' contribution bits -> reference masks
+__global__ void __launch_bounds__(128) k_masks_from_bits(const int64_t *__restrict__ bboxes,
+                                                         const int64_t *__restrict__ moff, const TileLists tls,
+                                                         const uint32_t *__restrict__ tcount,
+                                                         const uint32_t *__restrict__ cbits,
+                                                         const int64_t *__restrict__ cbase, int tiles_x,
+                                                         uint8_t *__restrict__ masks) {
+    const int64_t i = blockIdx.x;
+    const int x0 = (int)bboxes[4 * i], x1 = (int)bboxes[4 * i + 1], y0 = (int)bboxes[4 * i + 2],
+              y1 = (int)bboxes[4 * i + 3];
+    if (x1 <= x0 || y1 <= y0) return;
+    const int bw = x1 - x0;
+    const int64_t area = (int64_t)bw * (y1 - y0);
+    for (int64_t q = threadIdx.x; q < area; q += blockDim.x) {
+        const int iy = y0 + (int)(q / bw), ix = x0 + (int)(q % bw);
+        const int64_t g = (int64_t)(iy / kTile) * tiles_x + ix / kTile;
+        const int e = list_find(tls.list(g), tls.count(tcount, g), (uint32_t)i);
+        uint8_t m = 0;
+        if (e >= 0)
+            m = (cbits[cbase[g] + (int64_t)(e >> 5) * kTileThreads + (iy % kTile) * kTile + ix % kTile] >> (e & 31)) & 1u;
+        masks[moff[i] + q] = m;
+    }
+}
+
+// one block per tile: reference masks -> contribution bits of the tile's entries
+__global__ void __launch_bounds__(kTileThreads) k_bits_from_masks(const int64_t *__restrict__ bboxes,
+                                                                  const int64_t *__restrict__ moff,
+                                                                  const TileLists tls,
+                                                                  const uint32_t *__restrict__ tcount,
+                                                                  const int64_t *__restrict__ cbase, int tiles_x,
+                                                                  int w, int h, const uint8_t *__restrict__ masks,
+                                                                  uint32_t *__restrict__ cbits) {
+    const int64_t g = blockIdx.x;
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int ix = (int)(g % tiles_x) * kTile + lx, iy = (int)(g / tiles_x) * kTile + ly;
+    const int n = tls.count(tcount, g);
+    const uint64_t *lst = tls.list(g);
+    uint32_t word = 0;
+    for (int e = 0; e < n; ++e) {
+        const int64_t i = (uint32_t)lst[e];
+        const int x0 = (int)bboxes[4 * i], x1 = (int)bboxes[4 * i + 1], y0 = (int)bboxes[4 * i + 2],
+                  y1 = (int)bboxes[4 * i + 3];
+        if (ix < w && iy < h && ix >= x0 && ix < x1 && iy >= y0 && iy < y1 &&
+            masks[moff[i] + (int64_t)(iy - y0) * (x1 - x0) + (ix - x0)])
+            word |= 1u << (e & 31);
+        if ((e & 31) == 31 || e == n - 1) {
+            cbits[cbase[g] + (int64_t)(e >> 5) * kTileThreads + threadIdx.x] = word;
+            word = 0;
+        }
+    }
+}
+
 static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics, const double *alphas,
                       const double *colors, const int64_t *bboxes, int h, int w, double *image, double *tfinal,
-                      int64_t *usage, cudaStream_t st) {
+                      int64_t *usage, cudaStream_t st, RecordOut *rec = nullptr, Rec **recs_out = nullptr,
+                      int64_t *Tt_out = nullptr, uint32_t **tcount_out = nullptr) {
     if (h < 1 || w < 1) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad image size");
     if (k > 0x7fffffffLL) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");
     std::vector<ItemHost> ih(1);
@@ -2228,7 +2331,54 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
         check_launch();
     }
     // every in-image pixel of every tile is written by the composite kernel
-    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 1, nullptr, st, flags);
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 1, nullptr, st, flags, rec);
+    if (recs_out) *recs_out = recs;
+    if (Tt_out) *Tt_out = L.Tt;
+    if (tcount_out) *tcount_out = tile_count;
+}
+
+// forward(record=True): the seam forward plus the reference's masks
+static void seam_record_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics,
+                             const double *alphas, const double *colors, const int64_t *bboxes, int h, int w,
+                             double *image, double *tfinal, int64_t *usage, const int64_t *moff, uint8_t *masks,
+                             cudaStream_t st) {
+    RecordOut rec;
+    int64_t Tt = 0;
+    uint32_t *tcount = nullptr;
+    seam_impl(ctx, k, means2d, conics, alphas, colors, bboxes, h, w, image, tfinal, usage, st, &rec, nullptr, &Tt,
+              &tcount);
+    if (k > 0 && Tt > 0 && rec.cbits) {
+        k_masks_from_bits<<<(unsigned)k, 128, 0, st>>>(bboxes, moff, rec.tl, tcount, rec.cbits, rec.cbase,
+                                                       (w + kTile - 1) / kTile, masks);
+        ++ctx->launches;
+        check_launch();
+    }
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+}
+
+// backward(masks, t_final, d_image) of the seam (ss/_composite.pyx:77-152):
+// grads9 = [k][d_means2d x, y, d_conics a, b, c, d_alphas, d_colors r, g, b]
+static void seam_backward_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics,
+                               const double *alphas, const double *colors, const int64_t *bboxes, int h, int w,
+                               const int64_t *moff, const uint8_t *masks, const double *tfinal,
+                               const double *d_image, double *grads9, cudaStream_t st) {
+    if (k > 0) AIRGS_CUDA_TRY(cudaMemsetAsync(grads9, 0, sizeof(double) * 9 * k, st));
+    RecordOut rec;
+    Rec *recs = nullptr;
+    int64_t Tt = 0;
+    uint32_t *tcount = nullptr;
+    // the tile lists (and a record buffer of the right layout) from the seam pipeline
+    seam_impl(ctx, k, means2d, conics, alphas, colors, bboxes, h, w, nullptr, nullptr, nullptr, st, &rec, &recs, &Tt,
+              &tcount);
+    if (k <= 0 || Tt <= 0 || !rec.cbits) return;
+    const int tiles_x = (w + kTile - 1) / kTile;
+    k_bits_from_masks<<<(unsigned)Tt, kTileThreads, 0, st>>>(bboxes, moff, rec.tl, tcount, rec.cbase, tiles_x, w, h,
+                                                           masks, rec.cbits);
+    k_composite_bwd<<<(unsigned)Tt, kTileThreads, 0, st>>>(recs, rec.tl, tcount, rec.cbits, rec.cbase, tiles_x, w, h,
+                                                         tfinal, d_image, grads9);
+    ctx->launches += 2;
+    check_launch();
+    AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
 }
 
 static void sse_impl(airgs_ctx *ctx, const double *a, const double *b, int64_t n, double *out, cudaStream_t st) {
@@ -2276,6 +2426,28 @@ extern "C" int airgs_compositing_order(airgs_ctx *ctx, const airgs_frame *frame,
                                        void *stream) {
     return guarded(ctx, [&] {
         compositing_order_impl(ctx, frame, cam, frozen_pos, order_out, kept_out, (cudaStream_t)stream);
+    });
+}
+
+extern "C" int airgs_composite_forward_record(airgs_ctx *ctx, int64_t k, const double *means2d,
+                                              const double *conics, const double *alphas, const double *colors,
+                                              const int64_t *bboxes, int32_t height, int32_t width, double *image,
+                                              double *t_final, int64_t *usage, const int64_t *mask_offsets,
+                                              uint8_t *masks, void *stream) {
+    return guarded(ctx, [&] {
+        seam_record_impl(ctx, k, means2d, conics, alphas, colors, bboxes, height, width, image, t_final, usage,
+                         mask_offsets, masks, (cudaStream_t)stream);
+    });
+}
+
+extern "C" int airgs_composite_backward(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics,
+                                        const double *alphas, const double *colors, const int64_t *bboxes,
+                                        int32_t height, int32_t width, const int64_t *mask_offsets,
+                                        const uint8_t *masks, const double *t_final, const double *d_image,
+                                        double *grads9, void *stream) {
+    return guarded(ctx, [&] {
+        seam_backward_impl(ctx, k, means2d, conics, alphas, colors, bboxes, height, width, mask_offsets, masks,
+                           t_final, d_image, grads9, (cudaStream_t)stream);
     });
 }
 

@@ -276,19 +276,8 @@ def render_backward(state, d_image, as_numpy: bool = True):
     return grads.cpu().numpy() if as_numpy else grads
 
 
-def forward(means2d, conics, alphas, colors, bboxes, height, width, record=False):
-    """The reference kernel seam ``_composite.forward`` on the GPU.
-
-    Inputs are numpy arrays (or CUDA tensors) of depth-ordered primitives;
-    returns numpy ``(image (h,w,3) unclipped, t_final (h,w), usage (k,),
-    None)``.  ``record=True`` (training masks) is out of scope.
-    """
+def _seam_inputs(means2d, conics, alphas, colors, bboxes, dev):
     import torch
-
-    if record:
-        raise NotImplementedError("record=True (training contribution masks) is outside the evaluation path")
-    dev = dv.device_of(None)
-    eng = engine(dev)
 
     def t(a, dt):
         if isinstance(a, torch.Tensor):
@@ -296,17 +285,76 @@ def forward(means2d, conics, alphas, colors, bboxes, height, width, record=False
         return torch.from_numpy(np.ascontiguousarray(np.asarray(a), dtype=np.float64 if dt == torch.float64
                                                     else np.int64)).to(dev)
 
-    m2 = t(means2d, torch.float64)
+    return (t(means2d, torch.float64), t(conics, torch.float64), t(alphas, torch.float64),
+            t(colors, torch.float64), t(bboxes, torch.int64))
+
+
+def _mask_offsets(bb):
+    """Per-primitive offsets of the reference's mask layout and its total size
+    (ss/_composite.pyx:29-35: the buffer covers every bbox area, offsets
+    advance over the non-empty ones)."""
+    import torch
+
+    w = bb[:, 1] - bb[:, 0]
+    h = bb[:, 3] - bb[:, 2]
+    area = w * h
+    valid = (w > 0) & (h > 0)
+    off = torch.cumsum(torch.where(valid, area, torch.zeros_like(area)), 0) - torch.where(valid, area,
+                                                                                          torch.zeros_like(area))
+    return off.contiguous(), int(area.sum().item()) if area.numel() else 0
+
+
+def forward(means2d, conics, alphas, colors, bboxes, height, width, record=False):
+    """The reference kernel seam ``_composite.forward`` on the GPU.
+
+    Inputs are numpy arrays (or CUDA tensors) of depth-ordered primitives;
+    returns numpy ``(image (h,w,3) unclipped, t_final (h,w), usage (k,),
+    masks)`` with ``masks`` the reference's uint8 contribution masks when
+    ``record`` (ss/_composite.pyx:18-74), else None.
+    """
+    import torch
+
+    dev = dv.device_of(None)
+    eng = engine(dev)
+    m2, co, al, cl, bb = _seam_inputs(means2d, conics, alphas, colors, bboxes, dev)
     k = m2.shape[0]
-    co, al, cl, bb = t(conics, torch.float64), t(alphas, torch.float64), t(colors, torch.float64), t(bboxes, torch.int64)
     img = torch.empty((int(height), int(width), 3), dtype=torch.float64, device=dev)
     tr = torch.empty((int(height), int(width)), dtype=torch.float64, device=dev)
     us = torch.zeros((max(k, 1),), dtype=torch.int64, device=dev)
-    eng.call("airgs_composite_forward", k, ptr(m2), ptr(co), ptr(al), ptr(cl), ptr(bb), int(height), int(width),
-             ptr(img), ptr(tr), ptr(us), eng.stream())
-    return img.cpu().numpy(), tr.cpu().numpy(), us[:k].cpu().numpy(), None
+    if not record:
+        eng.call("airgs_composite_forward", k, ptr(m2), ptr(co), ptr(al), ptr(cl), ptr(bb), int(height),
+                 int(width), ptr(img), ptr(tr), ptr(us), eng.stream())
+        return img.cpu().numpy(), tr.cpu().numpy(), us[:k].cpu().numpy(), None
+    off, total = _mask_offsets(bb)
+    masks = torch.zeros((max(total, 1),), dtype=torch.uint8, device=dev)
+    eng.call("airgs_composite_forward_record", k, ptr(m2), ptr(co), ptr(al), ptr(cl), ptr(bb), int(height),
+             int(width), ptr(img), ptr(tr), ptr(us), ptr(off), ptr(masks), eng.stream())
+    return img.cpu().numpy(), tr.cpu().numpy(), us[:k].cpu().numpy(), masks[:total].cpu().numpy()
 
 
-def backward(*args, **kwargs):
-    raise NotImplementedError("the backward compositing pass is training-only and outside the evaluation path")
+def backward(means2d, conics, alphas, colors, bboxes, height, width, masks, t_final, d_image):
+    """The reference kernel seam ``_composite.backward`` on the GPU
+    (ss/_composite.pyx:77-152): returns numpy ``(d_means2d (k,2), d_conics
+    (k,3), d_alphas (k,), d_colors (k,3))``."""
+    import torch
+
+    dev = dv.device_of(None)
+    eng = engine(dev)
+    m2, co, al, cl, bb = _seam_inputs(means2d, conics, alphas, colors, bboxes, dev)
+    k = m2.shape[0]
+    off, total = _mask_offsets(bb)
+    mk = torch.as_tensor(np.ascontiguousarray(np.asarray(masks, dtype=np.uint8))).to(dev)
+    if mk.numel() < total:
+        raise StructuralError("masks shorter than the primitives' bbox areas")
+    tf = torch.as_tensor(np.ascontiguousarray(np.asarray(t_final, dtype=np.float64))).to(dev)
+    di = torch.as_tensor(np.ascontiguousarray(np.asarray(d_image, dtype=np.float64))).to(dev)
+    if tuple(tf.shape) != (int(height), int(width)) or tuple(di.shape) != (int(height), int(width), 3):
+        raise StructuralError("t_final / d_image shape mismatch")
+    g9 = torch.zeros((max(k, 1), 9), dtype=torch.float64, device=dev)
+    eng.call("airgs_composite_backward", k, ptr(m2), ptr(co), ptr(al), ptr(cl), ptr(bb), int(height), int(width),
+             ptr(off), ptr(mk), ptr(tf), ptr(di), ptr(g9), eng.stream())
+    g = g9[:k].cpu().numpy()
+    return (np.ascontiguousarray(g[:, 0:2]), np.ascontiguousarray(g[:, 2:5]), np.ascontiguousarray(g[:, 5]),
+            np.ascontiguousarray(g[:, 6:9]))
+
 

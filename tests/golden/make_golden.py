@@ -431,8 +431,48 @@ def gen_train(ss):
     np.savez_compressed(os.path.join(HERE, "train.npz"), **out)
 
 
+def gen_seam_backward(ss):
+    """The kernel seam's forward(record=True) masks and backward
+    (ss/_composite.pyx:18-152) on random primitives (with clipped and empty
+    bboxes) and on a prepared scene."""
+    from splatstream import _composite, camera, model, rasterizer
+
+    out = {}
+    rng = np.random.default_rng(1100)
+    cases = []
+    n, hh, ww = 60, 30, 37
+    means2d = rng.uniform(-3, ww + 3, (n, 2))
+    conics = np.zeros((n, 3))
+    conics[:, 0] = rng.uniform(0.05, 0.5, n)
+    conics[:, 1] = rng.uniform(-0.03, 0.03, n)
+    conics[:, 2] = rng.uniform(0.05, 0.5, n)
+    alphas = rng.uniform(0.2, 0.99, n)
+    colors = rng.uniform(0, 1, (n, 3))
+    r = rng.uniform(1, 9, n)
+    bb = np.stack([np.clip(np.floor(means2d[:, 0] - r), 0, ww), np.clip(np.ceil(means2d[:, 0] + r) + 1, 0, ww),
+                   np.clip(np.floor(means2d[:, 1] - r), 0, hh), np.clip(np.ceil(means2d[:, 1] + r) + 1, 0, hh)],
+                  axis=1).astype(np.int64)
+    bb[3] = [5, 5, 2, 9]  # empty bbox
+    cases.append((means2d, conics, alphas, colors, bb, hh, ww))
+    p = random_params(rng, 400, 0, 0.5)
+    cam = camera.ring_rig(1, radius=3.0, height=0.3, focal=40.0, resolution=(48, 40))[0]
+    pr = rasterizer._prepare(model.GaussianFrame(params=p), cam)
+    cases.append((pr.means2d, pr.conics, pr.alphas, pr.colors, pr.bboxes, 40, 48))
+    for cid, (m2, co, al, cl, bbx, h, w) in enumerate(cases):
+        img, tr, us, masks = _composite.forward(m2, co, al, cl, bbx, h, w, record=True)
+        d_image = rng.normal(0, 1, (h, w, 3))
+        grads = _composite.backward(m2, co, al, cl, bbx, h, w, masks, np.asarray(tr), d_image)
+        for k, v in dict(means2d=m2, conics=co, alphas=al, colors=cl, bboxes=bbx, hw=np.array([h, w]),
+                         image=np.asarray(img), trans=np.asarray(tr), usage=np.asarray(us), masks=np.asarray(masks),
+                         d_image=d_image).items():
+            out[f"s{cid}_{k}"] = v
+        for name, v in zip(("d_means2d", "d_conics", "d_alphas", "d_colors"), grads):
+            out[f"s{cid}_{name}"] = np.asarray(v)
+    np.savez_compressed(os.path.join(HERE, "seam_backward.npz"), **out)
+
+
 GENERATORS = ("gen_render", "gen_composite", "gen_codec", "gen_delta", "gen_pruning", "gen_grouping", "gen_session",
-              "gen_metrics", "gen_backward", "gen_io", "gen_train")
+              "gen_metrics", "gen_backward", "gen_io", "gen_train", "gen_seam_backward")
 
 
 def main():

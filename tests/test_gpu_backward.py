@@ -66,3 +66,25 @@ def test_render_backward_finite_difference():
     fd = (loss(p + h * direction) - loss(p - h * direction)) / (2 * h)
     an = float(np.sum(grads * direction))
     assert abs(fd - an) <= 1e-3 * abs(an) + 1e-9
+
+
+@pytest.mark.parametrize("cid", [0, 1])
+def test_seam_record_and_backward_match_reference(cid):
+    """The kernel seam (ss/_composite.pyx:18-152): forward(record=True) masks
+    identical to the reference's, backward(...) from the reference's masks and
+    t_final to 1e-9 of each output's scale."""
+    from paper_2512_20943_b200 import rasterizer
+
+    g = load_golden("seam_backward.npz")
+    a = [g[f"s{cid}_{k}"] for k in ("means2d", "conics", "alphas", "colors", "bboxes")]
+    h, w = (int(v) for v in g[f"s{cid}_hw"])
+    img, tr, us, masks = rasterizer.forward(*a, h, w, record=True)
+    np.testing.assert_array_equal(us, g[f"s{cid}_usage"])
+    np.testing.assert_array_equal(masks, g[f"s{cid}_masks"])
+    assert np.max(np.abs(img - g[f"s{cid}_image"])) <= 1e-12
+    assert np.max(np.abs(tr - g[f"s{cid}_trans"])) <= 1e-12
+    out = rasterizer.backward(*a, h, w, g[f"s{cid}_masks"], g[f"s{cid}_trans"], g[f"s{cid}_d_image"])
+    for name, v in zip(("d_means2d", "d_conics", "d_alphas", "d_colors"), out):
+        ref = g[f"s{cid}_{name}"]
+        assert v.shape == ref.shape
+        assert np.max(np.abs(v - ref)) <= 1e-9 * max(np.max(np.abs(ref)), 1e-300), name
