@@ -160,6 +160,7 @@ enum Slot : int {
     kSlotRecBits,
     kSlotBwdGrad,
     kSlotTFinal,
+    kSlotBinRec,
     kSlotCount
 };
 

@@ -43,6 +43,7 @@ struct ProjArgs {
     Rec *recs;                 // [nitems][stride]
     uint64_t *depth;           // [nitems][stride] orderable depth keys
     int32_t *ntiles;           // [nitems][stride] tiles touched (0 = empty bbox, -1 = no tile)
+    uint2 *binrec;             // [nitems][stride] tile range u0 | u1 << 16, v0 | v1 << 16 (when ntiles > 0)
     unsigned int *flags;
     int64_t stride;
     unsigned long long *stats;  // diagnostic decision margins (null: off)
@@ -240,7 +241,10 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
             }
             int u0, u1, v0, v1;
             const bool has_bbox = rec.x1 > rec.x0 && rec.y1 > rec.y0;
-            if (has_bbox && rec_tile_range(rec, u0, u1, v0, v1)) nt = (u1 - u0 + 1) * (v1 - v0 + 1);
+            if (has_bbox && rec_tile_range(rec, u0, u1, v0, v1)) {
+                nt = (u1 - u0 + 1) * (v1 - v0 + 1);
+                a.binrec[o] = make_uint2((uint32_t)u0 | ((uint32_t)u1 << 16), (uint32_t)v0 | ((uint32_t)v1 << 16));
+            }
             const int64_t *fz = a.item_frozen ? a.item_frozen[item] : nullptr;
             const unsigned long long zk = order_key_of(fz, i, tz);
             if (has_bbox) {  // (bbox-only records are read by the diagnostic counters alone)
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
 // (primitive, tile) pairs are spread over its lanes so that 32 counter
 // atomics are in flight per round instead of one serial chain per thread.
 struct BinArgs {
-    const Rec *recs;
+    const uint2 *binrec;
     const uint64_t *depth;
     const int32_t *ntiles;
     const int64_t *tile_base;
@@ -290,8 +294,11 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
     int u0 = 0, u1 = 0, v0 = 0, v1 = 0;
     uint64_t entry = 0;
     if (nt > 0) {
-        const Rec &r = a.recs[o];
-        rec_tile_range(r, u0, u1, v0, v1);
+        const uint2 br = a.binrec[o];  // 8 bytes instead of the 96-byte record
+        u0 = (int)(br.x & 0xffffu);
+        u1 = (int)(br.x >> 16);
+        v0 = (int)(br.y & 0xffffu);
+        v1 = (int)(br.y >> 16);
         const uint64_t zk = a.depth[o];
         // 32-bit order key: small keys (frozen positions, the seam's input order)
         // as they are; depth keys (z > 0) as their fp32 bits, monotone, behind them
@@ -1251,7 +1258,7 @@ __global__ void __launch_bounds__(256)
 k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__restrict__ conics,
                const double *__restrict__ alphas, const double *__restrict__ colors,
                const int64_t *__restrict__ bboxes, Rec *__restrict__ recs, int32_t *__restrict__ ntiles,
-               uint64_t *__restrict__ depth) {
+               uint64_t *__restrict__ depth, uint2 *__restrict__ binrec) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
     Rec r;
@@ -1279,7 +1286,10 @@ k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__re
     }
     recs[i] = r;
     int nt = 0, u0, u1, v0, v1;
-    if (r.x1 > r.x0 && r.y1 > r.y0 && rec_tile_range(r, u0, u1, v0, v1)) nt = (u1 - u0 + 1) * (v1 - v0 + 1);
+    if (r.x1 > r.x0 && r.y1 > r.y0 && rec_tile_range(r, u0, u1, v0, v1)) {
+        nt = (u1 - u0 + 1) * (v1 - v0 + 1);
+        binrec[i] = make_uint2((uint32_t)u0 | ((uint32_t)u1 << 16), (uint32_t)v0 | ((uint32_t)v1 << 16));
+    }
     ntiles[i] = nt > 0 ? nt : (r.x1 > r.x0 && r.y1 > r.y0 ? -1 : 0);
     depth[i] = (uint64_t)i;  // the input order is the depth order
 }
@@ -1601,7 +1611,7 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
 static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
                               const Rec *recs, const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count,
                               int index_order, double *sse, cudaStream_t st, unsigned int *flags,
-                              RecordOut *rec = nullptr) {
+                              const uint2 *binrec, RecordOut *rec = nullptr) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
@@ -1612,7 +1622,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     const uint32_t cap = ctx->bucket_cap;
     uint64_t *bucket = ctx->scratch_t<uint64_t>(kSlotPairKeysAlt, (size_t)std::max<int64_t>(Tt, 1) * cap);
     if (maxc > 0 && Tt > 0) {
-        BinArgs ba{recs, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tile_count, bucket, cap, flags, L.stride,
+        BinArgs ba{binrec, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tile_count, bucket, cap, flags, L.stride,
                    index_order};
         k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
         ++NL;
@@ -1736,6 +1746,8 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         if (f.count > 0x7fffffffLL) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");
         const airgs_camera &c = cams[v.camera];
         if (c.width < 1 || c.height < 1) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad camera resolution");
+        if (c.width > (65535 * kTile) || c.height > (65535 * kTile))
+            throw ApiFailure(AIRGS_E_CAPACITY, "camera resolution beyond the tile index range");
         ItemHost &h = ih[s];
         h.frame = v.frame;
         h.cam = v.camera;
@@ -1792,6 +1804,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     Rec *recs = ctx->scratch_t<Rec>(kSlotRecs, per);
     uint64_t *depth = ctx->scratch_t<uint64_t>(kSlotDepth, per);
     int32_t *ntiles = ctx->scratch_t<int32_t>(kSlotNtiles, per);
+    uint2 *binrec = ctx->scratch_t<uint2>(kSlotBinRec, per);
     uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
 
@@ -1807,6 +1820,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.recs = recs;
     pa.depth = depth;
     pa.ntiles = ntiles;
+    pa.binrec = binrec;
     pa.flags = flags;
     pa.stride = stride;
     pa.stats = (ctx->stats && ctx->d_stats) ? ctx->d_stats : nullptr;
@@ -1823,7 +1837,8 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         check_launch();
     }
     ctx->time_end(t_proj, st, 1);
-    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags, bwd ? &bwd->rec : nullptr);
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags, binrec,
+                      bwd ? &bwd->rec : nullptr);
     if (bwd) {
         bwd->recs = recs;
         bwd->Tt = L.Tt;
@@ -2298,6 +2313,7 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
                       int64_t *usage, cudaStream_t st, RecordOut *rec = nullptr, Rec **recs_out = nullptr,
                       int64_t *Tt_out = nullptr, uint32_t **tcount_out = nullptr) {
     if (h < 1 || w < 1) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad image size");
+    if (w > 65535 * kTile || h > 65535 * kTile) throw ApiFailure(AIRGS_E_CAPACITY, "image beyond the tile index range");
     if (k > 0x7fffffffLL) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");
     std::vector<ItemHost> ih(1);
     ItemHost &it = ih[0];
@@ -2318,6 +2334,7 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
     upload_layout(ctx, ih, L, st);
     Rec *recs = ctx->scratch_t<Rec>(kSlotRecs, L.stride);
     int32_t *ntiles = ctx->scratch_t<int32_t>(kSlotNtiles, L.stride);
+    uint2 *binrec = ctx->scratch_t<uint2>(kSlotBinRec, L.stride);
     uint64_t *depth = ctx->scratch_t<uint64_t>(kSlotDepth, L.stride);
     uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
@@ -2326,12 +2343,12 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
     if (usage && k > 0) AIRGS_CUDA_TRY(cudaMemsetAsync(usage, 0, sizeof(int64_t) * k, st));
     if (k > 0) {
         k_seam_records<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(k, means2d, conics, alphas, colors, bboxes, recs,
-                                                                  ntiles, depth);
+                                                                  ntiles, depth, binrec);
         ++ctx->launches;
         check_launch();
     }
     // every in-image pixel of every tile is written by the composite kernel
-    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 1, nullptr, st, flags, rec);
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 1, nullptr, st, flags, binrec, rec);
     if (recs_out) *recs_out = recs;
     if (Tt_out) *Tt_out = L.Tt;
     if (tcount_out) *tcount_out = tile_count;
