@@ -164,12 +164,17 @@ def run_gpu(args):
     from paper_2512_20943_b200 import _lib, synth
 
     rank, world, local = _dist()
+    local = local % torch.cuda.device_count()  # (identity with one rank per GPU)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("AIRGS_BENCH_BACKEND", "nccl")  # gloo: exercise N>1 on a single GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     cfg = synth.CONFIGS[args.config]
     total = args.warmup + args.steps
     space, cams, payloads, targets = build_workload(cfg, min(total, args.frames), seed=args.seed + rank,
