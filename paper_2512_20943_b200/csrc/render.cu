@@ -109,11 +109,14 @@ __device__ __forceinline__ bool rec_tile_range(const Rec &r, int &u0, int &u1, i
 }
 
 constexpr int kProjThreads = 128;
+#ifndef PROJ_MIN_BLOCKS
+#define PROJ_MIN_BLOCKS 6
+#endif
 
 // WMAX = 17 when every frame of the launch is SH degree 0 (fewer live registers),
 // 26 otherwise (handles both widths).
 template <int WMAX>
-__global__ void __launch_bounds__(kProjThreads) k_project(ProjArgs a) {
+__global__ void __launch_bounds__(kProjThreads, PROJ_MIN_BLOCKS) k_project(ProjArgs a) {
     const int f = blockIdx.y;
     const airgs_frame fr = a.frames[f];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -317,8 +320,9 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int64_t tb = a.tile_base[s];
     const int txn = a.tiles_x[s];
-    for (int k0 = 0; k0 < total; k0 += 32) {
-        const int k = k0 + lane;
+    // two rounds of 32 pairs per iteration: both counter atomics are in flight
+    // before either result is consumed
+    auto resolve = [&](int k, int64_t &g, uint64_t &oent) {
         // owner lane: the last lane whose first pair index is <= k
         int L = 0;
 #pragma unroll
@@ -329,12 +333,25 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
         const int j = k - __shfl_sync(0xffffffffu, excl, L);
         const int ou0 = __shfl_sync(0xffffffffu, u0, L), onu = __shfl_sync(0xffffffffu, nu, L);
         const int ov0 = __shfl_sync(0xffffffffu, v0, L);
-        const uint64_t oent = __shfl_sync(0xffffffffu, entry, L);
-        if (k < total) {
-            const int dv = j / onu;
-            const int64_t g = tb + (int64_t)(ov0 + dv) * txn + ou0 + (j - dv * onu);
-            const uint32_t pos = atomicAdd(a.tile_count + g, 1u);
-            if (pos < a.cap) a.bucket[g * a.cap + pos] = oent;
+        oent = __shfl_sync(0xffffffffu, entry, L);
+        const int dv = j / onu;
+        g = tb + (int64_t)(ov0 + dv) * txn + ou0 + (j - dv * onu);
+    };
+    for (int k0 = 0; k0 < total; k0 += 64) {
+        const int ka = k0 + lane, kb = k0 + 32 + lane;
+        int64_t ga = 0, gb = 0;
+        uint64_t ea = 0, eb = 0;
+        resolve(ka, ga, ea);
+        resolve(kb, gb, eb);
+        const bool va = ka < total, vb = kb < total;
+        const uint32_t pa = va ? atomicAdd(a.tile_count + ga, 1u) : 0u;
+        const uint32_t pb = vb ? atomicAdd(a.tile_count + gb, 1u) : 0u;
+        if (va) {
+            if (pa < a.cap) a.bucket[ga * a.cap + pa] = ea;
+            else atomicOr(a.flags, (unsigned)kFlagBucketOverflow);
+        }
+        if (vb) {
+            if (pb < a.cap) a.bucket[gb * a.cap + pb] = eb;
             else atomicOr(a.flags, (unsigned)kFlagBucketOverflow);
         }
     }
