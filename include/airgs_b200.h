@@ -168,6 +168,14 @@ AIRGS_API int airgs_l1(airgs_ctx *ctx, const double *a, const double *b, int64_t
 AIRGS_API int airgs_rows_to_planes(airgs_ctx *ctx, const uint8_t *bytes, int64_t byte_offset, int64_t n,
                                    int32_t width, double *planes, int64_t ld, void *stream);
 
+/* Deferred checking for pipelined batches: with enable = 1, airgs_gsdp_decode
+ * and airgs_render skip their host synchronisations (validity, bucket
+ * overflow) and fold the error flags into a device word; enable = 0
+ * synchronises and returns the accumulated flags in *flags_out (0: every call
+ * was valid; otherwise the caller re-runs the batch in checked mode, which
+ * raises the reference's exact errors and handles bucket overflow). */
+AIRGS_API int airgs_defer(airgs_ctx *ctx, int32_t enable, uint32_t *flags_out);
+
 /* ---- rasterizer --------------------------------------------------------- */
 
 /* Batched render: replaces ss/rasterizer.py:113-240 (_activate, _prepare,

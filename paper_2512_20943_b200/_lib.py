@@ -66,6 +66,7 @@ SIGNATURES = {
     "airgs_timing": (ctypes.c_int, [vp, i32, c_double_p, c_i64_p, c_double_p, c_i64_p]),
     "airgs_eval_stats": (ctypes.c_int, [vp, i32, c_i64_p]),
     "airgs_eval_margins": (ctypes.c_int, [vp, c_double_p]),
+    "airgs_defer": (ctypes.c_int, [vp, i32, ctypes.POINTER(ctypes.c_uint32)]),
     "airgs_render": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), i32, ctypes.POINTER(CameraC), i32,
                                     ctypes.POINTER(ItemC), i32, vp, vp]),
     "airgs_render_backward": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), ctypes.POINTER(CameraC), vp, vp, vp, vp]),

@@ -60,6 +60,7 @@ extern "C" int airgs_ctx_destroy(airgs_ctx *ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     if (ctx->d_stats) cudaFree(ctx->d_stats);
+    if (ctx->d_defer) cudaFree(ctx->d_defer);
     delete ctx;
     return AIRGS_OK;
 }
@@ -127,6 +128,27 @@ extern "C" int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts)
             if (int rc = stats_reset(ctx)) return rc;
         ctx->stats = enable != 0;
     }
+    return AIRGS_OK;
+}
+
+extern "C" int airgs_defer(airgs_ctx *ctx, int32_t enable, uint32_t *flags_out) {
+    if (!ctx) return AIRGS_E_INTERNAL;
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return AIRGS_E_CUDA;
+    if (enable) {
+        if (!ctx->d_defer && cudaMalloc(&ctx->d_defer, sizeof(unsigned int)) != cudaSuccess) return AIRGS_E_CUDA;
+        if (cudaMemset(ctx->d_defer, 0, sizeof(unsigned int)) != cudaSuccess) return AIRGS_E_CUDA;
+        ctx->defer = true;
+        if (flags_out) *flags_out = 0;
+        return AIRGS_OK;
+    }
+    unsigned int h = 0;
+    if (ctx->d_defer) {
+        if (cudaDeviceSynchronize() != cudaSuccess ||
+            cudaMemcpy(&h, ctx->d_defer, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return AIRGS_E_CUDA;
+    }
+    ctx->defer = false;
+    if (flags_out) *flags_out = h;
     return AIRGS_OK;
 }
 

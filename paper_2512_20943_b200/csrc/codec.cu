@@ -123,6 +123,15 @@ k_gsdp_rows(const uint8_t *__restrict__ qbytes, const int64_t *__restrict__ idx,
     present[i] = 1;
 }
 
+// Deferred validity check of a GSDP decode: any inconsistency marks the
+// context's deferred word (the caller re-runs the call in checked mode for the
+// reference's exact error).
+__global__ void k_gsdp_defer_check(const int64_t *nterm, int64_t E, const uint8_t *last, const unsigned int *flags,
+                                   unsigned int *defer) {
+    if (threadIdx.x || blockIdx.x) return;
+    if (*nterm != E || (*last & 0x80) || (*flags & (kFlagVarintLong | kFlagIndexRange))) atomicOr(defer, kDeferDecode);
+}
+
 // Sequential re-walk of the varint section in the reference's order
 // (ss/codec.py:44-58,229-242).  out[0] = error code (1 truncated varint,
 // 2 varint too long, 0 none), out[1] = position after the last varint.
@@ -337,6 +346,14 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
                                                                   (unsigned long long *)entries_out);
             ++L;
             check_launch();
+        }
+        if (ctx->defer && rows != nullptr) {
+            // deferred checking (airgs_defer): validity and error flags are folded
+            // into the context's deferred word on the device; no synchronisation
+            k_gsdp_defer_check<<<1, 1, 0, st>>>(misc + 1, E, payload + 24 + V - 1, flags, ctx->d_defer);
+            ++L;
+            check_launch();
+            return;
         }
         AIRGS_CUDA_TRY(cudaMemcpyAsync(hh, misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         AIRGS_CUDA_TRY(cudaMemcpyAsync(&last, payload + 24 + V - 1, 1, cudaMemcpyDeviceToHost, st));

@@ -67,6 +67,7 @@ enum DevFlag : unsigned int {
     kFlagIndexRange = 8u,     // delta index >= base_count
     kFlagQuantOverflow = 16u, // |q| > 2^31-1
     kFlagBucketOverflow = 32u, // a tile received more primitives than its bucket holds
+    kDeferDecode = 64u,        // deferred mode: a GSDP decode failed its checks
 };
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -30,7 +30,11 @@ struct airgs_ctx {
     // optional evaluation counters (diagnostic compositing kernel): bbox, live
     // and contributing (pixel, primitive) evaluations, accumulated on device
     bool stats = false;
-    uint32_t bucket_cap = 512;  // tile bucket capacity (doubled after an overflow, up to the sort cap)
+    uint32_t bucket_cap = 512;
+    // deferred checking (airgs_defer): calls skip their host synchronisations
+    // and fold error flags into d_defer, read once when the mode is left
+    bool defer = false;
+    unsigned int *d_defer = nullptr;  // tile bucket capacity (doubled after an overflow, up to the sort cap)
     unsigned long long *d_stats = nullptr;
     std::vector<cudaEvent_t> event_pool;
     cudaEvent_t take_event() {

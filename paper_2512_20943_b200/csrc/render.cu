@@ -1312,6 +1312,10 @@ k_seam_records(int64_t k, const double *__restrict__ means2d, const double *__re
 }
 
 
+__global__ void k_defer_flags(const unsigned int *__restrict__ flags, unsigned int *defer) {
+    if (threadIdx.x == 0 && *flags) atomicOr(defer, *flags);
+}
+
 __global__ void k_add_i64(int64_t *__restrict__ dst, const int64_t *__restrict__ src, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] += src[i];
@@ -1676,6 +1680,21 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
     }
     TileLists tl{bucket, nullptr, cap};
     sort_composite_sse(ctx, work, L, tl, recs, depth, ntiles, tile_count, sse, st, rec, index_order != 0);
+    if (ctx->defer) {  // deferred checking: fold the flags on the device, no synchronisation
+        k_defer_flags<<<1, 32, 0, st>>>(flags, ctx->d_defer);
+        ++NL;
+        check_launch();
+        for (const auto &m : usage_map) {
+            int64_t n = 0;
+            for (const ItemHost &h : items)
+                if (h.usage == m.first) n = h.count;
+            if (n > 0) {
+                k_add_i64<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(m.first, m.second, n);
+                ++NL;
+            }
+        }
+        return;
+    }
     // one host synchronisation per render: parameter validity and bucket overflow
     unsigned int hflags = 0;
     AIRGS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));

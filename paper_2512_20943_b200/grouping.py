@@ -190,6 +190,57 @@ def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_D
     return out
 
 
+def probe_payloads_device(space, cams, payloads, payload_devs, targets, tau_db: float = DEFAULT_TAU_DB,
+                          device=None):
+    """Keyframe probes of a batch of frames whose GSDP payloads and targets are
+    already in HBM, pipelined: every frame's decode -> apply -> render with
+    fused SSE is enqueued without host synchronisation (airgs_defer) and the
+    qualities are read once at the end.  If any call reports a problem (a
+    malformed payload, invalid parameters, a bucket overflow) the batch is
+    re-run frame by frame in checked mode, which raises the reference's exact
+    error or handles the overflow.  Returns [(quality_db, is_keyframe)]."""
+    import ctypes
+
+    import torch
+
+    from . import codec
+    from ._lib import engine
+    from .model import GaussianFrame, apply_overlay, as_space
+    from .rasterizer import render_views
+
+    space = as_space(space)
+    dev = dv.device_of(device)
+    cams = list(cams)
+    V = len(cams)
+    n, w = space.frame.count, space.frame.width
+    canon = space.frame.planes(dev)
+    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+    items = [(0, v) for v in range(V)]
+    datas = [p.data if hasattr(p, "data") else bytes(p) for p in payloads]
+
+    def one(t):
+        delta, _ = codec.decode_delta_device(datas[t], n, w, device=dev, payload_dev=payload_devs[t])
+        planes = apply_overlay(canon, n, delta.overlay(dev))
+        return render_views([GaussianFrame(device_params=planes, count=n)], cams, items, targets=targets[t],
+                            device=dev).sse
+
+    eng = engine(dev)
+    flags = ctypes.c_uint32(0)
+    eng.call("airgs_defer", 1, ctypes.byref(flags))
+    try:
+        sses = [one(t) for t in range(len(datas))]
+    finally:
+        eng.call("airgs_defer", 0, ctypes.byref(flags))
+    if flags.value:
+        sses = [one(t) for t in range(len(datas))]  # checked mode
+    host = torch.stack(sses).cpu().numpy() if sses else np.zeros((0, V))
+    out = []
+    for t in range(len(datas)):
+        q = float(np.mean([psnr_from_sse(host[t][v], px[v]) for v in range(V)]))
+        out.append((q, is_keyframe(q, tau_db)))
+    return out
+
+
 def is_keyframe(quality_db: float, tau_db: float = DEFAULT_TAU_DB) -> bool:
     """The grouping decision: re-anchor when the probe misses tau
     (ss/grouping.py:213)."""

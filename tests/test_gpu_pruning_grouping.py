@@ -190,3 +190,42 @@ def test_probe_sequence_streams_from_host():
     got = grouping.probe_sequence(space, cams, payloads, targets, tau_db=60.0)
     assert [q for q, _ in got] == ref
     assert [k for _, k in got] == [not q >= 60.0 for q in ref]
+
+
+def test_probe_payloads_device_pipelined_and_checked_rerun():
+    """The pipelined batch probe (deferred checking) gives the per-frame
+    probe's qualities bit for bit; a malformed payload in the batch is caught
+    by the deferred word and re-raised exactly by the checked re-run."""
+    import torch
+
+    from paper_2512_20943_b200 import codec, grouping
+    from paper_2512_20943_b200.errors import DecodeError
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+
+    base_p, _ = _scene(61, n=1500)
+    cams = _cams(3, (64, 48))
+    space = CanonicalSpace(GaussianFrame(params=base_p), capacity_U=base_p.shape[0])
+    payloads, pdevs, targets, ref = [], [], [], []
+    for s in range(4):
+        moved = base_p.copy()
+        rng = np.random.default_rng(s)
+        moved[::3, 0:3] += rng.normal(0, 0.01 * (s + 1), (moved[::3].shape[0], 3))
+        pay = codec.encode_delta(diff_frames(space.frame, GaussianFrame(params=moved)), 1e-4)
+        imgs = orc.render_with_usage(moved, cams)[0]
+        payloads.append(pay)
+        pdevs.append(torch.frombuffer(bytearray(pay.data), dtype=torch.uint8).cuda())
+        targets.append([torch.from_numpy(im).cuda() for im in imgs])
+        dec = codec.decode_delta(pay, base_p.shape[0], 17)
+        ref.append(grouping.quality_probe(space, dec, grouping.GroundTruth(images=imgs), cams))
+    got = grouping.probe_payloads_device(space, cams, payloads, pdevs, targets, tau_db=60.0)
+    assert [q for q, _ in got] == ref
+    # corrupt frame 2's varint section: the batch must raise the checked-mode error
+    bad = bytearray(payloads[2].data)
+    bad[24 + 3] |= 0x80
+    bad_dev = torch.frombuffer(bytearray(bad), dtype=torch.uint8).cuda()
+    with pytest.raises(DecodeError):
+        grouping.probe_payloads_device(space, cams, payloads[:2] + [bytes(bad)] + payloads[3:],
+                                       pdevs[:2] + [bad_dev] + pdevs[3:], targets)
+    # and the context is back in checked mode afterwards
+    got2 = grouping.probe_payloads_device(space, cams, payloads, pdevs, targets, tau_db=60.0)
+    assert [q for q, _ in got2] == ref
