@@ -548,6 +548,10 @@ constexpr int kSortCap = 2048;  // tile lists up to this length are sorted in sh
 #endif
 constexpr int kChunk = COMP_CHUNK;  // compacted entries per phase A / phase B round (T refreshed after each)
 static_assert(kChunk % 8 == 0 && kChunk <= 32, "chunk");
+#ifndef COMP_BRANCHFREE
+#define COMP_BRANCHFREE 1
+#endif
+constexpr bool kLeanComposite = COMP_BRANCHFREE != 0;
 #ifndef COMP_MIN_BLOCKS
 #define COMP_MIN_BLOCKS 4
 #endif
@@ -1098,6 +1102,29 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
                     const int4 b1 = sh.bbox[j1], b2 = sh.bbox[j2];
                     if (px < b1.x || px >= b1.y || py < b1.z || py >= b1.w) ap1 = 0.0;
                     if (px < b2.x || px >= b2.y || py < b2.z || py >= b2.w) ap2 = 0.0;
+                }
+                if (kLeanComposite && !USAGE && !STATS && !RECORD && !BBOX) {
+                    // evaluation variant, branch-free: a non-contributing candidate adds
+                    // exactly 0.0 to the (non-negative) colour sums and keeps T by a select
+                    const double2 rg1 = sh.rg[j1], rg2 = sh.rg[j2];
+                    const double bl1 = sh.bl[j1], bl2 = sh.bl[j2];
+                    double wa = ap1 * T;
+                    const bool c1 = wa > kCompC[7];
+                    wa = c1 ? wa : 0.0;
+                    cr += wa * rg1.x;
+                    cg += wa * rg1.y;
+                    cb += wa * bl1;
+                    const double T1 = T * (1.0 - ap1);
+                    T = c1 ? T1 : T;
+                    double wb = ap2 * T;
+                    const bool c2 = two && wb > kCompC[7];
+                    wb = c2 ? wb : 0.0;
+                    cr += wb * rg2.x;
+                    cg += wb * rg2.y;
+                    cb += wb * bl2;
+                    const double T2 = T * (1.0 - ap2);
+                    T = c2 ? T2 : T;
+                    continue;
                 }
                 double wgt = ap1 * T;
                 if (STATS) wmar = fmin(wmar, fabs(wgt - kEpsContrib));
