@@ -620,63 +620,6 @@ __device__ __forceinline__ void warp_bitonic_steps(uint64_t &k0, uint32_t &v0, u
     }
 }
 
-// Fast path: one 64-bit key per entry = (tile-local depth bucket << 32) | index.
-__device__ __forceinline__ void warp_bitonic_steps_u64(uint64_t &k0, uint64_t &k1, int e0, int size, int smax) {
-    const int lane = threadIdx.x & 31;
-    if (smax >= 32) {
-        const bool asc = (e0 & size) == 0;
-        if ((k0 > k1) == asc) {
-            const uint64_t t = k0;
-            k0 = k1;
-            k1 = t;
-        }
-        smax = 16;
-    }
-    for (int st = smax; st > 0; st >>= 1) {
-        const bool lower = (lane & st) == 0;
-        const uint64_t p0 = __shfl_xor_sync(0xffffffffu, k0, st);
-        const uint64_t p1 = __shfl_xor_sync(0xffffffffu, k1, st);
-        const bool a0 = (e0 & size) == 0, a1 = ((e0 + 32) & size) == 0;
-        k0 = (lower == a0) ? min(k0, p0) : max(k0, p0);
-        k1 = (lower == a1) ? min(k1, p1) : max(k1, p1);
-    }
-}
-
-__device__ __noinline__ void sort_tile_keys(uint64_t *k, int npad) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int seg = w; seg * 64 < npad; seg += kTileThreads / 32) {
-        const int e0 = seg * 64 + lane;
-        uint64_t k0 = k[e0], k1 = k[e0 + 32];
-        for (int size = 2; size <= 64; size <<= 1) warp_bitonic_steps_u64(k0, k1, e0, size, size >> 1);
-        k[e0] = k0;
-        k[e0 + 32] = k1;
-    }
-    __syncthreads();
-    for (int size = 128; size <= npad; size <<= 1) {
-        for (int st = size >> 1; st >= 64; st >>= 1) {
-            for (int i = threadIdx.x; i < (npad >> 1); i += kTileThreads) {
-                const int lo = ((i & ~(st - 1)) << 1) | (i & (st - 1));
-                const int hi = lo + st;
-                const bool asc = (lo & size) == 0;
-                const uint64_t ka = k[lo], kb = k[hi];
-                if ((ka > kb) == asc) {
-                    k[lo] = kb;
-                    k[hi] = ka;
-                }
-            }
-            __syncthreads();
-        }
-        for (int seg = w; seg * 64 < npad; seg += kTileThreads / 32) {
-            const int e0 = seg * 64 + lane;
-            uint64_t k0 = k[e0], k1 = k[e0 + 32];
-            warp_bitonic_steps_u64(k0, k1, e0, size, 32);
-            k[e0] = k0;
-            k[e0 + 32] = k1;
-        }
-        __syncthreads();
-    }
-}
-
 // Exact path: (64-bit depth key, index) pairs, used when two entries of a
 // tile share a 32-bit depth bucket.
 __device__ __noinline__ void sort_tile_list(uint64_t *k, uint32_t *v, int npad) {
@@ -1346,11 +1289,6 @@ __global__ void k_defer_flags(const unsigned int *__restrict__ flags, unsigned i
 __global__ void k_add_i64(int64_t *__restrict__ dst, const int64_t *__restrict__ src, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) dst[i] += src[i];
-}
-
-__global__ void k_fill_i64(int64_t *p, int64_t n, int64_t v) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v;
 }
 
 // ---------------------------------------------------------------------------
