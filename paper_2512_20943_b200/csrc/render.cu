@@ -505,14 +505,16 @@ __device__ __forceinline__ double exp_tab(double x, const double2 *__restrict__ 
     double r = fma(kd, kCompC[1], x);
     r = fma(kd, kCompC[2], r);
     const double2 t = tab[ki & (kExpN - 1)];
-    const unsigned long long sb = (unsigned long long)__double_as_longlong(t.y) + (ki << (52 - kExpBits));
+    // scale 2^(k/N): add k/N to the table entry's exponent -- only the high word changes
+    // ((ki << 44) has zero low word), so one 32-bit add instead of a 64-bit one
+    const int sb_hi = __double2hiint(t.y) + (int)((unsigned)ki << (52 - kExpBits - 32));
     const double r2 = r * r;
     const double p1 = fma(r, kCompC[3], 0.5);
     const double p2 = fma(r, kCompC[4], kCompC[5]);
     double tmp = t.x + r;
     tmp = fma(r2, p1, tmp);
     tmp = fma(r2 * r2, p2, tmp);
-    const double sc = __longlong_as_double((long long)sb);
+    const double sc = __hiloint2double(sb_hi, __double2loint(t.y));
     return fma(sc, tmp, sc);
 }
 
