@@ -117,6 +117,9 @@ class FrameSelection:
 # device helpers
 
 
+RENDER_PAIRS_PER_CALL = 96 * 1024 * 1024  # ~9 GB of 96-byte projected records per render call
+
+
 def _engine(dev):
     from ._lib import engine
 
@@ -300,8 +303,11 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
             for v in range(len(cams)):
                 items.append((li, v))
                 targets.append(rv.images[v])
-        lv = render_views(frames, cams, items, targets=targets)
-        sse = lv.sse.cpu().numpy()
+        # bounded working set: at most RENDER_PAIRS_PER_CALL (item, primitive)
+        # records per render call (C5: 2M primitives x 8 levels x 32 views)
+        per_call = max(1, RENDER_PAIRS_PER_CALL // max(p.n, 1))
+        sse = np.concatenate([render_views(frames, cams, items[k:k + per_call], targets=targets[k:k + per_call])
+                              .sse.cpu().numpy() for k in range(0, len(items), per_call)])
         V = len(cams)
         sizes_px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
         qualities = [float(np.mean([psnr_from_sse(sse[li * V + v], sizes_px[v]) for v in range(V)]))

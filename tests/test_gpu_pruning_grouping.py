@@ -229,3 +229,22 @@ def test_probe_payloads_device_pipelined_and_checked_rerun():
     # and the context is back in checked mode afterwards
     got2 = grouping.probe_payloads_device(space, cams, payloads, pdevs, targets, tau_db=60.0)
     assert [q for q, _ in got2] == ref
+
+
+def test_level_space_chunked_render_calls_equal_single_call(monkeypatch):
+    """build_level_space splits its (level, view) renders into calls of bounded
+    working set (RENDER_PAIRS_PER_CALL); the qualities do not depend on it."""
+    from paper_2512_20943_b200 import pruning, rasterizer
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+
+    base_p, moved = _scene(7)
+    cams = _cams()
+    space = CanonicalSpace(GaussianFrame(params=base_p, frame_index=0, group_key=0), capacity_U=base_p.shape[0])
+    gap = diff_frames(space.frame, GaussianFrame(params=moved))
+    _, usage = rasterizer.render_with_usage(GaussianFrame(params=moved), cams)
+    ratios = [i / 10 for i in range(8)]
+    one = pruning.build_level_space(gap, space, cams, ratios, usage, 1e-4)
+    monkeypatch.setattr(pruning, "RENDER_PAIRS_PER_CALL", base_p.shape[0] * 3)  # 3 items per call
+    many = pruning.build_level_space(gap, space, cams, ratios, usage, 1e-4)
+    assert [lv.quality_db for lv in one.levels] == [lv.quality_db for lv in many.levels]
+    assert [lv.size_bytes for lv in one.levels] == [lv.size_bytes for lv in many.levels]
