@@ -119,7 +119,7 @@ def main():
                "data": "synthetic (seeded SURVEY s8(d) generator)", "gpu": torch.cuda.get_device_name(dev)}
         t0 = time.time()
         rec["probe"] = probe(cfg, dev, args.steps, args.warmup)
-        if name in ("C3", "C4"):
+        if name in ("C3", "C4", "C5"):
             rec["sweep"] = sweep(cfg, dev, max(1, args.steps // 2), 1)
         if not args.no_cpu:
             ccfg = cfg if cfg.count <= 300_000 else replace(cfg, count=cfg.count)  # same scene, bounded views
