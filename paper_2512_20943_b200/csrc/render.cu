@@ -250,7 +250,8 @@ __global__ void __launch_bounds__(kProjThreads, PROJ_MIN_BLOCKS) k_project(ProjA
             }
             const int64_t *fz = a.item_frozen ? a.item_frozen[item] : nullptr;
             const unsigned long long zk = order_key_of(fz, i, tz);
-            if (has_bbox) {  // (bbox-only records are read by the diagnostic counters alone)
+            // records of primitives that reach no tile are read only by the diagnostic counters
+            if (nt > 0 || (has_bbox && a.stats)) {
                 a.recs[o] = rec;
                 a.depth[o] = zk;
             }
