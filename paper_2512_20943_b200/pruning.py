@@ -294,24 +294,33 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
     removed = _removed_sets(p, delta.overlay(), [kmins[j] for j in keep_levels])
     qualities = [100.0] * len(keep_levels)
     if cams:
-        ref = GaussianFrame(device_params=level_frame_planes(p, None), count=p.n, frame_index=frame_index,
-                            group_key=space.key_index)
+        import torch
+
+        ref_planes = level_frame_planes(p, None)
+        ref = GaussianFrame(device_params=ref_planes, count=p.n, frame_index=frame_index, group_key=space.key_index)
         rv = render_views([ref], cams, [(0, v) for v in range(len(cams))], want_images=True)
-        frames = [GaussianFrame(device_params=level_frame_planes(p, kmins[j]), count=p.n) for j in keep_levels]
+        planes = [level_frame_planes(p, kmins[j]) for j in keep_levels]
+        # a level whose parameters equal the reference's bit for bit renders the
+        # same image: SSE 0, the reference's 100 dB cap, no render needed (the
+        # mandatory ratio-0 level always, ss/pruning.py:102-104)
+        same = [bool(torch.equal(pl[:, : p.n], ref_planes[:, : p.n])) for pl in planes]
+        todo = [li for li in range(len(planes)) if not same[li]]
+        frames = [GaussianFrame(device_params=planes[li], count=p.n) for li in todo]
         items, targets = [], []
-        for li in range(len(frames)):
+        for fi in range(len(frames)):
             for v in range(len(cams)):
-                items.append((li, v))
+                items.append((fi, v))
                 targets.append(rv.images[v])
         # bounded working set: at most RENDER_PAIRS_PER_CALL (item, primitive)
         # records per render call (C5: 2M primitives x 8 levels x 32 views)
         per_call = max(1, RENDER_PAIRS_PER_CALL // max(p.n, 1))
         sse = np.concatenate([render_views(frames, cams, items[k:k + per_call], targets=targets[k:k + per_call])
-                              .sse.cpu().numpy() for k in range(0, len(items), per_call)])
+                              .sse.cpu().numpy() for k in range(0, len(items), per_call)]) if items else None
         V = len(cams)
         sizes_px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
-        qualities = [float(np.mean([psnr_from_sse(sse[li * V + v], sizes_px[v]) for v in range(V)]))
-                     for li in range(len(frames))]
+        qualities = [100.0] * len(planes)
+        for fi, li in enumerate(todo):
+            qualities[li] = float(np.mean([psnr_from_sse(sse[fi * V + v], sizes_px[v]) for v in range(V)]))
     levels = [PruningLevel(ratio=ratios[j], quality_db=q, size_bytes=sizes[j], pruned_indices=rm)
               for j, q, rm in zip(keep_levels, qualities, removed)]
     return PruningLevelSpace(levels=tuple(levels), frame_index=frame_index)
