@@ -56,7 +56,7 @@ def instrument():
 
         setattr(mod, name, timed)
 
-    wrap(streamsim, "_usage_only", "usage pass")
+    wrap(streamsim, "_server_pass", "server pass (usage + images)")
     wrap(pruning, "build_level_space", "level space")
     wrap(pruning, "prune_delta", "prune_delta")
     wrap(codec, "encode_delta", "encode_delta")
