@@ -22,8 +22,7 @@
 
 namespace airgs {
 
-constexpr int kWin = 11;
-constexpr int kHalf = 5;
+constexpr int kWin = 11;  // window edge (radius 5)
 constexpr double kC1 = 0.01 * 0.01;
 constexpr double kC2 = 0.03 * 0.03;
 

@@ -295,14 +295,13 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
     const int64_t o = (int64_t)s * a.stride + i;
     const int nt = i < a.count[s] ? max(a.ntiles[o], 0) : 0;
     if (__all_sync(0xffffffffu, nt == 0)) return;
-    int u0 = 0, u1 = 0, v0 = 0, v1 = 0;
+    int u0 = 0, u1 = 0, v0 = 0;  // tile range (the last row follows from nt)
     uint64_t entry = 0;
     if (nt > 0) {
         const uint2 br = a.binrec[o];  // 8 bytes instead of the 96-byte record
         u0 = (int)(br.x & 0xffffu);
         u1 = (int)(br.x >> 16);
         v0 = (int)(br.y & 0xffffu);
-        v1 = (int)(br.y >> 16);
         const uint64_t zk = a.depth[o];
         // 32-bit order key: small keys (frozen positions, the seam's input order)
         // as they are; depth keys (z > 0) as their fp32 bits, monotone, behind them
@@ -489,13 +488,36 @@ __device__ __forceinline__ float log2_inv_eps() { return 7.99435343685886f; }
 
 // fp64 constants of the exact path, read as constant-bank operands (no
 // per-iteration immediate materialisation)
-__constant__ double kCompC[8] = {kExpInvLn2N, kExpNegLn2HiN, kExpNegLn2LoN, 1.0 / 6.0,
-                                 1.0 / 120.0, 1.0 / 24.0, kAlphaClamp, kEpsContrib};
+__constant__ double kCompC[9] = {kExpInvLn2N, kExpNegLn2HiN, kExpNegLn2LoN, kExpC3,     kExpC5,
+                                 kExpC4,      kAlphaClamp,   kEpsContrib,   kExpC2};
 
-// exp(x) for the compositing weights: 256-entry table of 2^(i/256) in shared
-// memory + degree-5 polynomial on |r| <= ln2/512 (error < 0.51 ulp; agrees
-// with glibc's exp, which the reference's Cython kernel calls, on >99.9% of
-// inputs and never differs by more than 1 ulp -- tools/gen_exp_table.py).
+// exp(x) for the compositing weights, bit-identical to the reference's: the
+// table-driven algorithm of glibc 2.39's exp (FMA variant, 128-entry table of
+// 2^(i/128) + degree-5 polynomial, same constants and the same fma nesting --
+// tools/gen_exp_table.py; tests/test_exp_table.py checks it bit for bit
+// against the host libm), which the reference's Cython kernel calls at
+// _composite.pyx:57.  The table is replicated kExpRep times, entry-major, and
+// lane l reads copy l % kExpRep, so the 8 lanes of a 128-bit shared-memory
+// phase spread over more bank groups (random-index bank conflicts of a
+// single table were ~12% of the compositing kernel's shared wavefronts).
+#ifndef EXP_REP
+#define EXP_REP 2
+#endif
+constexpr int kExpRep = EXP_REP;
+
+// copy of the exp table for this lane (pass to exp_tab)
+__device__ __forceinline__ const double2 *exp_lane_tab(const double2 *tab) {
+    return tab + (threadIdx.x & (kExpRep - 1));
+}
+
+__device__ __forceinline__ void load_exp_table(double2 *tab, int nthreads) {
+    const unsigned long long *src = &kExpTable[0][0];
+    for (int k = threadIdx.x; k < kExpN * kExpRep; k += nthreads) {
+        const int i = k / kExpRep;
+        tab[k] = make_double2(__longlong_as_double((long long)src[2 * i]),
+                              __longlong_as_double((long long)src[2 * i + 1]));
+    }
+}
 
 __device__ __forceinline__ double exp_tab(double x, const double2 *__restrict__ tab) {
     const double shift = 6755399441055744.0;  // 1.5 * 2^52
@@ -505,12 +527,12 @@ __device__ __forceinline__ double exp_tab(double x, const double2 *__restrict__ 
     kd = kd - shift;
     double r = fma(kd, kCompC[1], x);
     r = fma(kd, kCompC[2], r);
-    const double2 t = tab[ki & (kExpN - 1)];
+    const double2 t = tab[(ki & (kExpN - 1)) * kExpRep];
     // scale 2^(k/N): add k/N to the table entry's exponent -- only the high word changes
-    // ((ki << 44) has zero low word), so one 32-bit add instead of a 64-bit one
+    // ((ki << (52 - kExpBits)) has a zero low word), so one 32-bit add instead of a 64-bit one
     const int sb_hi = __double2hiint(t.y) + (int)((unsigned)ki << (52 - kExpBits - 32));
     const double r2 = r * r;
-    const double p1 = fma(r, kCompC[3], 0.5);
+    const double p1 = fma(r, kCompC[3], kCompC[8]);
     const double p2 = fma(r, kCompC[4], kCompC[5]);
     double tmp = t.x + r;
     tmp = fma(r2, p1, tmp);
@@ -542,7 +564,7 @@ struct CompShared {
     // per warp, entry pairs (a, b): {-mx_a,-mx_b,-my_a,-my_b}, {A_a,A_b,B_a,B_b}, {C_a,C_b,-L_a,-L_b}
     float4 pl[kCompWarps][kWarpList / 2][3];
     uint8_t sidx[kCompWarps][kWarpList];  // compacted position -> staged position
-    double2 exptab[kExpN];
+    double2 exptab[kExpN * kExpRep];
 };
 
 constexpr int kSortCap = 2048;  // tile lists up to this length are sorted in shared memory
@@ -558,6 +580,9 @@ constexpr bool kLeanComposite = COMP_BRANCHFREE != 0;
 #ifndef COMP_MIN_BLOCKS
 #define COMP_MIN_BLOCKS 4
 #endif
+#ifndef COMP_PREFETCH
+#define COMP_PREFETCH 1  // 0: none, 1: next batch's records into L1, 2: into L2
+#endif
 
 // alpha' = min(al * exp(-e), 0.999) for staged primitive j at (dx, dy):
 // exact replay of _composite.pyx:56-60 (0.5*(A + C) == 0.5A + 0.5C exactly)
@@ -568,7 +593,7 @@ __device__ __forceinline__ double alpha_at(const CompShared &sh, int j, double p
     const double dx = pxd - mm.x;
     const double dy = pyd - mm.y;
     const double ee = (ab.x * dx * dx + ca.x * dy * dy) + ab.y * dx * dy;
-    const double ap = ca.y * exp_tab(-ee, sh.exptab);
+    const double ap = ca.y * exp_tab(-ee, exp_lane_tab(sh.exptab));
     return ap > kCompC[6] ? kCompC[6] : ap;
 }
 
@@ -895,13 +920,9 @@ template <bool USAGE, bool STATS, bool RECORD = false, bool BBOX = false>
 __global__ void __launch_bounds__(kTileThreads, COMP_MIN_BLOCKS)
 k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
             const TileLists tls, const uint32_t *__restrict__ tcount, unsigned long long *__restrict__ stats) {
-    __shared__ CompShared sh;
-    {
-        const unsigned long long *src = &kExpTable[0][0];
-        for (int k = threadIdx.x; k < kExpN; k += kTileThreads)
-            sh.exptab[k] = make_double2(__longlong_as_double((long long)src[2 * k]),
-                                        __longlong_as_double((long long)src[2 * k + 1]));
-    }
+    extern __shared__ __align__(16) unsigned char comp_smem[];  // > 48 KB: dynamic
+    CompShared &sh = *reinterpret_cast<CompShared *>(comp_smem);
+    load_exp_table(sh.exptab, kTileThreads);
     // locate item (binary search over tile_base)
     const int64_t g = blockIdx.x;
     int lo = 0, hi = nitems - 1;
@@ -938,9 +959,11 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
         const int nb = min(kBatch, n_all - base);
         // (the previous batch ended with a block-wide __syncthreads_count: every
         // warp is done with the staging arrays this batch overwrites)
+        uint32_t gnext = 0xffffffffu;  // next batch's entry of this thread (record prefetch)
         if ((int)threadIdx.x < nb) {
             const int t = threadIdx.x;
             const uint32_t gi = (uint32_t)glist[base + t];
+            if (COMP_PREFETCH && base + kBatch + t < n_all) gnext = (uint32_t)glist[base + kBatch + t];
             const Rec r = recs[gi];
             const float mxl = (float)(r.mx - (double)ox), myl = (float)(r.my - (double)oy);
             sh.gid[t] = gi;
@@ -974,6 +997,18 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
             if (USAGE) sh.cnt[t] = 0;
         }
         __syncthreads();
+        // the next batch's records travel while this batch is composited (its
+        // staging then waits on L1/L2 instead of DRAM latency)
+        if (COMP_PREFETCH && gnext != 0xffffffffu) {
+            const char *pa = reinterpret_cast<const char *>(recs + gnext);
+            if (COMP_PREFETCH == 1) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 95));
+            } else {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pa + 95));
+            }
+        }
         // compaction: this warp's entries of the batch, in depth order, pair-interleaved
         int ncomp = 0;  // warp-uniform
         if (!__all_sync(0xffffffffu, done)) {
@@ -1453,6 +1488,17 @@ struct RecWordsOut {
     __device__ void operator()(int, int64_t g, int64_t ex, int64_t) const { base[g] = ex; }
 };
 
+// k_composite instantiations take their CompShared (> 48 KB) as dynamic shared
+// memory; the opt-in is a per-function attribute, set before every launch
+// (cheap, and correct whichever device is current).
+template <bool USAGE, bool STATS, bool RECORD = false, bool BBOX = false>
+static void launch_composite(int64_t tiles, cudaStream_t st, const CompItem *items, const int64_t *tile_base,
+                             int nitems, const TileLists &tl, const uint32_t *tcount, unsigned long long *stats) {
+    auto *fn = k_composite<USAGE, STATS, RECORD, BBOX>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CompShared));
+    fn<<<(unsigned)tiles, kTileThreads, sizeof(CompShared), st>>>(items, tile_base, nitems, tl, tcount, stats);
+}
+
 static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
                                const TileLists &tl, const Rec *recs, const uint64_t *depth, const int32_t *ntiles,
                                uint32_t *tile_count, double *sse, cudaStream_t st, RecordOut *rec = nullptr,
@@ -1541,42 +1587,31 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
     cudaEvent_t t_comp = Tt > 0 ? ctx->time_begin(st) : nullptr;
     if (Tt > 0) {
         unsigned long long *cs = ctx->d_stats;
-        const dim3 grid((unsigned)Tt), block(kTileThreads);
         if (bbox) {  // the kernel seam (caller-supplied bboxes)
             if (rec) {
                 if (any_usage)
-                    k_composite<true, false, true, true><<<grid, block, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                                 tile_count, cs);
+                    launch_composite<true, false, true, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
                 else
-                    k_composite<false, false, true, true><<<grid, block, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                                  tile_count, cs);
+                    launch_composite<false, false, true, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
             } else if (any_usage) {
-                k_composite<true, false, false, true><<<grid, block, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                              tile_count, cs);
+                launch_composite<true, false, false, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
             } else {
-                k_composite<false, false, false, true><<<grid, block, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                               tile_count, cs);
+                launch_composite<false, false, false, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
             }
         } else if (rec) {
             if (any_usage)
-                k_composite<true, false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems,
-                                                                                      tl, tile_count, cs);
+                launch_composite<true, false, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
             else
-                k_composite<false, false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems,
-                                                                                       tl, tile_count, cs);
+                launch_composite<false, false, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         } else if (stats_on) {
             if (any_usage)
-                k_composite<true, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                               tile_count, cs);
+                launch_composite<true, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
             else
-                k_composite<false, true><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                                tile_count, cs);
+                launch_composite<false, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         } else if (any_usage) {
-            k_composite<true, false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                            tile_count, cs);
+            launch_composite<true, false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         } else {
-            k_composite<false, false><<<(unsigned)Tt, kTileThreads, 0, st>>>(d_ci, L.d_tile_base, nitems, tl,
-                                                                             tile_count, cs);
+            launch_composite<false, false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         }
         ++NL;
         check_launch();
@@ -1861,7 +1896,7 @@ struct BwdShared {
     double f[9][kBwdBatch];    // mx, my, a, b, c, al, cr, cg, cb of the staged entries
     double acc[9][kBwdBatch];  // d_means2d (2), d_conics (3), d_alphas, d_colors (3)
     uint32_t gid[kBwdBatch];
-    double2 exptab[kExpN];
+    double2 exptab[kExpN * kExpRep];
 };
 
 // One CTA per tile, one pixel per thread: the pixel's recorded contributors in
@@ -1878,12 +1913,7 @@ __global__ void __launch_bounds__(kTileThreads) k_composite_bwd(const Rec *__res
                                                                const double *__restrict__ d_image,
                                                                double *__restrict__ G) {
     __shared__ BwdShared sh;
-    {
-        const unsigned long long *src = &kExpTable[0][0];
-        for (int k = threadIdx.x; k < kExpN; k += kTileThreads)
-            sh.exptab[k] = make_double2(__longlong_as_double((long long)src[2 * k]),
-                                        __longlong_as_double((long long)src[2 * k + 1]));
-    }
+    load_exp_table(sh.exptab, kTileThreads);
     const int64_t g = blockIdx.x;
     const int tx = (int)(g % tiles_x), ty = (int)(g / tiles_x);
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
@@ -1940,7 +1970,7 @@ __global__ void __launch_bounds__(kTileThreads) k_composite_bwd(const Rec *__res
                     const double dy = pyd - my;
                     const double dx = pxd - mx;
                     const double e = 0.5 * (a * dx * dx + c * dy * dy) + bb * dx * dy;
-                    const double gg = exp_tab(-e, sh.exptab);
+                    const double gg = exp_tab(-e, exp_lane_tab(sh.exptab));
                     const double raw = al * gg;
                     const double ap = raw > kAlphaClamp ? kAlphaClamp : raw;
                     const double t_before = T / (1.0 - ap);
