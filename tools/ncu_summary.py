@@ -1,10 +1,22 @@
-"""Summarise an ncu report: key metrics + top source lines by instructions."""
+"""Summarise an ncu report: key metrics + top source lines by instructions.
+
+  python tools/ncu_summary.py REPORT [TOP] [--traffic-json OUT]
+
+--traffic-json writes the dominant kernel's measured DRAM bytes and SM-side
+figures in the form bench.py reads (profiles/composite_traffic.json)."""
 import csv
+import json
 import subprocess
 import sys
 
-rep = sys.argv[1]
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+rep = args[0]
+top = int(args[1]) if len(args) > 1 else 20
+tjson = sys.argv[sys.argv.index("--traffic-json") + 1] if "--traffic-json" in sys.argv else None
+if tjson in args:
+    args.remove(tjson)
+    top = int(args[1]) if len(args) > 1 else 20
+RAW = {}
 
 
 def run(args):
@@ -31,10 +43,34 @@ if len(raw) >= 3:
             except ValueError:
                 pass
         if name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-                    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum"):
+                    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum",
+                    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+                    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "derived__memory_l1_wavefronts_shared_excessive",
+                    "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+                    "sm__inst_executed.avg.per_cycle_active", "gpu__time_duration.sum"):
             print(f"{name:<60} {val} {unit}")
+            try:
+                scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit.strip(), 1.0)
+                RAW[name] = float(val.replace(",", "")) * scale
+            except ValueError:
+                pass
     tot = sum(v for v, _ in stalls) or 1
+    STALLS = ", ".join(f"{n} {100 * v / tot:.1f}%" for v, n in sorted(stalls, reverse=True)[:5])
     print("stalls:", ", ".join(f"{n} {100 * v / tot:.1f}%" for v, n in sorted(stalls, reverse=True)[:8]))
+    if tjson:
+        out = {"source": f"{rep} (ncu --set full --clock-control none, k_composite, one C2 step = 18 views "
+                         "1352x1014, 300k Gaussians)",
+               "dram_bytes_per_launch": int(RAW.get("dram__bytes_read.sum", 0) + RAW.get("dram__bytes_write.sum", 0)),
+               "sm": {"fp64_pipe_active_pct": round(RAW.get(
+                          "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 0), 1),
+                      "issue_slots_busy_pct": round(RAW.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0), 1),
+                      "ipc": round(RAW.get("sm__inst_executed.avg.per_cycle_active", 0), 2),
+                      "achieved_occupancy_pct": round(RAW.get("sm__warps_active.avg.pct_of_peak_sustained_active", 0), 1),
+                      "lsu_data_pipe_wavefronts_pct": round(RAW.get(
+                          "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", 0), 1),
+                      "top_stalls": STALLS}}
+        with open(tjson, "w") as fh:
+            json.dump(out, fh, indent=1)
 src = list(csv.reader(run(["--page", "source", "--csv", "--print-source=cuda,sass"]).splitlines()))
 lines = []
 for r in src[3:]:
