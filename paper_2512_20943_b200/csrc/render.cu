@@ -1199,6 +1199,312 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     }
 }
 
+// ---- two pixels per lane (evaluation and usage passes) ------------------------
+// Same per-pixel algorithm as k_composite, with 4 warps per 16x16 tile: a warp
+// owns an 8x8 sub-tile and every lane two pixels of one column (rows r and
+// r+4).  Each phase-A broadcast of an entry's fp32 fields then serves two
+// pixel tests (the shared-memory data pipe is the kernel's limiter), the
+// per-warp compaction is amortised over 64 pixels, and phase B runs the two
+// pixels' chains side by side (one candidate of each per iteration: two
+// independent exp / blend chains in flight instead of one dependent pair).
+
+#ifndef COMP_PX2
+#define COMP_PX2 1
+#endif
+#ifndef C2_BATCH
+#define C2_BATCH 96
+#endif
+#ifndef C2_MIN_BLOCKS
+#define C2_MIN_BLOCKS 8
+#endif
+constexpr int kC2Threads = 128;
+constexpr int kC2Warps = kC2Threads / 32;
+constexpr int kC2Batch = C2_BATCH;
+constexpr int kC2List = kC2Batch + 8;
+
+struct Comp2Shared {
+    double2 m[kC2Batch];     // mx, my
+    double2 hab[kC2Batch];   // 0.5*a, b
+    double2 hcal[kC2Batch];  // 0.5*c, alpha
+    double2 rg[kC2Batch];    // colour r, g
+    double bl[kC2Batch];     // colour b
+    float4 f0[kC2Batch];     // -(mx-ox), -(my-oy), A, B
+    float2 f1[kC2Batch];     // C, -L
+    uint32_t gid[kC2Batch];
+    int32_t cnt[kC2Batch];
+    uint8_t wmask[kC2Batch];  // bit w: may touch warp w's 8x8 sub-tile
+    float4 pl[kC2Warps][kC2List / 2][3];
+    uint8_t sidx[kC2Warps][kC2List];
+    double2 exptab[kExpN * kExpRep];
+};
+
+__device__ __forceinline__ double c2_alpha_at(const Comp2Shared &sh, const double2 *tab, int j, double pxd,
+                                              double pyd) {
+    const double2 mm = sh.m[j];
+    const double2 ab = sh.hab[j];
+    const double2 ca = sh.hcal[j];
+    const double dx = pxd - mm.x;
+    const double dy = pyd - mm.y;
+    const double ee = (ab.x * dx * dx + ca.x * dy * dy) + ab.y * dx * dy;
+    const double ap = ca.y * exp_tab(-ee, tab);
+    return ap > kCompC[6] ? kCompC[6] : ap;
+}
+
+template <bool USAGE>
+__global__ void __launch_bounds__(kC2Threads, C2_MIN_BLOCKS)
+k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
+             const TileLists tls, const uint32_t *__restrict__ tcount) {
+    extern __shared__ __align__(16) unsigned char comp2_smem[];
+    Comp2Shared &sh = *reinterpret_cast<Comp2Shared *>(comp2_smem);
+    load_exp_table(sh.exptab, kC2Threads);
+    const int64_t g = blockIdx.x;
+    int lo = 0, hi = nitems - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tile_base[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    const CompItem *__restrict__ itp = items + lo;
+    const int tl = (int)(g - tile_base[lo]);
+    const int tiles_x = itp->tiles_x, img_w = itp->w, img_h = itp->h;
+    const int tx = tl % tiles_x, ty = tl / tiles_x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int sx = (w & 1) * 8, sy = (w >> 1) * 8;
+    const int lx = sx + (lane & 7), ly0 = sy + (lane >> 3), ly1 = ly0 + 4;
+    const int ox = tx * kTile, oy = ty * kTile;
+    const int px = ox + lx, py0 = oy + ly0, py1 = oy + ly1;
+    const bool in0 = px < img_w && py0 < img_h, in1 = px < img_w && py1 < img_h;
+    const float2 px2 = make_float2((float)lx + 0.5f, (float)lx + 0.5f);
+    const float2 py2a = make_float2((float)ly0 + 0.5f, (float)ly0 + 0.5f);
+    const float2 py2b = make_float2((float)ly1 + 0.5f, (float)ly1 + 0.5f);
+    const double pxd = (double)px + 0.5, pyd0 = (double)py0 + 0.5, pyd1 = (double)py1 + 0.5;
+    const Rec *__restrict__ recs = itp->recs;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const double2 *tab = exp_lane_tab(sh.exptab);
+
+    const int n_all = tls.count(tcount, g);
+    const uint64_t *__restrict__ glist = tls.list(g);
+    double T0 = 1.0, r0 = 0.0, g0 = 0.0, b0 = 0.0;
+    double T1 = 1.0, r1 = 0.0, g1 = 0.0, b1 = 0.0;
+    bool done0 = !in0, done1 = !in1;
+    float thr0 = log2_inv_eps(), thr1 = log2_inv_eps();
+
+    for (int base = 0; base < n_all; base += kC2Batch) {
+        const int nb = min(kC2Batch, n_all - base);
+        for (int t = threadIdx.x; t < nb; t += kC2Threads) {
+            const uint32_t gi = (uint32_t)glist[base + t];
+            if (COMP_PREFETCH && base + kC2Batch + t < n_all) {
+                const char *pa = reinterpret_cast<const char *>(recs + (uint32_t)glist[base + kC2Batch + t]);
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(pa + 95));
+            }
+            const Rec r = recs[gi];
+            const float mxl = (float)(r.mx - (double)ox), myl = (float)(r.my - (double)oy);
+            sh.gid[t] = gi;
+            const double kap = 1.0 - 2e-5;
+            sh.f0[t] = make_float4(-mxl, -myl, (float)(0.5 * kLog2e * kap * r.ca), (float)(kLog2e * r.cb));
+            sh.f1[t] = make_float2((float)(0.5 * kLog2e * kap * r.cc), -(__log2f((float)r.al) + 6e-5f));
+            sh.m[t] = make_double2(r.mx, r.my);
+            sh.hab[t] = make_double2(0.5 * r.ca, r.cb);
+            sh.hcal[t] = make_double2(0.5 * r.cc, r.al);
+            sh.rg[t] = make_double2(r.cr, r.cg);
+            sh.bl[t] = r.cbl;
+            // 8x8 sub-tiles: columns 8k+0.5 .. 8k+7.5, rows 8k+0.5 .. 8k+7.5
+            unsigned xm = 0, ym = 0;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                xm |= (r.x0 < ox + 8 * k + 8 && r.x1 > ox + 8 * k && mxl - r.hx <= 8.0f * k + 7.5f &&
+                       mxl + r.hx >= 8.0f * k + 0.5f) ? (1u << k) : 0u;
+                ym |= (r.y0 < oy + 8 * k + 8 && r.y1 > oy + 8 * k && myl - r.hy <= 8.0f * k + 7.5f &&
+                       myl + r.hy >= 8.0f * k + 0.5f) ? (1u << k) : 0u;
+            }
+            unsigned mk = 0;
+#pragma unroll
+            for (int ww = 0; ww < 4; ++ww) mk |= (((xm >> (ww & 1)) & (ym >> (ww >> 1))) & 1u) << ww;
+            sh.wmask[t] = (uint8_t)mk;
+            if (USAGE) sh.cnt[t] = 0;
+        }
+        __syncthreads();
+        int ncomp = 0;
+        if (!__all_sync(0xffffffffu, done0 && done1)) {
+            for (int c0 = 0; c0 < nb; c0 += 32) {
+                const int j = c0 + lane;
+                const bool hit = j < nb && ((sh.wmask[j] >> w) & 1u);
+                const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                if (hit) {
+                    const int p = ncomp + __popc(bal & lt_mask);
+                    const float4 a0 = sh.f0[j];
+                    const float2 a1 = sh.f1[j];
+                    float *d = reinterpret_cast<float *>(&sh.pl[w][p >> 1][0]) + (p & 1);
+                    d[0] = a0.x;
+                    d[2] = a0.y;
+                    d[4] = a0.z;
+                    d[6] = a0.w;
+                    d[8] = a1.x;
+                    d[10] = a1.y;
+                    sh.sidx[w][p] = (uint8_t)j;
+                }
+                ncomp += __popc(bal);
+            }
+            if (lane < ((8 - (ncomp & 7)) & 7)) {
+                const int p = ncomp + lane;
+                float *d = reinterpret_cast<float *>(&sh.pl[w][p >> 1][0]) + (p & 1);
+                d[0] = 0.0f;
+                d[2] = 0.0f;
+                d[4] = 0.0f;
+                d[6] = 0.0f;
+                d[8] = 0.0f;
+                d[10] = __int_as_float(0x7f800000);
+            }
+            __syncwarp();
+        }
+        for (int c = 0; c < ncomp; c += kChunk) {
+            if (__all_sync(0xffffffffu, done0 && done1)) break;
+            // phase A: both pixels against two entries per f32x2 sequence (dx shared)
+            unsigned wa = 0, wb = 0;
+            const float4 *pl = &sh.pl[w][c >> 1][0];
+#pragma unroll
+            for (int gq = 0; gq < kChunk / 8; ++gq) {
+                if (c + 8 * gq >= ncomp) break;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int pr = 4 * gq + q;
+                    const float4 p0 = pl[3 * pr], p1 = pl[3 * pr + 1], p2 = pl[3 * pr + 2];
+                    const float2 A = make_float2(p1.x, p1.y), B = make_float2(p1.z, p1.w);
+                    const float2 C = make_float2(p2.x, p2.y), L = make_float2(p2.z, p2.w);
+                    const float2 dx = __fadd2_rn(px2, make_float2(p0.x, p0.y));
+                    const float2 my = make_float2(p0.z, p0.w);
+                    const float2 Adx = __fmul2_rn(A, dx);
+                    {
+                        const float2 dy = __fadd2_rn(py2a, my);
+                        const float2 u = __ffma2_rn(B, dy, Adx);
+                        const float2 qv = __ffma2_rn(__fmul2_rn(C, dy), dy, L);
+                        const float2 e = __ffma2_rn(u, dx, qv);
+                        wa |= (e.x <= thr0 ? 1u : 0u) << (2 * pr);
+                        wa |= (e.y <= thr0 ? 1u : 0u) << (2 * pr + 1);
+                    }
+                    {
+                        const float2 dy = __fadd2_rn(py2b, my);
+                        const float2 u = __ffma2_rn(B, dy, Adx);
+                        const float2 qv = __ffma2_rn(__fmul2_rn(C, dy), dy, L);
+                        const float2 e = __ffma2_rn(u, dx, qv);
+                        wb |= (e.x <= thr1 ? 1u : 0u) << (2 * pr);
+                        wb |= (e.y <= thr1 ? 1u : 0u) << (2 * pr + 1);
+                    }
+                }
+            }
+            if (done0) wa = 0;
+            if (done1) wb = 0;
+            // phase B: one candidate of each pixel per iteration (independent chains)
+            const uint8_t *sid = &sh.sidx[w][c];
+            while (wa | wb) {
+                const bool va = wa != 0, vb = wb != 0;
+                const int ja = sid[va ? __ffs(wa) - 1 : __ffs(wb) - 1];
+                const int jb = sid[vb ? __ffs(wb) - 1 : __ffs(wa) - 1];
+                wa &= wa - 1;
+                wb &= wb - 1;
+                const double apa = c2_alpha_at(sh, tab, ja, pxd, pyd0);
+                const double apb = c2_alpha_at(sh, tab, jb, pxd, pyd1);
+                if (!USAGE) {
+                    const double2 rga = sh.rg[ja], rgb = sh.rg[jb];
+                    const double bla = sh.bl[ja], blb = sh.bl[jb];
+                    double xa = apa * T0;
+                    const bool ca = va && xa > kCompC[7];
+                    xa = ca ? xa : 0.0;
+                    r0 += xa * rga.x;
+                    g0 += xa * rga.y;
+                    b0 += xa * bla;
+                    const double Ta = T0 * (1.0 - apa);
+                    T0 = ca ? Ta : T0;
+                    double xb = apb * T1;
+                    const bool cb = vb && xb > kCompC[7];
+                    xb = cb ? xb : 0.0;
+                    r1 += xb * rgb.x;
+                    g1 += xb * rgb.y;
+                    b1 += xb * blb;
+                    const double Tb = T1 * (1.0 - apb);
+                    T1 = cb ? Tb : T1;
+                    continue;
+                }
+                double x = apa * T0;
+                if (va && x > kCompC[7]) {
+                    const double2 rg = sh.rg[ja];
+                    r0 += x * rg.x;
+                    g0 += x * rg.y;
+                    b0 += x * sh.bl[ja];
+                    T0 = T0 * (1.0 - apa);
+                    atomicAdd(&sh.cnt[ja], 1);
+                }
+                x = apb * T1;
+                if (vb && x > kCompC[7]) {
+                    const double2 rg = sh.rg[jb];
+                    r1 += x * rg.x;
+                    g1 += x * rg.y;
+                    b1 += x * sh.bl[jb];
+                    T1 = T1 * (1.0 - apb);
+                    atomicAdd(&sh.cnt[jb], 1);
+                }
+            }
+            done0 = done0 || kAlphaClamp * T0 <= kEpsContrib;
+            done1 = done1 || kAlphaClamp * T1 <= kEpsContrib;
+            thr0 = __log2f((float)T0) + log2_inv_eps();
+            thr1 = __log2f((float)T1) + log2_inv_eps();
+        }
+        if (USAGE) {
+            __syncthreads();
+            for (int t = threadIdx.x; t < nb; t += kC2Threads)
+                if (sh.cnt[t] > 0)
+                    atomicAdd((unsigned long long *)(itp->usage + sh.gid[t]), (unsigned long long)sh.cnt[t]);
+        }
+        if (__syncthreads_count(!(done0 && done1)) == 0) break;
+    }
+
+    const CompItem it = *itp;
+    double sq = 0.0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int py = k ? py1 : py0;
+        const bool inside = k ? in1 : in0;
+        double vr = k ? r1 : r0, vg = k ? g1 : g0, vb = k ? b1 : b0;
+        const double T = k ? T1 : T0;
+        const int64_t pix = (int64_t)py * it.w + px;
+        if (it.clip) {
+            vr = fmin(fmax(vr, 0.0), 1.0);
+            vg = fmin(fmax(vg, 0.0), 1.0);
+            vb = fmin(fmax(vb, 0.0), 1.0);
+        }
+        if (inside) {
+            if (it.image) {
+                it.image[3 * pix] = vr;
+                it.image[3 * pix + 1] = vg;
+                it.image[3 * pix + 2] = vb;
+            }
+            if (it.trans) it.trans[pix] = T;
+            if (it.target) {
+                const double dr = vr - it.target[3 * pix];
+                const double dg = vg - it.target[3 * pix + 1];
+                const double db = vb - it.target[3 * pix + 2];
+                sq += (dr * dr + dg * dg) + db * db;
+            }
+        }
+    }
+    if (it.target) {
+        sq = warp_reduce_sum(sq);
+        // the per-tile partial slots (kCompWarps per tile) keep their layout: warps 0-3, then zeros
+        if (lane == 0) {
+            it.sse_tiles[(int64_t)tl * kCompWarps + w] = sq;
+            it.sse_tiles[(int64_t)tl * kCompWarps + kC2Warps + w] = 0.0;
+        }
+    }
+}
+
+template <bool USAGE>
+static void launch_composite2(int64_t tiles, cudaStream_t st, const CompItem *items, const int64_t *tile_base,
+                              int nitems, const TileLists &tl, const uint32_t *tcount) {
+    auto *fn = k_composite2<USAGE>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Comp2Shared));
+    fn<<<(unsigned)tiles, kC2Threads, sizeof(Comp2Shared), st>>>(items, tile_base, nitems, tl, tcount);
+}
+
 // Diagnostic counters: for every (primitive, pixel of its clipped bbox) pair of
 // the reference's loop, count it (bbox) and whether the pixel was still live
 // there, i.e. the primitive is not behind the pixel's terminating primitive in
@@ -1608,6 +1914,11 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
                 launch_composite<true, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
             else
                 launch_composite<false, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
+        } else if (COMP_PX2) {
+            if (any_usage)
+                launch_composite2<true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count);
+            else
+                launch_composite2<false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count);
         } else if (any_usage) {
             launch_composite<true, false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         } else {
