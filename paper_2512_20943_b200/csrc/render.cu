@@ -1238,11 +1238,8 @@ struct Comp2Shared {
     double2 exptab[kExpN * kExpRep];
 };
 
-__device__ __forceinline__ double c2_alpha_at(const Comp2Shared &sh, const double2 *tab, int j, double pxd,
-                                              double pyd) {
-    const double2 mm = sh.m[j];
-    const double2 ab = sh.hab[j];
-    const double2 ca = sh.hcal[j];
+__device__ __forceinline__ double c2_alpha(double2 mm, double2 ab, double2 ca, const double2 *tab, double pxd,
+                                           double pyd) {
     const double dx = pxd - mm.x;
     const double dy = pyd - mm.y;
     const double ee = (ab.x * dx * dx + ca.x * dy * dy) + ab.y * dx * dy;
@@ -1402,8 +1399,13 @@ k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                 const int jb = sid[vb ? __ffs(wb) - 1 : __ffs(wa) - 1];
                 wa &= wa - 1;
                 wb &= wb - 1;
-                const double apa = c2_alpha_at(sh, tab, ja, pxd, pyd0);
-                const double apb = c2_alpha_at(sh, tab, jb, pxd, pyd1);
+                // both candidates' staged fields are loaded up front (six independent
+                // 128-bit loads in flight before the fp64 chains start; sharing the
+                // loads when ja == jb measured slower: the branch serialises them)
+                const double2 ma = sh.m[ja], aba = sh.hab[ja], caa = sh.hcal[ja];
+                const double2 mb = sh.m[jb], abb = sh.hab[jb], cab = sh.hcal[jb];
+                const double apa = c2_alpha(ma, aba, caa, tab, pxd, pyd0);
+                const double apb = c2_alpha(mb, abb, cab, tab, pxd, pyd1);
                 if (!USAGE) {
                     const double2 rga = sh.rg[ja], rgb = sh.rg[jb];
                     const double bla = sh.bl[ja], blb = sh.bl[jb];

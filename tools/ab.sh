@@ -6,5 +6,6 @@ for v in "$@"; do
   AIRGS_B200_LIB=$L timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/ab_$v.json 2>gpurun_out/ab_$v.err
   python -c "
 import json,sys; d=json.loads(open('gpurun_out/ab_$v.json').read().strip().splitlines()[-1])
-print('$v', d['value'], 'views/s  step ms', d['ms_per_step'], ' composite ms', d['roofline']['kernel_ms_per_launch'], ' project ms', d['roofline']['project_ms_per_launch'], ' q0', d['qualities_db'][0])" || tail -3 gpurun_out/ab_$v.err
+c=d.get('clocks',{})
+print('$v', d['value'], 'views/s  step ms', d['ms_per_step'], ' composite ms', d['roofline']['kernel_ms_per_launch'], ' project ms', d['roofline']['project_ms_per_launch'], ' q0', d['qualities_db'][0], ' sm_mhz', c.get('sm_mhz'), c.get('reasons'))" || tail -3 gpurun_out/ab_$v.err
 done
