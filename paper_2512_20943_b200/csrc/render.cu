@@ -110,7 +110,10 @@ __device__ __forceinline__ bool rec_tile_range(const Rec &r, int &u0, int &u1, i
 
 constexpr int kProjThreads = 128;
 #ifndef PROJ_MIN_BLOCKS
-#define PROJ_MIN_BLOCKS 6
+#define PROJ_MIN_BLOCKS 4
+#endif
+#ifndef PROJ_STAGE_REC
+#define PROJ_STAGE_REC 1
 #endif
 
 // WMAX = 17 when every frame of the launch is SH degree 0 (fewer live registers),
@@ -166,11 +169,30 @@ __global__ void __launch_bounds__(kProjThreads, PROJ_MIN_BLOCKS) k_project(ProjA
         col0[1] = sigmoid_ref(p[12] + kShC0 * p[15]);
         col0[2] = sigmoid_ref(p[13] + kShC0 * p[16]);
     }
-    for (int it = ib; it < ie; ++it) {
-        const int item = a.frame_items[it];
+    // the frame's cameras, staged in shared memory a chunk at a time: the view
+    // loop then reads them as broadcasts instead of dependent global loads
+    constexpr int kCamStage = 32;
+    constexpr int kCamWords = (int)(sizeof(airgs_camera) / 8);
+    __shared__ unsigned long long scam_raw[kCamStage * kCamWords];
+    __shared__ int sitem[kCamStage];
+    const airgs_camera *scam = reinterpret_cast<const airgs_camera *>(scam_raw);
+    __shared__ Rec srec[PROJ_STAGE_REC ? kProjThreads : 1];
+    for (int cb = ib; cb < ie; cb += kCamStage) {
+        const int ncb = min(kCamStage, ie - cb);
+        __syncthreads();  // the previous chunk is consumed
+        for (int k = threadIdx.x; k < ncb * kCamWords; k += kProjThreads) {
+            const int q = k / kCamWords, wd = k - q * kCamWords;
+            const int item = a.frame_items[cb + q];
+            scam_raw[k] = reinterpret_cast<const unsigned long long *>(a.cams + a.item_cam[item])[wd];
+            if (wd == 0) sitem[q] = item;
+        }
+        __syncthreads();
+    for (int q = 0; q < ncb; ++q) {
+        const int item = sitem[q];
         const int64_t o = (int64_t)item * a.stride + i;
-        const airgs_camera &cam = a.cams[a.item_cam[item]];
+        const airgs_camera &cam = scam[q];
         const double *R = cam.rot;
+        bool need = false;
         int nt = 0;
         double tz = 0.0;
         double bbm = 1.0;  // stats: bbox floor/ceil argument margin
@@ -251,14 +273,37 @@ __global__ void __launch_bounds__(kProjThreads, PROJ_MIN_BLOCKS) k_project(ProjA
             const int64_t *fz = a.item_frozen ? a.item_frozen[item] : nullptr;
             const unsigned long long zk = order_key_of(fz, i, tz);
             // records of primitives that reach no tile are read only by the diagnostic counters
-            if (nt > 0 || (has_bbox && a.stats)) {
-                a.recs[o] = rec;
+            need = nt > 0 || (has_bbox && a.stats);
+            if (need) {
+                if (PROJ_STAGE_REC)
+                    srec[threadIdx.x] = rec;
+                else
+                    a.recs[o] = rec;
                 a.depth[o] = zk;
             }
             if (nt <= 0 && has_bbox) nt = -1;  // evaluated by the reference, but no pixel can pass the weight test
         }
         if (active) a.ntiles[o] = nt;
         if (a.stats) margin_min(a.stats, kMarginBBox, bbm);
+        if (PROJ_STAGE_REC) {
+            // the warp's 32 records leave as contiguous 16-byte chunks (each store
+            // instruction writes 512 consecutive bytes instead of 32 scattered pieces)
+            const unsigned needm = __ballot_sync(0xffffffffu, need);
+            if (needm) {
+                __syncwarp();
+                const int lane = threadIdx.x & 31;
+                const float4 *src = reinterpret_cast<const float4 *>(srec + (threadIdx.x & ~31));
+                float4 *dst = reinterpret_cast<float4 *>(a.recs + (o - lane));
+                constexpr int kChunks = (int)(sizeof(Rec) / 16);
+#pragma unroll
+                for (int k = 0; k < kChunks; ++k) {
+                    const int c = k * 32 + lane;
+                    if ((needm >> (c / kChunks)) & 1u) dst[c] = src[c];
+                }
+                __syncwarp();
+            }
+        }
+    }
     }
     if (a.stats)
         margin_min(a.stats, kMarginAlpha, valid ? fabs(alpha - kEpsContrib) / kEpsContrib : 1e300);
