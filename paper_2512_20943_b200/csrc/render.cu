@@ -1582,22 +1582,31 @@ k_count_pairs(const CompItem *__restrict__ items, const int32_t *__restrict__ nt
 }
 
 // one block per item: fixed-order reduction of that item's tile partials
-__global__ void __launch_bounds__(256)
+// (1024 threads, four independent accumulators each: the item's ~45k partials
+// are read with enough loads in flight; the order is fixed by the layout)
+constexpr int kSseThreads = 1024;
+__global__ void __launch_bounds__(kSseThreads)
 k_sse_items(const double *__restrict__ sse_tiles, const int64_t *__restrict__ tile_base,
             const uint8_t *__restrict__ has_target, double *__restrict__ out) {
     const int s = blockIdx.x;
     if (!has_target[s]) return;
     const int64_t b = tile_base[s] * kCompWarps, n = (tile_base[s + 1] - tile_base[s]) * kCompWarps;
-    double acc = 0.0;
-    for (int64_t k = threadIdx.x; k < n; k += 256) acc += sse_tiles[b + k];
-    acc = warp_reduce_sum(acc);
-    __shared__ double red[8];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t k = threadIdx.x;
+    for (; k + 3 * kSseThreads < n; k += 4 * kSseThreads) {
+        a0 += sse_tiles[b + k];
+        a1 += sse_tiles[b + k + kSseThreads];
+        a2 += sse_tiles[b + k + 2 * kSseThreads];
+        a3 += sse_tiles[b + k + 3 * kSseThreads];
+    }
+    for (; k < n; k += kSseThreads) a0 += sse_tiles[b + k];
+    double acc = warp_reduce_sum((a0 + a1) + (a2 + a3));
+    __shared__ double red[kSseThreads / 32];
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int k = 0; k < 8; ++k) t += red[k];
-        out[s] = t;
+    if (threadIdx.x < 32) {
+        acc = warp_reduce_sum(red[threadIdx.x]);
+        if (threadIdx.x == 0) out[s] = acc;
     }
 }
 
@@ -1983,7 +1992,7 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
     }
     ctx->time_end(t_comp, st, 0);
     if (sse && any_target) {
-        k_sse_items<<<nitems, 256, 0, st>>>(sse_tiles, L.d_tile_base, d_has, sse);
+        k_sse_items<<<nitems, kSseThreads, 0, st>>>(sse_tiles, L.d_tile_base, d_has, sse);
         ++NL;
         check_launch();
     }
