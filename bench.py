@@ -241,7 +241,7 @@ def run_gpu(args):
     views = V * args.steps * world
     value = views / (ms_max / 1e3)
 
-    # ---- roofline of the dominant kernel (k_composite2), timed live above
+    # ---- roofline of the dominant kernel (k_compositeN), timed live above
     roof = roofline(space, cams, payloads, ktime, ms_max / args.steps)
     # ---- its compute-side roofline: algorithmic fp64 work of the reference loop
     # (diagnostic counting pass over the timed frames, untimed)
@@ -280,7 +280,7 @@ def run_gpu(args):
 
 
 def roofline(space, cams, payloads, ktime, step_ms):
-    """Roofline of the dominant kernel, k_composite2 (one launch per step =
+    """Roofline of the dominant kernel, k_compositeN (one launch per step =
     all V views).  Algorithmic bytes per launch = V x (float64 target image
     P*3*8 + one 96-byte projected record per primitive, N*96): the data the
     kernel must read at least once.  Its duration is the CUDA-event time of
@@ -305,7 +305,7 @@ def roofline(space, cams, payloads, ktime, step_ms):
         pass
     out = {"bound": "hbm", "achieved": round(achieved, 2) if achieved else None, "peak": hbm, "unit": "GB/s",
            "frac": round(achieved / hbm, 4) if achieved else None, "traffic": traffic,
-           "peak_source": which, "kernel": "k_composite2", "kernel_ms_per_launch": round(k_ms, 4),
+           "peak_source": which, "kernel": "k_compositeN", "kernel_ms_per_launch": round(k_ms, 4),
            "kernel_share_of_step": round(k_ms / step_ms, 4) if step_ms else None,
            "algorithmic_bytes_per_launch": int(per_launch),
            "project_ms_per_launch": round(ktime["project_ms"] / max(ktime["project_launches"], 1), 4)}
@@ -324,7 +324,7 @@ OPS_PER_CONTRIB = 8
 
 
 def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames_used, k_ms):
-    """k_composite2 against the fp64 pipe (compositing is SM
+    """k_compositeN against the fp64 pipe (compositing is SM
     bound).  Algorithmic work per launch = live evaluations x 28 + contributions
     x 8 fp64 ops, with live / contributing (pixel, primitive) pairs counted
     exactly on the timed frames (airgs_eval_stats, verified against the CPU
@@ -353,7 +353,7 @@ def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames
     tot = {k: sum(counts[f][k] for f in frames_used) / len(frames_used) for k in ("bbox", "live", "contrib")}
     ops = tot["live"] * OPS_PER_LIVE_EVAL + tot["contrib"] * OPS_PER_CONTRIB
     achieved = ops / (k_ms / 1e3) / 1e12 if k_ms else None
-    return {"bound": "fp64", "kernel": "k_composite2", "achieved": round(achieved, 3) if achieved else None,
+    return {"bound": "fp64", "kernel": "k_compositeN", "achieved": round(achieved, 3) if achieved else None,
             "peak": round(peak, 3), "unit": "T fp64 ops/s", "frac": round(achieved / peak, 4) if achieved else None,
             "peak_source": src, "ops_per_live_eval": OPS_PER_LIVE_EVAL, "ops_per_contribution": OPS_PER_CONTRIB,
             "per_view": {k: int(round(v / V)) for k, v in tot.items()},

@@ -1244,32 +1244,43 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
     }
 }
 
-// ---- two pixels per lane (evaluation and usage passes) ------------------------
-// Same per-pixel algorithm as k_composite, with 4 warps per 16x16 tile: a warp
-// owns an 8x8 sub-tile and every lane two vertically adjacent pixels.  Each phase-A broadcast of an entry's fp32 fields then serves two
-// pixel tests (the shared-memory data pipe is the kernel's limiter), the
-// per-warp compaction is amortised over 64 pixels, and phase B runs the two
-// pixels' chains side by side (one candidate of each per iteration: two
-// independent exp / blend chains in flight instead of one dependent pair).
+// ---- NP pixels per lane (evaluation and usage passes) -------------------------
+// Same per-pixel algorithm as k_composite.  A lane owns NP vertically adjacent
+// pixels of one column; a warp owns an SW x 8 sub-tile (NP = 2: 8x8, 4 warps
+// per 16x16 tile -- the default; NP = 4: 16x8, 2 warps per tile, measured
+// 10% slower: more wasted exps over a 4-way union and 96+ registers).
+// Each phase-A broadcast of an entry's fp32 fields serves NP pixel tests and
+// the per-warp compaction is amortised over 32*NP pixels; phase B walks the
+// union of the lane's NP candidate sets in depth order, one entry per
+// iteration, loading its staged fp64 fields once for all NP pixels (the sets
+// of adjacent pixels overlap heavily) and sharing dx and fl(fl(a/2 dx) dx);
+// the NP exp / blend chains are independent.
 
 #ifndef COMP_PX2
 #define COMP_PX2 1
+#endif
+#ifndef C2_NP
+#define C2_NP 2
 #endif
 #ifndef C2_BATCH
 #define C2_BATCH 96
 #endif
 #ifndef C2_MIN_BLOCKS
-#define C2_MIN_BLOCKS 8
+#define C2_MIN_BLOCKS (C2_NP == 2 ? 8 : 10)
 #endif
-#ifndef C2_UNION
-#define C2_UNION 1
-#endif
-constexpr int kC2Threads = 128;
-constexpr int kC2Warps = kC2Threads / 32;
 constexpr int kC2Batch = C2_BATCH;
 constexpr int kC2List = kC2Batch + 8;
 
-struct Comp2Shared {
+template <int NP>
+struct CompNGeom {
+    static constexpr int kWarps = kTileThreads / (32 * NP);  // warps per tile
+    static constexpr int kThreads = 32 * kWarps;
+    static constexpr int kSW = 32 * NP / 8;                   // sub-tile width (height 8)
+    static constexpr int kLanesPerRow = kSW;                  // lanes across the sub-tile
+};
+
+template <int NP>
+struct CompNShared {
     double2 m[kC2Batch];     // mx, my
     double2 hab[kC2Batch];   // 0.5*a, b
     double2 hcal[kC2Batch];  // 0.5*c, alpha
@@ -1279,28 +1290,20 @@ struct Comp2Shared {
     float2 f1[kC2Batch];     // C, -L
     uint32_t gid[kC2Batch];
     int32_t cnt[kC2Batch];
-    uint8_t wmask[kC2Batch];  // bit w: may touch warp w's 8x8 sub-tile
-    float4 pl[kC2Warps][kC2List / 2][3];
-    uint8_t sidx[kC2Warps][kC2List];
+    uint8_t wmask[kC2Batch];  // bit w: may touch warp w's sub-tile
+    float4 pl[CompNGeom<NP>::kWarps][kC2List / 2][3];
+    uint8_t sidx[CompNGeom<NP>::kWarps][kC2List];
     double2 exptab[kExpN * kExpRep];
 };
 
-__device__ __forceinline__ double c2_alpha(double2 mm, double2 ab, double2 ca, const double2 *tab, double pxd,
-                                           double pyd) {
-    const double dx = pxd - mm.x;
-    const double dy = pyd - mm.y;
-    const double ee = (ab.x * dx * dx + ca.x * dy * dy) + ab.y * dx * dy;
-    const double ap = ca.y * exp_tab(-ee, tab);
-    return ap > kCompC[6] ? kCompC[6] : ap;
-}
-
-template <bool USAGE>
-__global__ void __launch_bounds__(kC2Threads, C2_MIN_BLOCKS)
-k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
+template <bool USAGE, int NP>
+__global__ void __launch_bounds__(CompNGeom<NP>::kThreads, C2_MIN_BLOCKS)
+k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
              const TileLists tls, const uint32_t *__restrict__ tcount) {
-    extern __shared__ __align__(16) unsigned char comp2_smem[];
-    Comp2Shared &sh = *reinterpret_cast<Comp2Shared *>(comp2_smem);
-    load_exp_table(sh.exptab, kC2Threads);
+    using G = CompNGeom<NP>;
+    extern __shared__ __align__(16) unsigned char compn_smem[];
+    CompNShared<NP> &sh = *reinterpret_cast<CompNShared<NP> *>(compn_smem);
+    load_exp_table(sh.exptab, G::kThreads);
     const int64_t g = blockIdx.x;
     int lo = 0, hi = nitems - 1;
     while (lo < hi) {
@@ -1312,32 +1315,41 @@ k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ til
     const int tiles_x = itp->tiles_x, img_w = itp->w, img_h = itp->h;
     const int tx = tl % tiles_x, ty = tl / tiles_x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int sx = (w & 1) * 8, sy = (w >> 1) * 8;
-    // the lane's two pixels are vertically adjacent (rows 2k, 2k+1): their
-    // candidate sets overlap most, which the phase-B union exploits (rows r and
-    // r+4 measured 5% slower)
-    const int lx = sx + (lane & 7), ly0 = sy + 2 * (lane >> 3), ly1 = ly0 + 1;
+    constexpr int kSubX = kTile / G::kSW;  // sub-tiles across the tile
+    const int sx = (w % kSubX) * G::kSW, sy = (w / kSubX) * 8;
+    // the lane's NP pixels are vertically adjacent: their candidate sets overlap
+    // most, which the phase-B union exploits (rows r, r+4 measured 5% slower at NP = 2)
+    const int lx = sx + lane % G::kLanesPerRow, ly0 = sy + NP * (lane / G::kLanesPerRow);
     const int ox = tx * kTile, oy = ty * kTile;
-    const int px = ox + lx, py0 = oy + ly0, py1 = oy + ly1;
-    const bool in0 = px < img_w && py0 < img_h, in1 = px < img_w && py1 < img_h;
+    const int px = ox + lx;
     const float2 px2 = make_float2((float)lx + 0.5f, (float)lx + 0.5f);
-    const float2 py2a = make_float2((float)ly0 + 0.5f, (float)ly0 + 0.5f);
-    const float2 py2b = make_float2((float)ly1 + 0.5f, (float)ly1 + 0.5f);
-    const double pxd = (double)px + 0.5, pyd0 = (double)py0 + 0.5, pyd1 = (double)py1 + 0.5;
+    const double pxd = (double)px + 0.5;
     const Rec *__restrict__ recs = itp->recs;
     const unsigned lt_mask = (1u << lane) - 1u;
     const double2 *tab = exp_lane_tab(sh.exptab);
 
     const int n_all = tls.count(tcount, g);
     const uint64_t *__restrict__ glist = tls.list(g);
-    double T0 = 1.0, r0 = 0.0, g0 = 0.0, b0 = 0.0;
-    double T1 = 1.0, r1 = 0.0, g1 = 0.0, b1 = 0.0;
-    bool done0 = !in0, done1 = !in1;
-    float thr0 = log2_inv_eps(), thr1 = log2_inv_eps();
+    double T[NP], cr[NP], cg[NP], cb[NP];
+    bool done[NP];
+    float thr[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+        T[k] = 1.0;
+        cr[k] = cg[k] = cb[k] = 0.0;
+        done[k] = !(px < img_w && oy + ly0 + k < img_h);
+        thr[k] = log2_inv_eps();
+    }
+    auto all_done = [&]() {
+        bool d = true;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) d = d && done[k];
+        return d;
+    };
 
     for (int base = 0; base < n_all; base += kC2Batch) {
         const int nb = min(kC2Batch, n_all - base);
-        for (int t = threadIdx.x; t < nb; t += kC2Threads) {
+        for (int t = threadIdx.x; t < nb; t += G::kThreads) {
             const uint32_t gi = (uint32_t)glist[base + t];
             if (COMP_PREFETCH && base + kC2Batch + t < n_all) {
                 const char *pa = reinterpret_cast<const char *>(recs + (uint32_t)glist[base + kC2Batch + t]);
@@ -1355,24 +1367,26 @@ k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             sh.hcal[t] = make_double2(0.5 * r.cc, r.al);
             sh.rg[t] = make_double2(r.cr, r.cg);
             sh.bl[t] = r.cbl;
-            // 8x8 sub-tiles: columns 8k+0.5 .. 8k+7.5, rows 8k+0.5 .. 8k+7.5
+            // sub-tiles: columns SW k + 0.5 .. SW k + SW - 0.5, rows 8k + 0.5 .. 8k + 7.5
             unsigned xm = 0, ym = 0;
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                xm |= (r.x0 < ox + 8 * k + 8 && r.x1 > ox + 8 * k && mxl - r.hx <= 8.0f * k + 7.5f &&
-                       mxl + r.hx >= 8.0f * k + 0.5f) ? (1u << k) : 0u;
+            for (int k = 0; k < kSubX; ++k)
+                xm |= (r.x0 < ox + G::kSW * k + G::kSW && r.x1 > ox + G::kSW * k &&
+                       mxl - r.hx <= (float)(G::kSW * k + G::kSW) - 0.5f && mxl + r.hx >= (float)(G::kSW * k) + 0.5f)
+                          ? (1u << k) : 0u;
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
                 ym |= (r.y0 < oy + 8 * k + 8 && r.y1 > oy + 8 * k && myl - r.hy <= 8.0f * k + 7.5f &&
                        myl + r.hy >= 8.0f * k + 0.5f) ? (1u << k) : 0u;
-            }
             unsigned mk = 0;
 #pragma unroll
-            for (int ww = 0; ww < 4; ++ww) mk |= (((xm >> (ww & 1)) & (ym >> (ww >> 1))) & 1u) << ww;
+            for (int ww = 0; ww < G::kWarps; ++ww) mk |= (((xm >> (ww % kSubX)) & (ym >> (ww / kSubX))) & 1u) << ww;
             sh.wmask[t] = (uint8_t)mk;
             if (USAGE) sh.cnt[t] = 0;
         }
         __syncthreads();
         int ncomp = 0;
-        if (!__all_sync(0xffffffffu, done0 && done1)) {
+        if (!__all_sync(0xffffffffu, all_done())) {
             for (int c0 = 0; c0 < nb; c0 += 32) {
                 const int j = c0 + lane;
                 const bool hit = j < nb && ((sh.wmask[j] >> w) & 1u);
@@ -1405,9 +1419,11 @@ k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             __syncwarp();
         }
         for (int c = 0; c < ncomp; c += kChunk) {
-            if (__all_sync(0xffffffffu, done0 && done1)) break;
-            // phase A: both pixels against two entries per f32x2 sequence (dx shared)
-            unsigned wa = 0, wb = 0;
+            if (__all_sync(0xffffffffu, all_done())) break;
+            // phase A: the NP pixels against two entries per f32x2 sequence (dx shared)
+            unsigned wd[NP];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) wd[k] = 0;
             const float4 *pl = &sh.pl[w][c >> 1][0];
 #pragma unroll
             for (int gq = 0; gq < kChunk / 8; ++gq) {
@@ -1421,173 +1437,95 @@ k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                     const float2 dx = __fadd2_rn(px2, make_float2(p0.x, p0.y));
                     const float2 my = make_float2(p0.z, p0.w);
                     const float2 Adx = __fmul2_rn(A, dx);
-                    {
-                        const float2 dy = __fadd2_rn(py2a, my);
+#pragma unroll
+                    for (int k = 0; k < NP; ++k) {
+                        const float yk = (float)(ly0 + k) + 0.5f;
+                        const float2 dy = __fadd2_rn(make_float2(yk, yk), my);
                         const float2 u = __ffma2_rn(B, dy, Adx);
                         const float2 qv = __ffma2_rn(__fmul2_rn(C, dy), dy, L);
                         const float2 e = __ffma2_rn(u, dx, qv);
-                        wa |= (e.x <= thr0 ? 1u : 0u) << (2 * pr);
-                        wa |= (e.y <= thr0 ? 1u : 0u) << (2 * pr + 1);
-                    }
-                    {
-                        const float2 dy = __fadd2_rn(py2b, my);
-                        const float2 u = __ffma2_rn(B, dy, Adx);
-                        const float2 qv = __ffma2_rn(__fmul2_rn(C, dy), dy, L);
-                        const float2 e = __ffma2_rn(u, dx, qv);
-                        wb |= (e.x <= thr1 ? 1u : 0u) << (2 * pr);
-                        wb |= (e.y <= thr1 ? 1u : 0u) << (2 * pr + 1);
+                        wd[k] |= (e.x <= thr[k] ? 1u : 0u) << (2 * pr);
+                        wd[k] |= (e.y <= thr[k] ? 1u : 0u) << (2 * pr + 1);
                     }
                 }
             }
-            if (done0) wa = 0;
-            if (done1) wb = 0;
+            unsigned wu = 0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                if (done[k]) wd[k] = 0;
+                wu |= wd[k];
+            }
+            // phase B: the union of the NP candidate sets in depth order
             const uint8_t *sid = &sh.sidx[w][c];
-#if C2_UNION
-            // phase B: the union of the two pixels' candidates in depth order, one
-            // entry per iteration: its staged fields are loaded once for both pixels
-            // (the two sets overlap heavily: |A u B| ~ 1.3 max(|A|, |B|)), dx and
-            // fl(fl(a/2 dx) dx) are shared, the two exp / blend chains independent
-            for (unsigned wu = wa | wb; wu; wu &= wu - 1) {
+            for (; wu; wu &= wu - 1) {
                 const int pos = __ffs(wu) - 1;
-                const bool va = (wa >> pos) & 1u, vb = (wb >> pos) & 1u;
                 const int j = sid[pos];
                 const double2 mm = sh.m[j], ab = sh.hab[j], ca = sh.hcal[j];
                 const double2 rg = sh.rg[j];
                 const double bl = sh.bl[j];
                 const double dx = pxd - mm.x;
                 const double ex = ab.x * dx * dx;
-                const double dya = pyd0 - mm.y, dyb = pyd1 - mm.y;
-                const double eea = (ex + ca.x * dya * dya) + ab.y * dx * dya;
-                const double eeb = (ex + ca.x * dyb * dyb) + ab.y * dx * dyb;
-                double apa = ca.y * exp_tab(-eea, tab);
-                double apb = ca.y * exp_tab(-eeb, tab);
-                apa = apa > kCompC[6] ? kCompC[6] : apa;
-                apb = apb > kCompC[6] ? kCompC[6] : apb;
-                double xa = apa * T0;
-                const bool cpa = va && xa > kCompC[7];
-                double xb = apb * T1;
-                const bool cpb = vb && xb > kCompC[7];
-                if (!USAGE) {
-                    xa = cpa ? xa : 0.0;
-                    r0 += xa * rg.x;
-                    g0 += xa * rg.y;
-                    b0 += xa * bl;
-                    const double Ta = T0 * (1.0 - apa);
-                    T0 = cpa ? Ta : T0;
-                    xb = cpb ? xb : 0.0;
-                    r1 += xb * rg.x;
-                    g1 += xb * rg.y;
-                    b1 += xb * bl;
-                    const double Tb = T1 * (1.0 - apb);
-                    T1 = cpb ? Tb : T1;
-                } else {
-                    if (cpa) {
-                        r0 += xa * rg.x;
-                        g0 += xa * rg.y;
-                        b0 += xa * bl;
-                        T0 = T0 * (1.0 - apa);
+                int nc = 0;
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    const double dy = ((double)(oy + ly0 + k) + 0.5) - mm.y;
+                    const double ee = (ex + ca.x * dy * dy) + ab.y * dx * dy;
+                    double ap = ca.y * exp_tab(-ee, tab);
+                    ap = ap > kCompC[6] ? kCompC[6] : ap;
+                    double x = ap * T[k];
+                    const bool cp = ((wd[k] >> pos) & 1u) && x > kCompC[7];
+                    if (!USAGE) {
+                        // branch-free: a non-contributing entry adds exact zeros, keeps T
+                        x = cp ? x : 0.0;
+                        cr[k] += x * rg.x;
+                        cg[k] += x * rg.y;
+                        cb[k] += x * bl;
+                        const double Tn = T[k] * (1.0 - ap);
+                        T[k] = cp ? Tn : T[k];
+                    } else if (cp) {
+                        cr[k] += x * rg.x;
+                        cg[k] += x * rg.y;
+                        cb[k] += x * bl;
+                        T[k] = T[k] * (1.0 - ap);
+                        ++nc;
                     }
-                    if (cpb) {
-                        r1 += xb * rg.x;
-                        g1 += xb * rg.y;
-                        b1 += xb * bl;
-                        T1 = T1 * (1.0 - apb);
-                    }
-                    const int nc = (int)cpa + (int)cpb;
-                    if (nc) atomicAdd(&sh.cnt[j], nc);
                 }
+                if (USAGE && nc) atomicAdd(&sh.cnt[j], nc);
             }
-#else
-            // phase B: one candidate of each pixel per iteration (independent chains)
-            while (wa | wb) {
-                const bool va = wa != 0, vb = wb != 0;
-                const int ja = sid[va ? __ffs(wa) - 1 : __ffs(wb) - 1];
-                const int jb = sid[vb ? __ffs(wb) - 1 : __ffs(wa) - 1];
-                wa &= wa - 1;
-                wb &= wb - 1;
-                // both candidates' staged fields are loaded up front (six independent
-                // 128-bit loads in flight before the fp64 chains start; sharing the
-                // loads when ja == jb measured slower: the branch serialises them)
-                const double2 ma = sh.m[ja], aba = sh.hab[ja], caa = sh.hcal[ja];
-                const double2 mb = sh.m[jb], abb = sh.hab[jb], cab = sh.hcal[jb];
-                const double apa = c2_alpha(ma, aba, caa, tab, pxd, pyd0);
-                const double apb = c2_alpha(mb, abb, cab, tab, pxd, pyd1);
-                if (!USAGE) {
-                    const double2 rga = sh.rg[ja], rgb = sh.rg[jb];
-                    const double bla = sh.bl[ja], blb = sh.bl[jb];
-                    double xa = apa * T0;
-                    const bool ca = va && xa > kCompC[7];
-                    xa = ca ? xa : 0.0;
-                    r0 += xa * rga.x;
-                    g0 += xa * rga.y;
-                    b0 += xa * bla;
-                    const double Ta = T0 * (1.0 - apa);
-                    T0 = ca ? Ta : T0;
-                    double xb = apb * T1;
-                    const bool cb = vb && xb > kCompC[7];
-                    xb = cb ? xb : 0.0;
-                    r1 += xb * rgb.x;
-                    g1 += xb * rgb.y;
-                    b1 += xb * blb;
-                    const double Tb = T1 * (1.0 - apb);
-                    T1 = cb ? Tb : T1;
-                    continue;
-                }
-                double x = apa * T0;
-                if (va && x > kCompC[7]) {
-                    const double2 rg = sh.rg[ja];
-                    r0 += x * rg.x;
-                    g0 += x * rg.y;
-                    b0 += x * sh.bl[ja];
-                    T0 = T0 * (1.0 - apa);
-                    atomicAdd(&sh.cnt[ja], 1);
-                }
-                x = apb * T1;
-                if (vb && x > kCompC[7]) {
-                    const double2 rg = sh.rg[jb];
-                    r1 += x * rg.x;
-                    g1 += x * rg.y;
-                    b1 += x * sh.bl[jb];
-                    T1 = T1 * (1.0 - apb);
-                    atomicAdd(&sh.cnt[jb], 1);
-                }
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+                done[k] = done[k] || kAlphaClamp * T[k] <= kEpsContrib;
+                thr[k] = __log2f((float)T[k]) + log2_inv_eps();
             }
-#endif
-            done0 = done0 || kAlphaClamp * T0 <= kEpsContrib;
-            done1 = done1 || kAlphaClamp * T1 <= kEpsContrib;
-            thr0 = __log2f((float)T0) + log2_inv_eps();
-            thr1 = __log2f((float)T1) + log2_inv_eps();
         }
         if (USAGE) {
             __syncthreads();
-            for (int t = threadIdx.x; t < nb; t += kC2Threads)
+            for (int t = threadIdx.x; t < nb; t += G::kThreads)
                 if (sh.cnt[t] > 0)
                     atomicAdd((unsigned long long *)(itp->usage + sh.gid[t]), (unsigned long long)sh.cnt[t]);
         }
-        if (__syncthreads_count(!(done0 && done1)) == 0) break;
+        if (__syncthreads_count(!all_done()) == 0) break;
     }
 
     const CompItem it = *itp;
     double sq = 0.0;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const int py = k ? py1 : py0;
-        const bool inside = k ? in1 : in0;
-        double vr = k ? r1 : r0, vg = k ? g1 : g0, vb = k ? b1 : b0;
-        const double T = k ? T1 : T0;
+    for (int k = 0; k < NP; ++k) {
+        const int py = oy + ly0 + k;
+        double vr = cr[k], vg = cg[k], vb = cb[k];
         const int64_t pix = (int64_t)py * it.w + px;
         if (it.clip) {
             vr = fmin(fmax(vr, 0.0), 1.0);
             vg = fmin(fmax(vg, 0.0), 1.0);
             vb = fmin(fmax(vb, 0.0), 1.0);
         }
-        if (inside) {
+        if (px < img_w && py < img_h) {
             if (it.image) {
                 it.image[3 * pix] = vr;
                 it.image[3 * pix + 1] = vg;
                 it.image[3 * pix + 2] = vb;
             }
-            if (it.trans) it.trans[pix] = T;
+            if (it.trans) it.trans[pix] = T[k];
             if (it.target) {
                 const double dr = vr - it.target[3 * pix];
                 const double dg = vg - it.target[3 * pix + 1];
@@ -1598,10 +1536,10 @@ k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ til
     }
     if (it.target) {
         sq = warp_reduce_sum(sq);
-        // the per-tile partial slots (kCompWarps per tile) keep their layout: warps 0-3, then zeros
+        // the per-tile partial slots (kCompWarps per tile) keep their layout: this kernel's warps, then zeros
         if (lane == 0) {
             it.sse_tiles[(int64_t)tl * kCompWarps + w] = sq;
-            it.sse_tiles[(int64_t)tl * kCompWarps + kC2Warps + w] = 0.0;
+            for (int k = G::kWarps + w; k < kCompWarps; k += G::kWarps) it.sse_tiles[(int64_t)tl * kCompWarps + k] = 0.0;
         }
     }
 }
@@ -1609,9 +1547,10 @@ k_composite2(const CompItem *__restrict__ items, const int64_t *__restrict__ til
 template <bool USAGE>
 static void launch_composite2(int64_t tiles, cudaStream_t st, const CompItem *items, const int64_t *tile_base,
                               int nitems, const TileLists &tl, const uint32_t *tcount) {
-    auto *fn = k_composite2<USAGE>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Comp2Shared));
-    fn<<<(unsigned)tiles, kC2Threads, sizeof(Comp2Shared), st>>>(items, tile_base, nitems, tl, tcount);
+    auto *fn = k_compositeN<USAGE, C2_NP>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CompNShared<C2_NP>));
+    fn<<<(unsigned)tiles, CompNGeom<C2_NP>::kThreads, sizeof(CompNShared<C2_NP>), st>>>(items, tile_base, nitems,
+                                                                                        tl, tcount);
 }
 
 // Diagnostic counters: for every (primitive, pixel of its clipped bbox) pair of
