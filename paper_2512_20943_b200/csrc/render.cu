@@ -1340,6 +1340,12 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
         done[k] = !(px < img_w && oy + ly0 + k < img_h);
         thr[k] = log2_inv_eps();
     }
+    if (COMP_PREFETCH && itp->target) {  // the epilogue's target pixels travel into L2 meanwhile
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+            if (px < img_w && oy + ly0 + k < img_h)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(itp->target + 3 * ((int64_t)(oy + ly0 + k) * img_w + px)));
+    }
     auto all_done = [&]() {
         bool d = true;
 #pragma unroll
