@@ -2272,22 +2272,16 @@ struct BwdShared {
     double2 exptab[kExpN * kExpRep];
 };
 
-// Per-contribution gradient term q of staged entry j, straight to the
-// per-primitive totals: global fp64 reductions are native fire-and-forget L2
-// operations (RED.ADD.F64), while shared-memory fp64 atomicAdd is a
-// compare-and-swap loop on sm_100 (ATOMS.CAST.SPIN.64) -- accumulating the
-// 9 terms per contribution in shared memory first made the training step
-// 37% slower (3.47 vs 2.53 ms per C2 view).
-__device__ __forceinline__ void bwd_acc(const BwdShared &sh, double *__restrict__ G, int j, int q, double v) {
-    atomicAdd(G + (int64_t)sh.gid[j] * 9 + q, v);
-}
 
 // One CTA per tile, one pixel per thread: the pixel's recorded contributors in
 // reverse depth order with the reference's per-pixel recurrences (t_before =
 // T / (1 - ap), the running colour accumulator, d_ap with the clamp rule);
-// every per-contribution term is added to the per-primitive totals G[id][9]
-// (fp64 reductions: the cross-pixel summation order differs from the
-// reference's row-major loop, the per-pixel terms do not).
+// each warp sums an entry's 9 per-contribution terms over its contributing
+// pixels and sends them to the per-primitive totals G[id][9] as native fp64
+// L2 reductions (RED.ADD.F64; shared-memory fp64 atomicAdd is a CAS loop on
+// sm_100 -- accumulating the terms there made the training step 37% slower).
+// The cross-pixel summation order differs from the reference's row-major
+// loop; the per-pixel terms do not.
 __global__ void __launch_bounds__(kTileThreads) k_composite_bwd(const Rec *__restrict__ recs, const TileLists tls,
                                                                const uint32_t *__restrict__ tcount,
                                                                const uint32_t *__restrict__ cbits,
@@ -2299,7 +2293,7 @@ __global__ void __launch_bounds__(kTileThreads) k_composite_bwd(const Rec *__res
     load_exp_table(sh.exptab, kTileThreads);
     const int64_t g = blockIdx.x;
     const int tx = (int)(g % tiles_x), ty = (int)(g / tiles_x);
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4, lane = threadIdx.x & 31;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const bool inside = px < w && py < h;
     const int64_t pix = (int64_t)py * w + px;
@@ -2334,17 +2328,26 @@ __global__ void __launch_bounds__(kTileThreads) k_composite_bwd(const Rec *__res
             sh.f[8][t] = r.cbl;
         }
         __syncthreads();
-        if (inside) {
-            for (int wd = (hi - 1) >> 5; wd >= (lo >> 5); --wd) {
-                uint32_t m = bits[(int64_t)wd * kTileThreads];
-                // keep entries in [lo, hi) of this word
-                const int e0 = wd << 5;
-                if (e0 < lo) m &= ~0u << (lo - e0);
-                if (e0 + 32 > hi) m &= (hi - e0) >= 32 ? ~0u : ((1u << (hi - e0)) - 1u);
-                while (m) {
-                    const int b = 31 - __clz(m);
-                    m &= ~(1u << b);
-                    const int j = e0 + b - lo;
+        // entry-synchronous per warp: the union of the warp's contributors of
+        // each bit word, in reverse depth order (each pixel still sees its own
+        // contributors in its own reverse order); an entry's 9 terms are summed
+        // over the warp's contributing lanes before they go to L2, so an entry
+        // costs 9 reductions per warp instead of 9 per contributing pixel
+        for (int wd = (hi - 1) >> 5; wd >= (lo >> 5); --wd) {
+            uint32_t m = inside ? bits[(int64_t)wd * kTileThreads] : 0u;
+            const int e0 = wd << 5;
+            if (e0 < lo) m &= ~0u << (lo - e0);
+            if (e0 + 32 > hi) m &= (hi - e0) >= 32 ? ~0u : ((1u << (hi - e0)) - 1u);
+            uint32_t wm = __reduce_or_sync(0xffffffffu, m);
+            while (wm) {
+                const int b = 31 - __clz(wm);
+                wm &= ~(1u << b);
+                const int j = e0 + b - lo;
+                const bool mine = (m >> b) & 1u;
+                double v[9];
+#pragma unroll
+                for (int q = 0; q < 9; ++q) v[q] = 0.0;
+                if (mine) {
                     const double mx = sh.f[0][j], my = sh.f[1][j], a = sh.f[2][j], bb = sh.f[3][j], c = sh.f[4][j];
                     const double al = sh.f[5][j], cr = sh.f[6][j], cg = sh.f[7][j], cb = sh.f[8][j];
                     // _composite.pyx:121-151, op for op
@@ -2356,24 +2359,36 @@ __global__ void __launch_bounds__(kTileThreads) k_composite_bwd(const Rec *__res
                     const double ap = raw > kAlphaClamp ? kAlphaClamp : raw;
                     const double t_before = T / (1.0 - ap);
                     const double wgt = ap * t_before;
-                    bwd_acc(sh, G, j, 6, wgt * dc0);
-                    bwd_acc(sh, G, j, 7, wgt * dc1);
-                    bwd_acc(sh, G, j, 8, wgt * dc2);
+                    v[6] = wgt * dc0;
+                    v[7] = wgt * dc1;
+                    v[8] = wgt * dc2;
                     const double dc_dot_col = (dc0 * cr + dc1 * cg) + dc2 * cb;
                     double d_ap = t_before * dc_dot_col - ((ac0 * dc0 + ac1 * dc1) + ac2 * dc2) / (1.0 - ap);
                     if (raw >= kAlphaClamp) d_ap = 0.0;
-                    bwd_acc(sh, G, j, 5, d_ap * gg);
+                    v[5] = d_ap * gg;
                     const double d_g = d_ap * al;
                     const double d_e = -gg * d_g;
-                    bwd_acc(sh, G, j, 0, -d_e * (a * dx + bb * dy));
-                    bwd_acc(sh, G, j, 1, -d_e * (bb * dx + c * dy));
-                    bwd_acc(sh, G, j, 2, d_e * 0.5 * dx * dx);
-                    bwd_acc(sh, G, j, 3, d_e * dx * dy);
-                    bwd_acc(sh, G, j, 4, d_e * 0.5 * dy * dy);
+                    v[0] = -d_e * (a * dx + bb * dy);
+                    v[1] = -d_e * (bb * dx + c * dy);
+                    v[2] = d_e * 0.5 * dx * dx;
+                    v[3] = d_e * dx * dy;
+                    v[4] = d_e * 0.5 * dy * dy;
                     ac0 += cr * wgt;
                     ac1 += cg * wgt;
                     ac2 += cb * wgt;
                     T = t_before;
+                }
+                const unsigned who = __ballot_sync(0xffffffffu, mine);
+                if (__popc(who) <= 2) {  // few contributors: their own reductions
+                    if (mine)
+#pragma unroll
+                        for (int q = 0; q < 9; ++q) atomicAdd(G + (int64_t)sh.gid[j] * 9 + q, v[q]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 9; ++q) v[q] = warp_reduce_sum(v[q]);
+                    if (lane == 0)
+#pragma unroll
+                        for (int q = 0; q < 9; ++q) atomicAdd(G + (int64_t)sh.gid[j] * 9 + q, v[q]);
                 }
             }
         }
