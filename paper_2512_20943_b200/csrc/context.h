@@ -165,6 +165,7 @@ enum Slot : int {
     kSlotBwdGrad,
     kSlotTFinal,
     kSlotBinRec,
+    kSlotBinCount,
     kSlotCount
 };
 
