@@ -1282,6 +1282,11 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_MIN_BLOCKS
 #define C2_MIN_BLOCKS (C2_NP == 2 ? 8 : 10)
 #endif
+#ifndef C2_CHUNK
+#define C2_CHUNK 24
+#endif
+constexpr int kC2Chunk = C2_CHUNK;  // compacted entries per phase A / phase B round (24 measured best of 8..32)
+static_assert(kC2Chunk % 8 == 0 && kC2Chunk <= 32, "chunk");
 constexpr int kC2Batch = C2_BATCH;
 constexpr int kC2List = kC2Batch + 8;
 
@@ -1438,7 +1443,7 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             }
             __syncwarp();
         }
-        for (int c = 0; c < ncomp; c += kChunk) {
+        for (int c = 0; c < ncomp; c += kC2Chunk) {
             if (__all_sync(0xffffffffu, all_done())) break;
             // phase A: the NP pixels against two entries per f32x2 sequence (dx shared)
             unsigned wd[NP];
@@ -1446,7 +1451,7 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             for (int k = 0; k < NP; ++k) wd[k] = 0;
             const float4 *pl = &sh.pl[w][c >> 1][0];
 #pragma unroll
-            for (int gq = 0; gq < kChunk / 8; ++gq) {
+            for (int gq = 0; gq < kC2Chunk / 8; ++gq) {
                 if (c + 8 * gq >= ncomp) break;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
