@@ -1277,7 +1277,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #define C2_NP 2
 #endif
 #ifndef C2_BATCH
-#define C2_BATCH 96
+#define C2_BATCH 88
 #endif
 #ifndef C2_MIN_BLOCKS
 #define C2_MIN_BLOCKS (C2_NP == 2 ? 8 : 10)
