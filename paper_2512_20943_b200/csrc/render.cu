@@ -555,12 +555,14 @@ __constant__ double kCompC[9] = {kExpInvLn2N, kExpNegLn2HiN, kExpNegLn2LoN, kExp
 // 2^(i/128) + degree-5 polynomial, same constants and the same fma nesting --
 // tools/gen_exp_table.py; tests/test_exp_table.py checks it bit for bit
 // against the host libm), which the reference's Cython kernel calls at
-// _composite.pyx:57.  The table is replicated kExpRep times, entry-major, and
-// lane l reads copy l % kExpRep, so the 8 lanes of a 128-bit shared-memory
-// phase spread over more bank groups (random-index bank conflicts of a
-// single table were ~12% of the compositing kernel's shared wavefronts).
+// _composite.pyx:57.  The table can be replicated kExpRep times, entry-major,
+// with lane l reading copy l % kExpRep, so that the 8 lanes of a 128-bit
+// shared-memory phase spread over more bank groups; that paid (x2) for the
+// one-pixel kernel, whose limiter was the shared-memory data pipe, but the
+// two-pixel union kernel is faster with one copy (less shared memory per CTA):
+// 3.24 vs 3.33 ms per C2 step.
 #ifndef EXP_REP
-#define EXP_REP 2
+#define EXP_REP 1
 #endif
 constexpr int kExpRep = EXP_REP;
 
@@ -1277,7 +1279,7 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #define C2_NP 2
 #endif
 #ifndef C2_BATCH
-#define C2_BATCH 88
+#define C2_BATCH 96
 #endif
 #ifndef C2_MIN_BLOCKS
 #define C2_MIN_BLOCKS (C2_NP == 2 ? 8 : 10)
