@@ -356,6 +356,8 @@ def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames
     return {"bound": "fp64", "kernel": "k_compositeN", "achieved": round(achieved, 3) if achieved else None,
             "peak": round(peak, 3), "unit": "T fp64 ops/s", "frac": round(achieved / peak, 4) if achieved else None,
             "peak_source": src, "ops_per_live_eval": OPS_PER_LIVE_EVAL, "ops_per_contribution": OPS_PER_CONTRIB,
+            "note": "reference-work rate, not pipe utilisation: the fp32 candidate pass skips most of the "
+                    "reference's fp64 work, so frac can exceed 1 (measured pipe use: roofline.sm)",
             "per_view": {k: int(round(v / V)) for k, v in tot.items()},
             "algorithmic_ops_per_launch": int(ops), "decision_margins": margins}
 
