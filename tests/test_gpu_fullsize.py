@@ -175,3 +175,32 @@ def test_seam_unit_colour_conservation_full_size():
     img, tr, us, _ = rasterizer.forward(pr.means2d, pr.conics, pr.alphas, np.ones_like(pr.colors), pr.bboxes, H, W)
     np.testing.assert_allclose(img[:, :, 0], 1.0 - tr, atol=1e-12)
     assert np.all(tr > 0) and np.all(tr <= 1)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C5"])
+def test_two_pixel_kernel_equals_one_pixel_kernel_bit_for_bit(cfg):
+    """The evaluation kernel (k_compositeN, two pixels per lane, union phase B)
+    and the one-pixel kernel (k_composite, the one the seam fixtures pin
+    bit-for-bit to the reference kernel; selected here through the diagnostic
+    counters) composite the same device projection to identical images and
+    usage at full size."""
+    import torch
+
+    from paper_2512_20943_b200 import _lib, synth
+    from paper_2512_20943_b200.model import GaussianFrame
+    from paper_2512_20943_b200.rasterizer import render_views
+
+    c = _cfg(cfg, views=2, count=400000 if cfg == "C5" else None)
+    fr = GaussianFrame(params=synth.Sequence(c, seed=3, event_every=0).frame(1))
+    cams = synth.cameras(c)
+    items = [(0, v) for v in range(len(cams))]
+    a = render_views([fr], cams, items, want_images=True, usage_frames=[0])
+    eng = _lib.engine()
+    eng.eval_stats(1)
+    try:
+        b = render_views([fr], cams, items, want_images=True, usage_frames=[0])
+    finally:
+        eng.eval_stats(0)
+    for x, y in zip(a.images, b.images):
+        assert torch.equal(x, y)
+    assert torch.equal(a.usage[0], b.usage[0])
