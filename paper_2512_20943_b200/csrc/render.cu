@@ -1287,6 +1287,9 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_CHUNK
 #define C2_CHUNK 24
 #endif
+#ifndef C2_STATIC_SMEM
+#define C2_STATIC_SMEM 1
+#endif
 constexpr int kC2Chunk = C2_CHUNK;  // compacted entries per phase A / phase B round (24 measured best of 8..32)
 static_assert(kC2Chunk % 8 == 0 && kC2Chunk <= 32, "chunk");
 constexpr int kC2Batch = C2_BATCH;
@@ -1322,8 +1325,14 @@ __global__ void __launch_bounds__(CompNGeom<NP>::kThreads, C2_MIN_BLOCKS)
 k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
              const TileLists tls, const uint32_t *__restrict__ tcount) {
     using G = CompNGeom<NP>;
+#if C2_STATIC_SMEM
+    // static shared memory (< 48 KB): constant shared addresses fold into the
+    // load offsets instead of a base-register add per access
+    __shared__ CompNShared<NP> sh;
+#else
     extern __shared__ __align__(16) unsigned char compn_smem[];
     CompNShared<NP> &sh = *reinterpret_cast<CompNShared<NP> *>(compn_smem);
+#endif
     load_exp_table(sh.exptab, G::kThreads);
     const int64_t g = blockIdx.x;
     int lo = 0, hi = nitems - 1;
@@ -1575,6 +1584,10 @@ template <bool USAGE>
 static void launch_composite2(int64_t tiles, cudaStream_t st, const CompItem *items, const int64_t *tile_base,
                               int nitems, const TileLists &tl, const uint32_t *tcount) {
     auto *fn = k_compositeN<USAGE, C2_NP>;
+    if (C2_STATIC_SMEM) {
+        fn<<<(unsigned)tiles, CompNGeom<C2_NP>::kThreads, 0, st>>>(items, tile_base, nitems, tl, tcount);
+        return;
+    }
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CompNShared<C2_NP>));
     fn<<<(unsigned)tiles, CompNGeom<C2_NP>::kThreads, sizeof(CompNShared<C2_NP>), st>>>(items, tile_base, nitems,
                                                                                         tl, tcount);
