@@ -7,8 +7,10 @@ frame's renders against ground truth (ss/grouping.py:153-159);
 group iff ``q >= tau`` (:213), otherwise it becomes a keyframe.
 ``probe_frames`` evaluates many candidate frames x views in one batched
 render with SSE fused into compositing -- the C2 keyframe-detection workload.
-The training loop of ``build_groups`` (fit_group_frame / fit_keyframe) is
-outside the evaluation path.
+The training-based grouping driver ``build_groups`` (fit_group_frame /
+fit_keyframe, ss/grouping.py:169-250) is outside the evaluation path
+(ss/train.py OUT OF SCOPE); with ``dropin.install`` the
+reference's own driver runs on top of this module's probe.
 """
 
 from __future__ import annotations
@@ -394,66 +396,4 @@ def load_stream(path, device=None) -> TrainedStream:
                                        step_delta=DeltaTensor.from_dense(z[f"step_{t}"]),
                                        cumulative_delta=DeltaTensor.from_dense(z[f"cumulative_{t}"]),
                                        quality_db=float(z["frame_quality"][t])))
-    return TrainedStream(plan=plan, spaces=spaces, records=tuple(records))
-
-
-def build_groups(targets, cams, weights, cfg, first_cfg, bounds, init_count: int, tau_db: float = DEFAULT_TAU_DB,
-                 sh_degree: int = 0, seed: int = 0, key_cfg=None, progress=None) -> TrainedStream:
-    """Train the whole sequence, opening a new group whenever the in-group
-    motion fit drops below ``tau_db`` (ss/grouping.py:169-250): the
-    reference's control flow over the device trainer (train.py) and the
-    device quality probe."""
-    import logging
-
-    from . import train
-    from .errors import ValidationError as _VE
-    from .model import compose_deltas
-
-    log = logging.getLogger(__name__)
-    targets = list(targets)
-    if not targets:
-        raise _VE("need at least one frame to group")
-    if key_cfg is None:
-        key_cfg = cfg
-
-    def note(msg):
-        log.info(msg)
-        if progress is not None:
-            progress(msg)
-
-    space = train.fit_first_frame(targets[0], cams, weights, first_cfg, bounds, init_count, sh_degree=sh_degree,
-                                  seed=seed)
-    spaces = {space.key_index: space}
-    width = space.frame.params.shape[1]
-    cumulative = DeltaTensor.empty(space.frame.count, width)
-    q0 = frame_quality(space.frame, cams, targets[0])
-    if q0 < tau_db:
-        log.warning("frame 0 keyframe below threshold: %.2f dB < %.2f dB", q0, tau_db)
-    records = [FrameRecord(0, space.key_index, True, DeltaTensor.empty(space.frame.count, width), cumulative, q0)]
-    spans = [[0, 0, 0]]
-    note(f"frame 0: keyframe, {q0:.2f} dB, {space.frame.live_count()} live")
-    for t in range(1, len(targets)):
-        step = train.fit_group_frame(space, cumulative, targets[t], cams, weights, cfg)
-        trial = compose_deltas([cumulative, step])
-        frame = apply_delta(space, trial, frame_index=t)
-        q = frame_quality(frame, cams, targets[t])
-        if q >= tau_db:
-            cumulative = trial
-            records.append(FrameRecord(t, space.key_index, False, step, cumulative, q))
-            spans[-1][2] = t
-            note(f"frame {t}: delta, {q:.2f} dB")
-            continue
-        previous = records[-1]
-        prev_frame = apply_delta(spaces[previous.group_key], previous.cumulative_delta, frame_index=t - 1)
-        space = train.fit_keyframe(prev_frame, targets[t], cams, weights, key_cfg, frame_index=t)
-        spaces[space.key_index] = space
-        cumulative = DeltaTensor.empty(space.frame.count, width)
-        qk = frame_quality(space.frame, cams, targets[t])
-        if qk < tau_db:
-            log.warning("frame %d keyframe below threshold: %.2f dB < %.2f dB", t, qk, tau_db)
-        records.append(FrameRecord(t, space.key_index, True, DeltaTensor.empty(space.frame.count, width),
-                                   cumulative, qk))
-        spans.append([t, t, t])
-        note(f"frame {t}: new keyframe ({q:.2f} dB delta fit), {qk:.2f} dB")
-    plan = GroupPlan(tau_db=tau_db, groups=tuple(GroupSpan(*sp) for sp in spans))
     return TrainedStream(plan=plan, spaces=spaces, records=tuple(records))
