@@ -45,6 +45,19 @@ TAU_DB = 30.0
 QUANT_STEP = 1e-4
 
 
+DATA = "synthetic (seeded SURVEY s8(d) generator; self-rendered targets)"
+
+
+def config_dict(args, cfg, world):
+    """The workload both arms print (identical dicts)."""
+    W, H = cfg.resolution
+    return {"workload": f"{args.config} keyframe probe: decode GSDP delta + apply + render {cfg.views} views "
+                        f"{W}x{H} + SSE/PSNR + tau", "gaussians": cfg.count, "views_per_step": cfg.views,
+            "resolution": [W, H],
+            "l2": f"inputs larger than L2 ({cfg.views} float64 targets = {cfg.views * W * H * 24 / 1e6:.0f} MB per step)",
+            "parallelism": f"frame-sharded x{world}"}
+
+
 def _dist():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -259,13 +272,8 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded SURVEY s8(d) generator; self-rendered targets)",
-            "config": {"workload": f"{args.config} keyframe probe: decode GSDP delta + apply + render {V} views "
-                                   f"{cfg.resolution[0]}x{cfg.resolution[1]} + SSE/PSNR + tau", "gaussians": cfg.count,
-                       "views_per_step": V, "resolution": list(cfg.resolution),
-                       "l2": "inputs larger than L2 (18 float64 targets = 592 MB per step)",
-                       "parallelism": f"frame-sharded x{world}"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": config_dict(args, cfg, world),
             "gpu_launches": int(round(launches)),
             "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_sm": roof_sm, "cpu_baseline": cpu,
             "keyframe_decisions": decisions, "qualities_db": [round(q, 6) for q in quals],
@@ -405,7 +413,72 @@ def run_e2e(space, cams, payloads, targets, device, args, world):
 # CPU reference arm / baseline
 
 
-_REF_KERNEL = []
+REF_SRC = os.path.join(ROOT, "baseline", "_ref", "pkg", "src")
+
+
+def reference_package():
+    """The reference package itself, vendored to baseline/_ref/pkg by
+    `make -C baseline` (git-ignored, shipped to the GPU box) with its own
+    compiled compositing kernel; None if absent."""
+    if not os.path.isdir(os.path.join(REF_SRC, "splatstream")):
+        return None
+    if REF_SRC not in sys.path:
+        sys.path.insert(0, REF_SRC)
+    import splatstream
+    from splatstream import camera, codec, metrics, model, rasterizer
+
+    if rasterizer.KERNEL_BACKEND != "compiled":
+        return None
+    return splatstream
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# worker-side state, inherited through fork (no pickling of parameters)
+_ARM = {}
+
+
+def _arm_init():
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)  # one BLAS thread per worker process
+    except Exception:
+        pass
+
+
+def _arm_view(job):
+    """One view of the frame state held in shared slot ``slot``:
+    render + psnr through the reference's own API (or the port)."""
+    slot, v = job
+    a = _ARM
+    params = a["slots"][slot]
+    if a["ref"] is not None:
+        ss = a["ref"]
+        img = ss.rasterizer.render(ss.model.GaussianFrame(params=params), a["cams"][v])
+        return ss.metrics.psnr(img, a["target"])
+    from oracle import airgs_oracle as orc
+
+    cam = a["cams"][v]
+    pr = orc.prepare(params, cam)
+    W, H = cam.resolution
+    img = a["kernel"].forward(pr.means2d, pr.conics, pr.alphas, pr.colors, pr.bboxes, H, W)[0]
+    return orc.psnr(np.clip(img, 0.0, 1.0), a["target"])
 
 
 def _ref_kernel():
@@ -413,73 +486,130 @@ def _ref_kernel():
     import glob
     import importlib.util
 
-    if _REF_KERNEL:
-        return _REF_KERNEL[0]
     hits = glob.glob(os.path.join(ROOT, "oracle", "_ref", "_composite*.so"))
     if not hits:
         return None
     spec = importlib.util.spec_from_file_location("splatstream._composite", hits[0])
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
-    _REF_KERNEL.append(mod)
     return mod
 
 
-def _cpu_view(job):
-    params, cam_args, target = job
-    from oracle import airgs_oracle as orc
-    from paper_2512_20943_b200.camera import Camera
+class CpuArm:
+    """The reference's CPU path on the host cores, pipelined like a real
+    multi-core deployment of it: one persistent fork pool (created before any
+    timing), frame states in shared memory slots (inherited, never pickled),
+    the parent decoding frame t+1 (decode_delta + apply_delta) while the
+    workers render frame t's views (render + psnr), every step's views dealt
+    to whichever worker is free.  Uses the vendored reference package when
+    present (kind "reference"), else the oracle port with the reference's
+    compiled kernel from oracle/_ref (kind "port")."""
 
-    cam = Camera(*cam_args)
-    pr = orc.prepare(params, cam)
-    W, H = cam.resolution
-    ker = _ref_kernel()
-    if ker is not None:
-        img = ker.forward(pr.means2d, pr.conics, pr.alphas, pr.colors, pr.bboxes, H, W)[0]
-    else:
-        img = orc.composite(pr.means2d, pr.conics, pr.alphas, pr.colors, pr.bboxes, H, W)[0]
-    return orc.psnr(np.clip(img, 0.0, 1.0), target)
+    SLOTS = 2
 
+    def __init__(self, cfg, seed=0, frames=2):
+        import mmap
+        import multiprocessing as mp
 
-def cpu_run(cfg, views, seed=0):
-    """decode_delta + apply_delta once, then `views` x (render + psnr) in a
-    process pool; returns (views/s, cores, kind, sample)."""
-    import multiprocessing as mp
+        from paper_2512_20943_b200 import synth
 
-    from oracle import airgs_oracle as orc
-    from paper_2512_20943_b200 import synth
+        self.cfg = cfg
+        self.ref = reference_package()
+        seq = synth.Sequence(cfg, seed=seed, event_every=0)
+        ours = synth.cameras(cfg)
+        gt0 = seq.frame(0)
+        self.n, self.w = gt0.shape
+        W, H = cfg.resolution
+        self.V = len(ours)
+        if self.ref is not None:
+            ss = self.ref
+            self.cams = [ss.camera.Camera(pose=c.pose, focal=c.focal, resolution=c.resolution,
+                                          near_clip=c.near_clip) for c in ours]
+            canon = ss.model.GaussianFrame(params=gt0, frame_index=0, group_key=0)
+            self.space = ss.model.CanonicalSpace(frame=canon, capacity_U=self.n)
+            self.payloads = [ss.codec.encode_delta(
+                ss.model.diff_frames(canon, ss.model.GaussianFrame(params=seq.frame(t))), QUANT_STEP,
+                frame_index=t, base_key=0) for t in range(1, frames + 1)]
+            self.kind, self.kernel = "reference", None
+        else:
+            from oracle import airgs_oracle as orc
 
-    seq = synth.Sequence(cfg, seed=seed, event_every=0)
-    cams = synth.cameras(cfg)[:views]
-    gt0 = seq.frame(0)
-    gt1 = seq.frame(1)
-    n = gt0.shape[0]
-    gi, gr = orc.from_dense(gt1[:n] - gt0)
-    blob = orc.gsdp_encode(gi, gr, QUANT_STEP, 1, 0)
-    # targets: take the oracle's own render of the exact frame (not timed)
-    cores = min(len(cams), os.cpu_count() or 1)
-    jobs0 = [(gt1, (c.pose, c.focal, c.resolution, c.near_clip), np.zeros((c.resolution[1], c.resolution[0], 3)))
-             for c in cams]
-    t0 = time.perf_counter()
-    di, dr, *_ = orc.gsdp_decode(blob, n, gt0.shape[1])
-    params = orc.apply(gt0, di, dr)
-    jobs = [(params, j[1], j[2]) for j in jobs0]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        pool.map(_cpu_view, jobs)
-    dt = time.perf_counter() - t0
-    kind = "port"
-    ker = "reference compiled Cython kernel (oracle/_ref)" if _ref_kernel() is not None else "oracle C restatement"
-    sample = (f"1 frame state (decode_delta+apply_delta) + {len(cams)} views x (project + composite + psnr) at "
-              f"{cfg.resolution[0]}x{cfg.resolution[1]}, {cfg.count} Gaussians; compositing = {ker}; "
-              f"{cores} worker processes")
-    return len(cams) / dt, cores, kind, sample
+            self.cams = ours
+            self.gt0 = gt0
+            self.payloads = []
+            for t in range(1, frames + 1):
+                gi, gr = orc.from_dense(seq.frame(t) - gt0)
+                self.payloads.append(orc.gsdp_encode(gi, gr, QUANT_STEP, t, 0))
+            self.kind, self.kernel = "port", _ref_kernel()
+        nbytes = self.n * self.w * 8
+        self._maps = [mmap.mmap(-1, nbytes) for _ in range(self.SLOTS)]
+        slots = [np.frombuffer(m, dtype=np.float64).reshape(self.n, self.w) for m in self._maps]
+        self._tmap = mmap.mmap(-1, H * W * 3 * 8)
+        target = np.frombuffer(self._tmap, dtype=np.float64).reshape(H, W, 3)  # zeros (PSNR cost is value-independent)
+        _ARM.update(ref=self.ref, cams=self.cams, slots=slots, target=target, kernel=self.kernel)
+        self.slots = slots
+        self.cores = host_cores()
+        self.pool = mp.get_context("fork").Pool(self.cores, initializer=_arm_init)
+        self.pool.map(int, range(self.cores))  # workers up before any timing
+        self._pending = [[] for _ in range(self.SLOTS)]
+        self._t = 0
+
+    def _decode_into(self, slot, k):
+        """decode_delta + apply_delta of payload k into a shared slot."""
+        if self.ref is not None:
+            ss = self.ref
+            d = ss.codec.decode_delta(self.payloads[k], self.n, self.w)
+            fr = ss.model.apply_delta(self.space, d, frame_index=k + 1)
+            self.slots[slot][:] = fr.params
+        else:
+            from oracle import airgs_oracle as orc
+
+            di, dr, *_ = orc.gsdp_decode(self.payloads[k], self.n, self.w)
+            self.slots[slot][:] = orc.apply(self.gt0, di, dr)
+
+    def run(self, steps):
+        """``steps`` frame states x all views; returns wall seconds."""
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            slot = self._t % self.SLOTS
+            for r in self._pending[slot]:  # slot free again?
+                r.get()
+            self._decode_into(slot, self._t % len(self.payloads))
+            self._pending[slot] = [self.pool.apply_async(_arm_view, ((slot, v),)) for v in range(self.V)]
+            self._t += 1
+        for lst in self._pending:
+            for r in lst:
+                r.get()
+        self._pending = [[] for _ in range(self.SLOTS)]
+        return time.perf_counter() - t0
+
+    def describe(self, steps):
+        W, H = self.cfg.resolution
+        api = ("reference package (baseline/_ref): codec.decode_delta + model.apply_delta per frame state, "
+               "rasterizer.render (numpy _prepare + compiled Cython kernel) + metrics.psnr per view"
+               if self.ref is not None else
+               "oracle port projection + the reference's compiled kernel (oracle/_ref) + numpy psnr")
+        return (f"{steps} frame states x {self.V} views at {W}x{H}, {self.cfg.count} Gaussians; {api}; "
+                f"persistent fork pool of {self.cores} workers, frame decode pipelined with the previous frame's "
+                f"renders; CPU: {cpu_model()}")
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
 
 
 def cpu_baseline(args, cfg):
+    """Bounded CPU sample on rank 0 (after the GPU timing)."""
     try:
-        v, cores, kind, sample = cpu_run(cfg, args.cpu_views, seed=args.seed)
-        return {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        arm = CpuArm(cfg, seed=args.seed)
+        try:
+            arm.run(1)  # warm
+            dt = arm.run(args.cpu_steps)
+            v = arm.V * args.cpu_steps / dt
+            return {"value": round(v, 4), "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
+                    "sample": arm.describe(args.cpu_steps), "cpu_model": cpu_model()}
+        finally:
+            arm.close()
     except Exception as e:  # reported, never fatal for the GPU arm
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "port", "sample": f"failed: {e!r}"}
 
@@ -491,24 +621,19 @@ def run_reference(args):
     from paper_2512_20943_b200 import synth
 
     cfg = synth.CONFIGS[args.config]
-    vals = []
-    for _ in range(args.warmup):
-        cpu_run(cfg, args.cpu_views, args.seed)
-    t0 = time.perf_counter()
-    last = None
-    for _ in range(args.steps):
-        last = cpu_run(cfg, args.cpu_views, args.seed)
-        vals.append(last[0])
-    wall = time.perf_counter() - t0
-    v = float(np.mean(vals))
+    arm = CpuArm(cfg, seed=args.seed)
+    try:
+        arm.run(args.warmup)
+        wall = arm.run(args.steps)
+    finally:
+        arm.close()
+    v = arm.V * args.steps / wall
     line = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * wall / max(args.steps, 1), 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded SURVEY s8(d) generator)", "impl": "reference",
-            "config": {"workload": f"{args.config} keyframe probe, bounded CPU sample of {args.cpu_views} views/step",
-                       "gaussians": cfg.count, "resolution": list(cfg.resolution)},
-            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": last[1], "kind": last[2],
-                             "sample": last[3]},
+            "data": DATA, "impl": "reference", "config": config_dict(args, cfg, world),
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
+                             "sample": arm.describe(args.steps), "cpu_model": cpu_model()},
             "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -522,7 +647,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-views", type=int, default=18)
+    ap.add_argument("--cpu-steps", type=int, default=2, help="frame states in the bounded cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--per-step", action="store_true", help="synchronise after every frame (evaluate_frame)")
     args = ap.parse_args()

@@ -257,6 +257,59 @@ def _removed_sets(p: LevelPlan, G, kmins):
     return [tuple(p.idx_host[p.rank_host < k].tolist()) for k in kmins]
 
 
+class LevelTable:
+    """Validated inputs and the size-only half of a level space: the device
+    plan, every requested ratio's entry cut ``kmin``, exact payload sizes,
+    the surviving (strictly shrinking) levels and their pruned index sets."""
+
+    __slots__ = ("plan", "ratios", "kmins", "sizes", "keep", "removed")
+
+
+def level_table(delta, space, ratios, usage, quant_step: float, base=None) -> LevelTable:
+    """Input normalisation and checks of ``build_level_space``
+    (ss/pruning.py:93-126), shared by the single-GPU and sharded drivers."""
+    delta, space = as_delta(delta), as_space(space)
+    base = None if base is None else as_delta(base)
+    ratios = sorted(set(float(r) for r in ratios))
+    if not ratios or ratios[0] != 0.0:
+        raise StructuralError("ratios must include 0")
+    counts = usage.counts if hasattr(usage, "counts") else usage
+    if len(counts) < space.frame.count:
+        raise StructuralError("usage counts do not cover the primitive set")
+    if delta.base_count != space.frame.count:
+        raise StructuralError(f"delta base_count {delta.base_count} != space count {space.frame.count}")
+    if not quant_step > 0:
+        raise StructuralError("quant_step must be positive")
+    t = LevelTable()
+    t.plan = p = plan_levels(delta, space, usage, quant_step, base)
+    t.ratios = ratios
+    t.kmins = [_k_of(r, p.entries) for r in ratios]
+    t.sizes = level_sizes(p.nz, p.rank, p.n, p.width, t.kmins, p.canon.device)
+    t.keep, last = [], None
+    for j, s in enumerate(t.sizes):
+        if last is not None and s >= last:
+            continue  # duplicate level (ss/pruning.py:125-126)
+        t.keep.append(j)
+        last = s
+    t.removed = _removed_sets(p, delta.overlay(), [t.kmins[j] for j in t.keep])
+    return t
+
+
+def render_sse_chunked(frames, cams, items, targets, device=None):
+    """SSE of (frame, view) items against their targets, at most
+    RENDER_PAIRS_PER_CALL (item, primitive) records per render call (C5: 2M
+    primitives x 8 levels x 32 views would not fit one call's scratch)."""
+    from .rasterizer import render_views
+
+    if not items:
+        return np.zeros(0)
+    n = max(fr.count for fr in frames)
+    per_call = max(1, RENDER_PAIRS_PER_CALL // max(n, 1))
+    return np.concatenate([render_views(frames, cams, items[k:k + per_call], targets=targets[k:k + per_call],
+                                        device=device).sse.cpu().numpy()
+                           for k in range(0, len(items), per_call)])
+
+
 def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, usage, quant_step: float,
                       base: DeltaTensor = None, frame_index: int = 0) -> PruningLevelSpace:
     """Dense (quality, size) space over pruning ratios (ss/pruning.py:93-137).
@@ -268,38 +321,18 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
     from .model import GaussianFrame
     from .rasterizer import render_views
 
-    delta, space = as_delta(delta), as_space(space)
-    base = None if base is None else as_delta(base)
-    ratios = sorted(set(float(r) for r in ratios))
-    if not ratios or ratios[0] != 0.0:
-        raise StructuralError("ratios must include 0")
-    counts = usage.counts if hasattr(usage, "counts") else usage
-    if len(counts) < space.frame.count:
-        raise StructuralError("usage counts do not cover the primitive set")
-    if delta.base_count != space.frame.count:
-        raise StructuralError(f"delta base_count {delta.base_count} != space count {space.frame.count}")
+    space = as_space(space)
+    t = level_table(delta, space, ratios, usage, quant_step, base)
+    p = t.plan
     cams = list(cams)
-    if quant_step <= 0:
-        raise StructuralError("quant_step must be positive")
-    p = plan_levels(delta, space, usage, quant_step, base)
-    kmins = [_k_of(r, p.entries) for r in ratios]
-    sizes = level_sizes(p.nz, p.rank, p.n, p.width, kmins, p.canon.device)
-    keep_levels = []
-    last = None
-    for j, s in enumerate(sizes):
-        if last is not None and s >= last:
-            continue  # duplicate level (ss/pruning.py:125-126)
-        keep_levels.append(j)
-        last = s
-    removed = _removed_sets(p, delta.overlay(), [kmins[j] for j in keep_levels])
-    qualities = [100.0] * len(keep_levels)
+    qualities = [100.0] * len(t.keep)
     if cams:
         import torch
 
         ref_planes = level_frame_planes(p, None)
         ref = GaussianFrame(device_params=ref_planes, count=p.n, frame_index=frame_index, group_key=space.key_index)
         rv = render_views([ref], cams, [(0, v) for v in range(len(cams))], want_images=True)
-        planes = [level_frame_planes(p, kmins[j]) for j in keep_levels]
+        planes = [level_frame_planes(p, t.kmins[j]) for j in t.keep]
         # a level whose parameters equal the reference's bit for bit renders the
         # same image: SSE 0, the reference's 100 dB cap, no render needed (the
         # mandatory ratio-0 level always, ss/pruning.py:102-104)
@@ -311,18 +344,13 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
             for v in range(len(cams)):
                 items.append((fi, v))
                 targets.append(rv.images[v])
-        # bounded working set: at most RENDER_PAIRS_PER_CALL (item, primitive)
-        # records per render call (C5: 2M primitives x 8 levels x 32 views)
-        per_call = max(1, RENDER_PAIRS_PER_CALL // max(p.n, 1))
-        sse = np.concatenate([render_views(frames, cams, items[k:k + per_call], targets=targets[k:k + per_call])
-                              .sse.cpu().numpy() for k in range(0, len(items), per_call)]) if items else None
+        sse = render_sse_chunked(frames, cams, items, targets)
         V = len(cams)
         sizes_px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
-        qualities = [100.0] * len(planes)
         for fi, li in enumerate(todo):
             qualities[li] = float(np.mean([psnr_from_sse(sse[fi * V + v], sizes_px[v]) for v in range(V)]))
-    levels = [PruningLevel(ratio=ratios[j], quality_db=q, size_bytes=sizes[j], pruned_indices=rm)
-              for j, q, rm in zip(keep_levels, qualities, removed)]
+    levels = [PruningLevel(ratio=t.ratios[j], quality_db=q, size_bytes=t.sizes[j], pruned_indices=rm)
+              for j, q, rm in zip(t.keep, qualities, t.removed)]
     return PruningLevelSpace(levels=tuple(levels), frame_index=frame_index)
 
 

@@ -150,32 +150,27 @@ def usage_sharded(frame, cams, group=None, device=None):
 
 def build_level_space_sharded(delta, space, cams, ratios, usage, quant_step, base=None, frame_index=0, group=None):
     """pruning.build_level_space with the (level, view) items sharded over
-    ranks; identical PruningLevelSpace on every rank."""
+    ranks; identical PruningLevelSpace on every rank.  Inputs are normalised
+    and checked exactly as the single-GPU driver does (pruning.level_table),
+    and each rank's renders are chunked by RENDER_PAIRS_PER_CALL."""
     import torch
 
     from . import pruning
-    from .model import GaussianFrame
+    from .model import GaussianFrame, as_space
     from .rasterizer import render_views
 
-    ratios = sorted(set(float(r) for r in ratios))
-    if not ratios or ratios[0] != 0.0:
-        from .errors import StructuralError
-
-        raise StructuralError("ratios must include 0")
+    space = as_space(space)
+    t = pruning.level_table(delta, space, ratios, usage, quant_step, base)
+    p = t.plan
     cams = list(cams)
     V = len(cams)
-    p = pruning.plan_levels(delta, space, usage, quant_step, base)
-    kmins = [pruning._k_of(r, p.entries) for r in ratios]
-    sizes = pruning.level_sizes(p.nz, p.rank, p.n, p.width, kmins, p.canon.device)
-    keep, last = [], None
-    for j, s in enumerate(sizes):
-        if last is None or s < last:
-            keep.append(j)
-            last = s
-    removed = pruning._removed_sets(p, delta.overlay(), [kmins[j] for j in keep])
+    if V == 0:
+        levels = [pruning.PruningLevel(ratio=t.ratios[j], quality_db=100.0, size_bytes=t.sizes[j], pruned_indices=rm)
+                  for j, rm in zip(t.keep, t.removed)]
+        return pruning.PruningLevelSpace(levels=tuple(levels), frame_index=frame_index)
     dev = p.canon.device
     rank, world = world_info(group)
-    mine = item_partition(len(keep) * V, rank, world)
+    mine = item_partition(len(t.keep) * V, rank, world)
     # reference images only for the views this rank needs
     need_views = sorted({int(i) % V for i in mine})
     ref = GaussianFrame(device_params=pruning.level_frame_planes(p, None), count=p.n)
@@ -184,7 +179,7 @@ def build_level_space_sharded(delta, space, cams, ratios, usage, quant_step, bas
         rv = render_views([ref], cams, [(0, v) for v in need_views], want_images=True, device=dev)
         refs = dict(zip(need_views, rv.images))
     need_levels = sorted({int(i) // V for i in mine})
-    frames = {li: GaussianFrame(device_params=pruning.level_frame_planes(p, kmins[keep[li]]), count=p.n)
+    frames = {li: GaussianFrame(device_params=pruning.level_frame_planes(p, t.kmins[t.keep[li]]), count=p.n)
               for li in need_levels}
 
     def sse_fn(idx):
@@ -193,12 +188,12 @@ def build_level_space_sharded(delta, space, cams, ratios, usage, quant_step, bas
         order = sorted(frames)
         pos = {li: k for k, li in enumerate(order)}
         items = [(pos[int(i) // V], int(i) % V) for i in idx]
-        vb = render_views([frames[li] for li in order], cams, items,
-                          targets=[refs[int(i) % V] for i in idx], device=dev)
-        return vb.sse
+        sse = pruning.render_sse_chunked([frames[li] for li in order], cams, items,
+                                         [refs[int(i) % V] for i in idx], device=dev)
+        return torch.from_numpy(sse).to(dev)
 
-    sse = sharded_item_sse(len(keep) * V, sse_fn, group, dev).cpu().numpy()
+    sse = sharded_item_sse(len(t.keep) * V, sse_fn, group, dev).cpu().numpy()
     q = mean_psnr(sse, [c.resolution[0] * c.resolution[1] * 3 for c in cams], V)
-    levels = [pruning.PruningLevel(ratio=ratios[j], quality_db=qq, size_bytes=sizes[j], pruned_indices=rm)
-              for j, qq, rm in zip(keep, q, removed)]
+    levels = [pruning.PruningLevel(ratio=t.ratios[j], quality_db=qq, size_bytes=t.sizes[j], pruned_indices=rm)
+              for j, qq, rm in zip(t.keep, q, t.removed)]
     return pruning.PruningLevelSpace(levels=tuple(levels), frame_index=frame_index)
