@@ -254,12 +254,13 @@ def run_gpu(args):
     views = V * args.steps * world
     value = views / (ms_max / 1e3)
 
-    # ---- roofline of the dominant kernel (k_compositeN), timed live above
-    roof = roofline(space, cams, payloads, ktime, ms_max / args.steps)
-    # ---- its compute-side roofline: algorithmic fp64 work of the reference loop
-    # (diagnostic counting pass over the timed frames, untimed)
+    # ---- compute-side roofline of k_compositeN: algorithmic fp64 work of the
+    # reference loop (diagnostic counting pass over the timed frames, untimed)
+    k_ms = ktime["composite_ms"] / max(ktime["composite_launches"], 1)
     roof_sm = roofline_sm(eng, space, cams, payload_dev, payloads, targets, device,
-                          [i % nf for i in range(args.warmup, total)], roof["kernel_ms_per_launch"])
+                          [i % nf for i in range(args.warmup, total)], k_ms)
+    # ---- roofline of the dominant kernel and of every stage, timed live above
+    roof = roofline(space, cams, payloads, ktime, ms_max / args.steps, args.steps, roof_sm.pop("counts"))
 
     # ---- e2e through the public API from pinned host buffers
     e2e = run_e2e(space, cams, payloads, targets, device, args, world)
@@ -287,19 +288,27 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-def roofline(space, cams, payloads, ktime, step_ms):
-    """Roofline of the dominant kernel, k_compositeN (one launch per step =
-    all V views).  Algorithmic bytes per launch = V x (float64 target image
+def roofline(space, cams, payloads, ktime, step_ms, steps, counts):
+    """Roofline of the dominant kernel (k_compositeN, one launch per step =
+    all V views) plus every stage of the step (`stages`).
+
+    Composite algorithmic bytes per launch = V x (float64 target image
     P*3*8 + one 96-byte projected record per primitive, N*96): the data the
-    kernel must read at least once.  Its duration is the CUDA-event time of
-    the kernel itself on its launch stream inside the timed region.  The
-    kernel is bound by the shared-memory data pipe, so the HBM fraction is low
-    by construction; `sm` reports the compute side from the committed ncu
-    capture."""
+    kernel must read at least once.  Stage times are CUDA events on the
+    launching stream around each stage's kernels inside the timed region
+    (airgs_timing_stages).  Stage bytes: decode = SURVEY s8(d) "decode alone"
+    (read canonical + payload + write params, 2*N*W*8 + S); projection = read
+    params once + the records it writes (counted per view by the diagnostic
+    pass); binning = read ntiles/binrec/depth + write the list entries; sort =
+    read + write the list entries; SSE = the per-tile partials.  Binning and
+    sort traffic is implementation overhead in s8(d)'s accounting, reported
+    here so every stage has a measured GB/s."""
     hbm, which = _peaks()
     n = space.frame.count
+    W = space.frame.width
     V = len(cams)
     P = cams[0].resolution[0] * cams[0].resolution[1]
+    S = float(np.mean([len(p.data) for p in payloads]))
     per_launch = V * (P * 3 * 8 + n * 96)
     k_ms = ktime["composite_ms"] / max(ktime["composite_launches"], 1)
     achieved = per_launch / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
@@ -315,10 +324,37 @@ def roofline(space, cams, payloads, ktime, step_ms):
            "frac": round(achieved / hbm, 4) if achieved else None, "traffic": traffic,
            "peak_source": which, "kernel": "k_compositeN", "kernel_ms_per_launch": round(k_ms, 4),
            "kernel_share_of_step": round(k_ms / step_ms, 4) if step_ms else None,
-           "algorithmic_bytes_per_launch": int(per_launch),
-           "project_ms_per_launch": round(ktime["project_ms"] / max(ktime["project_launches"], 1), 4)}
+           "algorithmic_bytes_per_launch": int(per_launch)}
     if sm:
         out["sm"] = sm
+    pairs, recs = counts.get("tile_pairs", 0), counts.get("records", 0)
+    tiles = V * ((cams[0].resolution[0] + 15) // 16) * ((cams[0].resolution[1] + 15) // 16)
+    stage_bytes = {
+        "decode": 2 * n * W * 8 + S,
+        "project": n * W * 8 + recs * (96 + 8 + 8) + V * n * 4,
+        "bin": V * n * 4 + recs * 16 + pairs * 8 + tiles * 4,
+        "sort": 2 * pairs * 8 + tiles * 4,
+        "composite": per_launch,
+        "sse": tiles * 4 * 8,
+    }
+    stages = {}
+    for name, keys in (("decode", ("decode", "apply")), ("project", ("project",)), ("bin", ("bin",)),
+                       ("sort", ("sort",)), ("composite", ("composite",)), ("sse", ("sse",))):
+        ms = sum(ktime[f"{k}_ms"] for k in keys) / steps
+        st = {"ms_per_step": round(ms, 4), "share_of_step": round(ms / step_ms, 4) if step_ms else None,
+              "bytes_per_step": int(stage_bytes[name])}
+        if ms > 0:
+            gbs = stage_bytes[name] / (ms / 1e3) / 1e9
+            st.update({"achieved_gbs": round(gbs, 1), "frac": round(gbs / hbm, 4)})
+        stages[name] = st
+    stages["decode"]["bytes_definition"] = "SURVEY s8(d) decode alone: 2*N*W*8 + payload"
+    stages["composite"]["bytes_definition"] = "V*(P*3*8 + N*96): targets + one record per primitive"
+    dec_rast = sum(stages[k]["ms_per_step"] for k in stages)
+    out["stages"] = stages
+    out["decode_plus_rasterize"] = {
+        "ms_per_step": round(dec_rast, 4),
+        "algorithmic_bytes_per_step": int(stage_bytes["decode"] + per_launch),
+        "frac": round((stage_bytes["decode"] + per_launch) / (dec_rast / 1e3) / 1e9 / hbm, 4) if dec_rast else None}
     return out
 
 
@@ -358,7 +394,8 @@ def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames
     finally:
         eng.eval_stats(0)
     V = len(cams)
-    tot = {k: sum(counts[f][k] for f in frames_used) / len(frames_used) for k in ("bbox", "live", "contrib")}
+    tot = {k: sum(counts[f][k] for f in frames_used) / len(frames_used)
+           for k in ("bbox", "live", "contrib", "tile_pairs", "records")}
     ops = tot["live"] * OPS_PER_LIVE_EVAL + tot["contrib"] * OPS_PER_CONTRIB
     achieved = ops / (k_ms / 1e3) / 1e12 if k_ms else None
     return {"bound": "fp64", "kernel": "k_compositeN", "achieved": round(achieved, 3) if achieved else None,
@@ -367,7 +404,7 @@ def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames
             "note": "reference-work rate, not pipe utilisation: the fp32 candidate pass skips most of the "
                     "reference's fp64 work, so frac can exceed 1 (measured pipe use: roofline.sm)",
             "per_view": {k: int(round(v / V)) for k, v in tot.items()},
-            "algorithmic_ops_per_launch": int(ops), "decision_margins": margins}
+            "algorithmic_ops_per_launch": int(ops), "decision_margins": margins, "counts": tot}
 
 
 def run_e2e(space, cams, payloads, targets, device, args, world):

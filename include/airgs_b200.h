@@ -95,6 +95,13 @@ AIRGS_API int64_t airgs_launch_count(const airgs_ctx *ctx);
 AIRGS_API int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms,
                            int64_t *composite_launches, double *project_ms,
                            int64_t *project_launches);
+/* Per-stage device timing, the generalisation of airgs_timing: ms[k] /
+ * launches[k] for stage k in 0..nstages-1 = 0 compositing, 1 projection,
+ * 2 tile binning, 3 tile-list sort, 4 GSDP decode, 5 delta apply,
+ * 6 SSE reduction, 7 quantisation (payload sizes) -- CUDA events on the
+ * launching stream around each stage's kernels.  enable as for airgs_timing. */
+AIRGS_API int airgs_timing_stages(airgs_ctx *ctx, int32_t enable, double *ms, int64_t *launches,
+                                  int32_t nstages);
 
 /* Diagnostic evaluation counters (no reference equivalent; used by bench.py
  * for the algorithmic-work roofline).  While armed, renders
@@ -102,7 +109,10 @@ AIRGS_API int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms,
  * all (pixel, primitive) pairs of the reference's Gaussian-major loop
  * (ss/_composite.pyx:42-73): counts[0] = pairs inside the clipped bbox,
  * counts[1] = those evaluated before the pixel terminated (0.999*T <= 1/255),
- * counts[2] = contributing pairs (= summed usage).  Returns the counts since
+ * counts[2] = contributing pairs (= summed usage), counts[3] = (tile,
+ * primitive) entries of the binned tile lists, counts[4] = projected records
+ * written (primitives reaching a tile, summed over views); counts holds 5
+ * int64.  Returns the counts since
  * the last (re)arm; enable = 1 arms, 0 disarms, -1 only reads.  Synchronises. */
 AIRGS_API int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts);
 
@@ -189,6 +199,18 @@ AIRGS_API int airgs_render(airgs_ctx *ctx, const airgs_frame *frames, int32_t nf
                  const airgs_camera *cams, int32_t ncams,
                  const airgs_view_item *items, int32_t nitems,
                  double *sse, void *stream);
+
+/* Debug capture of one view's depth-ordered tile lists (the binning + sort
+ * stage that precedes compositing; SURVEY.md s8(c) tile keys): for every
+ * 16x16 tile g (row-major, tiles_x = ceil(w/16)), counts[g] = list length and
+ * ids[g*max_per_tile + k] = the k-th primitive index of its list in
+ * compositing order (entries beyond max_per_tile are not written).  A
+ * primitive is listed in tile g iff its clipped bbox overlaps g and so does
+ * the padded AABB of its weight-threshold ellipse; within a
+ * list the order is the reference's stable depth order
+ * (ss/rasterizer.py:126-127).  Device buffers; synchronises. */
+AIRGS_API int airgs_debug_tile_lists(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
+                                     int64_t max_per_tile, int32_t *counts, int32_t *ids, void *stream);
 
 /* The reference's pluggable compositing seam, ss/_composite.pyx:18-74
  * forward(means2d, conics, alphas, colors, bboxes, height, width):

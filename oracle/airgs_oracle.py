@@ -115,7 +115,7 @@ def sh_degree_of(width):
 
 class Prepared:
     __slots__ = ("order", "means2d", "conics", "alphas", "colors", "bboxes", "depth",
-                 "radius", "z_all", "alpha_all")
+                 "radius", "z_all", "alpha_all", "cov2d", "det")
 
 
 def prepare(params, cam):
@@ -186,6 +186,7 @@ def prepare(params, cam):
     c2 = dot3_fma(MC[:, 1, 0], MC[:, 1, 1], MC[:, 1, 2], M[:, 1, 0], M[:, 1, 1], M[:, 1, 2]) + COV_BLUR
     det = a2 * c2 - b2 * b2
     out.conics = np.stack([c2 / det, -b2 / det, a2 / det], axis=1)
+    out.cov2d, out.det = np.stack([a2, b2, c2], axis=1), det
     d = a2 - c2
     eig = 0.5 * (a2 + c2) + np.sqrt(np.maximum(0.25 * (d * d) + b2 * b2, 0.0))
     rad = RADIUS_SIGMA * np.sqrt(eig)
@@ -293,17 +294,81 @@ def tile_keys(bboxes, width, height, tile=TILE):
     SURVEY.md s8(c)): for primitive position p (depth rank) with a non-empty
     clipped bbox, emit key (tile_id << 32) | p for every tile its bbox
     overlaps, tile_id = ty * tiles_x + tx; keys sorted ascending."""
-    bb = np.asarray(bboxes, dtype=np.int64)
+    bb = np.asarray(bboxes, dtype=np.int64).reshape(-1, 4)
     tx_n = (width + tile - 1) // tile
-    keys = []
-    for p in range(bb.shape[0]):
-        x0, x1, y0, y1 = (int(v) for v in bb[p])
-        if x1 <= x0 or y1 <= y0:
-            continue
-        for ty in range(y0 // tile, (y1 - 1) // tile + 1):
-            for tx in range(x0 // tile, (x1 - 1) // tile + 1):
-                keys.append(((ty * tx_n + tx) << 32) | p)
-    return np.sort(np.array(keys, dtype=np.int64))
+    ne = (bb[:, 1] > bb[:, 0]) & (bb[:, 3] > bb[:, 2])
+    p = np.nonzero(ne)[0]
+    if p.size == 0:
+        return np.zeros(0, dtype=np.int64)
+    u0, u1 = bb[p, 0] // tile, (bb[p, 1] - 1) // tile
+    v0, v1 = bb[p, 2] // tile, (bb[p, 3] - 1) // tile
+    nu, nv = u1 - u0 + 1, v1 - v0 + 1
+    cnt = nu * nv
+    rep = np.repeat(np.arange(p.size), cnt)
+    j = np.arange(rep.size) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    tx = u0[rep] + j % nu[rep]
+    ty = v0[rep] + j // nu[rep]
+    return np.sort(((ty * tx_n + tx) << 32) | p[rep])
+
+
+def threshold_tile_ranges(pr, tile=TILE):
+    """Tile range of each prepared primitive under the B200 binning's
+    weight-threshold narrowing (restated from render.cu k_project /
+    rec_tile_range): a pixel can pass the reference's weight
+    test (_composite.pyx:53-60) only if e <= t = ln(alpha/EPS), and
+    min_dy e(dx, dy) = dx^2 / (2 Sxx), so |dx| > sqrt(2 t Sxx) rejects it.
+    The half-extents are padded outwards (relative and absolute, in fp64, then
+    cast to fp32 and padded again), and the clipped bbox is intersected with
+    the pixel centres inside them.  Returns int64 (k, 4) [u0, u1, v0, v1] and a
+    bool (k,) mask of primitives that reach at least one tile."""
+    a2, c2, det = pr.cov2d[:, 0], pr.cov2d[:, 2], pr.det
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = np.log(pr.alphas / EPS_CONTRIB) * 1.0002 + 2e-4
+        hx = np.sqrt(2.0 * np.maximum(t, 0.0) * (a2 + 1e-9 * a2)) * 1.0002 + 1e-3
+        hy = np.sqrt(2.0 * np.maximum(t, 0.0) * (c2 + 1e-9 * c2)) * 1.0002 + 1e-3
+    f32 = np.float32
+    ok_x = (det > 0) & np.isfinite(hx)
+    ok_y = (det > 0) & np.isfinite(hy)
+    hxf = np.where(ok_x, hx.astype(f32) * f32(1.0001), f32(1e30)).astype(f32)
+    hyf = np.where(ok_y, hy.astype(f32) * f32(1.0001), f32(1e30)).astype(f32)
+    bb = pr.bboxes
+    xa, xb, ya, yb = bb[:, 0].copy(), bb[:, 1] - 1, bb[:, 2].copy(), bb[:, 3] - 1
+    mxf = (pr.means2d[:, 0] - 0.5).astype(f32)
+    myf = (pr.means2d[:, 1] - 0.5).astype(f32)
+    nx = hxf < f32(1e29)
+    ny = hyf < f32(1e29)
+    xa = np.where(nx, np.maximum(xa, np.ceil(mxf - hxf).astype(np.int64)), xa)
+    xb = np.where(nx, np.minimum(xb, np.floor(mxf + hxf).astype(np.int64)), xb)
+    ya = np.where(ny, np.maximum(ya, np.ceil(myf - hyf).astype(np.int64)), ya)
+    yb = np.where(ny, np.minimum(yb, np.floor(myf + hyf).astype(np.int64)), yb)
+    has = (bb[:, 1] > bb[:, 0]) & (bb[:, 3] > bb[:, 2]) & (xa <= xb) & (ya <= yb)
+    rng = np.stack([xa // tile, xb // tile, ya // tile, yb // tile], axis=1)
+    return rng, has
+
+
+def tile_lists_threshold(params, cam, tile=TILE):
+    """Expected per-tile lists of the B200 binning + sort stage for one view:
+    ``tile_keys`` over the reference's clipped bboxes,
+    restricted to the tiles of ``threshold_tile_ranges``, mapped back to
+    primitive indices.  Returns {tile_id: int64 array of primitive indices in
+    compositing order (prep.order position ascending)}."""
+    pr = prepare(params, cam)
+    ct = CamTerms(cam)
+    keys = tile_keys(pr.bboxes, ct.W, ct.H, tile)
+    rng, has = threshold_tile_ranges(pr, tile)
+    tx_n = (ct.W + tile - 1) // tile
+    tid = keys >> 32
+    pos = keys & 0xFFFFFFFF
+    tyy, txx = tid // tx_n, tid % tx_n
+    r = rng[pos]
+    keep = has[pos] & (txx >= r[:, 0]) & (txx <= r[:, 1]) & (tyy >= r[:, 2]) & (tyy <= r[:, 3])
+    tid, pos = tid[keep], pos[keep]
+    out = {}
+    if tid.size:
+        cuts = np.nonzero(np.diff(tid))[0] + 1
+        for a, b in zip(np.r_[0, cuts], np.r_[cuts, tid.size]):
+            out[int(tid[a])] = pr.order[pos[a:b]]
+    return out
 
 
 def render_full(params, cam, pixel_major=False):
@@ -573,8 +638,10 @@ def prune(idx, rows, usage, ratio):
     return np.asarray(idx)[keep], np.asarray(rows)[keep], removed
 
 
-def level_space(gap, canonical, cams, ratios, usage, step, base=None):
-    """-> list of (ratio, quality_db, size_bytes, removed) (ss/pruning.py:93-137)."""
+def level_plan(gap, canonical, ratios, usage, step, base=None):
+    """The render-free half of build_level_space (ss/pruning.py:93-126):
+    returns (reference params, [(ratio, size_bytes, removed, level params)])
+    for the surviving (strictly shrinking) levels."""
     ratios = sorted(set(float(r) for r in ratios))
     if not ratios or ratios[0] != 0.0:
         raise OracleError("StructuralError", "ratios must include 0")
@@ -594,7 +661,6 @@ def level_space(gap, canonical, cams, ratios, usage, step, base=None):
         return np.asarray(i)[keep], q[keep].astype(np.float64) * step
 
     ref = recon(*dec(gi, gr))
-    ref_imgs = [render(ref, c) for c in cams]
     out = []
     last = None
     for r in ratios:
@@ -602,11 +668,17 @@ def level_space(gap, canonical, cams, ratios, usage, step, base=None):
         size = gsdp_size(ki, kr, step)
         if last is not None and size >= last:
             continue
-        fr = recon(*dec(ki, kr))
-        q = float(np.mean([psnr(render(fr, c), im) for c, im in zip(cams, ref_imgs)]))
-        out.append((r, q, size, removed))
+        out.append((r, size, removed, recon(*dec(ki, kr))))
         last = size
-    return out
+    return ref, out
+
+
+def level_space(gap, canonical, cams, ratios, usage, step, base=None):
+    """-> list of (ratio, quality_db, size_bytes, removed) (ss/pruning.py:93-137)."""
+    ref, plan = level_plan(gap, canonical, ratios, usage, step, base)
+    ref_imgs = [render(ref, c) for c in cams]
+    return [(r, float(np.mean([psnr(render(fr, c), im) for c, im in zip(cams, ref_imgs)])), size, removed)
+            for r, size, removed, fr in plan]
 
 
 def select_level(qualities, sizes, bandwidth_B, rate_R, beta=2.0):

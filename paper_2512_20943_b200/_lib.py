@@ -64,6 +64,8 @@ SIGNATURES = {
     "airgs_last_error": (ctypes.c_char_p, [vp]),
     "airgs_launch_count": (i64, [vp]),
     "airgs_timing": (ctypes.c_int, [vp, i32, c_double_p, c_i64_p, c_double_p, c_i64_p]),
+    "airgs_timing_stages": (ctypes.c_int, [vp, i32, c_double_p, c_i64_p, i32]),
+    "airgs_debug_tile_lists": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), ctypes.POINTER(CameraC), i64, vp, vp, vp]),
     "airgs_eval_stats": (ctypes.c_int, [vp, i32, c_i64_p]),
     "airgs_eval_margins": (ctypes.c_int, [vp, c_double_p]),
     "airgs_defer": (ctypes.c_int, [vp, i32, ctypes.POINTER(ctypes.c_uint32)]),
@@ -156,22 +158,29 @@ class Engine:
             raise exc(msg)
         return rc
 
+    STAGES = ("composite", "project", "bin", "sort", "decode", "apply", "sse", "quantize")
+
     def timing(self, enable=-1):
-        """Read (and optionally re-arm/reset) the per-kernel event timers:
-        returns dict(composite_ms, composite_launches, project_ms, project_launches)."""
-        cm, pm = ctypes.c_double(0), ctypes.c_double(0)
-        cl, pl = ctypes.c_int64(0), ctypes.c_int64(0)
-        self.lib.airgs_timing(self.ctx, int(enable), ctypes.byref(cm), ctypes.byref(cl), ctypes.byref(pm),
-                              ctypes.byref(pl))
-        return {"composite_ms": cm.value, "composite_launches": cl.value, "project_ms": pm.value,
-                "project_launches": pl.value}
+        """Read (and optionally re-arm/reset) the per-stage event timers:
+        returns {stage}_ms and {stage}_launches for every stage of
+        airgs_timing_stages."""
+        k = len(self.STAGES)
+        ms, n = (ctypes.c_double * k)(), (ctypes.c_int64 * k)()
+        self.lib.airgs_timing_stages(self.ctx, int(enable), ms, n, k)
+        out = {}
+        for j, name in enumerate(self.STAGES):
+            out[f"{name}_ms"] = ms[j]
+            out[f"{name}_launches"] = n[j]
+        return out
 
     def eval_stats(self, enable=-1):
         """Read (and optionally re-arm/reset) the diagnostic evaluation counters:
-        returns dict(bbox, live, contrib) (pairs of the reference's loop)."""
-        c = (ctypes.c_int64 * 3)()
+        returns dict(bbox, live, contrib) (pairs of the reference's loop) and
+        tile_pairs (binned (tile, primitive) list entries) and records (projected
+        records written)."""
+        c = (ctypes.c_int64 * 5)()
         self.call("airgs_eval_stats", int(enable), c)
-        return {"bbox": c[0], "live": c[1], "contrib": c[2]}
+        return {"bbox": c[0], "live": c[1], "contrib": c[2], "tile_pairs": c[3], "records": c[4]}
 
     MARGIN_KEYS = ("min_rel_weight_margin", "min_rel_termination_margin", "min_depth_gap_ulps", "depth_ties",
                    "min_bbox_floor_margin_px", "min_near_clip_margin", "min_rel_alpha_cull_margin")

@@ -71,6 +71,18 @@ extern "C" int64_t airgs_launch_count(const airgs_ctx *ctx) { return ctx ? ctx->
 
 extern "C" int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms, int64_t *composite_launches,
                             double *project_ms, int64_t *project_launches) {
+    double ms[airgs_ctx::kStages];
+    int64_t n[airgs_ctx::kStages];
+    const int rc = airgs_timing_stages(ctx, enable, ms, n, airgs_ctx::kStages);
+    if (rc) return rc;
+    if (composite_ms) *composite_ms = ms[kStageComposite];
+    if (composite_launches) *composite_launches = n[kStageComposite];
+    if (project_ms) *project_ms = ms[kStageProject];
+    if (project_launches) *project_launches = n[kStageProject];
+    return AIRGS_OK;
+}
+
+extern "C" int airgs_timing_stages(airgs_ctx *ctx, int32_t enable, double *ms, int64_t *launches, int32_t nstages) {
     if (!ctx) return AIRGS_E_INTERNAL;
     try {
         cudaSetDevice(ctx->device);
@@ -78,14 +90,17 @@ extern "C" int airgs_timing(airgs_ctx *ctx, int32_t enable, double *composite_ms
     } catch (...) {
         return AIRGS_E_CUDA;
     }
-    if (composite_ms) *composite_ms = ctx->composite_ms;
-    if (composite_launches) *composite_launches = ctx->composite_launches;
-    if (project_ms) *project_ms = ctx->project_ms;
-    if (project_launches) *project_launches = ctx->project_launches;
+    for (int k = 0; k < nstages; ++k) {
+        const bool in = k < airgs_ctx::kStages;
+        if (ms) ms[k] = in ? ctx->stage_ms[k] : 0.0;
+        if (launches) launches[k] = in ? ctx->stage_launches[k] : 0;
+    }
     if (enable >= 0) {  // (re)arm or disarm and reset the counters
         ctx->timing = enable != 0;
-        ctx->composite_ms = ctx->project_ms = 0.0;
-        ctx->composite_launches = ctx->project_launches = 0;
+        for (int k = 0; k < airgs_ctx::kStages; ++k) {
+            ctx->stage_ms[k] = 0.0;
+            ctx->stage_launches[k] = 0;
+        }
     }
     return AIRGS_OK;
 }
@@ -118,6 +133,10 @@ extern "C" int airgs_eval_stats(airgs_ctx *ctx, int32_t enable, int64_t *counts)
     if (int rc = stats_read(ctx, h)) return rc;
     if (counts)
         for (int k = 0; k < 3; ++k) counts[k] = (int64_t)h[k];
+    if (counts) {
+        counts[3] = (int64_t)h[airgs::kStatTilePairs];
+        counts[4] = (int64_t)h[airgs::kStatRecords];
+    }
     if (enable >= 0) {  // (re)arm or disarm and reset the counters
         if (enable && !ctx->d_stats &&
             cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * airgs::kStatSlots) != cudaSuccess) {

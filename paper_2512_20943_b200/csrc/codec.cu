@@ -494,7 +494,9 @@ extern "C" int airgs_gsdp_decode(airgs_ctx *ctx, const uint8_t *payload, int64_t
                                  double quant_step, int32_t width, int64_t base_count, double *rows, int64_t ld,
                                  uint8_t *present, int64_t *idx_out, int64_t *entries_out, void *stream) {
     return guarded(ctx, [&] {
+        cudaEvent_t t0 = rows ? ctx->time_begin((cudaStream_t)stream) : nullptr;
         gsdp_impl(ctx, payload, nbytes, entry_count, quant_step, width, base_count, rows, ld, present, idx_out,
                   entries_out, (cudaStream_t)stream);
+        ctx->time_end(t0, (cudaStream_t)stream, kStageDecode);
     });
 }

@@ -57,7 +57,9 @@ enum MarginSlot {
     kMarginBBox = 7,         // min distance of a bbox floor/ceil argument to an integer (px)
     kMarginNear = 8,         // min |z - near_clip|
     kMarginAlpha = 9,        // min |alpha - 1/255| / (1/255) (opacity cull)
-    kStatSlots = 10
+    kStatTilePairs = 10,     // (tile, primitive) list entries after binning (counter)
+    kStatRecords = 11,       // projected records written (primitives reaching >= 1 tile, per view)
+    kStatSlots = 12
 };
 
 enum DevFlag : unsigned int {

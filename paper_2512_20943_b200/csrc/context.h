@@ -17,25 +17,33 @@ struct airgs_ctx {
     std::vector<Buf> bufs;
     void *host = nullptr;
     size_t host_cap = 0;
-    // optional per-kernel timing: event pairs recorded around the dominant
-    // kernels on their stream, resolved lazily (no synchronisation in the hot path)
+    // optional per-stage timing: event pairs recorded around each stage's
+    // kernels on their stream, resolved lazily (no synchronisation in the hot
+    // path).  Stage ids: see airgs_timing_stages in airgs_b200.h.
+    static constexpr int kStages = 8;
     bool timing = false;
-    double composite_ms = 0.0, project_ms = 0.0;
-    int64_t composite_launches = 0, project_launches = 0;
+    double stage_ms[kStages] = {};
+    int64_t stage_launches[kStages] = {};
     struct Pending {
         cudaEvent_t a, b;
-        int kind;  // 0 composite, 1 project
+        int kind;
     };
     std::vector<Pending> pending;
     // optional evaluation counters (diagnostic compositing kernel): bbox, live
     // and contributing (pixel, primitive) evaluations, accumulated on device
     bool stats = false;
-    uint32_t bucket_cap = 512;
+    uint32_t bucket_cap = 512;  // tile bucket capacity (doubled after an overflow, up to the sort cap)
     // deferred checking (airgs_defer): calls skip their host synchronisations
     // and fold error flags into d_defer, read once when the mode is left
     bool defer = false;
-    unsigned int *d_defer = nullptr;  // tile bucket capacity (doubled after an overflow, up to the sort cap)
+    unsigned int *d_defer = nullptr;
     unsigned long long *d_stats = nullptr;
+    // debug capture of the depth-ordered tile lists (airgs_debug_tile_lists)
+    struct TileDump {
+        int32_t *counts = nullptr;  // [tiles] list lengths
+        int32_t *ids = nullptr;     // [tiles][max_per_tile] primitive indices in compositing order
+        int64_t max_per_tile = 0;
+    } dump;
     std::vector<cudaEvent_t> event_pool;
     cudaEvent_t take_event() {
         if (event_pool.empty()) {
@@ -47,7 +55,7 @@ struct airgs_ctx {
         event_pool.pop_back();
         return e;
     }
-    // record the start of a timed kernel; returns the start event (or null)
+    // record the start of a timed stage; returns the start event (or null)
     cudaEvent_t time_begin(cudaStream_t st) {
         if (!timing) return nullptr;
         cudaEvent_t e = take_event();
@@ -59,19 +67,16 @@ struct airgs_ctx {
         cudaEvent_t b = take_event();
         AIRGS_CUDA_TRY(cudaEventRecord(b, st));
         pending.push_back({a, b, kind});
-        if (pending.size() > 256) resolve_timing();
+        if (pending.size() > 1024) resolve_timing();
     }
     void resolve_timing() {
         for (auto &p : pending) {
             AIRGS_CUDA_TRY(cudaEventSynchronize(p.b));
             float ms = 0.f;
             AIRGS_CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
-            if (p.kind == 0) {
-                composite_ms += ms;
-                ++composite_launches;
-            } else {
-                project_ms += ms;
-                ++project_launches;
+            if (p.kind >= 0 && p.kind < kStages) {
+                stage_ms[p.kind] += ms;
+                ++stage_launches[p.kind];
             }
             event_pool.push_back(p.a);
             event_pool.push_back(p.b);
@@ -166,7 +171,20 @@ enum Slot : int {
     kSlotTFinal,
     kSlotBinRec,
     kSlotBinCount,
+    kSlotDebug,
     kSlotCount
+};
+
+// timed stages (airgs_timing_stages)
+enum Stage : int {
+    kStageComposite = 0,
+    kStageProject = 1,
+    kStageBin = 2,
+    kStageSort = 3,
+    kStageDecode = 4,
+    kStageApply = 5,
+    kStageSse = 6,
+    kStageQuantize = 7,
 };
 
 // Run fn() translating failures into status codes / messages on ctx.

@@ -285,6 +285,10 @@ __global__ void __launch_bounds__(kProjThreads, PROJ_MIN_BLOCKS) k_project(ProjA
         }
         if (active) a.ntiles[o] = nt;
         if (a.stats) margin_min(a.stats, kMarginBBox, bbm);
+        if (a.stats) {
+            const unsigned nm = __ballot_sync(0xffffffffu, need && nt > 0);
+            if ((threadIdx.x & 31) == 0 && nm) atomicAdd(a.stats + kStatRecords, (unsigned long long)__popc(nm));
+        }
         if (PROJ_STAGE_REC) {
             // the warp's 32 records leave as contiguous 16-byte chunks (each store
             // instruction writes 512 consecutive bytes instead of 32 scattered pieces)
@@ -938,6 +942,28 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs 
         __syncthreads();
         sort_one_slow_tile(a, a.slow_list[b], skey, sid);
     }
+}
+
+// Debug capture (airgs_debug_tile_lists): tile g's list length and its
+// primitive indices in compositing order (the low 32 bits of each entry).
+__global__ void __launch_bounds__(128) k_dump_tiles(TileLists tl, const uint32_t *__restrict__ tcount, int64_t Tt,
+                                                    int32_t *__restrict__ counts, int32_t *__restrict__ ids,
+                                                    int64_t max_per_tile) {
+    const int64_t g = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (g >= Tt) return;
+    const int n = tl.count(tcount, g);
+    const uint64_t *lst = tl.list(g);
+    if (lane == 0) counts[g] = n;
+    for (int k = lane; k < n && k < max_per_tile; k += 32) ids[g * max_per_tile + k] = (int32_t)(uint32_t)lst[k];
+}
+
+__global__ void __launch_bounds__(256) k_sum_lists(TileLists tl, const uint32_t *__restrict__ tcount, int64_t Tt,
+                                                   unsigned long long *out) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long v = g < Tt ? (unsigned long long)tl.count(tcount, g) : 0ull;
+    v = warp_reduce_sum(v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
 }
 
 // Diagnostic: depth-order margins of the sorted tile lists -- the smallest
@@ -1916,14 +1942,23 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         uint32_t *slow_list = ctx->scratch_t<uint32_t>(kSlotSlowTiles, (size_t)Tt);
         AIRGS_CUDA_TRY(cudaMemsetAsync(slow_n, 0, sizeof(unsigned int), st));
         TileSortArgs ta{tl, tile_count, L.d_tile_base, nitems, depth, L.stride, slow_list, slow_n, Tt};
+        cudaEvent_t t_sort = ctx->time_begin(st);
         k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
         // the exact block sort walks the device-side slow list (no host readback)
         k_sort_tiles_block<<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
         NL += 2;
         check_launch();
-        if (ctx->stats && ctx->d_stats) {  // diagnostic depth-order margins
-            k_depth_gaps<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta, ctx->d_stats);
+        ctx->time_end(t_sort, st, kStageSort);
+        if (ctx->dump.counts) {  // debug capture of the depth-ordered lists (airgs_debug_tile_lists)
+            k_dump_tiles<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(tl, tile_count, Tt, ctx->dump.counts,
+                                                                   ctx->dump.ids, ctx->dump.max_per_tile);
             ++NL;
+            check_launch();
+        }
+        if (ctx->stats && ctx->d_stats) {  // diagnostic depth-order margins, list entries
+            k_depth_gaps<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta, ctx->d_stats);
+            k_sum_lists<<<(unsigned)ceil_div(Tt, 256), 256, 0, st>>>(tl, tile_count, Tt, ctx->d_stats + kStatTilePairs);
+            NL += 2;
             check_launch();
         }
     }
@@ -2031,11 +2066,13 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         ++NL;
         check_launch();
     }
-    ctx->time_end(t_comp, st, 0);
+    ctx->time_end(t_comp, st, kStageComposite);
     if (sse && any_target) {
+        cudaEvent_t t_sse = ctx->time_begin(st);
         k_sse_items<<<nitems, kSseThreads, 0, st>>>(sse_tiles, L.d_tile_base, d_has, sse);
         ++NL;
         check_launch();
+        ctx->time_end(t_sse, st, kStageSse);
     }
     // small uploads travel as kernel parameters: nothing host-side must outlive the launches
 }
@@ -2061,6 +2098,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         }
         BinArgs ba{binrec, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, pad, bucket, cap, flags, L.stride,
                    index_order};
+        cudaEvent_t t_bin = ctx->time_begin(st);
         k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
         ++NL;
         if (kBinCountStride > 1) {
@@ -2068,6 +2106,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
             ++NL;
         }
         check_launch();
+        ctx->time_end(t_bin, st, kStageBin);
     }
     // usage counts are ADDED to the caller's arrays (airgs_b200.h): accumulate
     // this call's counts in zeroed scratch first, so that a redone call cannot
@@ -2292,7 +2331,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         ++NL;
         check_launch();
     }
-    ctx->time_end(t_proj, st, 1);
+    ctx->time_end(t_proj, st, kStageProject);
     bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags, binrec,
                       bwd ? &bwd->rec : nullptr);
     if (bwd) {
@@ -2884,6 +2923,31 @@ using namespace airgs;
 extern "C" int airgs_render(airgs_ctx *ctx, const airgs_frame *frames, int32_t nframes, const airgs_camera *cams,
                             int32_t ncams, const airgs_view_item *items, int32_t nitems, double *sse, void *stream) {
     return guarded(ctx, [&] { render_impl(ctx, frames, nframes, cams, ncams, items, nitems, sse, (cudaStream_t)stream); });
+}
+
+extern "C" int airgs_debug_tile_lists(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
+                                      int64_t max_per_tile, int32_t *counts, int32_t *ids, void *stream) {
+    return guarded(ctx, [&] {
+        if (max_per_tile <= 0 || !counts || !ids) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad tile dump buffers");
+        struct Reset {
+            airgs_ctx *c;
+            ~Reset() { c->dump = airgs_ctx::TileDump{}; }
+        } reset{ctx};
+        ctx->dump.counts = counts;
+        ctx->dump.ids = ids;
+        ctx->dump.max_per_tile = max_per_tile;
+        airgs_view_item it{0, 0, nullptr, nullptr, nullptr, nullptr};
+        const bool deferred = ctx->defer;
+        ctx->defer = false;  // checked call: an overflowing bucket is redone through scanned ranges
+        try {
+            render_impl(ctx, frame, 1, cam, 1, &it, 1, nullptr, (cudaStream_t)stream);
+        } catch (...) {
+            ctx->defer = deferred;
+            throw;
+        }
+        ctx->defer = deferred;
+        AIRGS_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    });
 }
 
 extern "C" int airgs_composite_forward(airgs_ctx *ctx, int64_t k, const double *means2d, const double *conics,

@@ -235,6 +235,36 @@ def compositing_orders(frame, cams, frozen_orders=None) -> list:
     return out
 
 
+def tile_lists(frame, cam, max_per_tile: int = 4096):
+    """Debug view of the binning + sort stage for one camera
+    (airgs_debug_tile_lists): returns ``(counts, lists)`` where ``counts`` is
+    int32[tiles_y, tiles_x] and ``lists[g]`` the primitive indices of 16x16
+    tile g (row-major) in compositing order."""
+    import ctypes
+
+    import torch
+
+    dev = dv.device_of(None)
+    eng = engine(dev)
+    p, n, w = _frame_planes(frame, dev)
+    if n == 0:
+        raise StructuralError("cannot render an empty frame")
+    fc = FrameC()
+    fc.params, fc.count, fc.ld, fc.width = p.data_ptr(), n, p.shape[1], w
+    cc = camera_struct(cam)
+    W, H = cam.resolution
+    tx, ty = (W + 15) // 16, (H + 15) // 16
+    counts = torch.zeros((tx * ty,), dtype=torch.int32, device=dev)
+    ids = torch.full((tx * ty * max_per_tile,), -1, dtype=torch.int32, device=dev)
+    eng.call("airgs_debug_tile_lists", ctypes.byref(fc), ctypes.byref(cc), int(max_per_tile), ptr(counts), ptr(ids),
+             eng.stream())
+    c = counts.cpu().numpy()
+    if c.size and int(c.max()) > max_per_tile:
+        raise ValueError(f"a tile list holds {int(c.max())} entries > max_per_tile={max_per_tile}")
+    flat = ids.view(tx * ty, max_per_tile).cpu().numpy()
+    return c.reshape(ty, tx), [flat[g, : c[g]].astype(np.int64) for g in range(tx * ty)]
+
+
 def render_forward(frame, cam, frozen_order=None):
     """Forward pass that records what backward needs (ss/rasterizer.py:248-257).
     Returns ``(image, state)``; ``image`` is the forward image (h, w, 3) (the
