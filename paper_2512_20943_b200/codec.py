@@ -333,7 +333,9 @@ def decode_delta_device(data, base_count: int = None, param_width: int = None, d
     """GSDP bytes -> device overlay.  Returns (DeltaTensor, idx tensor)."""
     import torch
 
-    data = data.data if isinstance(data, DeltaPayload) else bytes(data)
+    # a DeltaPayload of either package, or raw bytes
+    data = bytes(data.data) if hasattr(data, "data") and not isinstance(data, (bytes, bytearray, memoryview)) \
+        else bytes(data)
     _, _, entry_count, quant_step = parse_delta_header(data)
     dev = dv.device_of(device)
     pd = payload_dev if payload_dev is not None else _to_device_bytes(data, dev)

@@ -52,6 +52,11 @@ class RenderedImage:
     def __setattr__(self, k, v):
         raise AttributeError("RenderedImage is immutable")
 
+    def __array__(self, dtype=None, copy=None):
+        # np.asarray(image) is its pixels: reference helpers that accept
+        # "a RenderedImage or an array" (ss/metrics.py:23-26) take this one too
+        return self.pixels if dtype is None else self.pixels.astype(dtype)
+
 
 class UsageFrequency:
     """Per-primitive count of (pixel, view) pairs with perceptible weight."""

@@ -255,6 +255,16 @@ def test_dropin_installs_into_the_reference_package():
         assert ref_pruning.build_level_space is pruning.build_level_space
         assert ref_ras._kernels.forward.__func__ if hasattr(ref_ras._kernels.forward, "__func__") else True
         assert ref_ras.KERNEL_BACKEND == rasterizer.KERNEL_BACKEND
+        # from-imported aliases inside the reference's modules are rebound too
+        from paper_2512_20943_b200 import errors, model, streamsim
+
+        assert ref_sim.apply_delta is model.apply_delta and ref_sim.compose_deltas is model.compose_deltas
+        assert ref_pruning.apply_delta is model.apply_delta
+        assert sys.modules["splatstream.grouping"].apply_delta is model.apply_delta
+        assert ref_sim.step_frame is streamsim.step_frame
+        # the device path's exceptions are caught as the reference's classes
+        assert issubclass(errors.StructuralError, sys.modules["splatstream.errors"].StructuralError)
+        assert issubclass(errors.DecodeError, sys.modules["splatstream.errors"].SplatStreamError)
     finally:
         sys.path.remove("/root/reference/pkg/src")
         for k in [k for k in sys.modules if k == "splatstream" or k.startswith("splatstream.")]:
