@@ -6,22 +6,28 @@ Workload (configs[1], "N3DV-shaped"): 300k Gaussians, 18 views 1352x1014.
 One step = one frame of keyframe detection: decode that frame's GSDP delta
 payload, apply it to the canonical set, render all 18 views with SSE against
 the frame's 18 ground-truth images fused into compositing, PSNR per view,
-mean, and the tau = 30 dB decision.  Unit = evaluated views.
+mean, and the tau = 30 dB decision.  Unit = evaluated views.  The frames
+cycle through 8 distinct payload/target sets of a sequence with appearance
+events (12% new primitives at frames 4 and 8), so the window holds frames
+on both sides of tau.
 
 value : device-resident inputs (payload bytes and targets already in HBM),
-        the K frames through the pipelined batch probe
-        (grouping.probe_payloads_device: deferred checking, no host
+        the K frames through the pipelined probe (deferred checking, no host
         synchronisation between frames; --per-step synchronises per frame).
-e2e   : the same through the public API from pinned HOST buffers (payload
-        bytes + float64 target images copied H2D every step, qualities read
+e2e   : the same through the public streaming API from pinned HOST buffers
+        (payload bytes + float64 target images copied H2D every step,
+        overlapped with the previous frame on a copy stream; qualities read
         back D2H), timed inside the region.
-Multi-GPU (torchrun): weak scaling over frames -- each rank evaluates its
-own frames (all views), the per-frame qualities are all-gathered for the
-keyframe decisions.
+Multi-GPU (torchrun, one rank per GPU, NCCL): the K frames' frame-major
+(frame, view) items are split into contiguous blocks over the ranks
+(sharding.probe_payloads_sharded): every rank decodes only the frames its
+block touches and renders only its views; one NCCL all-gather of the per-view
+SSE gives every rank every frame's quality and keyframe decision (identical
+at any N).  The total work (K x 18 views) is fixed: strong scaling.
 
---impl reference: the CPU reference path (projection = oracle port, compositing
-= the reference's own compiled Cython kernel from oracle/_ref when present)
-on the host cores, same metric/config.
+--impl reference: the reference's own CPU path (the vendored reference
+package: decode_delta + apply_delta + render + psnr) on the host cores, same
+metric/config.
 """
 
 from __future__ import annotations
@@ -55,7 +61,8 @@ def config_dict(args, cfg, world):
                         f"{W}x{H} + SSE/PSNR + tau", "gaussians": cfg.count, "views_per_step": cfg.views,
             "resolution": [W, H],
             "l2": f"inputs larger than L2 ({cfg.views} float64 targets = {cfg.views * W * H * 24 / 1e6:.0f} MB per step)",
-            "parallelism": f"frame-sharded x{world}"}
+            "parallelism": f"(frame, view) items in contiguous blocks over {world} rank(s), NCCL all-gather of "
+                           f"per-view SSE"}
 
 
 def _dist():
@@ -137,8 +144,7 @@ def build_workload(cfg, frames, seed, device):
     from paper_2512_20943_b200 import codec, rasterizer, synth
     from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
 
-    seq = synth.Sequence(cfg, seed=seed, event_every=max(3, frames // 2) if frames > 3 else 0,
-                         event_fraction=0.02)
+    seq = synth.Sequence(cfg, seed=seed, event_every=4 if frames >= 4 else 0, event_fraction=0.12)
     cams = synth.cameras(cfg)
     gt0 = seq.frame(0)
     space = CanonicalSpace(GaussianFrame(params=gt0, frame_index=0, group_key=0), capacity_U=gt0.shape[0])
@@ -187,13 +193,14 @@ def run_gpu(args):
         import torch.distributed as dist
 
         backend = os.environ.get("AIRGS_BENCH_BACKEND", "nccl")  # gloo: exercise N>1 on a single GPU
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) in the run's log
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group(backend)
     cfg = synth.CONFIGS[args.config]
     total = args.warmup + args.steps
-    space, cams, payloads, targets = build_workload(cfg, min(total, args.frames), seed=args.seed + rank,
+    space, cams, payloads, targets = build_workload(cfg, min(total, args.frames), seed=args.seed,
                                                     device=device)
     eng = _lib.engine(device)
     payload_dev = [torch.frombuffer(bytearray(p.data), dtype=torch.uint8).to(device) for p in payloads]
@@ -206,9 +213,10 @@ def run_gpu(args):
             dist.barrier()
         torch.cuda.synchronize(device)
 
-    # ---- device-resident: the K frames through the pipelined batch probe
-    # (grouping.probe_payloads_device: no host synchronisation between frames)
-    from paper_2512_20943_b200.grouping import probe_payloads_device
+    # ---- device-resident: the K frames through the pipelined probe, (frame,
+    # view) items sharded over the ranks (sharding.probe_payloads_sharded:
+    # no host synchronisation between frames, one NCCL all-gather of SSE)
+    from paper_2512_20943_b200.sharding import probe_payloads_sharded
 
     quals = []
     nf = len(payloads)
@@ -217,15 +225,17 @@ def run_gpu(args):
         idx = [i % nf for i in range(lo, hi)]
         return [payloads[i] for i in idx], [payload_dev[i] for i in idx], [targets[i] for i in idx]
 
+    if args.per_step and world > 1:
+        raise SystemExit("--per-step is a single-GPU mode")
     if args.per_step:
         for i in range(args.warmup):
             evaluate_frame(space, cams, payload_dev[i % nf], payloads[i % nf].data, targets[i % nf], device)
     else:
-        probe_payloads_device(space, cams, *frames(0, args.warmup), tau_db=TAU_DB, device=device)
+        probe_payloads_sharded(space, cams, *frames(0, args.warmup), tau_db=TAU_DB, device=device)
     barrier()
     sampler = ClockSampler(local)
     sampler.start()
-    eng.timing(1)  # CUDA events around the compositing / projection kernels on their stream
+    eng.timing(1)  # CUDA events around every stage's kernels on their stream
     launches0 = eng.launches
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -235,8 +245,8 @@ def run_gpu(args):
             q, _ = evaluate_frame(space, cams, payload_dev[i % nf], payloads[i % nf].data, targets[i % nf], device)
             quals.append(q)
     else:
-        quals = [q for q, _ in probe_payloads_device(space, cams, *frames(args.warmup, total), tau_db=TAU_DB,
-                                                     device=device)]
+        quals = [q for q, _ in probe_payloads_sharded(space, cams, *frames(args.warmup, total), tau_db=TAU_DB,
+                                                      device=device)]
     ev1.record(stream)
     barrier()
     clocks = sampler.stop()
@@ -251,7 +261,7 @@ def run_gpu(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     V = len(cams)
-    views = V * args.steps * world
+    views = V * args.steps  # the whole job's views (strong scaling: fixed total work)
     value = views / (ms_max / 1e3)
 
     # ---- compute-side roofline of k_compositeN: algorithmic fp64 work of the
@@ -273,7 +283,7 @@ def run_gpu(args):
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
             "config": config_dict(args, cfg, world),
             "gpu_launches": int(round(launches)),
             "clocks": clocks, "e2e": e2e, "roofline": roof, "roofline_sm": roof_sm, "cpu_baseline": cpu,
@@ -408,13 +418,15 @@ def roofline_sm(eng, space, cams, payload_dev, payloads, targets, device, frames
 
 
 def run_e2e(space, cams, payloads, targets, device, args, world):
-    """Same metric through the public streaming API (grouping.probe_sequence)
-    from pinned host buffers: per step the frame's GSDP bytes and its 18
-    float64 target images are copied H2D (overlapped with the previous
-    frame's evaluation on a copy stream) and the qualities are read back."""
+    """Same metric through the public streaming API from pinned host buffers
+    (sharding.probe_sequence_sharded = grouping.probe_sequence with the
+    (frame, view) items split over the ranks): per step the frame's GSDP
+    bytes and its 18 float64 target images are copied H2D (each rank copies
+    its own items', overlapped with the previous frame's evaluation on a copy
+    stream) and the qualities come back D2H."""
     import torch
 
-    from paper_2512_20943_b200.grouping import probe_sequence
+    from paper_2512_20943_b200.sharding import probe_sequence_sharded
 
     stream = torch.cuda.current_stream(device)
     pool = min(4, len(targets))  # pinned host copies of a few frames' targets, used cyclically
@@ -423,15 +435,19 @@ def run_e2e(space, cams, payloads, targets, device, args, world):
     h2d = len(host_p[0].data) + sum(t.numel() * 8 for t in host_t[0])
     d2h = len(cams) * 8
     warm = min(args.warmup, 3)
-    probe_sequence(space, cams, [host_p[i % pool] for i in range(warm)], [host_t[i % pool] for i in range(warm)],
-                   device=device)
+    probe_sequence_sharded(space, cams, [host_p[i % pool] for i in range(warm)],
+                           [host_t[i % pool] for i in range(warm)], device=device)
     torch.cuda.synchronize(device)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     steps = args.steps
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    probe_sequence(space, cams, [host_p[i % pool] for i in range(steps)], [host_t[i % pool] for i in range(steps)],
-                   device=device)
+    probe_sequence_sharded(space, cams, [host_p[i % pool] for i in range(steps)],
+                           [host_t[i % pool] for i in range(steps)], device=device)
     ev1.record(stream)
     torch.cuda.synchronize(device)
     ms = ev0.elapsed_time(ev1)
@@ -441,9 +457,10 @@ def run_e2e(space, cams, payloads, targets, device, args, world):
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    views = len(cams) * steps * world
+    views = len(cams) * steps
     return {"value": round(views / (ms / 1e3), 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "api": "grouping.probe_sequence (copy stream overlapped)"}
+            "d2h_bytes_per_step": int(d2h),
+            "api": "sharding.probe_sequence_sharded -> grouping.probe_sequence_items (copy stream overlapped)"}
 
 
 # ---------------------------------------------------------------------------
@@ -667,7 +684,7 @@ def run_reference(args):
     v = arm.V * args.steps / wall
     line = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * wall / max(args.steps, 1), 2),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": DATA, "impl": "reference", "config": config_dict(args, cfg, world),
             "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
                              "sample": arm.describe(args.steps), "cpu_model": cpu_model()},

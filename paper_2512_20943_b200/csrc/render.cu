@@ -1346,6 +1346,11 @@ struct CompNShared {
     double2 exptab[kExpN * kExpRep];
 };
 
+#ifdef C2_COUNT
+// experiment builds only (tools/c2_counts.py): work counters of k_compositeN
+__device__ unsigned long long g_c2c[8];
+#endif
+
 template <bool USAGE, int NP>
 __global__ void __launch_bounds__(CompNGeom<NP>::kThreads, C2_MIN_BLOCKS)
 k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
@@ -1447,6 +1452,9 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             if (USAGE) sh.cnt[t] = 0;
         }
         __syncthreads();
+#ifdef C2_COUNT
+        if (threadIdx.x == 0) atomicAdd(&g_c2c[5], (unsigned long long)nb);
+#endif
         int ncomp = 0;
         if (!__all_sync(0xffffffffu, all_done())) {
             for (int c0 = 0; c0 < nb; c0 += 32) {
@@ -1517,6 +1525,22 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                 if (done[k]) wd[k] = 0;
                 wu |= wd[k];
             }
+#ifdef C2_COUNT
+            {
+                unsigned long long cand = 0;
+#pragma unroll
+                for (int k = 0; k < NP; ++k) cand += __popc(wd[k]);
+                const unsigned it = __popc(wu);
+                const unsigned long long sc = warp_reduce_sum(cand), si = warp_reduce_sum((unsigned long long)it);
+                const unsigned mx = __reduce_max_sync(0xffffffffu, it);
+                if (lane == 0) {
+                    atomicAdd(&g_c2c[0], sc);
+                    atomicAdd(&g_c2c[1], si);
+                    atomicAdd(&g_c2c[2], (unsigned long long)mx);
+                    atomicAdd(&g_c2c[4], (unsigned long long)min(kC2Chunk, ncomp - c));
+                }
+            }
+#endif
             // phase B: the union of the NP candidate sets in depth order
             const uint8_t *sid = &sh.sidx[w][c];
             for (; wu; wu &= wu - 1) {
@@ -1536,6 +1560,13 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                     ap = ap > kCompC[6] ? kCompC[6] : ap;
                     double x = ap * T[k];
                     const bool cp = ((wd[k] >> pos) & 1u) && x > kCompC[7];
+#ifdef C2_COUNT
+                    if (cp) atomicAdd(&g_c2c[3], 1ull);
+                    if ((wd[k] >> pos) & 1u) {
+                        if (kAlphaClamp * T[k] <= kEpsContrib) atomicAdd(&g_c2c[6], 1ull);  // already terminated
+                        else if (!cp) atomicAdd(&g_c2c[7], 1ull);  // alive, weight test fails
+                    }
+#endif
                     if (!USAGE) {
                         // branch-free: a non-contributing entry adds exact zeros, keeps T
                         x = cp ? x : 0.0;
@@ -2924,6 +2955,18 @@ extern "C" int airgs_render(airgs_ctx *ctx, const airgs_frame *frames, int32_t n
                             int32_t ncams, const airgs_view_item *items, int32_t nitems, double *sse, void *stream) {
     return guarded(ctx, [&] { render_impl(ctx, frames, nframes, cams, ncams, items, nitems, sse, (cudaStream_t)stream); });
 }
+
+#ifdef C2_COUNT
+extern "C" __attribute__((visibility("default"))) int airgs_c2_counts(unsigned long long *out, int reset) {
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, g_c2c, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_c2c, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 extern "C" int airgs_debug_tile_lists(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cam,
                                       int64_t max_per_tile, int32_t *counts, int32_t *ids, void *stream) {

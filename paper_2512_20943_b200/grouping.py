@@ -111,17 +111,14 @@ def probe_frames(frames, cams, targets, device=None) -> list:
     return [float(np.mean([psnr_from_sse(sse[f * V + v], px[v]) for v in range(V)])) for f in range(len(frames))]
 
 
-def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_DB, device=None):
-    """Keyframe detection over a sequence of frames of one group, streamed
-    from host memory: for frame t, decode its GSDP delta payload against the
-    group's canonical space, apply it, render every camera with SSE against
-    the frame's ground-truth images, and decide ``q < tau``.
-
-    ``payloads``: per frame GSDP bytes / DeltaPayload; ``targets``: per frame
-    a sequence of (h, w, 3) float64 host images (pinned torch tensors give
-    asynchronous copies).  Host->device copies of frame t+1 run on a copy
-    stream while frame t is evaluated (double buffering).  Returns a list of
-    (quality_db, is_keyframe) per frame."""
+def probe_sequence_items(space, cams, payloads, targets, items, device=None):
+    """Per-item SSE of (frame t, view v) items streamed from host memory: for
+    each frame that has items, its GSDP payload and the items' (h, w, 3)
+    float64 host targets (pinned torch tensors give asynchronous copies) are
+    copied H2D on a copy stream while the previous frame is evaluated (double
+    buffering), then the frame is decoded, applied and its items rendered
+    with SSE fused into compositing.  Returns a device float64 tensor in
+    ``items`` order.  ``targets[t][v]`` need only exist for listed items."""
     import torch
 
     from . import codec
@@ -131,38 +128,43 @@ def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_D
     space = as_space(space)
     dev = dv.device_of(device)
     cams = list(cams)
-    V = len(cams)
     n, w = space.frame.count, space.frame.width
     canon = space.frame.planes(dev)
-    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
-    used = [None, None]
-    ready = [None, None]
-    if len(payloads) != len(targets):
-        raise StructuralError("one target set per payload required")
-    datas = [payloads[t].data if hasattr(payloads[t], "data") else bytes(payloads[t]) for t in range(len(payloads))]
-    cap = max((len(d) for d in datas), default=1)
+    by_frame = {}
+    for k, (t, v) in enumerate(items):
+        by_frame.setdefault(int(t), []).append((k, int(v)))
+    order = list(by_frame)
+    datas = {t: (payloads[t].data if hasattr(payloads[t], "data") else bytes(payloads[t])) for t in order}
+    cap = max((len(d) for d in datas.values()), default=1)
     # double buffers allocated once: pinned payload staging (no per-frame cudaHostAlloc,
     # which synchronises the device) and device targets / payloads (no allocator churn)
-    pinned = [torch.empty((cap,), dtype=torch.uint8).pin_memory() for _ in range(2)]
-    dpay = [torch.empty((cap,), dtype=torch.uint8, device=dev) for _ in range(2)]
-    dtg = [[torch.empty((c.resolution[1], c.resolution[0], 3), dtype=torch.float64, device=dev) for c in cams]
-           for _ in range(2)]
+    pinned = [torch.empty((max(cap, 1),), dtype=torch.uint8).pin_memory() for _ in range(2)]
+    dpay = [torch.empty((max(cap, 1),), dtype=torch.uint8, device=dev) for _ in range(2)]
+    res = [(c.resolution[1], c.resolution[0], 3) for c in cams]
+    dtg = [{} for _ in range(2)]
+    used = [None, None]
+    ready = [None, None]
+    out = torch.zeros((len(items),), dtype=torch.float64, device=dev)
 
     def host_tensor(im):
         return im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im, dtype=np.float64))
 
-    def stage(t):
-        b = t % 2
+    def stage(k):
+        t = order[k]
+        b = k % 2
         data = datas[t]
-        host = [host_tensor(im) for im in targets[t]]
-        check_targets(host, cams)
         with torch.cuda.stream(copy):
             if used[b] is not None:
                 copy.wait_event(used[b])  # buffer b's previous frame is done
-            for d, h in zip(dtg[b], host):
-                d.copy_(h, non_blocking=True)
+            for _, v in by_frame[t]:
+                h = host_tensor(targets[t][v])
+                if tuple(h.shape) != res[v]:
+                    raise StructuralError("target resolution does not match camera")
+                if v not in dtg[b]:
+                    dtg[b][v] = torch.empty(res[v], dtype=torch.float64, device=dev)
+                dtg[b][v].copy_(h, non_blocking=True)
             if data:
                 pinned[b][: len(data)].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
                 dpay[b][: len(data)].copy_(pinned[b][: len(data)], non_blocking=True)
@@ -170,37 +172,61 @@ def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_D
             ev.record(copy)
         ready[b] = ev
 
-    out = []
-    if payloads:
+    if order:
         stage(0)
-    for t in range(len(payloads)):
-        b = t % 2
+    for k, t in enumerate(order):
+        b = k % 2
         comp.wait_event(ready[b])
-        if t + 1 < len(payloads):
-            stage(t + 1)
-        data, pd, tg = datas[t], dpay[b][: len(datas[t])], dtg[b]
-        delta, _ = codec.decode_delta_device(data, n, w, device=dev, payload_dev=pd)
+        if k + 1 < len(order):
+            stage(k + 1)
+        data = datas[t]
+        delta, _ = codec.decode_delta_device(data, n, w, device=dev, payload_dev=dpay[b][: len(data)])
         planes = apply_overlay(canon, n, delta.overlay(dev))
-        vb = render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for v in range(V)],
-                          targets=tg, device=dev)
+        lst = by_frame[t]
+        sse = render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for _, v in lst],
+                           targets=[dtg[b][v] for _, v in lst], device=dev).sse
+        out[torch.tensor([i for i, _ in lst], device=dev)] = sse
         u = torch.cuda.Event()
         u.record(comp)
         used[b] = u
-        sse = vb.sse.cpu().numpy()
-        q = float(np.mean([psnr_from_sse(sse[v], px[v]) for v in range(V)]))
+    return out
+
+
+def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_DB, device=None):
+    """Keyframe detection over a sequence of frames of one group, streamed
+    from host memory (probe_sequence_items over every (frame, view) item):
+    for frame t, decode its GSDP delta payload against the group's canonical
+    space, apply it, render every camera with SSE against the frame's
+    ground-truth images, and decide ``q < tau``.  Host->device copies of
+    frame t+1 overlap frame t's evaluation.  Returns a list of
+    (quality_db, is_keyframe) per frame."""
+    cams = list(cams)
+    V = len(cams)
+    if len(payloads) != len(targets):
+        raise StructuralError("one target set per payload required")
+    for tg in targets:
+        if len(tg) != V:
+            raise StructuralError("target image count does not match cameras")
+    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+    items = [(t, v) for t in range(len(payloads)) for v in range(V)]
+    host = probe_sequence_items(space, cams, payloads, targets, items, device).cpu().numpy()
+    out = []
+    for t in range(len(payloads)):
+        q = float(np.mean([psnr_from_sse(host[t * V + v], px[v]) for v in range(V)]))
         out.append((q, is_keyframe(q, tau_db)))
     return out
 
 
-def probe_payloads_device(space, cams, payloads, payload_devs, targets, tau_db: float = DEFAULT_TAU_DB,
-                          device=None):
-    """Keyframe probes of a batch of frames whose GSDP payloads and targets are
-    already in HBM, pipelined: every frame's decode -> apply -> render with
-    fused SSE is enqueued without host synchronisation (airgs_defer) and the
-    qualities are read once at the end.  If any call reports a problem (a
-    malformed payload, invalid parameters, a bucket overflow) the batch is
-    re-run frame by frame in checked mode, which raises the reference's exact
-    error or handles the overflow.  Returns [(quality_db, is_keyframe)]."""
+def probe_payload_items(space, cams, payloads, payload_devs, targets, items, device=None):
+    """Per-item SSE of (frame t, view v) items of a probe batch whose GSDP
+    payloads and targets are already in HBM: each frame that has items is
+    decoded and applied once, its items rendered with SSE fused into
+    compositing, all enqueued without host synchronisation (airgs_defer).  If
+    any call reports a problem (a malformed payload, invalid parameters, a
+    bucket overflow) the batch is re-run in checked mode, which raises the
+    reference's exact error or handles the overflow.  Returns a device
+    float64 tensor, one SSE per item in ``items`` order (``targets[t][v]``:
+    device (h, w, 3) float64; only the listed items' targets are read)."""
     import ctypes
 
     import torch
@@ -213,32 +239,51 @@ def probe_payloads_device(space, cams, payloads, payload_devs, targets, tau_db: 
     space = as_space(space)
     dev = dv.device_of(device)
     cams = list(cams)
-    V = len(cams)
     n, w = space.frame.count, space.frame.width
     canon = space.frame.planes(dev)
-    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
-    items = [(0, v) for v in range(V)]
-    datas = [p.data if hasattr(p, "data") else bytes(p) for p in payloads]
+    datas = {}
+    by_frame = {}
+    for k, (t, v) in enumerate(items):
+        by_frame.setdefault(int(t), []).append((k, int(v)))
+    for t in by_frame:
+        p = payloads[t]
+        datas[t] = p.data if hasattr(p, "data") else bytes(p)
+    out = torch.zeros((len(items),), dtype=torch.float64, device=dev)
 
-    def one(t):
-        delta, _ = codec.decode_delta_device(datas[t], n, w, device=dev, payload_dev=payload_devs[t])
-        planes = apply_overlay(canon, n, delta.overlay(dev))
-        return render_views([GaussianFrame(device_params=planes, count=n)], cams, items, targets=targets[t],
-                            device=dev).sse
+    def run():
+        for t, lst in by_frame.items():
+            delta, _ = codec.decode_delta_device(datas[t], n, w, device=dev, payload_dev=payload_devs[t])
+            planes = apply_overlay(canon, n, delta.overlay(dev))
+            sse = render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for _, v in lst],
+                               targets=[targets[t][v] for _, v in lst], device=dev).sse
+            out[torch.tensor([k for k, _ in lst], device=dev)] = sse
 
     eng = engine(dev)
     flags = ctypes.c_uint32(0)
     eng.call("airgs_defer", 1, ctypes.byref(flags))
     try:
-        sses = [one(t) for t in range(len(datas))]
+        run()
     finally:
         eng.call("airgs_defer", 0, ctypes.byref(flags))
     if flags.value:
-        sses = [one(t) for t in range(len(datas))]  # checked mode
-    host = torch.stack(sses).cpu().numpy() if sses else np.zeros((0, V))
+        run()  # checked mode
+    return out
+
+
+def probe_payloads_device(space, cams, payloads, payload_devs, targets, tau_db: float = DEFAULT_TAU_DB,
+                          device=None):
+    """Keyframe probes of a batch of frames whose GSDP payloads and targets are
+    already in HBM, pipelined (probe_payload_items over every (frame, view)
+    item; one host synchronisation for the whole batch).  Returns
+    [(quality_db, is_keyframe)]."""
+    cams = list(cams)
+    V = len(cams)
+    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+    items = [(t, v) for t in range(len(payloads)) for v in range(V)]
+    host = probe_payload_items(space, cams, payloads, payload_devs, targets, items, device).cpu().numpy()
     out = []
-    for t in range(len(datas)):
-        q = float(np.mean([psnr_from_sse(host[t][v], px[v]) for v in range(V)]))
+    for t in range(len(payloads)):
+        q = float(np.mean([psnr_from_sse(host[t * V + v], px[v]) for v in range(V)]))
         out.append((q, is_keyframe(q, tau_db)))
     return out
 

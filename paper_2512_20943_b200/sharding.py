@@ -43,16 +43,27 @@ def item_partition(n_items: int, rank: int, world: int) -> np.ndarray:
     return np.arange(rank, n_items, world, dtype=np.int64)
 
 
-def gather_ordered(local, n_items: int, rank: int, world: int, group=None, device=None):
-    """All-gather per-item float64 values computed round-robin into the
-    global item order.  ``local`` holds this rank's values in the order of
-    ``item_partition``.  Returns a float64 tensor of length n_items."""
+def block_partition(n_items: int, rank: int, world: int) -> np.ndarray:
+    """Contiguous blocks of the item order (balanced to +-1 item).  Over
+    frame-major (frame, view) items a rank touches ~n_frames/world + 1
+    frames, so per-frame work such as the delta decode is barely repeated."""
+    lo = (n_items * rank) // world
+    hi = (n_items * (rank + 1)) // world
+    return np.arange(lo, hi, dtype=np.int64)
+
+
+def gather_ordered(local, n_items: int, rank: int, world: int, group=None, device=None, partition=None):
+    """All-gather per-item float64 values into the global item order.
+    ``local`` holds this rank's values in the order of ``partition``
+    (default: round-robin ``item_partition``).  Returns a float64 tensor of
+    length n_items on every rank."""
     import torch
 
     if world == 1:
         return local
+    partition = partition or item_partition
     dist = _dist()
-    per = math.ceil(n_items / world)
+    per = math.ceil(n_items / world) + 1
     dev = device if device is not None else local.device
     buf = torch.zeros((per,), dtype=torch.float64, device=dev)
     buf[: local.numel()] = local
@@ -60,7 +71,7 @@ def gather_ordered(local, n_items: int, rank: int, world: int, group=None, devic
     dist.all_gather(parts, buf, group=group)
     out = torch.empty((n_items,), dtype=torch.float64, device=dev)
     for r in range(world):
-        idx = item_partition(n_items, r, world)
+        idx = partition(n_items, r, world)
         out[torch.from_numpy(idx).to(dev)] = parts[r][: idx.size]
     return out
 
@@ -127,6 +138,57 @@ def probe_frames_sharded(frames, cams, targets, group=None, device=None):
     sse = sharded_item_sse(len(frames) * V, sse_fn, group, dev)
     px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
     return mean_psnr(sse.cpu().numpy(), px, V)
+
+
+def probe_payloads_sharded(space, cams, payloads, payload_devs, targets, tau_db: float = 30.0, group=None,
+                           device=None):
+    """The pipelined device probe (grouping.probe_payload_items) of a batch
+    of frames with the frame-major (frame, view) items split into contiguous
+    blocks over the ranks: each rank decodes only the frames its block
+    touches and renders only its views; one NCCL all-gather of the per-item
+    SSE (8 bytes per view) gives every rank every frame's mean PSNR and
+    keyframe decision, identical at any world size.  ``targets[t][v]`` need
+    only exist for this rank's items.  Returns [(quality_db, is_keyframe)]."""
+    from . import device as dv
+    from .grouping import is_keyframe, probe_payload_items
+
+    dev = dv.device_of(device)
+    cams = list(cams)
+    V = len(cams)
+    n_items = len(payloads) * V
+    rank, world = world_info(group)
+    mine = block_partition(n_items, rank, world)
+    items = [(int(i) // V, int(i) % V) for i in mine]
+    if items:
+        local = probe_payload_items(space, cams, payloads, payload_devs, targets, items, dev)
+    else:
+        import torch
+
+        local = torch.zeros((0,), dtype=torch.float64, device=dev)
+    sse = gather_ordered(local, n_items, rank, world, group, dev, partition=block_partition).cpu().numpy()
+    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+    return [(q, is_keyframe(q, tau_db)) for q in mean_psnr(sse, px, V)]
+
+
+def probe_sequence_sharded(space, cams, payloads, targets, tau_db: float = 30.0, group=None, device=None):
+    """grouping.probe_sequence from host buffers with the frame-major
+    (frame, view) items split into contiguous blocks over the ranks: each
+    rank copies H2D only its own items' targets (and the payloads of the
+    frames its block touches), evaluates them, and one NCCL all-gather of the
+    per-item SSE gives every rank every frame's quality and decision."""
+    from . import device as dv
+    from .grouping import is_keyframe, probe_sequence_items
+
+    dev = dv.device_of(device)
+    cams = list(cams)
+    V = len(cams)
+    n_items = len(payloads) * V
+    rank, world = world_info(group)
+    mine = block_partition(n_items, rank, world)
+    local = probe_sequence_items(space, cams, payloads, targets, [(int(i) // V, int(i) % V) for i in mine], dev)
+    sse = gather_ordered(local, n_items, rank, world, group, dev, partition=block_partition).cpu().numpy()
+    px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+    return [(q, is_keyframe(q, tau_db)) for q in mean_psnr(sse, px, V)]
 
 
 def usage_sharded(frame, cams, group=None, device=None):

@@ -67,21 +67,34 @@ def _worker(rank, world, port, out_q):
             return torch.from_numpy(c)
 
         counts = sharding.sharded_usage(V, usage_fn)
-        out_q.put((rank, sorted(seen), sharded_sse.numpy(), q, counts.numpy()))
+        # the bench's split: contiguous blocks of the frame-major (frame, view) items
+        mine = sharding.block_partition(len(frames) * V, rank, world)
+        local = torch.tensor([float(np.sum((orc.render(frames[int(i) // V], cams[int(i) % V])
+                                            - targets[int(i) // V][int(i) % V]) ** 2)) for i in mine],
+                             dtype=torch.float64)
+        blocks = sharding.gather_ordered(local, len(frames) * V, rank, world, partition=sharding.block_partition)
+        out_q.put((rank, sorted(seen), sharded_sse.numpy(), q, counts.numpy(), blocks.numpy()))
     finally:
         dist.destroy_process_group()
 
 
 def test_partition_balanced_and_complete():
-    from paper_2512_20943_b200.sharding import item_partition
+    from paper_2512_20943_b200.sharding import block_partition, item_partition
 
-    for n in (1, 7, 18, 144, 13 * 8):
-        for world in (1, 2, 4, 8):
-            parts = [item_partition(n, r, world) for r in range(world)]
-            allidx = np.sort(np.concatenate(parts))
-            np.testing.assert_array_equal(allidx, np.arange(n))
-            sizes = [p.size for p in parts]
-            assert max(sizes) - min(sizes) <= 1
+    for fn in (item_partition, block_partition):
+        for n in (1, 7, 18, 144, 13 * 8, 20 * 18):
+            for world in (1, 2, 4, 8):
+                parts = [fn(n, r, world) for r in range(world)]
+                allidx = np.sort(np.concatenate(parts))
+                np.testing.assert_array_equal(allidx, np.arange(n))
+                sizes = [p.size for p in parts]
+                assert max(sizes) - min(sizes) <= 1
+    # blocks of frame-major (frame, view) items: a rank touches at most
+    # ceil(frames / world) + 1 frames (the per-frame decode is barely repeated)
+    for world in (2, 4, 8):
+        for r in range(world):
+            frames = {int(i) // 18 for i in block_partition(20 * 18, r, world)}
+            assert len(frames) <= -(-20 // world) + 1
 
 
 def test_gloo_world2_matches_single_process():
@@ -104,9 +117,10 @@ def test_gloo_world2_matches_single_process():
                         for i in range(len(frames) * V)])
     ref_q = sharding.mean_psnr(ref_sse, [48 * 40 * 3] * V, V)
     ref_counts = orc.render_with_usage(frames[0], cams)[1]
-    (r0, seen0, sse0, q0, c0), (r1, seen1, sse1, q1, c1) = res
+    (r0, seen0, sse0, q0, c0, b0), (r1, seen1, sse1, q1, c1, b1) = res
     assert sorted(seen0 + seen1) == list(range(len(frames) * V)) and not set(seen0) & set(seen1)
-    for sse, q, c in ((sse0, q0, c0), (sse1, q1, c1)):
+    for sse, q, c, b in ((sse0, q0, c0, b0), (sse1, q1, c1, b1)):
         np.testing.assert_array_equal(sse, ref_sse)  # same per-item numbers, global order
         assert q == ref_q  # identical decisions on every rank
         np.testing.assert_array_equal(c, ref_counts)  # exact integer all-reduce
+        np.testing.assert_array_equal(b, ref_sse)  # block partition gathers into the same order

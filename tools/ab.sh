@@ -7,5 +7,6 @@ for v in "$@"; do
   python -c "
 import json,sys; d=json.loads(open('gpurun_out/ab_$v.json').read().strip().splitlines()[-1])
 c=d.get('clocks',{})
-print('$v', d['value'], 'views/s  step ms', d['ms_per_step'], ' composite ms', d['roofline']['kernel_ms_per_launch'], ' project ms', d['roofline']['project_ms_per_launch'], ' q0', d['qualities_db'][0], ' sm_mhz', c.get('sm_mhz'), c.get('reasons'))" || tail -3 gpurun_out/ab_$v.err
+st=d['roofline']['stages']
+print('$v', d['value'], 'views/s  step ms', d['ms_per_step'], ' '.join('%s %.4f' % (k, v['ms_per_step']) for k, v in st.items()), ' q0', d['qualities_db'][0], ' sm_mhz', c.get('sm_mhz'), c.get('reasons'))" || tail -3 gpurun_out/ab_$v.err
 done
