@@ -165,12 +165,12 @@ def evaluate_frame(space, cams, payload_dev, payload_bytes, targets_dev, device)
     """One step: decode -> apply -> render+SSE (18 views) -> PSNR -> tau."""
     from paper_2512_20943_b200 import codec
     from paper_2512_20943_b200.metrics import psnr_from_sse
-    from paper_2512_20943_b200.model import GaussianFrame, apply_overlay
+    from paper_2512_20943_b200.model import GaussianFrame
     from paper_2512_20943_b200.rasterizer import render_views
 
     n = space.frame.count
-    delta, _ = codec.decode_delta_device(payload_bytes, n, space.frame.width, device=device, payload_dev=payload_dev)
-    planes = apply_overlay(space.frame.planes(device), n, delta.overlay(device))
+    planes = codec.decode_apply_device(payload_bytes, space.frame.planes(device), n, space.frame.width,
+                                       device=device, payload_dev=payload_dev)
     fr = GaussianFrame(device_params=planes, count=n)
     V = len(cams)
     vb = render_views([fr], cams, [(0, v) for v in range(V)], targets=targets_dev, device=device)

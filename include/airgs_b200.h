@@ -277,6 +277,19 @@ AIRGS_API int airgs_gsdp_decode(airgs_ctx *ctx, const uint8_t *payload, int64_t 
                       uint8_t *present, int64_t *idx_out, int64_t *entries_out,
                       void *stream);
 
+/* Fused decode_delta + apply_delta for the keyframe probe (ss/codec.py:217-248
+ * then ss/model.py:269-284): params_out (plane-major, width x ld, device) =
+ * canonical with rows[idx] += (double)q * quant_step for every entry of the
+ * GSDP payload, without materialising the dense overlay.  Single-pass varint
+ * decode (per-block counts, then each block numbers its varints and streams
+ * its entries' i32 values).  Bit-identical to airgs_gsdp_decode followed by
+ * airgs_delta_apply; malformed payloads take the exact decoder's path and
+ * return its status (AIRGS_E_DECODE / AIRGS_E_STRUCTURAL, same messages).
+ * Under airgs_defer the checks fold into the deferred word instead. */
+AIRGS_API int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, int64_t entry_count,
+                                      double quant_step, int32_t width, const double *canonical, int64_t count,
+                                      int64_t ld, double *params_out, void *stream);
+
 /* Position after the entry_count gap varints (sequential walk, reference
  * order); *err_out: 0 ok, 1 truncated varint, 2 varint too long.  Used to
  * infer param_width when the caller does not pin it (ss/codec.py:235-240). */

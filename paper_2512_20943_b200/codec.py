@@ -385,6 +385,27 @@ def _decode_call(eng, pd, data, entry_count, quant_step, width, base_count, dev,
     return ov, idx[:entry_count]
 
 
+def decode_apply_device(data, canon, n: int, width: int, device=None, payload_dev=None, out=None):
+    """decode_delta + apply_delta fused (airgs_gsdp_decode_apply): GSDP bytes
+    applied to the plane-major canonical parameters ``canon`` (width, ld) ->
+    a new (width, ld) device tensor, bit-identical to
+    ``apply_overlay(canon, n, decode_delta_device(data, n, width)[0].overlay())``
+    without the dense overlay."""
+    import torch
+
+    data = bytes(data.data) if hasattr(data, "data") and not isinstance(data, (bytes, bytearray, memoryview)) \
+        else bytes(data)
+    _, _, entry_count, quant_step = parse_delta_header(data)
+    dev = dv.device_of(device)
+    pd = payload_dev if payload_dev is not None else _to_device_bytes(data, dev)
+    if out is None:
+        out = torch.empty_like(canon)
+    eng = _engine(dev)
+    eng.call("airgs_gsdp_decode_apply", _ptr(pd), len(data), entry_count, float(quant_step), int(width),
+             _ptr(canon), int(n), int(canon.shape[1]), _ptr(out), eng.stream())
+    return out
+
+
 def decode_delta(payload, base_count: int = None, param_width: int = None) -> DeltaTensor:
     """Inverse of encode_delta (ss/codec.py:217-248); device-resident result."""
     return decode_delta_device(payload, base_count, param_width)[0]

@@ -391,9 +391,247 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
         throw ApiFailure(AIRGS_E_STRUCTURAL, "delta index " + std::to_string((long long)hbad) + " out of range");
 }
 
+// ---------------------------------------------------------------------------
+// Fused GSDP decode + apply (the probe path: decode_delta then apply_delta,
+// ss/codec.py:217-248 + ss/model.py:269-284, without the dense overlay).
+//
+//   k_copy_planes     params = canonical, 4 x 128-bit per thread per step
+//   k_gsdp_da_count   per 2048-byte block of the varint section: varints
+//                     ending in it and the sum of their gaps
+//   k_gsdp_da_rows    each block adds up the preceding blocks' totals (no
+//                     look-back chain), numbers its varints, prefix-sums the
+//                     gaps to indices, then the whole block streams its
+//                     entries' (entry, component) i32 values in order:
+//                     params[c][idx] = canonical[c][idx] + (double)q * step
+// Every check of the reference decoder is a flag (truncation, varint length,
+// index range, duplicate index); a flagged call is redone by the exact
+// decoder for the reference's error (or folded into the deferred word).
+
+constexpr int kDaThreads = 256;
+constexpr int kDaBytes = 8;                      // varint bytes per thread
+constexpr int kDaTile = kDaThreads * kDaBytes;   // per block
+
+__global__ void __launch_bounds__(256) k_copy_planes(const double2 *__restrict__ src, double2 *__restrict__ dst,
+                                                     int64_t n2) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < n2; i += 4 * stride) {
+        const double2 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
+        dst[i] = a;
+        dst[i + stride] = b;
+        dst[i + 2 * stride] = c;
+        dst[i + 3 * stride] = d;
+    }
+    for (; i < n2; i += stride) dst[i] = src[i];
+}
+
+// value of the varint that ends at section byte i (its terminator); sets
+// *len to its byte count (> 10: too long)
+__device__ __forceinline__ uint64_t varint_ending_at(const uint8_t *__restrict__ p, int64_t i, int *len,
+                                                     bool *big) {
+    int l = 1;
+    while (i - l >= 0 && (p[i - l] & 0x80) && l <= 10) ++l;
+    uint64_t v = 0;
+    bool b = false;
+    for (int k = 0; k < l && k < 10; ++k) {
+        const uint64_t x = p[i - l + 1 + k] & 0x7f;
+        if (k == 9 && x > 1) b = true;
+        v |= x << (7 * k);
+    }
+    *len = l;
+    *big = b;
+    return v;
+}
+
+struct DaAgg {
+    unsigned long long count, gsum;
+};
+
+__global__ void __launch_bounds__(kDaThreads)
+k_gsdp_da_count(const uint8_t *__restrict__ sec, int64_t V, DaAgg *__restrict__ agg) {
+    const int64_t lo = (int64_t)blockIdx.x * kDaTile + (int64_t)threadIdx.x * kDaBytes;
+    unsigned long long c = 0, g = 0;
+    for (int k = 0; k < kDaBytes; ++k) {
+        const int64_t i = lo + k;
+        if (i < V && !(sec[i] & 0x80)) {
+            int len;
+            bool big;
+            ++c;
+            g += varint_ending_at(sec, i, &len, &big);
+        }
+    }
+    c = warp_reduce_sum(c);
+    g = warp_reduce_sum(g);
+    __shared__ unsigned long long wc[kDaThreads / 32], wg[kDaThreads / 32];
+    if ((threadIdx.x & 31) == 0) {
+        wc[threadIdx.x >> 5] = c;
+        wg[threadIdx.x >> 5] = g;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tc = 0, tg = 0;
+        for (int w = 0; w < kDaThreads / 32; ++w) {
+            tc += wc[w];
+            tg += wg[w];
+        }
+        agg[blockIdx.x] = DaAgg{tc, tg};
+    }
+}
+
+__global__ void __launch_bounds__(kDaThreads)
+k_gsdp_da_rows(const uint8_t *__restrict__ payload, int64_t V, int64_t E, int W, double step, int64_t base_count,
+               const DaAgg *__restrict__ agg, const double *__restrict__ canon, double *__restrict__ out, int64_t ld,
+               unsigned int *flags, unsigned int *defer) {
+    const uint8_t *sec = payload + 24;
+    __shared__ int64_t sidx[kDaTile];
+    __shared__ unsigned long long red[2][kDaThreads / 32];
+    // preceding blocks' varint count and gap sum
+    unsigned long long pc = 0, pg = 0;
+    for (int b = threadIdx.x; b < (int)blockIdx.x; b += kDaThreads) {
+        pc += agg[b].count;
+        pg += agg[b].gsum;
+    }
+    pc = warp_reduce_sum(pc);
+    pg = warp_reduce_sum(pg);
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = pc;
+        red[1][threadIdx.x >> 5] = pg;
+    }
+    __syncthreads();
+    unsigned long long e0 = 0, g0 = 0;
+    for (int w = 0; w < kDaThreads / 32; ++w) {
+        e0 += red[0][w];
+        g0 += red[1][w];
+    }
+    // this thread's varints: values, block-local numbering and index prefix
+    const int64_t lo = (int64_t)blockIdx.x * kDaTile + (int64_t)threadIdx.x * kDaBytes;
+    uint64_t val[kDaBytes];
+    unsigned c = 0;
+    unsigned long long g = 0;
+    unsigned fl = 0;
+#pragma unroll
+    for (int k = 0; k < kDaBytes; ++k) {
+        const int64_t i = lo + k;
+        val[k] = ~0ull;
+        if (i < V && !(sec[i] & 0x80)) {
+            int len;
+            bool big;
+            const uint64_t v = varint_ending_at(sec, i, &len, &big);
+            if (len > 10) fl |= kFlagVarintLong;
+            if (big) fl |= kFlagIndexRange;
+            val[k] = v;
+            ++c;
+            g += v;
+        }
+    }
+    unsigned long long ctot, gtot;
+    const unsigned long long cex = block_exclusive_scan<unsigned long long, kDaThreads>(c, &ctot);
+    const unsigned long long gex = block_exclusive_scan<unsigned long long, kDaThreads>(g, &gtot);
+    {
+        unsigned long long e = e0 + cex;  // global entry number of the next varint
+        unsigned long long acc = g0 + gex;
+#pragma unroll
+        for (int k = 0; k < kDaBytes; ++k) {
+            if (val[k] == ~0ull) continue;
+            acc += val[k];
+            const int64_t idx = (int64_t)acc;  // index = inclusive prefix sum of gaps
+            if (e > 0 && val[k] == 0) fl |= kFlagDecodeTrunc;  // duplicate index: exact path decides
+            if (acc >= (unsigned long long)base_count) fl |= kFlagIndexRange;
+            sidx[e - e0] = idx;
+            ++e;
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kDaThreads - 1) {
+        // the section must end on a terminator and hold exactly E varints
+        if ((sec[V - 1] & 0x80) || e0 + ctot != (unsigned long long)E) fl |= kFlagDecodeTrunc;
+    }
+    if (fl) {
+        atomicOr(flags, fl);
+        if (defer) atomicOr(defer, (unsigned)kDeferDecode);
+    }
+    __syncthreads();
+    // rows: (entry, component) pairs of this block's entries, entry-major, so
+    // consecutive threads read consecutive i32 values of the payload
+    const int64_t nloc = (int64_t)(ctot < (unsigned long long)kDaTile ? ctot : (unsigned long long)kDaTile);
+    if (e0 + nloc > (unsigned long long)E) return;  // malformed (flagged above)
+    const uint8_t *q0 = payload + 24 + V + 4 * (int64_t)W * (int64_t)e0;
+    for (int64_t k = threadIdx.x; k < nloc * W; k += kDaThreads) {
+        const int64_t le = k / W;
+        const int comp = (int)(k - le * W);
+        const int64_t idx = sidx[le];
+        if (idx < 0 || idx >= base_count) continue;
+        const uint8_t *q = q0 + 4 * k;
+        const int32_t v = (int32_t)((uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) |
+                                    ((uint32_t)q[3] << 24));
+        const int64_t o = (int64_t)comp * ld + idx;
+        out[o] = canon[o] + (double)v * step;  // q.astype(f64) * quant_step, then canonical + delta
+    }
+}
+
 }  // namespace airgs
 
 using namespace airgs;
+
+extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, int64_t entry_count,
+                                       double quant_step, int32_t width, const double *canonical, int64_t count,
+                                       int64_t ld, double *params_out, void *stream) {
+    return guarded(ctx, [&] {
+        cudaStream_t st = (cudaStream_t)stream;
+        if (nbytes < 24) throw ApiFailure(AIRGS_E_DECODE, "delta payload shorter than its header");
+        if (width <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad parameter width");
+        if (count <= 0 || ld < count) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad canonical layout");
+        cudaEvent_t t0 = ctx->time_begin(st);
+        const int64_t E = entry_count;
+        const int64_t V = nbytes - 24 - 4 * E * (int64_t)width;
+        bool ok = V >= 0 && V >= E && V <= 10 * E;
+        if (ok && E == 0) ok = V == 0;
+        // params = canonical (every plane, padding included)
+        const int64_t n2 = (int64_t)width * ld / 2;
+        const int cblocks = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, ceil_div(n2, 256 * 4)));
+        k_copy_planes<<<cblocks, 256, 0, st>>>(reinterpret_cast<const double2 *>(canonical),
+                                                reinterpret_cast<double2 *>(params_out), n2);
+        ++ctx->launches;
+        check_launch();
+        unsigned int *flags = ctx->scratch_t<unsigned int>(kSlotFlags, 4);
+        if (ok && E > 0) {
+            AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
+            const int nb = (int)ceil_div(V, kDaTile);
+            DaAgg *agg = (DaAgg *)ctx->scratch(kSlotMisc3, sizeof(DaAgg) * (size_t)nb);
+            k_gsdp_da_count<<<nb, kDaThreads, 0, st>>>(payload + 24, V, agg);
+            k_gsdp_da_rows<<<nb, kDaThreads, 0, st>>>(payload, V, E, width, quant_step, count, agg, canonical,
+                                                     params_out, ld, flags, ctx->defer ? ctx->d_defer : nullptr);
+            ctx->launches += 2;
+            check_launch();
+        }
+        ctx->time_end(t0, st, kStageDecode);
+        if (ctx->defer) {
+            if (!ok) {  // structurally inconsistent lengths: fold into the deferred word
+                const unsigned int bad = kDeferDecode;
+                h2d_small(ctx, ctx->d_defer, &bad, sizeof(bad), st);
+            }
+            return;
+        }
+        unsigned int hf = 0;
+        if (ok && E > 0) {
+            AIRGS_CUDA_TRY(cudaMemcpyAsync(&hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, st));
+            AIRGS_CUDA_TRY(cudaStreamSynchronize(st));
+        }
+        if (!ok || hf) {
+            // the exact decoder raises the reference's error -- or, for a payload
+            // the reference accepts (duplicate indices: later entries win), yields
+            // the dense overlay that the apply kernel then adds to the canonical set
+            double *rows = ctx->scratch_t<double>(kSlotFusedRows, (size_t)width * ld);
+            uint8_t *present = ctx->scratch_t<uint8_t>(kSlotFusedPresent, (size_t)ld);
+            int64_t *idx = ctx->scratch_t<int64_t>(kSlotFusedIdx, (size_t)std::max<int64_t>(E, 1) + 1);
+            AIRGS_CUDA_TRY(cudaMemsetAsync(rows, 0, sizeof(double) * (size_t)width * ld, st));
+            AIRGS_CUDA_TRY(cudaMemsetAsync(present, 0, (size_t)ld, st));
+            gsdp_impl(ctx, payload, nbytes, E, quant_step, width, count, rows, ld, present, idx, idx + E, st);
+            const int rc = airgs_delta_apply(ctx, canonical, rows, present, nullptr, nullptr, 0, nullptr, nullptr,
+                                             count, width, ld, params_out, stream);
+            if (rc) throw ApiFailure(rc, ctx->err);
+        }
+    });
+}
 
 
 extern "C" int airgs_plane_minmax(airgs_ctx *ctx, const double *params, int64_t n, int32_t m, int64_t ld,

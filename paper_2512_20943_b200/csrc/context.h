@@ -172,6 +172,9 @@ enum Slot : int {
     kSlotBinRec,
     kSlotBinCount,
     kSlotDebug,
+    kSlotFusedRows,
+    kSlotFusedPresent,
+    kSlotFusedIdx,
     kSlotCount
 };
 

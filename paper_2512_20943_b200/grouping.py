@@ -111,6 +111,22 @@ def probe_frames(frames, cams, targets, device=None) -> list:
     return [float(np.mean([psnr_from_sse(sse[f * V + v], px[v]) for v in range(V)])) for f in range(len(frames))]
 
 
+def _in_item_order(pieces, order, n_items, dev):
+    """Concatenate per-frame SSE pieces (evaluation order ``order``) into
+    item order on the device -- no per-frame host->device index copies,
+    which would stall the stream pipeline."""
+    import torch
+
+    if not pieces:
+        return torch.zeros((n_items,), dtype=torch.float64, device=dev)
+    cat = torch.cat(pieces)
+    if order == list(range(n_items)):
+        return cat
+    out = torch.empty((n_items,), dtype=torch.float64, device=dev)
+    out[torch.tensor(order, dtype=torch.int64).to(dev, non_blocking=False)] = cat
+    return out
+
+
 def probe_sequence_items(space, cams, payloads, targets, items, device=None):
     """Per-item SSE of (frame t, view v) items streamed from host memory: for
     each frame that has items, its GSDP payload and the items' (h, w, 3)
@@ -122,7 +138,7 @@ def probe_sequence_items(space, cams, payloads, targets, items, device=None):
     import torch
 
     from . import codec
-    from .model import GaussianFrame, apply_overlay, as_space
+    from .model import GaussianFrame, as_space
     from .rasterizer import render_views
 
     space = as_space(space)
@@ -146,7 +162,7 @@ def probe_sequence_items(space, cams, payloads, targets, items, device=None):
     dtg = [{} for _ in range(2)]
     used = [None, None]
     ready = [None, None]
-    out = torch.zeros((len(items),), dtype=torch.float64, device=dev)
+    pieces = []
 
     def host_tensor(im):
         return im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im, dtype=np.float64))
@@ -180,16 +196,14 @@ def probe_sequence_items(space, cams, payloads, targets, items, device=None):
         if k + 1 < len(order):
             stage(k + 1)
         data = datas[t]
-        delta, _ = codec.decode_delta_device(data, n, w, device=dev, payload_dev=dpay[b][: len(data)])
-        planes = apply_overlay(canon, n, delta.overlay(dev))
+        planes = codec.decode_apply_device(data, canon, n, w, device=dev, payload_dev=dpay[b][: len(data)])
         lst = by_frame[t]
-        sse = render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for _, v in lst],
-                           targets=[dtg[b][v] for _, v in lst], device=dev).sse
-        out[torch.tensor([i for i, _ in lst], device=dev)] = sse
+        pieces.append(render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for _, v in lst],
+                                   targets=[dtg[b][v] for _, v in lst], device=dev).sse)
         u = torch.cuda.Event()
         u.record(comp)
         used[b] = u
-    return out
+    return _in_item_order(pieces, [i for t in order for i, _ in by_frame[t]], len(items), dev)
 
 
 def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_DB, device=None):
@@ -233,7 +247,7 @@ def probe_payload_items(space, cams, payloads, payload_devs, targets, items, dev
 
     from . import codec
     from ._lib import engine
-    from .model import GaussianFrame, apply_overlay, as_space
+    from .model import GaussianFrame, as_space
     from .rasterizer import render_views
 
     space = as_space(space)
@@ -248,15 +262,16 @@ def probe_payload_items(space, cams, payloads, payload_devs, targets, items, dev
     for t in by_frame:
         p = payloads[t]
         datas[t] = p.data if hasattr(p, "data") else bytes(p)
-    out = torch.zeros((len(items),), dtype=torch.float64, device=dev)
+    order = [k for lst in by_frame.values() for k, _ in lst]  # item positions in evaluation order
+    pieces = []
 
     def run():
+        pieces.clear()
         for t, lst in by_frame.items():
-            delta, _ = codec.decode_delta_device(datas[t], n, w, device=dev, payload_dev=payload_devs[t])
-            planes = apply_overlay(canon, n, delta.overlay(dev))
-            sse = render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for _, v in lst],
-                               targets=[targets[t][v] for _, v in lst], device=dev).sse
-            out[torch.tensor([k for k, _ in lst], device=dev)] = sse
+            planes = codec.decode_apply_device(datas[t], canon, n, w, device=dev, payload_dev=payload_devs[t])
+            pieces.append(render_views([GaussianFrame(device_params=planes, count=n)], cams,
+                                       [(0, v) for _, v in lst], targets=[targets[t][v] for _, v in lst],
+                                       device=dev).sse)
 
     eng = engine(dev)
     flags = ctypes.c_uint32(0)
@@ -267,7 +282,7 @@ def probe_payload_items(space, cams, payloads, payload_devs, targets, items, dev
         eng.call("airgs_defer", 0, ctypes.byref(flags))
     if flags.value:
         run()  # checked mode
-    return out
+    return _in_item_order(pieces, order, len(items), dev)
 
 
 def probe_payloads_device(space, cams, payloads, payload_devs, targets, tau_db: float = DEFAULT_TAU_DB,

@@ -175,3 +175,64 @@ def test_diff_frames_exact(rng):
     np.testing.assert_array_equal(d.indices(), ri)
     back = apply_delta(CanonicalSpace(GaussianFrame(params=a), 500), d)
     np.testing.assert_array_equal(back.params, orc.apply(a, ri, rr))
+
+
+def _fused_vs_two_step(blob, n, w=17, seed=0):
+    import torch
+
+    from paper_2512_20943_b200 import codec, device as dv
+    from paper_2512_20943_b200.model import apply_overlay
+
+    rng = np.random.default_rng(seed)
+    canon = dv.upload_params(rng.normal(size=(n, w)))
+    fused = codec.decode_apply_device(blob, canon, n, w)
+    delta, _ = codec.decode_delta_device(blob, n, w)
+    two = apply_overlay(canon, n, delta.overlay())
+    assert torch.equal(fused[:, :n], two[:, :n])
+    return fused
+
+
+@pytest.mark.parametrize("n,k,step", [(12, 3, 1e-4), (5000, 1000, 1e-4), (300000, 60000, 1e-4), (100000, 2, 1e-3),
+                                      (300, 300, 1e-2), (70000, 69999, 1e-3)])
+def test_fused_decode_apply_equals_decode_then_apply(n, k, step):
+    """airgs_gsdp_decode_apply (single-pass varint decode + streamed rows into
+    a copy of the canonical planes) == decode_delta + apply_delta, bit for
+    bit, from tiny to C2-sized payloads (60k entries), dense and sparse."""
+    from paper_2512_20943_b200 import codec
+
+    rng = np.random.default_rng(k + n)
+    d, idx, rows = _delta(rng, n, 17, k)
+    _fused_vs_two_step(codec.encode_delta(d, step).data, n)
+
+
+def test_fused_decode_apply_edge_cases_and_errors():
+    """Empty delta (params = canonical), a duplicate index (the exact path's
+    dict semantics), and every malformed payload raising the reference's
+    error class through the fused entry, in checked and deferred mode."""
+    import ctypes
+    import struct
+
+    from paper_2512_20943_b200 import _lib, codec, device as dv
+    from paper_2512_20943_b200.errors import DecodeError, StructuralError
+    from paper_2512_20943_b200.model import DeltaTensor
+
+    _fused_vs_two_step(codec.encode_delta(DeltaTensor.empty(10, 17), 1e-4).data, 10)
+    q = np.arange(34, dtype="<i4").reshape(2, 17)
+    _fused_vs_two_step(struct.pack("<4sIIId", b"GSDP", 0, 0, 2, 0.5) + bytes([3, 0]) + q.tobytes(), 6)
+    canon = dv.upload_params(np.zeros((4, 17)))
+    pay = codec.encode_delta(DeltaTensor(4, 17, {0: np.ones(17)}), 1e-3)
+    bad = [(pay.data[:-8], DecodeError), (pay.data[:10], DecodeError),
+           (struct.pack("<4sIIId", b"GSDP", 0, 0, 1, 1e-3) + bytes([0xFF] * 10 + [0x01]) + bytes(68), DecodeError),
+           (codec.encode_delta(DeltaTensor(100, 17, {99: np.ones(17)}), 1e-3).data, StructuralError)]
+    for blob, exc in bad:
+        with pytest.raises(exc):
+            codec.decode_apply_device(blob, canon, 4, 17)
+    eng = _lib.engine()
+    flags = ctypes.c_uint32(0)
+    for blob, _ in bad:
+        eng.call("airgs_defer", 1, ctypes.byref(flags))
+        try:
+            codec.decode_apply_device(blob, canon, 4, 17)
+        finally:
+            eng.call("airgs_defer", 0, ctypes.byref(flags))
+        assert flags.value != 0  # folded into the deferred word, no exception
