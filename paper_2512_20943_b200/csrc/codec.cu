@@ -398,10 +398,10 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
 //   k_copy_planes     params = canonical, 4 x 128-bit per thread per step
 //   k_gsdp_da_count   per 2048-byte block of the varint section: varints
 //                     ending in it and the sum of their gaps
-//   k_gsdp_da_rows    each block adds up the preceding blocks' totals (no
-//                     look-back chain), numbers its varints, prefix-sums the
-//                     gaps to indices, then the whole block streams its
-//                     entries' (entry, component) i32 values in order:
+//   k_gsdp_da_index   each block adds up the preceding blocks' totals (no
+//                     look-back chain), numbers its varints and prefix-sums
+//                     the gaps to entry indices
+//   k_gsdp_da_scatter one thread per (entry, component), entry-major:
 //                     params[c][idx] = canonical[c][idx] + (double)q * step
 // Every check of the reference decoder is a flag (truncation, varint length,
 // index range, duplicate index); a flagged call is redone by the exact
@@ -479,11 +479,9 @@ k_gsdp_da_count(const uint8_t *__restrict__ sec, int64_t V, DaAgg *__restrict__ 
 }
 
 __global__ void __launch_bounds__(kDaThreads)
-k_gsdp_da_rows(const uint8_t *__restrict__ payload, int64_t V, int64_t E, int W, double step, int64_t base_count,
-               const DaAgg *__restrict__ agg, const double *__restrict__ canon, double *__restrict__ out, int64_t ld,
-               unsigned int *flags, unsigned int *defer) {
+k_gsdp_da_index(const uint8_t *__restrict__ payload, int64_t V, int64_t E, int64_t base_count,
+                const DaAgg *__restrict__ agg, int64_t *__restrict__ idx_out, unsigned int *flags, unsigned int *defer) {
     const uint8_t *sec = payload + 24;
-    __shared__ int64_t sidx[kDaTile];
     __shared__ unsigned long long red[2][kDaThreads / 32];
     // preceding blocks' varint count and gap sum
     unsigned long long pc = 0, pg = 0;
@@ -537,7 +535,7 @@ k_gsdp_da_rows(const uint8_t *__restrict__ payload, int64_t V, int64_t E, int W,
             const int64_t idx = (int64_t)acc;  // index = inclusive prefix sum of gaps
             if (e > 0 && val[k] == 0) fl |= kFlagDecodeTrunc;  // duplicate index: exact path decides
             if (acc >= (unsigned long long)base_count) fl |= kFlagIndexRange;
-            sidx[e - e0] = idx;
+            if (e < (unsigned long long)E) idx_out[e] = idx;
             ++e;
         }
     }
@@ -549,23 +547,25 @@ k_gsdp_da_rows(const uint8_t *__restrict__ payload, int64_t V, int64_t E, int W,
         atomicOr(flags, fl);
         if (defer) atomicOr(defer, (unsigned)kDeferDecode);
     }
-    __syncthreads();
-    // rows: (entry, component) pairs of this block's entries, entry-major, so
-    // consecutive threads read consecutive i32 values of the payload
-    const int64_t nloc = (int64_t)(ctot < (unsigned long long)kDaTile ? ctot : (unsigned long long)kDaTile);
-    if (e0 + nloc > (unsigned long long)E) return;  // malformed (flagged above)
-    const uint8_t *q0 = payload + 24 + V + 4 * (int64_t)W * (int64_t)e0;
-    for (int64_t k = threadIdx.x; k < nloc * W; k += kDaThreads) {
-        const int64_t le = k / W;
-        const int comp = (int)(k - le * W);
-        const int64_t idx = sidx[le];
-        if (idx < 0 || idx >= base_count) continue;
-        const uint8_t *q = q0 + 4 * k;
-        const int32_t v = (int32_t)((uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) |
-                                    ((uint32_t)q[3] << 24));
-        const int64_t o = (int64_t)comp * ld + idx;
-        out[o] = canon[o] + (double)v * step;  // q.astype(f64) * quant_step, then canonical + delta
-    }
+}
+
+// rows: one thread per (entry, component), entry-major so that consecutive
+// threads read consecutive i32 values of the payload
+__global__ void __launch_bounds__(256)
+k_gsdp_da_scatter(const uint8_t *__restrict__ qbytes, const int64_t *__restrict__ idx, int64_t E, int W,
+                  double step, int64_t base_count, const double *__restrict__ canon, double *__restrict__ out,
+                  int64_t ld) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= E * W) return;
+    const int64_t e = k / W;
+    const int comp = (int)(k - e * W);
+    const int64_t i = idx[e];
+    if (i < 0 || i >= base_count) return;  // flagged by k_gsdp_da_index
+    const uint8_t *q = qbytes + 4 * k;
+    const int32_t v = (int32_t)((uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) |
+                                ((uint32_t)q[3] << 24));
+    const int64_t o = (int64_t)comp * ld + i;
+    out[o] = canon[o] + (double)v * step;  // q.astype(f64) * quant_step, then canonical + delta
 }
 
 }  // namespace airgs
@@ -597,10 +597,14 @@ extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, i
             AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
             const int nb = (int)ceil_div(V, kDaTile);
             DaAgg *agg = (DaAgg *)ctx->scratch(kSlotMisc3, sizeof(DaAgg) * (size_t)nb);
+            int64_t *idx = ctx->scratch_t<int64_t>(kSlotFusedIdx, (size_t)E + 1);
             k_gsdp_da_count<<<nb, kDaThreads, 0, st>>>(payload + 24, V, agg);
-            k_gsdp_da_rows<<<nb, kDaThreads, 0, st>>>(payload, V, E, width, quant_step, count, agg, canonical,
-                                                     params_out, ld, flags, ctx->defer ? ctx->d_defer : nullptr);
-            ctx->launches += 2;
+            k_gsdp_da_index<<<nb, kDaThreads, 0, st>>>(payload, V, E, count, agg, idx, flags,
+                                                      ctx->defer ? ctx->d_defer : nullptr);
+            k_gsdp_da_scatter<<<(unsigned)ceil_div(E * width, 256), 256, 0, st>>>(payload + 24 + V, idx, E, width,
+                                                                                 quant_step, count, canonical,
+                                                                                 params_out, ld);
+            ctx->launches += 3;
             check_launch();
         }
         ctx->time_end(t0, st, kStageDecode);

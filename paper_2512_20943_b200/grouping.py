@@ -132,12 +132,18 @@ def probe_sequence_items(space, cams, payloads, targets, items, device=None):
     each frame that has items, its GSDP payload and the items' (h, w, 3)
     float64 host targets (pinned torch tensors give asynchronous copies) are
     copied H2D on a copy stream while the previous frame is evaluated (double
-    buffering), then the frame is decoded, applied and its items rendered
-    with SSE fused into compositing.  Returns a device float64 tensor in
-    ``items`` order.  ``targets[t][v]`` need only exist for listed items."""
+    buffering), then the frame is decoded and applied (fused) and its items
+    rendered with SSE fused into compositing.  The whole batch runs under
+    deferred checking (no host synchronisation per frame); a flagged batch is
+    re-run in checked mode for the reference's exact error.  Returns a device
+    float64 tensor in ``items`` order.  ``targets[t][v]`` need only exist for
+    listed items."""
+    import ctypes
+
     import torch
 
     from . import codec
+    from ._lib import engine
     from .model import GaussianFrame, as_space
     from .rasterizer import render_views
 
@@ -154,55 +160,73 @@ def probe_sequence_items(space, cams, payloads, targets, items, device=None):
     order = list(by_frame)
     datas = {t: (payloads[t].data if hasattr(payloads[t], "data") else bytes(payloads[t])) for t in order}
     cap = max((len(d) for d in datas.values()), default=1)
+    res = [(c.resolution[1], c.resolution[0], 3) for c in cams]
+    for t in order:
+        for _, v in by_frame[t]:
+            if tuple(targets[t][v].shape) != res[v]:
+                raise StructuralError("target resolution does not match camera")
     # double buffers allocated once: pinned payload staging (no per-frame cudaHostAlloc,
     # which synchronises the device) and device targets / payloads (no allocator churn)
     pinned = [torch.empty((max(cap, 1),), dtype=torch.uint8).pin_memory() for _ in range(2)]
     dpay = [torch.empty((max(cap, 1),), dtype=torch.uint8, device=dev) for _ in range(2)]
-    res = [(c.resolution[1], c.resolution[0], 3) for c in cams]
-    dtg = [{} for _ in range(2)]
-    used = [None, None]
-    ready = [None, None]
-    pieces = []
+    views = sorted({v for lst in by_frame.values() for _, v in lst})
+    dtg = [{v: torch.empty(res[v], dtype=torch.float64, device=dev) for v in views} for _ in range(2)]
 
     def host_tensor(im):
         return im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im, dtype=np.float64))
 
-    def stage(k):
-        t = order[k]
-        b = k % 2
-        data = datas[t]
-        with torch.cuda.stream(copy):
-            if used[b] is not None:
-                copy.wait_event(used[b])  # buffer b's previous frame is done
-            for _, v in by_frame[t]:
-                h = host_tensor(targets[t][v])
-                if tuple(h.shape) != res[v]:
-                    raise StructuralError("target resolution does not match camera")
-                if v not in dtg[b]:
-                    dtg[b][v] = torch.empty(res[v], dtype=torch.float64, device=dev)
-                dtg[b][v].copy_(h, non_blocking=True)
+    def run():
+        used = [None, None]  # compute finished with buffer b (device event)
+        copied = [None, None]  # H2D out of pinned[b] finished (host waits before rewriting it)
+        ready = [None, None]
+        pieces = []
+
+        def stage(k):
+            t = order[k]
+            b = k % 2
+            data = datas[t]
+            if copied[b] is not None:
+                copied[b].synchronize()
             if data:
                 pinned[b][: len(data)].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
-                dpay[b][: len(data)].copy_(pinned[b][: len(data)], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(copy)
-        ready[b] = ev
+            with torch.cuda.stream(copy):
+                if used[b] is not None:
+                    copy.wait_event(used[b])  # buffer b's previous frame is done
+                for _, v in by_frame[t]:
+                    dtg[b][v].copy_(host_tensor(targets[t][v]), non_blocking=True)
+                if data:
+                    dpay[b][: len(data)].copy_(pinned[b][: len(data)], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            ready[b] = copied[b] = ev
 
-    if order:
-        stage(0)
-    for k, t in enumerate(order):
-        b = k % 2
-        comp.wait_event(ready[b])
-        if k + 1 < len(order):
-            stage(k + 1)
-        data = datas[t]
-        planes = codec.decode_apply_device(data, canon, n, w, device=dev, payload_dev=dpay[b][: len(data)])
-        lst = by_frame[t]
-        pieces.append(render_views([GaussianFrame(device_params=planes, count=n)], cams, [(0, v) for _, v in lst],
-                                   targets=[dtg[b][v] for _, v in lst], device=dev).sse)
-        u = torch.cuda.Event()
-        u.record(comp)
-        used[b] = u
+        if order:
+            stage(0)
+        for k, t in enumerate(order):
+            b = k % 2
+            comp.wait_event(ready[b])
+            if k + 1 < len(order):
+                stage(k + 1)
+            data = datas[t]
+            planes = codec.decode_apply_device(data, canon, n, w, device=dev, payload_dev=dpay[b][: len(data)])
+            lst = by_frame[t]
+            pieces.append(render_views([GaussianFrame(device_params=planes, count=n)], cams,
+                                       [(0, v) for _, v in lst], targets=[dtg[b][v] for _, v in lst],
+                                       device=dev).sse)
+            u = torch.cuda.Event()
+            u.record(comp)
+            used[b] = u
+        return pieces
+
+    eng = engine(dev)
+    flags = ctypes.c_uint32(0)
+    eng.call("airgs_defer", 1, ctypes.byref(flags))
+    try:
+        pieces = run()
+    finally:
+        eng.call("airgs_defer", 0, ctypes.byref(flags))
+    if flags.value:
+        pieces = run()  # checked mode
     return _in_item_order(pieces, [i for t in order for i, _ in by_frame[t]], len(items), dev)
 
 
