@@ -317,6 +317,11 @@ AIRGS_API int airgs_gsdp_encode(airgs_ctx *ctx, const double *rows, const uint8_
                                 void *stream);
 
 /* ---- delta algebra (ss/model.py:241-311) -------------------------------- */
+/* Layout contract of the plane-major kernels below (compose, apply,
+ * quantize): planes start 16-byte aligned, ld is even, and every per-primitive
+ * array (present, sel, rank, nz) holds ld entries -- the kernels move two
+ * primitives per thread as 128-bit double2 (the padding lane i + 1 >= n is
+ * written as 0).  paper_2512_20943_b200.device allocates ld = ceil8(n). */
 
 /* n-way compose of dense overlays in list order with one |.|max > eps filter
  * at the end (ss/model.py:294-311); sign[d] = -1 negates overlay d

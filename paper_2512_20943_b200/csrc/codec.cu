@@ -408,7 +408,7 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
 // decoder for the reference's error (or folded into the deferred word).
 
 constexpr int kDaThreads = 256;
-constexpr int kDaBytes = 8;                      // varint bytes per thread
+constexpr int kDaBytes = 2;                      // varint bytes per thread (many small blocks: latency)
 constexpr int kDaTile = kDaThreads * kDaBytes;   // per block
 
 __global__ void __launch_bounds__(256) k_copy_planes(const double2 *__restrict__ src, double2 *__restrict__ dst,
@@ -585,13 +585,18 @@ extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, i
         const int64_t V = nbytes - 24 - 4 * E * (int64_t)width;
         bool ok = V >= 0 && V >= E && V <= 10 * E;
         if (ok && E == 0) ok = V == 0;
-        // params = canonical (every plane, padding included)
+        // params = canonical (every plane, padding included), on the side stream
+        // so the copy overlaps the varint scans; joined before the row scatter
         const int64_t n2 = (int64_t)width * ld / 2;
         const int cblocks = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, ceil_div(n2, 256 * 4)));
-        k_copy_planes<<<cblocks, 256, 0, st>>>(reinterpret_cast<const double2 *>(canonical),
-                                                reinterpret_cast<double2 *>(params_out), n2);
+        cudaStream_t side = ctx->side_stream();
+        AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
+        AIRGS_CUDA_TRY(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+        k_copy_planes<<<cblocks, 256, 0, side>>>(reinterpret_cast<const double2 *>(canonical),
+                                                  reinterpret_cast<double2 *>(params_out), n2);
         ++ctx->launches;
         check_launch();
+        AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev_join, side));
         unsigned int *flags = ctx->scratch_t<unsigned int>(kSlotFlags, 4);
         if (ok && E > 0) {
             AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
@@ -601,12 +606,14 @@ extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, i
             k_gsdp_da_count<<<nb, kDaThreads, 0, st>>>(payload + 24, V, agg);
             k_gsdp_da_index<<<nb, kDaThreads, 0, st>>>(payload, V, E, count, agg, idx, flags,
                                                       ctx->defer ? ctx->d_defer : nullptr);
+            AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0));
             k_gsdp_da_scatter<<<(unsigned)ceil_div(E * width, 256), 256, 0, st>>>(payload + 24 + V, idx, E, width,
                                                                                  quant_step, count, canonical,
                                                                                  params_out, ld);
             ctx->launches += 3;
             check_launch();
         }
+        AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // (E == 0: the copy is the result)
         ctx->time_end(t0, st, kStageDecode);
         if (ctx->defer) {
             if (!ok) {  // structurally inconsistent lengths: fold into the deferred word

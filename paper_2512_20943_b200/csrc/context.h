@@ -44,6 +44,18 @@ struct airgs_ctx {
         int32_t *ids = nullptr;     // [tiles][max_per_tile] primitive indices in compositing order
         int64_t max_per_tile = 0;
     } dump;
+    // side stream for work that overlaps the caller's stream inside one call
+    // (fork/join through events; created on first use)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side_stream() {
+        if (!side) {
+            AIRGS_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            AIRGS_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+            AIRGS_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        }
+        return side;
+    }
     std::vector<cudaEvent_t> event_pool;
     cudaEvent_t take_event() {
         if (event_pool.empty()) {
@@ -119,6 +131,11 @@ struct airgs_ctx {
         return host;
     }
     ~airgs_ctx() {
+        if (side) {
+            cudaStreamDestroy(side);
+            cudaEventDestroy(ev_fork);
+            cudaEventDestroy(ev_join);
+        }
         for (auto &b : bufs)
             if (b.p) cudaFree(b.p);
         if (host) cudaFreeHost(host);

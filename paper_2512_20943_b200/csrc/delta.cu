@@ -9,7 +9,8 @@
 //                    decode(encode(.)) values
 //   prune ranks      ss/pruning.py:72-76 via compaction + stable radix sort
 //   level sizes      ss/codec.py:200-207 exact GSDP size per pruning level
-// All kernels stream the planes with unit stride across threads (coalesced).
+// All kernels stream the planes with unit stride across threads, two
+// primitives per thread as 128-bit double2 accesses.
 #include <algorithm>
 #include <vector>
 
@@ -27,37 +28,57 @@ struct ComposeArgs {
     int nd;
 };
 
+// Two adjacent primitives (i, i+1; i even) per thread: every plane is read and
+// written as 128-bit double2 (planes are 64-byte aligned, ld a multiple of 8,
+// so i + 1 < ld always addresses the plane's padding at worst).  The padding
+// lane (i + 1 >= n) is written as 0.
+__device__ __forceinline__ double2 ld2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+__device__ __forceinline__ void st2(double *p, double2 v) { *reinterpret_cast<double2 *>(p) = v; }
+__device__ __forceinline__ uint32_t ld_u8x2(const uint8_t *p) {
+    const uint16_t v = *reinterpret_cast<const uint16_t *>(p);
+    return (uint32_t)v;
+}
+
 template <int W>
 __global__ void __launch_bounds__(256)
 k_compose(ComposeArgs a, int64_t n, int64_t ld, double eps, int apply_eps, double *__restrict__ out,
           uint8_t *__restrict__ outp) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (i >= n) return;
-    double acc[W];
-    bool any = false;
+    const bool two = i + 1 < n;
+    double2 acc[W];
+    bool any0 = false, any1 = false;
     for (int d = 0; d < a.nd; ++d) {
-        if (!a.present[d][i]) continue;
+        const uint32_t pr = ld_u8x2(a.present[d] + i);
+        const bool p0 = (pr & 0xffu) != 0, p1 = two && (pr >> 8) != 0;
+        if (!p0 && !p1) continue;
         const double *r = a.rows[d] + i;
         const double s = a.sign[d];
-        if (!any) {
 #pragma unroll
-            for (int c = 0; c < W; ++c) acc[c] = s * r[c * ld];  // b.copy() / -b
-            any = true;
-        } else {
-#pragma unroll
-            for (int c = 0; c < W; ++c) acc[c] = acc[c] + s * r[c * ld];  // acc + b
+        for (int c = 0; c < W; ++c) {
+            const double2 v = ld2(r + c * ld);
+            // b.copy() / -b for the first present delta, acc + b afterwards
+            if (p0) acc[c].x = any0 ? acc[c].x + s * v.x : s * v.x;
+            if (p1) acc[c].y = any1 ? acc[c].y + s * v.y : s * v.y;
         }
+        any0 |= p0;
+        any1 |= p1;
     }
-    bool keep = any;
-    if (any && apply_eps) {
-        double mx = 0.0;
+    bool keep0 = any0, keep1 = any1;
+    if (apply_eps) {
+        double m0 = 0.0, m1 = 0.0;
 #pragma unroll
-        for (int c = 0; c < W; ++c) mx = fmax(mx, fabs(acc[c]));
-        keep = mx > eps;
+        for (int c = 0; c < W; ++c) {
+            if (any0) m0 = fmax(m0, fabs(acc[c].x));
+            if (any1) m1 = fmax(m1, fabs(acc[c].y));
+        }
+        keep0 = any0 && m0 > eps;
+        keep1 = any1 && m1 > eps;
     }
-    outp[i] = keep ? 1 : 0;
+    *reinterpret_cast<uint16_t *>(outp + i) = (uint16_t)((keep0 ? 1u : 0u) | (keep1 ? 0x100u : 0u));
 #pragma unroll
-    for (int c = 0; c < W; ++c) out[c * ld + i] = keep ? acc[c] : 0.0;
+    for (int c = 0; c < W; ++c)
+        st2(out + c * ld + i, make_double2(keep0 ? acc[c].x : 0.0, keep1 ? acc[c].y : 0.0));
 }
 
 template <int W>
@@ -66,21 +87,35 @@ k_apply(const double *__restrict__ canon, const double *__restrict__ ra, const u
         const uint8_t *__restrict__ sel, const int32_t *__restrict__ rank, int32_t kmin,
         const double *__restrict__ rb, const uint8_t *__restrict__ pb, int64_t n, int64_t ld,
         double *__restrict__ out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (i >= n) return;
-    const bool useA = (!sel || sel[i]) && (!rank || rank[i] >= kmin);
-    const double *r = nullptr;
-    if (useA) {
-        if (ra && pa[i]) r = ra;
-    } else if (rb && pb[i]) {
-        r = rb;
-    }
-    if (r) {
+    const bool two = i + 1 < n;
+    const double *r[2] = {nullptr, nullptr};
 #pragma unroll
-        for (int c = 0; c < W; ++c) out[c * ld + i] = canon[c * ld + i] + r[c * ld + i];
+    for (int h = 0; h < 2; ++h) {
+        const int64_t j = i + h;
+        if (h && !two) break;
+        const bool useA = (!sel || sel[j]) && (!rank || rank[j] >= kmin);
+        if (useA) {
+            if (ra && pa[j]) r[h] = ra;
+        } else if (rb && pb[j]) {
+            r[h] = rb;
+        }
+    }
+    if (r[0] && r[0] == r[1]) {  // both rows from the same overlay: 128-bit loads
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+            const double2 cv = ld2(canon + c * ld + i), dv = ld2(r[0] + c * ld + i);
+            st2(out + c * ld + i, make_double2(cv.x + dv.x, cv.y + dv.y));
+        }
     } else {
 #pragma unroll
-        for (int c = 0; c < W; ++c) out[c * ld + i] = canon[c * ld + i];
+        for (int c = 0; c < W; ++c) {
+            const double2 cv = ld2(canon + c * ld + i);
+            const double x = r[0] ? cv.x + r[0][c * ld + i] : cv.x;
+            const double y = !two ? 0.0 : r[1] ? cv.y + r[1][c * ld + i + 1] : cv.y;
+            st2(out + c * ld + i, make_double2(x, y));
+        }
     }
 }
 
@@ -88,25 +123,38 @@ template <int W>
 __global__ void __launch_bounds__(256)
 k_quantize(const double *__restrict__ rows, const uint8_t *__restrict__ present, int64_t n, int64_t ld,
            double step, uint8_t *__restrict__ nz, double *__restrict__ deq, unsigned long long *bad) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (i >= n) return;
-    if (!present[i]) {
-        nz[i] = 0;
+    const uint32_t pr = ld_u8x2(present + i);
+    const bool p0 = (pr & 0xffu) != 0, p1 = i + 1 < n && (pr >> 8) != 0;
+    if (!p0 && !p1) {
+        *reinterpret_cast<uint16_t *>(nz + i) = 0;
         return;
     }
-    double q[W];
-    bool any = false, over = false;
+    double2 q[W];
+    bool any0 = false, any1 = false, over0 = false, over1 = false;
 #pragma unroll
     for (int c = 0; c < W; ++c) {
-        q[c] = rint(rows[c * ld + i] / step);  // np.rint(v / quant_step): half-even
-        any |= q[c] != 0.0;
-        over |= fabs(q[c]) > 2147483647.0;
+        const double2 v = ld2(rows + c * ld + i);
+        q[c] = make_double2(rint(v.x / step), rint(v.y / step));  // np.rint(v / quant_step): half-even
+        any0 |= q[c].x != 0.0;
+        any1 |= q[c].y != 0.0;
+        over0 |= fabs(q[c].x) > 2147483647.0;
+        over1 |= fabs(q[c].y) > 2147483647.0;
     }
-    nz[i] = any ? 1 : 0;
-    if (any && over) atomicMin(bad, (unsigned long long)i);
-    if (deq && any) {
+    any0 &= p0;
+    any1 &= p1;
+    *reinterpret_cast<uint16_t *>(nz + i) = (uint16_t)((any0 ? 1u : 0u) | (any1 ? 0x100u : 0u));
+    if (any0 && over0) atomicMin(bad, (unsigned long long)i);
+    if (any1 && over1) atomicMin(bad, (unsigned long long)(i + 1));
+    if (deq && (any0 || any1)) {
 #pragma unroll
-        for (int c = 0; c < W; ++c) deq[c * ld + i] = q[c] * step;  // q.astype(f64) * quant_step
+        for (int c = 0; c < W; ++c) {  // q.astype(f64) * quant_step
+            double *o = deq + c * ld + i;
+            if (any0 && any1) st2(o, make_double2(q[c].x * step, q[c].y * step));
+            else if (any0) o[0] = q[c].x * step;
+            else o[1] = q[c].y * step;
+        }
     }
 }
 
@@ -283,7 +331,7 @@ extern "C" int airgs_delta_compose(airgs_ctx *ctx, int32_t ndeltas, const double
             a.present[d] = present[d];
             a.sign[d] = signs ? signs[d] : 1.0;
         }
-        launch_w<ComposeK>(width, dim3((unsigned)ceil_div(n, 256)), dim3(256), (cudaStream_t)stream, a, n, ld, eps,
+        launch_w<ComposeK>(width, dim3((unsigned)ceil_div(n, 512)), dim3(256), (cudaStream_t)stream, a, n, ld, eps,
                            (int)apply_eps, out_rows, out_present);
         ++ctx->launches;
         check_launch();
@@ -297,7 +345,7 @@ extern "C" int airgs_delta_apply(airgs_ctx *ctx, const double *canonical, const 
     return guarded(ctx, [&] {
         if (n <= 0) return;
         cudaEvent_t t0 = ctx->time_begin((cudaStream_t)stream);
-        launch_w<ApplyK>(width, dim3((unsigned)ceil_div(n, 256)), dim3(256), (cudaStream_t)stream, canonical, rows_a,
+        launch_w<ApplyK>(width, dim3((unsigned)ceil_div(n, 512)), dim3(256), (cudaStream_t)stream, canonical, rows_a,
                          present_a, sel_a, keep_rank, keep_min, rows_b, present_b, n, ld, params_out);
         ++ctx->launches;
         check_launch();
@@ -316,7 +364,7 @@ extern "C" int airgs_quantize(airgs_ctx *ctx, const double *rows, const uint8_t 
         unsigned long long *bad = ctx->scratch_t<unsigned long long>(kSlotFlags, 2);
         const unsigned long long mx = ~0ull;
         h2d_small(ctx, bad, &mx, sizeof(mx), st);
-        launch_w<QuantK>(width, dim3((unsigned)ceil_div(n, 256)), dim3(256), st, rows, present, n, ld, step, nz_out,
+        launch_w<QuantK>(width, dim3((unsigned)ceil_div(n, 512)), dim3(256), st, rows, present, n, ld, step, nz_out,
                          deq_out, bad);
         ++ctx->launches;
         check_launch();
