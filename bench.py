@@ -25,6 +25,13 @@ block touches and renders only its views; one NCCL all-gather of the per-view
 SSE gives every rank every frame's quality and keyframe decision (identical
 at any N).  The total work (K x 18 views) is fixed: strong scaling.
 
+--workload eval (auxiliary, not the headline): the per-frame evaluation of
+SURVEY s8(d) (C4 by default): usage pass on the server frame with views
+dealt over the ranks and an NCCL all-reduce (SUM) of the int64 counts, then
+the pruning-level space (8 ratios x all views, (level, view) items dealt
+round-robin, NCCL all-gather of SSE) and Algorithm-1 selection.  Unit =
+rendered (level, view) evaluations incl. the usage pass, per second.
+
 --impl reference: the reference's own CPU path (the vendored reference
 package: decode_delta + apply_delta + render + psnr) on the host cores, same
 metric/config.
@@ -178,6 +185,109 @@ def evaluate_frame(space, cams, payload_dev, payload_bytes, targets_dev, device)
     px = cams[0].resolution[0] * cams[0].resolution[1] * 3
     q = float(np.mean([psnr_from_sse(s, px) for s in sse]))
     return q, vb.launches
+
+
+EVAL_RATIOS = tuple(i / 10 for i in range(8))
+
+
+def run_eval(args):
+    """--workload eval: usage pass + level sweep + selection per frame, sharded
+    over the ranks (sharding.usage_sharded / build_level_space_sharded)."""
+    import torch
+
+    from paper_2512_20943_b200 import _lib, synth
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+    from paper_2512_20943_b200.pruning import SelectionContext, select_pruning_level
+    from paper_2512_20943_b200.sharding import build_level_space_sharded, usage_sharded
+
+    rank, world, local = _dist()
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        backend = os.environ.get("AIRGS_BENCH_BACKEND", "nccl")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
+    cfg = synth.CONFIGS[args.config]
+    seq = synth.Sequence(cfg, seed=args.seed, event_every=0)
+    base = seq.frame(0)
+    cams = synth.cameras(cfg)
+    space = CanonicalSpace(GaussianFrame(params=base, frame_index=0, group_key=0), capacity_U=base.shape[0])
+    nfr = min(args.frames, args.warmup + args.steps)
+    servers, gaps = [], []
+    for t in range(1, nfr + 1):
+        mv = seq.frame(t)
+        servers.append(GaussianFrame(params=mv, frame_index=t, group_key=0))
+        gaps.append(diff_frames(space.frame, GaussianFrame(params=mv)))
+    for f in servers:
+        f.planes(device)  # server frames resident in HBM (inputs of the timed region)
+    V, L = len(cams), len(EVAL_RATIOS)
+    results = []
+
+    def frame_eval(k):
+        usage = usage_sharded(servers[k], cams, device=device)
+        lv = build_level_space_sharded(gaps[k], space, cams, list(EVAL_RATIOS), usage, QUANT_STEP,
+                                       frame_index=k + 1)
+        mid = len(lv.levels) // 2
+        budget = 0.5 * (lv.levels[mid - 1].size_bytes + lv.levels[mid].size_bytes)
+        ctx = SelectionContext(bandwidth_B=budget * 8.0, target_rate_R=1.0, cliff_beta=2.0)
+        results.append((select_pruning_level(lv, ctx), [round(x.quality_db, 6) for x in lv.levels]))
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize(device)
+
+    for i in range(args.warmup):
+        frame_eval(i % nfr)
+    barrier()
+    results.clear()
+    eng = _lib.engine(device)
+    launches0 = eng.launches
+    sampler = ClockSampler(local)
+    sampler.start()
+    stream = torch.cuda.current_stream(device)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.warmup, args.warmup + args.steps):
+        frame_eval(i % nfr)
+    ev1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    evals = (L + 1) * V * args.steps
+    if rank == 0:
+        W, H = cfg.resolution
+        print(json.dumps({
+            "metric": f"per-frame evaluation: usage pass + {L}-level sweep renders/sec at {W}x{H}, "
+                      f"{cfg.count // 1000}k Gaussians",
+            "value": round(evals / (ms / 1e3), 2), "unit": "evaluated views/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": {"workload": f"{args.config} per-frame evaluation: usage pass ({V} views, NCCL all-reduce of "
+                                   f"int64 counts) + level space ({L} ratios x {V} views, (level, view) items "
+                                   f"round-robin, NCCL all-gather of SSE) + Algorithm 1",
+                       "gaussians": cfg.count, "views": V, "levels": L, "resolution": [W, H],
+                       "parallelism": f"views / (level, view) items over {world} rank(s)"},
+            "gpu_launches": int(round((eng.launches - launches0) / args.steps)), "clocks": clocks,
+            "selected_levels": [r[0] for r in results], "quality_tables_db": [r[1] for r in results]}))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
 
 
 def run_gpu(args):
@@ -704,8 +814,19 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=2, help="frame states in the bounded cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--per-step", action="store_true", help="synchronise after every frame (evaluate_frame)")
+    ap.add_argument("--workload", default="probe", choices=["probe", "eval"],
+                    help="probe: the headline keyframe probe; eval: usage pass + level sweep per frame")
     args = ap.parse_args()
-    if args.impl == "reference":
+    if args.workload == "eval":
+        if args.impl == "reference":
+            if _dist()[0] == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "--workload eval has no CPU arm (the "
+                                  "reference's build_level_space is single-threaded: ~2 min per C4 frame)"}))
+            return
+        if "--config" not in sys.argv:
+            args.config = "C4"
+        run_eval(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)

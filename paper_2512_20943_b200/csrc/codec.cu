@@ -549,23 +549,48 @@ k_gsdp_da_index(const uint8_t *__restrict__ payload, int64_t V, int64_t E, int64
     }
 }
 
-// rows: one thread per (entry, component), entry-major so that consecutive
-// threads read consecutive i32 values of the payload
+// rows: one thread per entry, every component.  Consecutive threads take
+// consecutive entries, whose sorted indices are close together, so each
+// plane's canonical reads and parameter writes coalesce; the entry's W int32
+// values are read as aligned 32-bit words (funnel shift: the value block
+// starts at an arbitrary byte offset) -- the first load brings the entry's
+// bytes into L1 for the rest.
+__device__ __forceinline__ int32_t ld_i32_unaligned(const uint8_t *p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
+    const unsigned sh = (unsigned)(a & 3u) * 8u;
+    const uint32_t lo = __ldg(w);
+    const uint32_t hi = sh ? __ldg(w + 1) : 0u;  // (sh > 0: the value's last byte lies in w[1])
+    return (int32_t)__funnelshift_r(lo, hi, sh);
+}
+
+template <int WMAX>
 __global__ void __launch_bounds__(256)
 k_gsdp_da_scatter(const uint8_t *__restrict__ qbytes, const int64_t *__restrict__ idx, int64_t E, int W,
                   double step, int64_t base_count, const double *__restrict__ canon, double *__restrict__ out,
                   int64_t ld) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= E * W) return;
-    const int64_t e = k / W;
-    const int comp = (int)(k - e * W);
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
     const int64_t i = idx[e];
     if (i < 0 || i >= base_count) return;  // flagged by k_gsdp_da_index
-    const uint8_t *q = qbytes + 4 * k;
-    const int32_t v = (int32_t)((uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) |
-                                ((uint32_t)q[3] << 24));
-    const int64_t o = (int64_t)comp * ld + i;
-    out[o] = canon[o] + (double)v * step;  // q.astype(f64) * quant_step, then canonical + delta
+    const uint8_t *q = qbytes + 4 * e * W;
+    if (WMAX == 0) {  // any width: plain loop
+        for (int c = 0; c < W; ++c)
+            out[(int64_t)c * ld + i] = canon[(int64_t)c * ld + i] + (double)ld_i32_unaligned(q + 4 * c) * step;
+        return;
+    }
+    constexpr int WA = WMAX > 0 ? WMAX : 1;
+    int32_t v[WA];
+    double c0[WA];
+#pragma unroll
+    for (int c = 0; c < WA; ++c)
+        if (c < W) {
+            v[c] = ld_i32_unaligned(q + 4 * c);
+            c0[c] = canon[(int64_t)c * ld + i];
+        }
+#pragma unroll
+    for (int c = 0; c < WA; ++c)
+        if (c < W) out[(int64_t)c * ld + i] = c0[c] + (double)v[c] * step;  // q.astype(f64) * quant_step, then canonical + delta
 }
 
 }  // namespace airgs
@@ -580,7 +605,7 @@ extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, i
         if (nbytes < 24) throw ApiFailure(AIRGS_E_DECODE, "delta payload shorter than its header");
         if (width <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad parameter width");
         if (count <= 0 || ld < count) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad canonical layout");
-        cudaEvent_t t0 = ctx->time_begin(st);
+        StageScope t0(ctx, st, kStageDecode);
         const int64_t E = entry_count;
         const int64_t V = nbytes - 24 - 4 * E * (int64_t)width;
         bool ok = V >= 0 && V >= E && V <= 10 * E;
@@ -607,14 +632,20 @@ extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, i
             k_gsdp_da_index<<<nb, kDaThreads, 0, st>>>(payload, V, E, count, agg, idx, flags,
                                                       ctx->defer ? ctx->d_defer : nullptr);
             AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-            k_gsdp_da_scatter<<<(unsigned)ceil_div(E * width, 256), 256, 0, st>>>(payload + 24 + V, idx, E, width,
-                                                                                 quant_step, count, canonical,
-                                                                                 params_out, ld);
+            if (width <= 17)
+                k_gsdp_da_scatter<17><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
+                    payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
+            else if (width <= 26)
+                k_gsdp_da_scatter<26><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
+                    payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
+            else
+                k_gsdp_da_scatter<0><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
+                    payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
             ctx->launches += 3;
             check_launch();
         }
         AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // (E == 0: the copy is the result)
-        ctx->time_end(t0, st, kStageDecode);
+        t0.end();
         if (ctx->defer) {
             if (!ok) {  // structurally inconsistent lengths: fold into the deferred word
                 const unsigned int bad = kDeferDecode;
@@ -743,9 +774,9 @@ extern "C" int airgs_gsdp_decode(airgs_ctx *ctx, const uint8_t *payload, int64_t
                                  double quant_step, int32_t width, int64_t base_count, double *rows, int64_t ld,
                                  uint8_t *present, int64_t *idx_out, int64_t *entries_out, void *stream) {
     return guarded(ctx, [&] {
-        cudaEvent_t t0 = rows ? ctx->time_begin((cudaStream_t)stream) : nullptr;
+        StageScope t0(ctx, (cudaStream_t)stream, kStageDecode, rows != nullptr);
         gsdp_impl(ctx, payload, nbytes, entry_count, quant_step, width, base_count, rows, ld, present, idx_out,
                   entries_out, (cudaStream_t)stream);
-        ctx->time_end(t0, (cudaStream_t)stream, kStageDecode);
+        t0.end();
     });
 }

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 struct airgs_ctx {
     int device = 0;
@@ -205,6 +206,43 @@ enum Stage : int {
     kStageApply = 5,
     kStageSse = 6,
     kStageQuantize = 7,
+};
+
+inline const char *stage_name(int kind) {
+    static const char *names[airgs_ctx::kStages] = {"airgs/composite", "airgs/project", "airgs/bin",
+                                                   "airgs/sort",      "airgs/decode",  "airgs/apply",
+                                                   "airgs/sse",       "airgs/quantize"};
+    return kind >= 0 && kind < airgs_ctx::kStages ? names[kind] : "airgs/other";
+}
+
+// One pipeline stage: an NVTX range (host side, visible to nsys / ncu
+// --nvtx) and, when per-stage timing is on, a CUDA-event pair on the stage's
+// stream.  end() closes both; the destructor closes the range on an error path.
+class StageScope {
+   public:
+    StageScope(airgs_ctx *ctx, cudaStream_t st, int kind, bool on = true) : ctx_(ctx), st_(st), kind_(kind), on_(on) {
+        if (!on_) return;
+        nvtxRangePushA(stage_name(kind));
+        ev_ = ctx_->time_begin(st_);
+    }
+    void end() {
+        if (!on_) return;
+        on_ = false;
+        ctx_->time_end(ev_, st_, kind_);
+        nvtxRangePop();
+    }
+    ~StageScope() {
+        if (on_) nvtxRangePop();
+    }
+    StageScope(const StageScope &) = delete;
+    StageScope &operator=(const StageScope &) = delete;
+
+   private:
+    airgs_ctx *ctx_;
+    cudaStream_t st_;
+    int kind_;
+    bool on_;
+    cudaEvent_t ev_ = nullptr;
 };
 
 // Run fn() translating failures into status codes / messages on ctx.

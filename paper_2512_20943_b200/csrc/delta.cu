@@ -344,12 +344,12 @@ extern "C" int airgs_delta_apply(airgs_ctx *ctx, const double *canonical, const 
                                  int32_t width, int64_t ld, double *params_out, void *stream) {
     return guarded(ctx, [&] {
         if (n <= 0) return;
-        cudaEvent_t t0 = ctx->time_begin((cudaStream_t)stream);
+        StageScope t0(ctx, (cudaStream_t)stream, kStageApply);
         launch_w<ApplyK>(width, dim3((unsigned)ceil_div(n, 512)), dim3(256), (cudaStream_t)stream, canonical, rows_a,
                          present_a, sel_a, keep_rank, keep_min, rows_b, present_b, n, ld, params_out);
         ++ctx->launches;
         check_launch();
-        ctx->time_end(t0, (cudaStream_t)stream, kStageApply);
+        t0.end();
     });
 }
 

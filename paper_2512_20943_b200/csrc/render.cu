@@ -1316,6 +1316,29 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_STATIC_SMEM
 #define C2_STATIC_SMEM 1
 #endif
+#ifndef C2_ELLIPSE_CULL
+#define C2_ELLIPSE_CULL 0  // measured slower (profiles/r2_composite_experiments.md): off
+#endif
+
+// Lower bound (conservative by 1e-4 of the terms' magnitude + 1e-3, far above
+// fp32 rounding) of min Q(dx, dy) = A dx^2 + B dx dy + C dy^2 over the
+// rectangle [x0, x1] x [y0, y1] (A, C > 0, positive definite): 0 if the
+// rectangle holds the origin, else the smallest of the four edges' minima
+// (each a 1-D quadratic minimised at its clamped vertex).
+__device__ __forceinline__ float quad_rect_min_lb(float A, float B, float C, float x0, float x1, float y0,
+                                                  float y1) {
+    if (x0 <= 0.0f && x1 >= 0.0f && y0 <= 0.0f && y1 >= 0.0f) return 0.0f;
+    if (!(A > 0.0f && C > 0.0f)) return 0.0f;
+    auto edge = [B](float P, float Q, float X, float lo, float hi) {
+        // min over t in [lo, hi] of P X^2 + B X t + Q t^2
+        const float t = fminf(fmaxf(-B * X / (2.0f * Q), lo), hi);
+        const float a = P * X * X, b = B * X * t, c = Q * t * t;
+        return (a + b + c) - (1e-4f * (a + fabsf(b) + c) + 1e-3f);
+    };
+    const float ex = fminf(edge(A, C, x0, y0, y1), edge(A, C, x1, y0, y1));
+    const float ey = fminf(edge(C, A, y0, x0, x1), edge(C, A, y1, x0, x1));
+    return fminf(ex, ey);
+}
 constexpr int kC2Chunk = C2_CHUNK;  // compacted entries per phase A / phase B round (24 measured best of 8..32)
 static_assert(kC2Chunk % 8 == 0 && kC2Chunk <= 32, "chunk");
 constexpr int kC2Batch = C2_BATCH;
@@ -1348,7 +1371,7 @@ struct CompNShared {
 
 #ifdef C2_COUNT
 // experiment builds only (tools/c2_counts.py): work counters of k_compositeN
-__device__ unsigned long long g_c2c[8];
+__device__ unsigned long long g_c2c[10];
 #endif
 
 template <bool USAGE, int NP>
@@ -1448,6 +1471,28 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             unsigned mk = 0;
 #pragma unroll
             for (int ww = 0; ww < G::kWarps; ++ww) mk |= (((xm >> (ww % kSubX)) & (ym >> (ww / kSubX))) & 1u) << ww;
+#ifdef C2_COUNT
+            atomicAdd(&g_c2c[8], (unsigned long long)__popc(mk));
+#endif
+#if C2_ELLIPSE_CULL
+            // exact ellipse test: drop a sub-tile whose pixel-centre rectangle lies
+            // wholly outside the phase-A candidate region Q(dx, dy) <= log2(1/EPS) + L
+            if (mk && r.hx < 1e29f && r.hy < 1e29f) {
+                const float4 f0 = sh.f0[t];
+                const float lim = log2_inv_eps() - sh.f1[t].y;
+#pragma unroll
+                for (int ww = 0; ww < G::kWarps; ++ww) {
+                    if (!((mk >> ww) & 1u)) continue;
+                    const float x0 = (float)(G::kSW * (ww % kSubX)) + 0.5f + f0.x;
+                    const float y0 = 8.0f * (ww / kSubX) + 0.5f + f0.y;
+                    if (quad_rect_min_lb(f0.z, f0.w, sh.f1[t].x, x0, x0 + (float)(G::kSW - 1), y0, y0 + 7.0f) > lim)
+                        mk &= ~(1u << ww);
+                }
+            }
+#endif
+#ifdef C2_COUNT
+            atomicAdd(&g_c2c[9], (unsigned long long)__popc(mk));
+#endif
             sh.wmask[t] = (uint8_t)mk;
             if (USAGE) sh.cnt[t] = 0;
         }
@@ -1973,13 +2018,13 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         uint32_t *slow_list = ctx->scratch_t<uint32_t>(kSlotSlowTiles, (size_t)Tt);
         AIRGS_CUDA_TRY(cudaMemsetAsync(slow_n, 0, sizeof(unsigned int), st));
         TileSortArgs ta{tl, tile_count, L.d_tile_base, nitems, depth, L.stride, slow_list, slow_n, Tt};
-        cudaEvent_t t_sort = ctx->time_begin(st);
+        StageScope t_sort(ctx, st, kStageSort);
         k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
         // the exact block sort walks the device-side slow list (no host readback)
         k_sort_tiles_block<<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
         NL += 2;
         check_launch();
-        ctx->time_end(t_sort, st, kStageSort);
+        t_sort.end();
         if (ctx->dump.counts) {  // debug capture of the depth-ordered lists (airgs_debug_tile_lists)
             k_dump_tiles<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(tl, tile_count, Tt, ctx->dump.counts,
                                                                    ctx->dump.ids, ctx->dump.max_per_tile);
@@ -2053,7 +2098,7 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
     uint8_t *d_has = (uint8_t *)ctx->scratch(kSlotMisc2, nitems);
     h2d_small(ctx, d_ci, ci.data(), sizeof(CompItem) * nitems, st);
     h2d_small(ctx, d_has, has_t.data(), nitems, st);
-    cudaEvent_t t_comp = Tt > 0 ? ctx->time_begin(st) : nullptr;
+    StageScope t_comp(ctx, st, kStageComposite, Tt > 0);
     if (Tt > 0) {
         unsigned long long *cs = ctx->d_stats;
         if (bbox) {  // the kernel seam (caller-supplied bboxes)
@@ -2097,13 +2142,13 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         ++NL;
         check_launch();
     }
-    ctx->time_end(t_comp, st, kStageComposite);
+    t_comp.end();
     if (sse && any_target) {
-        cudaEvent_t t_sse = ctx->time_begin(st);
+        StageScope t_sse(ctx, st, kStageSse);
         k_sse_items<<<nitems, kSseThreads, 0, st>>>(sse_tiles, L.d_tile_base, d_has, sse);
         ++NL;
         check_launch();
-        ctx->time_end(t_sse, st, kStageSse);
+        t_sse.end();
     }
     // small uploads travel as kernel parameters: nothing host-side must outlive the launches
 }
@@ -2129,7 +2174,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         }
         BinArgs ba{binrec, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, pad, bucket, cap, flags, L.stride,
                    index_order};
-        cudaEvent_t t_bin = ctx->time_begin(st);
+        StageScope t_bin(ctx, st, kStageBin);
         k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
         ++NL;
         if (kBinCountStride > 1) {
@@ -2137,7 +2182,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
             ++NL;
         }
         check_launch();
-        ctx->time_end(t_bin, st, kStageBin);
+        t_bin.end();
     }
     // usage counts are ADDED to the caller's arrays (airgs_b200.h): accumulate
     // this call's counts in zeroed scratch first, so that a redone call cannot
@@ -2350,7 +2395,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.flags = flags;
     pa.stride = stride;
     pa.stats = (ctx->stats && ctx->d_stats) ? ctx->d_stats : nullptr;
-    cudaEvent_t t_proj = ctx->time_begin(st);
+    StageScope t_proj(ctx, st, kStageProject);
     {
         dim3 grid((unsigned)ceil_div(stride, kProjThreads), (unsigned)nframes);
         bool all17 = true;
@@ -2362,7 +2407,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         ++NL;
         check_launch();
     }
-    ctx->time_end(t_proj, st, kStageProject);
+    t_proj.end();
     bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags, binrec,
                       bwd ? &bwd->rec : nullptr);
     if (bwd) {
@@ -2959,9 +3004,9 @@ extern "C" int airgs_render(airgs_ctx *ctx, const airgs_frame *frames, int32_t n
 #ifdef C2_COUNT
 extern "C" __attribute__((visibility("default"))) int airgs_c2_counts(unsigned long long *out, int reset) {
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-    if (cudaMemcpyFromSymbol(out, g_c2c, sizeof(unsigned long long) * 8) != cudaSuccess) return -1;
+    if (cudaMemcpyFromSymbol(out, g_c2c, sizeof(unsigned long long) * 10) != cudaSuccess) return -1;
     if (reset) {
-        unsigned long long z[8] = {};
+        unsigned long long z[10] = {};
         cudaMemcpyToSymbol(g_c2c, z, sizeof(z));
     }
     return 0;

@@ -28,14 +28,15 @@ def main():
     pdev = [torch.frombuffer(bytearray(p.data), dtype=torch.uint8).to(dev) for p in payloads]
     lib = _lib.load_library()
     fn = lib.airgs_c2_counts
-    out = (ctypes.c_ulonglong * 8)()
+    out = (ctypes.c_ulonglong * 10)()
     bench.evaluate_frame(space, cams, pdev[0], payloads[0].data, targets[0], dev)
     fn(out, 1)
     bench.evaluate_frame(space, cams, pdev[1], payloads[1].data, targets[1], dev)
     fn(out, 1)
     V = len(cams)
     names = ["candidate_evals", "lane_iterations", "warp_iterations", "contributions", "phaseA_entries_per_warp",
-             "staged_entries", "evals_after_termination", "evals_alive_failing"]
+             "staged_entries", "evals_after_termination", "evals_alive_failing", "subtile_pairs_aabb",
+             "subtile_pairs_after_cull"]
     d = {k: out[i] / V for i, k in enumerate(names)}
     d["candidates_per_contribution"] = d["candidate_evals"] / max(d["contributions"], 1)
     d["lane_efficiency"] = d["lane_iterations"] / max(32 * d["warp_iterations"], 1)
