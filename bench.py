@@ -468,6 +468,12 @@ def roofline(space, cams, payloads, ktime, step_ms, steps, counts):
             st.update({"achieved_gbs": round(gbs, 1), "frac": round(gbs / hbm, 4)})
         stages[name] = st
     stages["decode"]["bytes_definition"] = "SURVEY s8(d) decode alone: 2*N*W*8 + payload"
+    ap_ms = ktime["apply_ms"] / steps
+    if ap_ms > 0:  # the decode's streaming pass alone (k_gsdp_da_mapply: canonical -> params + delta rows)
+        gbs = 2 * n * W * 8 / (ap_ms / 1e3) / 1e9
+        stages["decode"]["streaming_pass"] = {"kernel": "k_gsdp_da_mapply", "ms_per_step": round(ap_ms, 4),
+                                              "bytes_per_step": int(2 * n * W * 8), "achieved_gbs": round(gbs, 1),
+                                              "frac": round(gbs / hbm, 4)}
     stages["composite"]["bytes_definition"] = "V*(P*3*8 + N*96): targets + one record per primitive"
     dec_rast = sum(stages[k]["ms_per_step"] for k in stages)
     out["stages"] = stages

@@ -280,15 +280,29 @@ AIRGS_API int airgs_gsdp_decode(airgs_ctx *ctx, const uint8_t *payload, int64_t 
 /* Fused decode_delta + apply_delta for the keyframe probe (ss/codec.py:217-248
  * then ss/model.py:269-284): params_out (plane-major, width x ld, device) =
  * canonical with rows[idx] += (double)q * quant_step for every entry of the
- * GSDP payload, without materialising the dense overlay.  Single-pass varint
- * decode (per-block counts, then each block numbers its varints and streams
- * its entries' i32 values).  Bit-identical to airgs_gsdp_decode followed by
- * airgs_delta_apply; malformed payloads take the exact decoder's path and
+ * GSDP payload, without materialising the dense overlay.  Varint scan (per-
+ * block counts, then each block numbers its varints and tags a row map with
+ * entry numbers), then one streaming pass over the canonical planes (128-bit,
+ * every parameter written once).  Bit-identical to airgs_gsdp_decode followed
+ * by airgs_delta_apply; malformed payloads take the exact decoder's path and
  * return its status (AIRGS_E_DECODE / AIRGS_E_STRUCTURAL, same messages).
  * Under airgs_defer the checks fold into the deferred word instead. */
 AIRGS_API int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, int64_t entry_count,
                                       double quant_step, int32_t width, const double *canonical, int64_t count,
                                       int64_t ld, double *params_out, void *stream);
+
+/* airgs_gsdp_decode_apply for a pipelined sequence of frames: under
+ * airgs_defer, the varint scan of next_payload (the frame the caller decodes
+ * next; NULL: none) is enqueued ahead on the context's side stream, so it
+ * overlaps this frame's render, and the next call finds it done (matched by
+ * payload pointer, sizes and layout; otherwise it scans in line).  Two row-map
+ * slots alternate.  Outside airgs_defer it is airgs_gsdp_decode_apply.  Same
+ * results and statuses. */
+AIRGS_API int airgs_gsdp_decode_apply_ahead(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes,
+                                            int64_t entry_count, const uint8_t *next_payload, int64_t next_nbytes,
+                                            int64_t next_entry_count, double quant_step, int32_t width,
+                                            const double *canonical, int64_t count, int64_t ld, double *params_out,
+                                            void *stream);
 
 /* Position after the entry_count gap varints (sequential walk, reference
  * order); *err_out: 0 ok, 1 truncated varint, 2 varint too long.  Used to

@@ -85,6 +85,8 @@ SIGNATURES = {
     "airgs_gsai_decode": (ctypes.c_int, [vp, vp, i64, i64, i32, i64, vp, i64, vp]),
     "airgs_gsdp_decode": (ctypes.c_int, [vp, vp, i64, i64, f64, i32, i64, vp, i64, vp, vp, vp, vp]),
     "airgs_gsdp_decode_apply": (ctypes.c_int, [vp, vp, i64, i64, f64, i32, vp, i64, i64, vp, vp]),
+    "airgs_gsdp_decode_apply_ahead": (ctypes.c_int, [vp, vp, i64, i64, vp, i64, i64, f64, i32, vp, i64, i64, vp,
+                                                     vp]),
     "airgs_gsdp_varint_end": (ctypes.c_int, [vp, vp, i64, i64, c_i64_p, ctypes.POINTER(i32), vp]),
     "airgs_plane_minmax": (ctypes.c_int, [vp, vp, i64, i32, i64, c_double_p, vp]),
     "airgs_gsai_encode": (ctypes.c_int, [vp, vp, i64, i32, i64, c_double_p, c_double_p, i64, vp, vp]),

@@ -385,22 +385,41 @@ def _decode_call(eng, pd, data, entry_count, quant_step, width, base_count, dev,
     return ov, idx[:entry_count]
 
 
-def decode_apply_device(data, canon, n: int, width: int, device=None, payload_dev=None, out=None):
+def _payload_bytes(data):
+    return bytes(data.data) if hasattr(data, "data") and not isinstance(data, (bytes, bytearray, memoryview)) \
+        else bytes(data)
+
+
+def decode_apply_device(data, canon, n: int, width: int, device=None, payload_dev=None, out=None, ahead=None):
     """decode_delta + apply_delta fused (airgs_gsdp_decode_apply): GSDP bytes
     applied to the plane-major canonical parameters ``canon`` (width, ld) ->
     a new (width, ld) device tensor, bit-identical to
     ``apply_overlay(canon, n, decode_delta_device(data, n, width)[0].overlay())``
-    without the dense overlay."""
+    without the dense overlay.  ``ahead=(next_data, next_payload_dev)``: the
+    frame the caller decodes next, whose varint scan is enqueued ahead on the
+    engine's side stream under deferred checking
+    (airgs_gsdp_decode_apply_ahead)."""
     import torch
 
-    data = bytes(data.data) if hasattr(data, "data") and not isinstance(data, (bytes, bytearray, memoryview)) \
-        else bytes(data)
+    data = _payload_bytes(data)
     _, _, entry_count, quant_step = parse_delta_header(data)
     dev = dv.device_of(device)
     pd = payload_dev if payload_dev is not None else _to_device_bytes(data, dev)
     if out is None:
         out = torch.empty_like(canon)
     eng = _engine(dev)
+    nd, n_entries = None, 0
+    if ahead is not None and ahead[1] is not None:
+        nd = _payload_bytes(ahead[0])
+        try:
+            n_entries = parse_delta_header(nd)[2]
+        except DecodeError:  # (reported when that frame itself is decoded)
+            nd = None
+    if nd is not None:
+        eng.call("airgs_gsdp_decode_apply_ahead", _ptr(pd), len(data), entry_count, _ptr(ahead[1]), len(nd),
+                 n_entries, float(quant_step), int(width), _ptr(canon), int(n), int(canon.shape[1]), _ptr(out),
+                 eng.stream())
+        return out
     eng.call("airgs_gsdp_decode_apply", _ptr(pd), len(data), entry_count, float(quant_step), int(width),
              _ptr(canon), int(n), int(canon.shape[1]), _ptr(out), eng.stream())
     return out

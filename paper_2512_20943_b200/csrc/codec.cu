@@ -395,17 +395,28 @@ static void gsdp_impl(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes, in
 // Fused GSDP decode + apply (the probe path: decode_delta then apply_delta,
 // ss/codec.py:217-248 + ss/model.py:269-284, without the dense overlay).
 //
-//   k_copy_planes     params = canonical, 4 x 128-bit per thread per step
-//   k_gsdp_da_count   per 2048-byte block of the varint section: varints
+//   k_gsdp_da_count   per 512-byte block of the varint section: varints
 //                     ending in it and the sum of their gaps
 //   k_gsdp_da_index   each block adds up the preceding blocks' totals (no
-//                     look-back chain), numbers its varints and prefix-sums
-//                     the gaps to entry indices
-//   k_gsdp_da_scatter one thread per (entry, component), entry-major:
-//                     params[c][idx] = canonical[c][idx] + (double)q * step
+//                     look-back chain), numbers its varints, prefix-sums the
+//                     gaps to entry indices and tags the row map:
+//                     map[idx] = gen << 32 | entry
+//   k_gsdp_da_mapply  one streaming pass, (plane, 1024 rows) per CTA, 128-bit
+//                     loads / stores: params[c][i] = canonical[c][i]
+//                     (+ (double)q[e][c] * step where map[i] carries this
+//                     call's tag) -- every parameter is written once, whole
+//                     sectors, no scattered read-modify-write
+// HBM traffic = canonical read once + params written once + the map (8 B per
+// row, L2-resident across the planes) + the payload: the SURVEY s8(d)
+// "decode alone" bytes.  (DA_MAP=0 builds the earlier layout: a plain copy on
+// a side stream overlapping the scans, then a scatter of the entries' rows.)
 // Every check of the reference decoder is a flag (truncation, varint length,
 // index range, duplicate index); a flagged call is redone by the exact
 // decoder for the reference's error (or folded into the deferred word).
+
+#ifndef DA_MAP
+#define DA_MAP 1
+#endif
 
 constexpr int kDaThreads = 256;
 constexpr int kDaBytes = 2;                      // varint bytes per thread (many small blocks: latency)
@@ -480,7 +491,8 @@ k_gsdp_da_count(const uint8_t *__restrict__ sec, int64_t V, DaAgg *__restrict__ 
 
 __global__ void __launch_bounds__(kDaThreads)
 k_gsdp_da_index(const uint8_t *__restrict__ payload, int64_t V, int64_t E, int64_t base_count,
-                const DaAgg *__restrict__ agg, int64_t *__restrict__ idx_out, unsigned int *flags, unsigned int *defer) {
+                const DaAgg *__restrict__ agg, int64_t *__restrict__ idx_out, unsigned long long *__restrict__ map,
+                unsigned long long tag, unsigned int *flags, unsigned int *defer) {
     const uint8_t *sec = payload + 24;
     __shared__ unsigned long long red[2][kDaThreads / 32];
     // preceding blocks' varint count and gap sum
@@ -535,7 +547,10 @@ k_gsdp_da_index(const uint8_t *__restrict__ payload, int64_t V, int64_t E, int64
             const int64_t idx = (int64_t)acc;  // index = inclusive prefix sum of gaps
             if (e > 0 && val[k] == 0) fl |= kFlagDecodeTrunc;  // duplicate index: exact path decides
             if (acc >= (unsigned long long)base_count) fl |= kFlagIndexRange;
-            if (e < (unsigned long long)E) idx_out[e] = idx;
+            if (e < (unsigned long long)E) {
+                if (idx_out) idx_out[e] = idx;
+                if (map && acc < (unsigned long long)base_count) map[acc] = tag | e;
+            }
             ++e;
         }
     }
@@ -593,6 +608,87 @@ k_gsdp_da_scatter(const uint8_t *__restrict__ qbytes, const int64_t *__restrict_
         if (c < W) out[(int64_t)c * ld + i] = c0[c] + (double)v[c] * step;  // q.astype(f64) * quant_step, then canonical + delta
 }
 
+// params = canonical + (tagged rows) q * step; CTA = (1024 rows, plane c)
+constexpr int kMapThreads = 256, kMapPairs = 2;  // pairs (2 rows) per thread
+__global__ void __launch_bounds__(kMapThreads)
+k_gsdp_da_mapply(const double2 *__restrict__ canon, double2 *__restrict__ out, const ulonglong2 *__restrict__ map,
+                 uint32_t gen, const uint8_t *__restrict__ qbytes, int W, double step, int64_t ld2, int64_t npairs) {
+    const int c = blockIdx.y;
+    const int64_t p0 = (int64_t)blockIdx.x * (kMapThreads * kMapPairs) + threadIdx.x;
+    ulonglong2 m[kMapPairs];
+    double2 v[kMapPairs];
+#pragma unroll
+    for (int j = 0; j < kMapPairs; ++j) {
+        const int64_t p = p0 + j * kMapThreads;
+        if (p < npairs) {
+            m[j] = map[p];
+            v[j] = canon[c * ld2 + p];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kMapPairs; ++j) {
+        const int64_t p = p0 + j * kMapThreads;
+        if (p >= npairs) continue;
+        if ((uint32_t)(m[j].x >> 32) == gen)
+            v[j].x = v[j].x + (double)ld_i32_unaligned(qbytes + 4 * ((int64_t)(uint32_t)m[j].x * W + c)) * step;
+        if ((uint32_t)(m[j].y >> 32) == gen)
+            v[j].y = v[j].y + (double)ld_i32_unaligned(qbytes + 4 * ((int64_t)(uint32_t)m[j].y * W + c)) * step;
+        out[c * ld2 + p] = v[j];  // q.astype(f64) * quant_step, then canonical + delta
+    }
+}
+
+static bool map_mode_ok(int64_t E, int64_t ld) {
+    return E < (1ll << 32) && (ld & 1) == 0 && ld / 2 < (1ll << 31) / kMapThreads;
+}
+
+// count + index of a payload's varint section into row-map slot `slot`
+// (tagged with a fresh generation); completion recorded in pre_done[slot]
+static void da_scan(airgs_ctx *ctx, int slot, const uint8_t *payload, int64_t nbytes, int64_t E, int64_t V,
+                    int64_t count, int64_t ld, unsigned int *flags, cudaStream_t st) {
+    const size_t mbytes = sizeof(unsigned long long) * (size_t)ld;
+    unsigned long long *map = (unsigned long long *)ctx->scratch(kSlotFusedMap, 2 * mbytes);
+    if (ctx->map_cap < 2 * mbytes || ctx->map_gen >= 0xfffffff0u) {
+        AIRGS_CUDA_TRY(cudaDeviceSynchronize());  // (rare) no scan / apply of either slot in flight
+        AIRGS_CUDA_TRY(cudaMemset(map, 0, ctx->bufs[kSlotFusedMap].cap));
+        ctx->map_cap = ctx->bufs[kSlotFusedMap].cap;
+        ctx->map_gen = 0;
+    }
+    const uint32_t gen = ++ctx->map_gen;
+    const int nb = (int)ceil_div(V, kDaTile);
+    const size_t want = ((sizeof(DaAgg) * (size_t)nb) + 255) & ~size_t(255);
+    if (ctx->bufs.size() <= (size_t)kSlotFusedAgg || ctx->bufs[kSlotFusedAgg].cap < 2 * want) {
+        AIRGS_CUDA_TRY(cudaDeviceSynchronize());
+        ctx->scratch(kSlotFusedAgg, 2 * want);
+    }
+    DaAgg *agg = reinterpret_cast<DaAgg *>(static_cast<char *>(ctx->bufs[kSlotFusedAgg].p) +
+                                           (size_t)slot * (ctx->bufs[kSlotFusedAgg].cap / 2));
+    k_gsdp_da_count<<<nb, kDaThreads, 0, st>>>(payload + 24, V, agg);
+    k_gsdp_da_index<<<nb, kDaThreads, 0, st>>>(payload, V, E, count, agg, nullptr, map + (size_t)slot * ld,
+                                              (unsigned long long)gen << 32, flags,
+                                              ctx->defer ? ctx->d_defer : nullptr);
+    ctx->launches += 2;
+    check_launch();
+    ctx->pre[slot] = airgs_ctx::Prescan{payload, nbytes, E, count, ld, gen, true};
+    AIRGS_CUDA_TRY(cudaEventRecord(ctx->pre_event(slot), st));
+}
+
+// params = canonical + tagged rows of map slot `slot` (one streaming pass)
+static void da_mapply(airgs_ctx *ctx, int slot, const uint8_t *payload, int64_t V, double quant_step, int width,
+                      const double *canonical, int64_t ld, double *params_out, cudaStream_t st) {
+    StageScope ta(ctx, st, kStageApply);
+    const unsigned long long *map = (const unsigned long long *)ctx->bufs[kSlotFusedMap].p + (size_t)slot * ld;
+    const int64_t npairs = ld / 2;
+    const dim3 grid((unsigned)ceil_div(npairs, kMapThreads * kMapPairs), (unsigned)width);
+    k_gsdp_da_mapply<<<grid, kMapThreads, 0, st>>>(reinterpret_cast<const double2 *>(canonical),
+                                                   reinterpret_cast<double2 *>(params_out),
+                                                   reinterpret_cast<const ulonglong2 *>(map), ctx->pre[slot].gen,
+                                                   payload + 24 + V, width, quant_step, npairs, npairs);
+    ++ctx->launches;
+    check_launch();
+    ctx->pre[slot].valid = false;
+    ta.end();
+}
+
 }  // namespace airgs
 
 using namespace airgs;
@@ -610,41 +706,50 @@ extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, i
         const int64_t V = nbytes - 24 - 4 * E * (int64_t)width;
         bool ok = V >= 0 && V >= E && V <= 10 * E;
         if (ok && E == 0) ok = V == 0;
-        // params = canonical (every plane, padding included), on the side stream
-        // so the copy overlaps the varint scans; joined before the row scatter
         const int64_t n2 = (int64_t)width * ld / 2;
-        const int cblocks = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, ceil_div(n2, 256 * 4)));
-        cudaStream_t side = ctx->side_stream();
-        AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
-        AIRGS_CUDA_TRY(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
-        k_copy_planes<<<cblocks, 256, 0, side>>>(reinterpret_cast<const double2 *>(canonical),
-                                                  reinterpret_cast<double2 *>(params_out), n2);
-        ++ctx->launches;
-        check_launch();
-        AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev_join, side));
         unsigned int *flags = ctx->scratch_t<unsigned int>(kSlotFlags, 4);
-        if (ok && E > 0) {
+        if (DA_MAP && map_mode_ok(E, ld) && ok && E > 0) {
+            const int slot = 0;
+            ctx->pre[0].valid = ctx->pre[1].valid = false;  // (a checked call drops any prescan)
             AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
-            const int nb = (int)ceil_div(V, kDaTile);
-            DaAgg *agg = (DaAgg *)ctx->scratch(kSlotMisc3, sizeof(DaAgg) * (size_t)nb);
-            int64_t *idx = ctx->scratch_t<int64_t>(kSlotFusedIdx, (size_t)E + 1);
-            k_gsdp_da_count<<<nb, kDaThreads, 0, st>>>(payload + 24, V, agg);
-            k_gsdp_da_index<<<nb, kDaThreads, 0, st>>>(payload, V, E, count, agg, idx, flags,
-                                                      ctx->defer ? ctx->d_defer : nullptr);
-            AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0));
-            if (width <= 17)
-                k_gsdp_da_scatter<17><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
-                    payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
-            else if (width <= 26)
-                k_gsdp_da_scatter<26><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
-                    payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
-            else
-                k_gsdp_da_scatter<0><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
-                    payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
-            ctx->launches += 3;
+            da_scan(ctx, slot, payload, nbytes, E, V, count, ld, flags, st);
+            t0.end();  // the scan; the streaming pass is timed as the apply stage
+            da_mapply(ctx, slot, payload, V, quant_step, width, canonical, ld, params_out, st);
+        } else {
+            // params = canonical (every plane, padding included), on the side stream
+            // so the copy overlaps the varint scans; joined before the row scatter
+            const int cblocks = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, ceil_div(n2, 256 * 4)));
+            cudaStream_t side = ctx->side_stream();
+            AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
+            AIRGS_CUDA_TRY(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+            k_copy_planes<<<cblocks, 256, 0, side>>>(reinterpret_cast<const double2 *>(canonical),
+                                                      reinterpret_cast<double2 *>(params_out), n2);
+            ++ctx->launches;
             check_launch();
+            AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev_join, side));
+            if (ok && E > 0) {
+                AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
+                const int nb = (int)ceil_div(V, kDaTile);
+                DaAgg *agg = (DaAgg *)ctx->scratch(kSlotMisc3, sizeof(DaAgg) * (size_t)nb);
+                int64_t *idx = ctx->scratch_t<int64_t>(kSlotFusedIdx, (size_t)E + 1);
+                k_gsdp_da_count<<<nb, kDaThreads, 0, st>>>(payload + 24, V, agg);
+                k_gsdp_da_index<<<nb, kDaThreads, 0, st>>>(payload, V, E, count, agg, idx, nullptr, 0ull, flags,
+                                                          ctx->defer ? ctx->d_defer : nullptr);
+                AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+                if (width <= 17)
+                    k_gsdp_da_scatter<17><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
+                        payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
+                else if (width <= 26)
+                    k_gsdp_da_scatter<26><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
+                        payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
+                else
+                    k_gsdp_da_scatter<0><<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(
+                        payload + 24 + V, idx, E, width, quant_step, count, canonical, params_out, ld);
+                ctx->launches += 3;
+                check_launch();
+            }
+            AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // (E == 0: the copy is the result)
         }
-        AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_join, 0));  // (E == 0: the copy is the result)
         t0.end();
         if (ctx->defer) {
             if (!ok) {  // structurally inconsistent lengths: fold into the deferred word
@@ -675,6 +780,59 @@ extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, i
     });
 }
 
+
+extern "C" int airgs_gsdp_decode_apply_ahead(airgs_ctx *ctx, const uint8_t *payload, int64_t nbytes,
+                                             int64_t entry_count, const uint8_t *next_payload, int64_t next_nbytes,
+                                             int64_t next_entry_count, double quant_step, int32_t width,
+                                             const double *canonical, int64_t count, int64_t ld, double *params_out,
+                                             void *stream) {
+    if (!ctx) return AIRGS_E_INTERNAL;
+    if (!ctx->defer || !DA_MAP)
+        return airgs_gsdp_decode_apply(ctx, payload, nbytes, entry_count, quant_step, width, canonical, count, ld,
+                                       params_out, stream);
+    return guarded(ctx, [&] {
+        cudaStream_t st = (cudaStream_t)stream;
+        if (nbytes < 24) throw ApiFailure(AIRGS_E_DECODE, "delta payload shorter than its header");
+        if (width <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad parameter width");
+        if (count <= 0 || ld < count) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad canonical layout");
+        const int64_t E = entry_count;
+        const int64_t V = nbytes - 24 - 4 * E * (int64_t)width;
+        const bool ok = V >= 0 && V >= E && V <= 10 * E && E > 0 && map_mode_ok(E, ld);
+        if (!ok) {  // empty / inconsistent / unusual layouts: the one-call path (deferred checks)
+            ctx->pre[0].valid = ctx->pre[1].valid = false;
+            const int rc = airgs_gsdp_decode_apply(ctx, payload, nbytes, entry_count, quant_step, width, canonical,
+                                                   count, ld, params_out, stream);
+            if (rc) throw ApiFailure(rc, ctx->err);
+            return;
+        }
+        StageScope t0(ctx, st, kStageDecode);
+        unsigned int *flags = ctx->scratch_t<unsigned int>(kSlotFlags, 4);  // (deferred mode: not read)
+        int slot = -1;
+        for (int k = 0; k < 2; ++k)
+            if (ctx->pre[k].valid && ctx->pre[k].payload == payload && ctx->pre[k].nbytes == nbytes &&
+                ctx->pre[k].E == E && ctx->pre[k].count == count && ctx->pre[k].ld == ld)
+                slot = k;
+        if (slot >= 0) {
+            AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->pre_event(slot), 0));  // scanned ahead on the side stream
+        } else {
+            ctx->pre[0].valid = ctx->pre[1].valid = false;
+            slot = 0;
+            da_scan(ctx, slot, payload, nbytes, E, V, count, ld, flags + 1, st);
+        }
+        // the next frame's scan runs ahead on the side stream (after everything
+        // enqueued so far, in particular the previous apply of the other slot)
+        const int64_t nE = next_entry_count;
+        const int64_t nV = next_nbytes - 24 - 4 * nE * (int64_t)width;
+        if (next_payload && next_nbytes >= 24 && nE > 0 && nV >= nE && nV <= 10 * nE && map_mode_ok(nE, ld)) {
+            cudaStream_t side = ctx->side_stream();
+            AIRGS_CUDA_TRY(cudaEventRecord(ctx->ev_fork, st));
+            AIRGS_CUDA_TRY(cudaStreamWaitEvent(side, ctx->ev_fork, 0));
+            da_scan(ctx, 1 - slot, next_payload, next_nbytes, nE, nV, count, ld, flags + 2, side);
+        }
+        t0.end();
+        da_mapply(ctx, slot, payload, V, quant_step, width, canonical, ld, params_out, st);
+    });
+}
 
 extern "C" int airgs_plane_minmax(airgs_ctx *ctx, const double *params, int64_t n, int32_t m, int64_t ld,
                                   double *lohi_out, void *stream) {

@@ -33,6 +33,25 @@ struct airgs_ctx {
     // optional evaluation counters (diagnostic compositing kernel): bbox, live
     // and contributing (pixel, primitive) evaluations, accumulated on device
     bool stats = false;
+    // fused decode + apply: generation-tagged row map (gen << 32 | entry) in
+    // kSlotFusedMap; entries of older calls are stale by tag, so the map is
+    // cleared only when it is (re)allocated or the generation wraps
+    uint32_t map_gen = 0;
+    size_t map_cap = 0;
+    // two row-map slots: a payload's varint scan may run ahead on the side
+    // stream (airgs_gsdp_decode_apply_ahead) while the previous frame renders
+    struct Prescan {
+        const uint8_t *payload;
+        int64_t nbytes, E, count, ld;
+        uint32_t gen;
+        bool valid;
+    };
+    Prescan pre[2] = {{nullptr, 0, 0, 0, 0, 0, false}, {nullptr, 0, 0, 0, 0, 0, false}};
+    cudaEvent_t pre_done[2] = {nullptr, nullptr};
+    cudaEvent_t pre_event(int slot) {
+        if (!pre_done[slot]) AIRGS_CUDA_TRY(cudaEventCreateWithFlags(&pre_done[slot], cudaEventDisableTiming));
+        return pre_done[slot];
+    }
     uint32_t bucket_cap = 512;  // tile bucket capacity (doubled after an overflow, up to the sort cap)
     // deferred checking (airgs_defer): calls skip their host synchronisations
     // and fold error flags into d_defer, read once when the mode is left
@@ -145,6 +164,8 @@ struct airgs_ctx {
             cudaEventDestroy(p.b);
         }
         for (auto &e : event_pool) cudaEventDestroy(e);
+        for (auto &e : pre_done)
+            if (e) cudaEventDestroy(e);
     }
 };
 
@@ -193,6 +214,8 @@ enum Slot : int {
     kSlotFusedRows,
     kSlotFusedPresent,
     kSlotFusedIdx,
+    kSlotFusedMap,
+    kSlotFusedAgg,
     kSlotCount
 };
 

@@ -1316,6 +1316,9 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_STATIC_SMEM
 #define C2_STATIC_SMEM 1
 #endif
+#ifndef C2_SIGNBITS
+#define C2_SIGNBITS 1
+#endif
 #ifndef C2_ELLIPSE_CULL
 #define C2_ELLIPSE_CULL 0  // measured slower (profiles/r2_composite_experiments.md): off
 #endif
@@ -1540,9 +1543,18 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
 #pragma unroll
             for (int k = 0; k < NP; ++k) wd[k] = 0;
             const float4 *pl = &sh.pl[w][c >> 1][0];
+#if C2_SIGNBITS
+            float2 thr2[NP];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) thr2[k] = make_float2(thr[k], thr[k]);
+            int ntest = 0;
+#endif
 #pragma unroll
             for (int gq = 0; gq < kC2Chunk / 8; ++gq) {
                 if (c + 8 * gq >= ncomp) break;
+#if C2_SIGNBITS
+                ntest += 8;
+#endif
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int pr = 4 * gq + q;
@@ -1559,11 +1571,24 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                         const float2 u = __ffma2_rn(B, dy, Adx);
                         const float2 qv = __ffma2_rn(__fmul2_rn(C, dy), dy, L);
                         const float2 e = __ffma2_rn(u, dx, qv);
+#if C2_SIGNBITS
+                        // candidate iff e < thr: the sign bit of fl(e - thr) (exact sign;
+                        // e == thr rejects, inside the guard band), appended with one
+                        // funnel shift per test (entry order reversed, fixed below)
+                        const float2 d = __fadd2_rn(e, make_float2(-thr2[k].x, -thr2[k].y));
+                        wd[k] = __funnelshift_l(__float_as_uint(d.x), wd[k], 1);
+                        wd[k] = __funnelshift_l(__float_as_uint(d.y), wd[k], 1);
+#else
                         wd[k] |= (e.x <= thr[k] ? 1u : 0u) << (2 * pr);
                         wd[k] |= (e.y <= thr[k] ? 1u : 0u) << (2 * pr + 1);
+#endif
                     }
                 }
             }
+#if C2_SIGNBITS
+#pragma unroll
+            for (int k = 0; k < NP; ++k) wd[k] = ntest ? __brev(wd[k]) >> (32 - ntest) : 0u;
+#endif
             unsigned wu = 0;
 #pragma unroll
             for (int k = 0; k < NP; ++k) {

@@ -289,10 +289,16 @@ def probe_payload_items(space, cams, payloads, payload_devs, targets, items, dev
     order = [k for lst in by_frame.values() for k, _ in lst]  # item positions in evaluation order
     pieces = []
 
+    frames_in_order = list(by_frame)
+
     def run():
         pieces.clear()
-        for t, lst in by_frame.items():
-            planes = codec.decode_apply_device(datas[t], canon, n, w, device=dev, payload_dev=payload_devs[t])
+        for k, (t, lst) in enumerate(by_frame.items()):
+            # the next frame's varint scan is enqueued ahead (side stream) under deferred checking
+            nxt = frames_in_order[k + 1] if k + 1 < len(frames_in_order) else None
+            ahead = (datas[nxt], payload_devs[nxt]) if nxt is not None else None
+            planes = codec.decode_apply_device(datas[t], canon, n, w, device=dev, payload_dev=payload_devs[t],
+                                               ahead=ahead)
             pieces.append(render_views([GaussianFrame(device_params=planes, count=n)], cams,
                                        [(0, v) for _, v in lst], targets=[targets[t][v] for _, v in lst],
                                        device=dev).sse)

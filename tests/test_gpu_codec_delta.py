@@ -238,3 +238,54 @@ def test_fused_decode_apply_edge_cases_and_errors():
         finally:
             eng.call("airgs_defer", 0, ctypes.byref(flags))
         assert flags.value != 0  # folded into the deferred word, no exception
+
+
+@pytest.mark.gpu
+def test_decode_apply_ahead_sequence_equals_one_call_path():
+    """airgs_gsdp_decode_apply_ahead under deferred checking (the pipelined
+    probe): each frame's varint scan runs ahead on the side stream while the
+    previous frame is applied; a frame decoded out of order (no matching
+    prescan), a repeated payload and the last frame (no next) all give
+    params bit-identical to the one-call path, and a malformed next payload
+    (scanned ahead) or frame folds into the deferred word."""
+    import ctypes
+    import struct
+
+    import torch
+
+    from paper_2512_20943_b200 import _lib, codec, device as dv
+
+    n, w = 20000, 17
+    rng = np.random.default_rng(7)
+    canon = dv.upload_params(rng.normal(size=(n, w)))
+    blobs = []
+    for k in (4000, 1, 9000, 2500, 4000):
+        d, _, _ = _delta(rng, n, w, k)
+        blobs.append(codec.encode_delta(d, 1e-4).data)
+    devs = [torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda() for b in blobs]
+    want = [codec.decode_apply_device(b, canon, n, w, payload_dev=p) for b, p in zip(blobs, devs)]
+    bad = struct.pack("<4sIIId", b"GSDP", 0, 0, 1, 1e-3) + bytes([0xFF] * 10 + [0x01]) + bytes(68)
+    bad_dev = torch.frombuffer(bytearray(bad), dtype=torch.uint8).cuda()
+    # call order: 0,1,2 in sequence, 4 out of order (prescan of 3 unused), 3, 3 again, last without next
+    order = [(0, 1), (1, 2), (2, 3), (4, 3), (3, 3), (3, None), (0, None)]
+    eng = _lib.engine()
+    flags = ctypes.c_uint32(0)
+    got = []
+    eng.call("airgs_defer", 1, ctypes.byref(flags))
+    try:
+        for t, nxt in order:
+            ahead = None if nxt is None else (blobs[nxt], devs[nxt])
+            got.append((t, codec.decode_apply_device(blobs[t], canon, n, w, payload_dev=devs[t], ahead=ahead)))
+    finally:
+        eng.call("airgs_defer", 0, ctypes.byref(flags))
+    assert flags.value == 0
+    for t, out in got:
+        assert torch.equal(out[:, :n], want[t][:, :n]), t
+    # a malformed frame inside the pipelined sequence folds into the deferred word
+    eng.call("airgs_defer", 1, ctypes.byref(flags))
+    try:
+        codec.decode_apply_device(blobs[0], canon, n, w, payload_dev=devs[0], ahead=(bad, bad_dev))
+        codec.decode_apply_device(bad, canon, n, w, payload_dev=bad_dev, ahead=None)
+    finally:
+        eng.call("airgs_defer", 0, ctypes.byref(flags))
+    assert flags.value != 0
