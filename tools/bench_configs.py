@@ -6,9 +6,9 @@ For every BASELINE.json config (C1..C5) on synthetic scenes:
   sweep  : (C3, C4) pruning-level space of one delta frame: usage pass on the
            server frame + build_level_space over 8 ratios x all views --
            (level, view) evaluations/s and ms per frame;
-  cpu    : the CPU reference path (oracle projection + the reference's own
-           compiled compositing kernel, 16 worker processes) on a bounded
-           sample of views of the same scene -- views/s.
+  cpu    : the reference arm of bench.py (the vendored reference package:
+           decode_delta + apply_delta + render + psnr, persistent fork pool of
+           the host's cores) on one frame state x all views -- views/s.
 Timing: CUDA events on the current stream around `--steps` repetitions after
 `--warmup`; inputs larger than L2 for C2..C5 (targets).  Prints one JSON line
 per config and writes them to --out.
@@ -21,7 +21,6 @@ import json
 import os
 import sys
 import time
-from dataclasses import replace
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -96,9 +95,17 @@ def sweep(cfg, dev, steps, warmup, ratios=tuple(i / 10 for i in range(8))):
             "decision_margins": selection_margins(lv, ctx, entries=len(gap.indices()))}
 
 
-def cpu(cfg, views):
-    v, cores, kind, sample = bench.cpu_run(cfg, views)
-    return {"views_per_s": round(v, 4), "cores": cores, "kind": kind, "sample": sample}
+def cpu(cfg, steps=1):
+    """The reference arm (bench.CpuArm: the vendored reference package on a
+    persistent fork pool of the host's cores) on `steps` frame states."""
+    arm = bench.CpuArm(cfg)
+    try:
+        arm.run(1)  # warm
+        dt = arm.run(steps)
+        return {"views_per_s": round(arm.V * steps / dt, 4), "cores": arm.cores, "kind": arm.kind,
+                "sample": arm.describe(steps), "cpu_model": bench.cpu_model()}
+    finally:
+        arm.close()
 
 
 def main():
@@ -106,7 +113,7 @@ def main():
     ap.add_argument("--configs", default="C1,C2,C3,C4,C5")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--cpu-views", type=int, default=16)
+    ap.add_argument("--cpu-steps", type=int, default=1, help="frame states (x all views) in the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
@@ -122,8 +129,7 @@ def main():
         if name in ("C3", "C4", "C5"):
             rec["sweep"] = sweep(cfg, dev, max(1, args.steps // 2), 1)
         if not args.no_cpu:
-            ccfg = cfg if cfg.count <= 300_000 else replace(cfg, count=cfg.count)  # same scene, bounded views
-            rec["cpu_reference"] = cpu(ccfg, min(args.cpu_views, cfg.views))
+            rec["cpu_reference"] = cpu(cfg, args.cpu_steps)
             rec["gpu_over_cpu_probe"] = round(rec["probe"]["views_per_s"] / rec["cpu_reference"]["views_per_s"], 1)
         rec["wall_s"] = round(time.time() - t0, 1)
         print(json.dumps(rec), flush=True)
