@@ -1319,6 +1319,9 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_SIGNBITS
 #define C2_SIGNBITS 1
 #endif
+#ifndef C2_FACTOR_BLEND
+#define C2_FACTOR_BLEND 0  // measured slower (profiles/r2_composite_experiments.md): off
+#endif
 #ifndef C2_ELLIPSE_CULL
 #define C2_ELLIPSE_CULL 0  // measured slower (profiles/r2_composite_experiments.md): off
 #endif
@@ -1638,6 +1641,17 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                     }
 #endif
                     if (!USAGE) {
+#if C2_FACTOR_BLEND
+                        // branch-free through one factor f = cp ? ap : 0: x = f*T is the
+                        // reference's ap*T (or 0), T*(1 - f) its T*(1 - ap) (or T*1 = T)
+                        // -- one select pair and one extra DMUL instead of two select pairs
+                        const double f = cp ? ap : 0.0;
+                        x = f * T[k];
+                        cr[k] += x * rg.x;
+                        cg[k] += x * rg.y;
+                        cb[k] += x * bl;
+                        T[k] = T[k] * (1.0 - f);
+#else
                         // branch-free: a non-contributing entry adds exact zeros, keeps T
                         x = cp ? x : 0.0;
                         cr[k] += x * rg.x;
@@ -1645,6 +1659,7 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                         cb[k] += x * bl;
                         const double Tn = T[k] * (1.0 - ap);
                         T[k] = cp ? Tn : T[k];
+#endif
                     } else if (cp) {
                         cr[k] += x * rg.x;
                         cg[k] += x * rg.y;

@@ -249,11 +249,19 @@ def level_frame_planes(p: LevelPlan, kmin):
     return apply_overlay(p.canon, p.n, p.A, sel=p.nz, rank=p.rank, keep_min=int(kmin), ov_b=p.B)
 
 
-def _removed_sets(p: LevelPlan, G, kmins):
+def _removed_prepare(p: LevelPlan, G):
+    """Entry indices (ascending) and their prune ranks on the host: two small
+    downloads (the rows themselves stay on the device)."""
     if p.idx_host is None:
-        idx, _ = G.entries()
-        p.idx_host = idx
-        p.rank_host = p.rank[: p.n].cpu().numpy()[idx] if idx.size else np.zeros(0, dtype=np.int32)
+        import torch
+
+        idx = torch.nonzero(G.present[: G.n]).flatten()
+        p.idx_host = idx.cpu().numpy().astype(np.int64)
+        p.rank_host = p.rank[idx].cpu().numpy() if idx.numel() else np.zeros(0, dtype=np.int32)
+
+
+def _removed_sets(p: LevelPlan, G, kmins):
+    _removed_prepare(p, G)
     return [tuple(p.idx_host[p.rank_host < k].tolist()) for k in kmins]
 
 
@@ -262,12 +270,14 @@ class LevelTable:
     plan, every requested ratio's entry cut ``kmin``, exact payload sizes,
     the surviving (strictly shrinking) levels and their pruned index sets."""
 
-    __slots__ = ("plan", "ratios", "kmins", "sizes", "keep", "removed")
+    __slots__ = ("plan", "ratios", "kmins", "sizes", "keep", "removed", "delta")
 
 
-def level_table(delta, space, ratios, usage, quant_step: float, base=None) -> LevelTable:
+def level_table(delta, space, ratios, usage, quant_step: float, base=None, removed=True) -> LevelTable:
     """Input normalisation and checks of ``build_level_space``
-    (ss/pruning.py:93-126), shared by the single-GPU and sharded drivers."""
+    (ss/pruning.py:93-126), shared by the single-GPU and sharded drivers.
+    ``removed=False`` leaves the pruned index sets to ``level_removed`` (the
+    drivers build them on the host while the level renders run)."""
     delta, space = as_delta(delta), as_space(space)
     base = None if base is None else as_delta(base)
     ratios = sorted(set(float(r) for r in ratios))
@@ -291,23 +301,56 @@ def level_table(delta, space, ratios, usage, quant_step: float, base=None) -> Le
             continue  # duplicate level (ss/pruning.py:125-126)
         t.keep.append(j)
         last = s
-    t.removed = _removed_sets(p, delta.overlay(), [t.kmins[j] for j in t.keep])
+    t.removed = None
+    t.delta = delta
+    if removed:
+        level_removed(t)
     return t
 
 
-def render_sse_chunked(frames, cams, items, targets, device=None):
+def level_removed(t: LevelTable):
+    """The surviving levels' pruned index sets (sorted tuples, as the
+    reference's PruningLevel.pruned_indices)."""
+    if t.removed is None:
+        t.removed = _removed_sets(t.plan, t.delta.overlay(), [t.kmins[j] for j in t.keep])
+    return t.removed
+
+
+def render_sse_chunked(frames, cams, items, targets, device=None, host=True):
     """SSE of (frame, view) items against their targets, at most
     RENDER_PAIRS_PER_CALL (item, primitive) records per render call (C5: 2M
-    primitives x 8 levels x 32 views would not fit one call's scratch)."""
+    primitives x 8 levels x 32 views would not fit one call's scratch).
+    ``host=False`` returns the device tensor without synchronising."""
+    import torch
+
     from .rasterizer import render_views
 
     if not items:
-        return np.zeros(0)
+        return np.zeros(0) if host else None
     n = max(fr.count for fr in frames)
     per_call = max(1, RENDER_PAIRS_PER_CALL // max(n, 1))
-    return np.concatenate([render_views(frames, cams, items[k:k + per_call], targets=targets[k:k + per_call],
-                                        device=device).sse.cpu().numpy()
-                           for k in range(0, len(items), per_call)])
+    parts = [render_views(frames, cams, items[k:k + per_call], targets=targets[k:k + per_call], device=device).sse
+             for k in range(0, len(items), per_call)]
+    sse = torch.cat(parts) if len(parts) > 1 else parts[0]
+    return sse.cpu().numpy() if host else sse
+
+
+def deferred(dev, run):
+    """Run ``run()`` (device work that may synchronise only at its end) under
+    deferred checking: the calls enqueue without host round trips and fold
+    any problem into one device word; if it is set, ``run()`` is repeated in
+    checked mode, which raises the reference's exact error or handles the
+    condition (bucket overflow).  Returns run()'s result."""
+    eng = _engine(dev)
+    flags = ctypes.c_uint32(0)
+    eng.call("airgs_defer", 1, ctypes.byref(flags))
+    try:
+        out = run()
+    finally:
+        eng.call("airgs_defer", 0, ctypes.byref(flags))
+    if flags.value:
+        out = run()
+    return out
 
 
 def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, usage, quant_step: float,
@@ -316,41 +359,48 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
 
     Quality of a level = mean over ``cams`` of PSNR of its reconstruction
     against the unpruned quantised reconstruction; sizes are exact GSDP
-    payload sizes; a level whose size does not shrink is dropped.
+    payload sizes; a level whose size does not shrink is dropped.  The
+    reference render and every (level, view) render are enqueued under
+    deferred checking; the pruned index sets are built on the host while they
+    run, and one synchronisation reads the SSE.
     """
     from .model import GaussianFrame
     from .rasterizer import render_views
 
     space = as_space(space)
-    t = level_table(delta, space, ratios, usage, quant_step, base)
+    t = level_table(delta, space, ratios, usage, quant_step, base, removed=False)
     p = t.plan
     cams = list(cams)
     qualities = [100.0] * len(t.keep)
     if cams:
-        import torch
-
-        ref_planes = level_frame_planes(p, None)
-        ref = GaussianFrame(device_params=ref_planes, count=p.n, frame_index=frame_index, group_key=space.key_index)
-        rv = render_views([ref], cams, [(0, v) for v in range(len(cams))], want_images=True)
-        planes = [level_frame_planes(p, t.kmins[j]) for j in t.keep]
-        # a level whose parameters equal the reference's bit for bit renders the
-        # same image: SSE 0, the reference's 100 dB cap, no render needed (the
-        # mandatory ratio-0 level always, ss/pruning.py:102-104)
-        same = [bool(torch.equal(pl[:, : p.n], ref_planes[:, : p.n])) for pl in planes]
-        todo = [li for li in range(len(planes)) if not same[li]]
-        frames = [GaussianFrame(device_params=planes[li], count=p.n) for li in todo]
-        items, targets = [], []
-        for fi in range(len(frames)):
-            for v in range(len(cams)):
-                items.append((fi, v))
-                targets.append(rv.images[v])
-        sse = render_sse_chunked(frames, cams, items, targets)
+        dev = p.canon.device
+        # a level that prunes no entry has the reference's parameters bit for bit:
+        # SSE 0, the reference's 100 dB cap, no render (the mandatory ratio-0 level,
+        # ss/pruning.py:102-104)
+        todo = [li for li, j in enumerate(t.keep) if t.kmins[j] > 0]
         V = len(cams)
-        sizes_px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
-        for fi, li in enumerate(todo):
-            qualities[li] = float(np.mean([psnr_from_sse(sse[fi * V + v], sizes_px[v]) for v in range(V)]))
+
+        def run():
+            ref = GaussianFrame(device_params=level_frame_planes(p, None), count=p.n, frame_index=frame_index,
+                                group_key=space.key_index)
+            rv = render_views([ref], cams, [(0, v) for v in range(V)], want_images=True, device=dev)
+            frames = [GaussianFrame(device_params=level_frame_planes(p, t.kmins[t.keep[li]]), count=p.n)
+                      for li in todo]
+            items = [(fi, v) for fi in range(len(frames)) for v in range(V)]
+            targets = [rv.images[v] for _ in range(len(frames)) for v in range(V)]
+            out = render_sse_chunked(frames, cams, items, targets, device=dev, host=False)
+            level_removed(t)  # host-only work (after _removed_prepare), overlapping the enqueued renders
+            return out
+
+        _removed_prepare(p, t.delta.overlay())
+        sse_dev = deferred(dev, run) if todo else None
+        if todo:
+            sse = sse_dev.cpu().numpy()
+            sizes_px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
+            for fi, li in enumerate(todo):
+                qualities[li] = float(np.mean([psnr_from_sse(sse[fi * V + v], sizes_px[v]) for v in range(V)]))
     levels = [PruningLevel(ratio=t.ratios[j], quality_db=q, size_bytes=t.sizes[j], pruned_indices=rm)
-              for j, q, rm in zip(t.keep, qualities, t.removed)]
+              for j, q, rm in zip(t.keep, qualities, level_removed(t))]
     return PruningLevelSpace(levels=tuple(levels), frame_index=frame_index)
 
 

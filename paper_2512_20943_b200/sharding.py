@@ -222,40 +222,46 @@ def build_level_space_sharded(delta, space, cams, ratios, usage, quant_step, bas
     from .rasterizer import render_views
 
     space = as_space(space)
-    t = pruning.level_table(delta, space, ratios, usage, quant_step, base)
+    t = pruning.level_table(delta, space, ratios, usage, quant_step, base, removed=False)
     p = t.plan
     cams = list(cams)
     V = len(cams)
     if V == 0:
         levels = [pruning.PruningLevel(ratio=t.ratios[j], quality_db=100.0, size_bytes=t.sizes[j], pruned_indices=rm)
-                  for j, rm in zip(t.keep, t.removed)]
+                  for j, rm in zip(t.keep, pruning.level_removed(t))]
         return pruning.PruningLevelSpace(levels=tuple(levels), frame_index=frame_index)
     dev = p.canon.device
     rank, world = world_info(group)
     mine = item_partition(len(t.keep) * V, rank, world)
-    # reference images only for the views this rank needs
-    need_views = sorted({int(i) % V for i in mine})
-    ref = GaussianFrame(device_params=pruning.level_frame_planes(p, None), count=p.n)
-    refs = {}
-    if need_views:
-        rv = render_views([ref], cams, [(0, v) for v in need_views], want_images=True, device=dev)
-        refs = dict(zip(need_views, rv.images))
-    need_levels = sorted({int(i) // V for i in mine})
-    frames = {li: GaussianFrame(device_params=pruning.level_frame_planes(p, t.kmins[t.keep[li]]), count=p.n)
-              for li in need_levels}
+    pruning._removed_prepare(p, t.delta.overlay())
 
-    def sse_fn(idx):
-        if idx.size == 0:
-            return torch.zeros((0,), dtype=torch.float64, device=dev)
-        order = sorted(frames)
-        pos = {li: k for k, li in enumerate(order)}
-        items = [(pos[int(i) // V], int(i) % V) for i in idx]
-        sse = pruning.render_sse_chunked([frames[li] for li in order], cams, items,
-                                         [refs[int(i) % V] for i in idx], device=dev)
-        return torch.from_numpy(sse).to(dev)
+    def run():
+        # reference images only for the views this rank needs
+        need_views = sorted({int(i) % V for i in mine})
+        ref = GaussianFrame(device_params=pruning.level_frame_planes(p, None), count=p.n)
+        refs = {}
+        if need_views:
+            rv = render_views([ref], cams, [(0, v) for v in need_views], want_images=True, device=dev)
+            refs = dict(zip(need_views, rv.images))
+        need_levels = sorted({int(i) // V for i in mine})
+        frames = {li: GaussianFrame(device_params=pruning.level_frame_planes(p, t.kmins[t.keep[li]]), count=p.n)
+                  for li in need_levels}
+        if mine.size == 0:
+            local = torch.zeros((0,), dtype=torch.float64, device=dev)
+        else:
+            order = sorted(frames)
+            pos = {li: k for k, li in enumerate(order)}
+            items = [(pos[int(i) // V], int(i) % V) for i in mine]
+            local = pruning.render_sse_chunked([frames[li] for li in order], cams, items,
+                                               [refs[int(i) % V] for i in mine], device=dev, host=False)
+        pruning.level_removed(t)  # host-only work overlapping the enqueued renders
+        return local
 
-    sse = sharded_item_sse(len(t.keep) * V, sse_fn, group, dev).cpu().numpy()
+    # renders enqueued under deferred checking (re-run checked on a flag); the
+    # collective follows on every rank exactly once
+    local = pruning.deferred(dev, run)
+    sse = gather_ordered(local, len(t.keep) * V, rank, world, group, dev).cpu().numpy()
     q = mean_psnr(sse, [c.resolution[0] * c.resolution[1] * 3 for c in cams], V)
     levels = [pruning.PruningLevel(ratio=t.ratios[j], quality_db=qq, size_bytes=t.sizes[j], pruned_indices=rm)
-              for j, qq, rm in zip(t.keep, q, t.removed)]
+              for j, qq, rm in zip(t.keep, q, pruning.level_removed(t))]
     return pruning.PruningLevelSpace(levels=tuple(levels), frame_index=frame_index)
