@@ -7,6 +7,7 @@ GPU is visible, every compute entry point raises.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 import threading
@@ -208,10 +209,12 @@ class Engine:
 
 
 _engines: dict = {}
+_tls = threading.local()
 
 
 def engine(device=None) -> Engine:
-    """The process-wide engine for ``device`` (default: torch's current)."""
+    """The process-wide engine for ``device`` (default: torch's current), or
+    the current thread's engine lane on it (see ``engine_lane``)."""
     import torch
 
     if device is None:
@@ -219,13 +222,27 @@ def engine(device=None) -> Engine:
     if isinstance(device, torch.device):
         device = device.index if device.index is not None else torch.cuda.current_device()
     device = int(device)
+    key = device if getattr(_tls, "lane", 0) == 0 else (device, _tls.lane)
     with _lock:
-        eng = _engines.get(device)
+        eng = _engines.get(key)
     if eng is None:
         eng = Engine(device)
         with _lock:
-            _engines[device] = eng
+            _engines[key] = eng
     return eng
+
+
+@contextlib.contextmanager
+def engine_lane(lane: int):
+    """Route this thread's calls to a second (third, ...) engine on the same
+    device: its own context and scratch, so that independent work on another
+    stream (e.g. the next frame of a probe batch) can be in flight at once."""
+    prev = getattr(_tls, "lane", 0)
+    _tls.lane = int(lane)
+    try:
+        yield
+    finally:
+        _tls.lane = prev
 
 
 def ptr(t) -> vp:

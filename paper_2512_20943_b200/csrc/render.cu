@@ -1319,6 +1319,9 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_SIGNBITS
 #define C2_SIGNBITS 1
 #endif
+#ifndef C2_EXTRA_SMEM
+#define C2_EXTRA_SMEM 0
+#endif
 #ifndef C2_FACTOR_BLEND
 #define C2_FACTOR_BLEND 0  // measured slower (profiles/r2_composite_experiments.md): off
 #endif
@@ -1727,7 +1730,9 @@ static void launch_composite2(int64_t tiles, cudaStream_t st, const CompItem *it
                               int nitems, const TileLists &tl, const uint32_t *tcount) {
     auto *fn = k_compositeN<USAGE, C2_NP>;
     if (C2_STATIC_SMEM) {
-        fn<<<(unsigned)tiles, CompNGeom<C2_NP>::kThreads, 0, st>>>(items, tile_base, nitems, tl, tcount);
+        // C2_EXTRA_SMEM (experiments): unused dynamic shared memory that caps the
+        // CTAs per SM, leaving registers for kernels of another stream
+        fn<<<(unsigned)tiles, CompNGeom<C2_NP>::kThreads, C2_EXTRA_SMEM, st>>>(items, tile_base, nitems, tl, tcount);
         return;
     }
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CompNShared<C2_NP>));

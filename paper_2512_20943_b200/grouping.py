@@ -16,6 +16,7 @@ reference's own driver runs on top of this module's probe.
 from __future__ import annotations
 
 import json
+import os
 
 import numpy as np
 
@@ -255,6 +256,19 @@ def probe_sequence(space, cams, payloads, targets, tau_db: float = DEFAULT_TAU_D
     return out
 
 
+PROBE_LANES = 1  # frames of a pipelined probe batch alternate over this many (engine, stream) lanes
+_lane_streams: dict = {}
+
+
+def _lane_stream(dev, lane):
+    import torch
+
+    key = (str(dev), lane)
+    if key not in _lane_streams:
+        _lane_streams[key] = torch.cuda.Stream(device=dev)
+    return _lane_streams[key]
+
+
 def probe_payload_items(space, cams, payloads, payload_devs, targets, items, device=None):
     """Per-item SSE of (frame t, view v) items of a probe batch whose GSDP
     payloads and targets are already in HBM: each frame that has items is
@@ -270,7 +284,7 @@ def probe_payload_items(space, cams, payloads, payload_devs, targets, items, dev
     import torch
 
     from . import codec
-    from ._lib import engine
+    from ._lib import engine, engine_lane
     from .model import GaussianFrame, as_space
     from .rasterizer import render_views
 
@@ -290,28 +304,47 @@ def probe_payload_items(space, cams, payloads, payload_devs, targets, items, dev
     pieces = []
 
     frames_in_order = list(by_frame)
+    lanes = max(1, int(os.environ.get("AIRGS_PROBE_LANES", str(PROBE_LANES))))
+    lanes = min(lanes, len(frames_in_order))
+    main = torch.cuda.current_stream(dev)
+    streams = [main] + [_lane_stream(dev, k) for k in range(1, lanes)]
 
-    def run():
+    def run(nl):
         pieces.clear()
+        for s in streams[1:nl]:
+            s.wait_stream(main)  # inputs enqueued on the caller's stream
         for k, (t, lst) in enumerate(by_frame.items()):
-            # the next frame's varint scan is enqueued ahead (side stream) under deferred checking
-            nxt = frames_in_order[k + 1] if k + 1 < len(frames_in_order) else None
+            lane = k % nl
+            # the lane's next frame: its varint scan is enqueued ahead (side stream)
+            nxt = frames_in_order[k + nl] if k + nl < len(frames_in_order) else None
             ahead = (datas[nxt], payload_devs[nxt]) if nxt is not None else None
-            planes = codec.decode_apply_device(datas[t], canon, n, w, device=dev, payload_dev=payload_devs[t],
-                                               ahead=ahead)
-            pieces.append(render_views([GaussianFrame(device_params=planes, count=n)], cams,
-                                       [(0, v) for _, v in lst], targets=[targets[t][v] for _, v in lst],
-                                       device=dev).sse)
+            with torch.cuda.stream(streams[lane]), engine_lane(lane):
+                planes = codec.decode_apply_device(datas[t], canon, n, w, device=dev, payload_dev=payload_devs[t],
+                                                   ahead=ahead)
+                sse = render_views([GaussianFrame(device_params=planes, count=n)], cams,
+                                   [(0, v) for _, v in lst], targets=[targets[t][v] for _, v in lst],
+                                   device=dev).sse
+            if lane:
+                sse.record_stream(main)  # consumed on the caller's stream
+            pieces.append(sse)
+        for s in streams[1:nl]:
+            main.wait_stream(s)
 
-    eng = engine(dev)
-    flags = ctypes.c_uint32(0)
-    eng.call("airgs_defer", 1, ctypes.byref(flags))
+    engs = []
+    flags = []
+    for lane in range(lanes):
+        with engine_lane(lane):
+            engs.append(engine(dev))
+        flags.append(ctypes.c_uint32(0))
+    for e, f in zip(engs, flags):
+        e.call("airgs_defer", 1, ctypes.byref(f))
     try:
-        run()
+        run(lanes)
     finally:
-        eng.call("airgs_defer", 0, ctypes.byref(flags))
-    if flags.value:
-        run()  # checked mode
+        for e, f in zip(engs, flags):
+            e.call("airgs_defer", 0, ctypes.byref(f))
+    if any(f.value for f in flags):
+        run(1)  # checked mode, one lane
     return _in_item_order(pieces, order, len(items), dev)
 
 

@@ -12,7 +12,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 python tools/launches.py gpurun_out/launches_$TAG.csv > gpurun_out/launches_summary_$TAG.txt
 timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:k_composite -c 1 \
   -o gpurun_out/prof_composite_$TAG -f python tools/step_once.py --reps 1 > gpurun_out/ncu2_$TAG.log 2>&1; echo "ncu2=$?"
-timeout 900 ncu --set full --clock-control none --profile-from-start off -k "regex:k_project|k_bin|k_sort_tiles" -c 4 \
+timeout 900 ncu --set full --clock-control none --profile-from-start off -k "regex:k_project|k_bin|k_sort_tiles|k_gsdp_da" -c 7 \
   -o gpurun_out/prof_others_$TAG -f python tools/step_once.py --reps 1 > gpurun_out/ncu3_$TAG.log 2>&1; echo "ncu3=$?"
 python tools/ncu_summary.py gpurun_out/prof_composite_$TAG.ncu-rep 40 --traffic-json gpurun_out/composite_traffic_$TAG.json \
   > gpurun_out/composite_ncu_$TAG.txt 2>&1
