@@ -20,7 +20,9 @@
 // Tiles whose list exceeds the in-shared-memory sort capacity are sorted
 // beforehand by a segmented radix sort over (index, then depth key).
 #include <algorithm>
+#include <cstring>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "context.h"
@@ -1322,11 +1324,18 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_EXTRA_SMEM
 #define C2_EXTRA_SMEM 0
 #endif
-#ifndef C2_FACTOR_BLEND
-#define C2_FACTOR_BLEND 0  // measured slower (profiles/r2_composite_experiments.md): off
-#endif
 #ifndef C2_ELLIPSE_CULL
 #define C2_ELLIPSE_CULL 0  // measured slower (profiles/r2_composite_experiments.md): off
+#endif
+#ifndef C2_PERSIST
+#define C2_PERSIST 0  // measured slower (profiles/r2_composite_experiments.md): off
+#endif
+#ifndef C2_NOCLAMP
+#define C2_NOCLAMP 1
+#endif
+constexpr double kNoClampAlpha = 0.998;
+#ifndef C2_PA2
+#define C2_PA2 1  // phase A as dy (C dy + B dx) + (A dx dx - L): -1.7% composite (r2 experiments)
 #endif
 
 // Lower bound (conservative by 1e-4 of the terms' magnitude + 1e-3, far above
@@ -1386,7 +1395,8 @@ __device__ unsigned long long g_c2c[10];
 template <bool USAGE, int NP>
 __global__ void __launch_bounds__(CompNGeom<NP>::kThreads, C2_MIN_BLOCKS)
 k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
-             const TileLists tls, const uint32_t *__restrict__ tcount) {
+             const TileLists tls, const uint32_t *__restrict__ tcount, unsigned int *__restrict__ work,
+             int64_t ntiles_all) {
     using G = CompNGeom<NP>;
 #if C2_STATIC_SMEM
     // static shared memory (< 48 KB): constant shared addresses fold into the
@@ -1397,7 +1407,19 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
     CompNShared<NP> &sh = *reinterpret_cast<CompNShared<NP> *>(compn_smem);
 #endif
     load_exp_table(sh.exptab, G::kThreads);
+#if C2_PERSIST
+    // persistent CTAs take tiles from a counter: one exp-table load and CTA
+    // start per SM slot instead of per tile (the grab's barrier also separates
+    // a tile's last batch from the next tile's staging)
+    __shared__ unsigned int s_tile;
+    for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(work, 1u);
+    __syncthreads();
+    const int64_t g = s_tile;
+    if (g >= ntiles_all) break;
+#else
     const int64_t g = blockIdx.x;
+#endif
     int lo = 0, hi = nitems - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -1448,6 +1470,7 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
 
     for (int base = 0; base < n_all; base += kC2Batch) {
         const int nb = min(kC2Batch, n_all - base);
+        bool hi_alpha = false;
         for (int t = threadIdx.x; t < nb; t += G::kThreads) {
             const uint32_t gi = (uint32_t)glist[base + t];
             if (COMP_PREFETCH && base + kC2Batch + t < n_all) {
@@ -1504,8 +1527,9 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
 #endif
             sh.wmask[t] = (uint8_t)mk;
             if (USAGE) sh.cnt[t] = 0;
+            hi_alpha |= r.al > kNoClampAlpha;
         }
-        __syncthreads();
+        const bool batch_clamp = __syncthreads_or(hi_alpha) != 0;
 #ifdef C2_COUNT
         if (threadIdx.x == 0) atomicAdd(&g_c2c[5], (unsigned long long)nb);
 #endif
@@ -1569,14 +1593,26 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                     const float2 C = make_float2(p2.x, p2.y), L = make_float2(p2.z, p2.w);
                     const float2 dx = __fadd2_rn(px2, make_float2(p0.x, p0.y));
                     const float2 my = make_float2(p0.z, p0.w);
+#if C2_PA2
+                    // e' - L = dy (C dy + B dx) + (A dx dx - L): the dx terms once per pair,
+                    // 4 packed ops per pixel instead of 5 (same error class as below: every
+                    // rounding is relative to terms bounded by 2 (A dx^2 + C dy^2))
+                    const float2 Bdx = __fmul2_rn(B, dx);
+                    const float2 K = __ffma2_rn(__fmul2_rn(A, dx), dx, L);
+#else
                     const float2 Adx = __fmul2_rn(A, dx);
+#endif
 #pragma unroll
                     for (int k = 0; k < NP; ++k) {
                         const float yk = (float)(ly0 + k) + 0.5f;
                         const float2 dy = __fadd2_rn(make_float2(yk, yk), my);
+#if C2_PA2
+                        const float2 e = __ffma2_rn(dy, __ffma2_rn(C, dy, Bdx), K);
+#else
                         const float2 u = __ffma2_rn(B, dy, Adx);
                         const float2 qv = __ffma2_rn(__fmul2_rn(C, dy), dy, L);
                         const float2 e = __ffma2_rn(u, dx, qv);
+#endif
 #if C2_SIGNBITS
                         // candidate iff e < thr: the sign bit of fl(e - thr) (exact sign;
                         // e == thr rejects, inside the guard band), appended with one
@@ -1617,62 +1653,61 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                 }
             }
 #endif
-            // phase B: the union of the NP candidate sets in depth order
+            // phase B: the union of the NP candidate sets in depth order.  The
+            // alpha clamp is compiled out for batches whose opacities are all
+            // <= kNoClampAlpha: g = exp(-e) <= 1 + 1e-12 (e >= -1e-12: the conic
+            // is positive definite, e only rounds), so ap = fl(al g) < 0.999
+            // and min(ap, 0.999) = ap exactly.
             const uint8_t *sid = &sh.sidx[w][c];
-            for (; wu; wu &= wu - 1) {
-                const int pos = __ffs(wu) - 1;
-                const int j = sid[pos];
-                const double2 mm = sh.m[j], ab = sh.hab[j], ca = sh.hcal[j];
-                const double2 rg = sh.rg[j];
-                const double bl = sh.bl[j];
-                const double dx = pxd - mm.x;
-                const double ex = ab.x * dx * dx;
-                int nc = 0;
+            auto phase_b = [&](auto clamp_tag) {
+                constexpr bool kClamp = decltype(clamp_tag)::value;
+                for (; wu; wu &= wu - 1) {
+                    const int pos = __ffs(wu) - 1;
+                    const int j = sid[pos];
+                    const double2 mm = sh.m[j], ab = sh.hab[j], ca = sh.hcal[j];
+                    const double2 rg = sh.rg[j];
+                    const double bl = sh.bl[j];
+                    const double dx = pxd - mm.x;
+                    const double ex = ab.x * dx * dx;
+                    int nc = 0;
 #pragma unroll
-                for (int k = 0; k < NP; ++k) {
-                    const double dy = ((double)(oy + ly0 + k) + 0.5) - mm.y;
-                    const double ee = (ex + ca.x * dy * dy) + ab.y * dx * dy;
-                    double ap = ca.y * exp_tab(-ee, tab);
-                    ap = ap > kCompC[6] ? kCompC[6] : ap;
-                    double x = ap * T[k];
-                    const bool cp = ((wd[k] >> pos) & 1u) && x > kCompC[7];
+                    for (int k = 0; k < NP; ++k) {
+                        const double dy = ((double)(oy + ly0 + k) + 0.5) - mm.y;
+                        const double ee = (ex + ca.x * dy * dy) + ab.y * dx * dy;
+                        double ap = ca.y * exp_tab(-ee, tab);
+                        if (kClamp) ap = ap > kCompC[6] ? kCompC[6] : ap;
+                        double x = ap * T[k];
+                        const bool cp = ((wd[k] >> pos) & 1u) && x > kCompC[7];
 #ifdef C2_COUNT
-                    if (cp) atomicAdd(&g_c2c[3], 1ull);
-                    if ((wd[k] >> pos) & 1u) {
-                        if (kAlphaClamp * T[k] <= kEpsContrib) atomicAdd(&g_c2c[6], 1ull);  // already terminated
-                        else if (!cp) atomicAdd(&g_c2c[7], 1ull);  // alive, weight test fails
-                    }
+                        if (cp) atomicAdd(&g_c2c[3], 1ull);
+                        if ((wd[k] >> pos) & 1u) {
+                            if (kAlphaClamp * T[k] <= kEpsContrib) atomicAdd(&g_c2c[6], 1ull);  // already terminated
+                            else if (!cp) atomicAdd(&g_c2c[7], 1ull);  // alive, weight test fails
+                        }
 #endif
-                    if (!USAGE) {
-#if C2_FACTOR_BLEND
-                        // branch-free through one factor f = cp ? ap : 0: x = f*T is the
-                        // reference's ap*T (or 0), T*(1 - f) its T*(1 - ap) (or T*1 = T)
-                        // -- one select pair and one extra DMUL instead of two select pairs
-                        const double f = cp ? ap : 0.0;
-                        x = f * T[k];
-                        cr[k] += x * rg.x;
-                        cg[k] += x * rg.y;
-                        cb[k] += x * bl;
-                        T[k] = T[k] * (1.0 - f);
-#else
-                        // branch-free: a non-contributing entry adds exact zeros, keeps T
-                        x = cp ? x : 0.0;
-                        cr[k] += x * rg.x;
-                        cg[k] += x * rg.y;
-                        cb[k] += x * bl;
-                        const double Tn = T[k] * (1.0 - ap);
-                        T[k] = cp ? Tn : T[k];
-#endif
-                    } else if (cp) {
-                        cr[k] += x * rg.x;
-                        cg[k] += x * rg.y;
-                        cb[k] += x * bl;
-                        T[k] = T[k] * (1.0 - ap);
-                        ++nc;
+                        if (!USAGE) {
+                            // branch-free: a non-contributing entry adds exact zeros, keeps T
+                            x = cp ? x : 0.0;
+                            cr[k] += x * rg.x;
+                            cg[k] += x * rg.y;
+                            cb[k] += x * bl;
+                            const double Tn = T[k] * (1.0 - ap);
+                            T[k] = cp ? Tn : T[k];
+                        } else if (cp) {
+                            cr[k] += x * rg.x;
+                            cg[k] += x * rg.y;
+                            cb[k] += x * bl;
+                            T[k] = T[k] * (1.0 - ap);
+                            ++nc;
+                        }
                     }
+                    if (USAGE && nc) atomicAdd(&sh.cnt[j], nc);
                 }
-                if (USAGE && nc) atomicAdd(&sh.cnt[j], nc);
-            }
+            };
+            if (C2_NOCLAMP && !batch_clamp)
+                phase_b(std::false_type{});
+            else
+                phase_b(std::true_type{});
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
                 done[k] = done[k] || kAlphaClamp * T[k] <= kEpsContrib;
@@ -1723,21 +1758,35 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             for (int k = G::kWarps + w; k < kCompWarps; k += G::kWarps) it.sse_tiles[(int64_t)tl * kCompWarps + k] = 0.0;
         }
     }
+#if C2_PERSIST
+    __syncthreads();  // s_tile is read by every thread before the next grab
+    }
+#endif
 }
 
 template <bool USAGE>
 static void launch_composite2(int64_t tiles, cudaStream_t st, const CompItem *items, const int64_t *tile_base,
-                              int nitems, const TileLists &tl, const uint32_t *tcount) {
+                              int nitems, const TileLists &tl, const uint32_t *tcount, unsigned int *work) {
     auto *fn = k_compositeN<USAGE, C2_NP>;
+    unsigned grid = (unsigned)tiles;
+    if (C2_PERSIST) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * C2_MIN_BLOCKS);
+    }
     if (C2_STATIC_SMEM) {
         // C2_EXTRA_SMEM (experiments): unused dynamic shared memory that caps the
         // CTAs per SM, leaving registers for kernels of another stream
-        fn<<<(unsigned)tiles, CompNGeom<C2_NP>::kThreads, C2_EXTRA_SMEM, st>>>(items, tile_base, nitems, tl, tcount);
+        fn<<<grid, CompNGeom<C2_NP>::kThreads, C2_EXTRA_SMEM, st>>>(items, tile_base, nitems, tl, tcount, work, tiles);
         return;
     }
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CompNShared<C2_NP>));
-    fn<<<(unsigned)tiles, CompNGeom<C2_NP>::kThreads, sizeof(CompNShared<C2_NP>), st>>>(items, tile_base, nitems,
-                                                                                        tl, tcount);
+    fn<<<grid, CompNGeom<C2_NP>::kThreads, sizeof(CompNShared<C2_NP>), st>>>(items, tile_base, nitems, tl, tcount,
+                                                                             work, tiles);
 }
 
 // Diagnostic counters: for every (primitive, pixel of its clipped bbox) pair of
@@ -2139,9 +2188,14 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         rec->cbits = cbits;
         rec->cbase = cbase;
     }
-    CompItem *d_ci = (CompItem *)ctx->scratch(kSlotMisc1, sizeof(CompItem) * nitems);
+    // item descriptors, then the persistent compositing kernel's work counter (zero)
+    const size_t ci_bytes = sizeof(CompItem) * nitems;
+    CompItem *d_ci = (CompItem *)ctx->scratch(kSlotMisc1, ci_bytes + 16);
     uint8_t *d_has = (uint8_t *)ctx->scratch(kSlotMisc2, nitems);
-    h2d_small(ctx, d_ci, ci.data(), sizeof(CompItem) * nitems, st);
+    std::vector<unsigned char> ci_up(ci_bytes + 16, 0);
+    std::memcpy(ci_up.data(), ci.data(), ci_bytes);
+    h2d_small(ctx, d_ci, ci_up.data(), ci_bytes + 16, st);
+    unsigned int *d_work = reinterpret_cast<unsigned int *>(reinterpret_cast<char *>(d_ci) + ci_bytes);
     h2d_small(ctx, d_has, has_t.data(), nitems, st);
     StageScope t_comp(ctx, st, kStageComposite, Tt > 0);
     if (Tt > 0) {
@@ -2169,9 +2223,9 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
                 launch_composite<false, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         } else if (COMP_PX2) {
             if (any_usage)
-                launch_composite2<true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count);
+                launch_composite2<true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, d_work);
             else
-                launch_composite2<false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count);
+                launch_composite2<false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, d_work);
         } else if (any_usage) {
             launch_composite<true, false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         } else {
