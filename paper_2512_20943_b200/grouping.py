@@ -128,6 +128,36 @@ def _in_item_order(pieces, order, n_items, dev):
     return out
 
 
+_STREAM_BUFS: dict = {}
+
+
+def _stream_buffers(dev, cap, view_shapes):
+    """Double buffers of the streamed probe, kept per device across calls and
+    grown on demand: two pinned host payload buffers of >= cap bytes (a
+    cudaHostAlloc synchronises the device and costs milliseconds), two device
+    payload buffers, and per buffer one device float64 target image per
+    (view, shape) in ``view_shapes``.  Returns (pinned[2], dpay[2],
+    [{view: tensor}] * 2)."""
+    import torch
+
+    key = str(dev)
+    st = _STREAM_BUFS.get(key)
+    if st is None or st["cap"] < cap:
+        c = max(int(cap), 1)
+        st = {"cap": c, "tg": [{}, {}] if st is None else st["tg"],
+              "pinned": [torch.empty((c,), dtype=torch.uint8).pin_memory() for _ in range(2)],
+              "dpay": [torch.empty((c,), dtype=torch.uint8, device=dev) for _ in range(2)]}
+        _STREAM_BUFS[key] = st
+    dtg = []
+    for b in range(2):
+        cache = st["tg"][b]
+        for v, shp in view_shapes.items():
+            if (v, shp) not in cache:
+                cache[(v, shp)] = torch.empty(shp, dtype=torch.float64, device=dev)
+        dtg.append({v: cache[(v, shp)] for v, shp in view_shapes.items()})
+    return st["pinned"], st["dpay"], dtg
+
+
 def probe_sequence_items(space, cams, payloads, targets, items, device=None):
     """Per-item SSE of (frame t, view v) items streamed from host memory: for
     each frame that has items, its GSDP payload and the items' (h, w, 3)
@@ -154,7 +184,6 @@ def probe_sequence_items(space, cams, payloads, targets, items, device=None):
     n, w = space.frame.count, space.frame.width
     canon = space.frame.planes(dev)
     comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
     by_frame = {}
     for k, (t, v) in enumerate(items):
         by_frame.setdefault(int(t), []).append((k, int(v)))
@@ -166,57 +195,60 @@ def probe_sequence_items(space, cams, payloads, targets, items, device=None):
         for _, v in by_frame[t]:
             if tuple(targets[t][v].shape) != res[v]:
                 raise StructuralError("target resolution does not match camera")
-    # double buffers allocated once: pinned payload staging (no per-frame cudaHostAlloc,
-    # which synchronises the device) and device targets / payloads (no allocator churn)
-    pinned = [torch.empty((max(cap, 1),), dtype=torch.uint8).pin_memory() for _ in range(2)]
-    dpay = [torch.empty((max(cap, 1),), dtype=torch.uint8, device=dev) for _ in range(2)]
-    views = sorted({v for lst in by_frame.values() for _, v in lst})
-    dtg = [{v: torch.empty(res[v], dtype=torch.float64, device=dev) for v in views} for _ in range(2)]
+    # double buffers, kept across calls (_stream_buffers): pinned payload staging (a
+    # cudaHostAlloc synchronises the device and costs milliseconds) and device
+    # targets / payloads (no allocator churn)
+    pinned, dpay, dtg = _stream_buffers(dev, cap, {v: res[v] for lst in by_frame.values() for _, v in lst})
+    bufst = _STREAM_BUFS[str(dev)]
+    copy = bufst.setdefault("copy", torch.cuda.Stream(dev))
 
     def host_tensor(im):
         return im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im, dtype=np.float64))
 
     def run():
-        used = [None, None]  # compute finished with buffer b (device event)
-        copied = [None, None]  # H2D out of pinned[b] finished (host waits before rewriting it)
+        # the buffers outlive the call: start from the previous call's last uses
+        used = list(bufst.get("used", [None, None]))  # compute finished with buffer b (device event)
+        copied = list(bufst.get("copied", [None, None]))  # H2D out of pinned[b] finished (host waits before rewriting it)
         ready = [None, None]
         pieces = []
-
-        def stage(k):
-            t = order[k]
-            b = k % 2
-            data = datas[t]
-            if copied[b] is not None:
-                copied[b].synchronize()
-            if data:
-                pinned[b][: len(data)].copy_(torch.frombuffer(bytearray(data), dtype=torch.uint8))
-            with torch.cuda.stream(copy):
-                if used[b] is not None:
-                    copy.wait_event(used[b])  # buffer b's previous frame is done
-                for _, v in by_frame[t]:
-                    dtg[b][v].copy_(host_tensor(targets[t][v]), non_blocking=True)
+        try:
+            def stage(k):
+                t = order[k]
+                b = k % 2
+                data = datas[t]
+                if copied[b] is not None:
+                    copied[b].synchronize()
                 if data:
-                    dpay[b][: len(data)].copy_(pinned[b][: len(data)], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(copy)
-            ready[b] = copied[b] = ev
+                    pinned[b].numpy()[: len(data)] = np.frombuffer(data, dtype=np.uint8)
+                with torch.cuda.stream(copy):
+                    if used[b] is not None:
+                        copy.wait_event(used[b])  # buffer b's previous frame is done
+                    for _, v in by_frame[t]:
+                        dtg[b][v].copy_(host_tensor(targets[t][v]), non_blocking=True)
+                    if data:
+                        dpay[b][: len(data)].copy_(pinned[b][: len(data)], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy)
+                ready[b] = copied[b] = ev
 
-        if order:
-            stage(0)
-        for k, t in enumerate(order):
-            b = k % 2
-            comp.wait_event(ready[b])
-            if k + 1 < len(order):
-                stage(k + 1)
-            data = datas[t]
-            planes = codec.decode_apply_device(data, canon, n, w, device=dev, payload_dev=dpay[b][: len(data)])
-            lst = by_frame[t]
-            pieces.append(render_views([GaussianFrame(device_params=planes, count=n)], cams,
-                                       [(0, v) for _, v in lst], targets=[dtg[b][v] for _, v in lst],
-                                       device=dev).sse)
-            u = torch.cuda.Event()
-            u.record(comp)
-            used[b] = u
+            if order:
+                stage(0)
+            for k, t in enumerate(order):
+                b = k % 2
+                comp.wait_event(ready[b])
+                if k + 1 < len(order):
+                    stage(k + 1)
+                data = datas[t]
+                planes = codec.decode_apply_device(data, canon, n, w, device=dev, payload_dev=dpay[b][: len(data)])
+                lst = by_frame[t]
+                pieces.append(render_views([GaussianFrame(device_params=planes, count=n)], cams,
+                                           [(0, v) for _, v in lst], targets=[dtg[b][v] for _, v in lst],
+                                           device=dev).sse)
+                u = torch.cuda.Event()
+                u.record(comp)
+                used[b] = u
+        finally:
+            bufst["used"], bufst["copied"] = used, copied
         return pieces
 
     eng = engine(dev)

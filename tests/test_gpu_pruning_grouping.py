@@ -190,6 +190,12 @@ def test_probe_sequence_streams_from_host():
     got = grouping.probe_sequence(space, cams, payloads, targets, tau_db=60.0)
     assert [q for q, _ in got] == ref
     assert [k for _, k in got] == [not q >= 60.0 for q in ref]
+    # the double buffers outlive a call: back-to-back calls (reversed frame
+    # order, odd frame counts so buffer parity shifts) must not see each other's data
+    got2 = grouping.probe_sequence(space, cams, payloads[::-1][:3], targets[::-1][:3], tau_db=60.0)
+    got3 = grouping.probe_sequence(space, cams, payloads, targets, tau_db=60.0)
+    assert [q for q, _ in got2] == ref[::-1][:3]
+    assert [q for q, _ in got3] == ref
 
 
 def test_probe_payloads_device_pipelined_and_checked_rerun():
