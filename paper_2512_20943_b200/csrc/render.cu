@@ -1330,6 +1330,12 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_PERSIST
 #define C2_PERSIST 0  // measured slower (profiles/r2_composite_experiments.md): off
 #endif
+#ifndef C2_MSB
+#define C2_MSB 1  // -0.3% (r2 experiments)
+#endif
+#ifndef C2_PRED_BLEND
+#define C2_PRED_BLEND 1  // predicated blend, no selects: with C2_MSB -1.0% (r2 experiments)
+#endif
 #ifndef C2_NOCLAMP
 #define C2_NOCLAMP 1
 #endif
@@ -1566,6 +1572,9 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             }
             __syncwarp();
         }
+#ifdef C2_SKIP_AB  // experiment builds only: time without phases A and B (results wrong)
+        ncomp = 0;
+#endif
         for (int c = 0; c < ncomp; c += kC2Chunk) {
             if (__all_sync(0xffffffffu, all_done())) break;
             // phase A: the NP pixels against two entries per f32x2 sequence (dx shared)
@@ -1629,7 +1638,9 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             }
 #if C2_SIGNBITS
 #pragma unroll
-            for (int k = 0; k < NP; ++k) wd[k] = ntest ? __brev(wd[k]) >> (32 - ntest) : 0u;
+            // C2_MSB: keep the funnel-shift order (test i at bit ntest-1-i) and walk it from the
+            // most significant bit in phase B (one FLO per entry instead of BREV + FLO)
+            for (int k = 0; k < NP; ++k) wd[k] = C2_MSB ? wd[k] : (ntest ? __brev(wd[k]) >> (32 - ntest) : 0u);
 #endif
             unsigned wu = 0;
 #pragma unroll
@@ -1661,8 +1672,18 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             const uint8_t *sid = &sh.sidx[w][c];
             auto phase_b = [&](auto clamp_tag) {
                 constexpr bool kClamp = decltype(clamp_tag)::value;
+#if C2_MSB
+                for (; wu;) {
+                    const int hb = 31 - __clz(wu);
+                    const unsigned bm = 1u << hb;
+                    wu ^= bm;
+                    const int pos = ntest - 1 - hb;
+#define C2_CAND(k) ((wd[k] & bm) != 0u)
+#else
                 for (; wu; wu &= wu - 1) {
                     const int pos = __ffs(wu) - 1;
+#define C2_CAND(k) (((wd[k] >> pos) & 1u) != 0u)
+#endif
                     const int j = sid[pos];
                     const double2 mm = sh.m[j], ab = sh.hab[j], ca = sh.hcal[j];
                     const double2 rg = sh.rg[j];
@@ -1677,15 +1698,15 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                         double ap = ca.y * exp_tab(-ee, tab);
                         if (kClamp) ap = ap > kCompC[6] ? kCompC[6] : ap;
                         double x = ap * T[k];
-                        const bool cp = ((wd[k] >> pos) & 1u) && x > kCompC[7];
+                        const bool cp = C2_CAND(k) && x > kCompC[7];
 #ifdef C2_COUNT
                         if (cp) atomicAdd(&g_c2c[3], 1ull);
-                        if ((wd[k] >> pos) & 1u) {
+                        if (C2_CAND(k)) {
                             if (kAlphaClamp * T[k] <= kEpsContrib) atomicAdd(&g_c2c[6], 1ull);  // already terminated
                             else if (!cp) atomicAdd(&g_c2c[7], 1ull);  // alive, weight test fails
                         }
 #endif
-                        if (!USAGE) {
+                        if (!USAGE && !C2_PRED_BLEND) {
                             // branch-free: a non-contributing entry adds exact zeros, keeps T
                             x = cp ? x : 0.0;
                             cr[k] += x * rg.x;
@@ -1693,6 +1714,13 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                             cb[k] += x * bl;
                             const double Tn = T[k] * (1.0 - ap);
                             T[k] = cp ? Tn : T[k];
+                        } else if (!USAGE) {
+                            if (cp) {  // predicated, no selects
+                                cr[k] += x * rg.x;
+                                cg[k] += x * rg.y;
+                                cb[k] += x * bl;
+                                T[k] = T[k] * (1.0 - ap);
+                            }
                         } else if (cp) {
                             cr[k] += x * rg.x;
                             cg[k] += x * rg.y;
@@ -1704,6 +1732,10 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                     if (USAGE && nc) atomicAdd(&sh.cnt[j], nc);
                 }
             };
+#undef C2_CAND
+#ifdef C2_SKIP_B  // experiment builds only: time without phase B (results wrong)
+            if (wu == 0x12345678u)
+#endif
             if (C2_NOCLAMP && !batch_clamp)
                 phase_b(std::false_type{});
             else
@@ -1769,15 +1801,13 @@ static void launch_composite2(int64_t tiles, cudaStream_t st, const CompItem *it
                               int nitems, const TileLists &tl, const uint32_t *tcount, unsigned int *work) {
     auto *fn = k_compositeN<USAGE, C2_NP>;
     unsigned grid = (unsigned)tiles;
-    if (C2_PERSIST) {
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        }
-        grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * C2_MIN_BLOCKS);
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    if (C2_PERSIST) grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * C2_MIN_BLOCKS);
     if (C2_STATIC_SMEM) {
         // C2_EXTRA_SMEM (experiments): unused dynamic shared memory that caps the
         // CTAs per SM, leaving registers for kernels of another stream
