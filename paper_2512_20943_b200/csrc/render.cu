@@ -573,19 +573,22 @@ __constant__ double kCompC[9] = {kExpInvLn2N, kExpNegLn2HiN, kExpNegLn2LoN, kExp
 constexpr int kExpRep = EXP_REP;
 
 // copy of the exp table for this lane (pass to exp_tab)
+template <int REP = kExpRep>
 __device__ __forceinline__ const double2 *exp_lane_tab(const double2 *tab) {
-    return tab + (threadIdx.x & (kExpRep - 1));
+    return tab + (threadIdx.x & (REP - 1));
 }
 
+template <int REP = kExpRep>
 __device__ __forceinline__ void load_exp_table(double2 *tab, int nthreads) {
     const unsigned long long *src = &kExpTable[0][0];
-    for (int k = threadIdx.x; k < kExpN * kExpRep; k += nthreads) {
-        const int i = k / kExpRep;
+    for (int k = threadIdx.x; k < kExpN * REP; k += nthreads) {
+        const int i = k / REP;
         tab[k] = make_double2(__longlong_as_double((long long)src[2 * i]),
                               __longlong_as_double((long long)src[2 * i + 1]));
     }
 }
 
+template <int REP = kExpRep>
 __device__ __forceinline__ double exp_tab(double x, const double2 *__restrict__ tab) {
     const double shift = 6755399441055744.0;  // 1.5 * 2^52
     const double z = x * kCompC[0];
@@ -594,7 +597,7 @@ __device__ __forceinline__ double exp_tab(double x, const double2 *__restrict__ 
     kd = kd - shift;
     double r = fma(kd, kCompC[1], x);
     r = fma(kd, kCompC[2], r);
-    const double2 t = tab[(ki & (kExpN - 1)) * kExpRep];
+    const double2 t = tab[(ki & (kExpN - 1)) * REP];
     // scale 2^(k/N): add k/N to the table entry's exponent -- only the high word changes
     // ((ki << (52 - kExpBits)) has a zero low word), so one 32-bit add instead of a 64-bit one
     const int sb_hi = __double2hiint(t.y) + (int)((unsigned)ki << (52 - kExpBits - 32));
@@ -1330,6 +1333,12 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_PERSIST
 #define C2_PERSIST 0  // measured slower (profiles/r2_composite_experiments.md): off
 #endif
+#ifndef C2_EXP_REP
+#define C2_EXP_REP 1  // 2 and 4 copies measured slower (less L1 left for records)
+#endif
+// exp table copies of the evaluation kernel: lane l reads copy l % 4, entry-major,
+// so a quarter-warp's 128-bit lookups spread over more bank groups
+constexpr int kC2ExpRep = C2_EXP_REP;
 #ifndef C2_MSB
 #define C2_MSB 1  // -0.3% (r2 experiments)
 #endif
@@ -1376,7 +1385,7 @@ struct CompNGeom {
     static constexpr int kLanesPerRow = kSW;                  // lanes across the sub-tile
 };
 
-template <int NP>
+template <int NP, bool USAGE>
 struct CompNShared {
     double2 m[kC2Batch];     // mx, my
     double2 hab[kC2Batch];   // 0.5*a, b
@@ -1385,12 +1394,12 @@ struct CompNShared {
     double bl[kC2Batch];     // colour b
     float4 f0[kC2Batch];     // -(mx-ox), -(my-oy), A, B
     float2 f1[kC2Batch];     // C, -L
-    uint32_t gid[kC2Batch];
-    int32_t cnt[kC2Batch];
+    uint32_t gid[USAGE ? kC2Batch : 1];  // usage pass only
+    int32_t cnt[USAGE ? kC2Batch : 1];
     uint8_t wmask[kC2Batch];  // bit w: may touch warp w's sub-tile
     float4 pl[CompNGeom<NP>::kWarps][kC2List / 2][3];
     uint8_t sidx[CompNGeom<NP>::kWarps][kC2List];
-    double2 exptab[kExpN * kExpRep];
+    double2 exptab[kExpN * kC2ExpRep];
 };
 
 #ifdef C2_COUNT
@@ -1407,12 +1416,12 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
 #if C2_STATIC_SMEM
     // static shared memory (< 48 KB): constant shared addresses fold into the
     // load offsets instead of a base-register add per access
-    __shared__ CompNShared<NP> sh;
+    __shared__ CompNShared<NP, USAGE> sh;
 #else
     extern __shared__ __align__(16) unsigned char compn_smem[];
-    CompNShared<NP> &sh = *reinterpret_cast<CompNShared<NP> *>(compn_smem);
+    CompNShared<NP, USAGE> &sh = *reinterpret_cast<CompNShared<NP, USAGE> *>(compn_smem);
 #endif
-    load_exp_table(sh.exptab, G::kThreads);
+    load_exp_table<kC2ExpRep>(sh.exptab, G::kThreads);
 #if C2_PERSIST
     // persistent CTAs take tiles from a counter: one exp-table load and CTA
     // start per SM slot instead of per tile (the grab's barrier also separates
@@ -1447,7 +1456,7 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
     const double pxd = (double)px + 0.5;
     const Rec *__restrict__ recs = itp->recs;
     const unsigned lt_mask = (1u << lane) - 1u;
-    const double2 *tab = exp_lane_tab(sh.exptab);
+    const double2 *tab = exp_lane_tab<kC2ExpRep>(sh.exptab);
 
     const int n_all = tls.count(tcount, g);
     const uint64_t *__restrict__ glist = tls.list(g);
@@ -1486,7 +1495,7 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             }
             const Rec r = recs[gi];
             const float mxl = (float)(r.mx - (double)ox), myl = (float)(r.my - (double)oy);
-            sh.gid[t] = gi;
+            if (USAGE) sh.gid[t] = gi;
             const double kap = 1.0 - 2e-5;
             sh.f0[t] = make_float4(-mxl, -myl, (float)(0.5 * kLog2e * kap * r.ca), (float)(kLog2e * r.cb));
             sh.f1[t] = make_float2((float)(0.5 * kLog2e * kap * r.cc), -(__log2f((float)r.al) + 6e-5f));
@@ -1695,7 +1704,7 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                     for (int k = 0; k < NP; ++k) {
                         const double dy = ((double)(oy + ly0 + k) + 0.5) - mm.y;
                         const double ee = (ex + ca.x * dy * dy) + ab.y * dx * dy;
-                        double ap = ca.y * exp_tab(-ee, tab);
+                        double ap = ca.y * exp_tab<kC2ExpRep>(-ee, tab);
                         if (kClamp) ap = ap > kCompC[6] ? kCompC[6] : ap;
                         double x = ap * T[k];
                         const bool cp = C2_CAND(k) && x > kCompC[7];
@@ -1814,8 +1823,8 @@ static void launch_composite2(int64_t tiles, cudaStream_t st, const CompItem *it
         fn<<<grid, CompNGeom<C2_NP>::kThreads, C2_EXTRA_SMEM, st>>>(items, tile_base, nitems, tl, tcount, work, tiles);
         return;
     }
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CompNShared<C2_NP>));
-    fn<<<grid, CompNGeom<C2_NP>::kThreads, sizeof(CompNShared<C2_NP>), st>>>(items, tile_base, nitems, tl, tcount,
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CompNShared<C2_NP, USAGE>));
+    fn<<<grid, CompNGeom<C2_NP>::kThreads, sizeof(CompNShared<C2_NP, USAGE>), st>>>(items, tile_base, nitems, tl, tcount,
                                                                              work, tiles);
 }
 
