@@ -164,6 +164,8 @@ __global__ void __launch_bounds__(kProjThreads, PROJ_MIN_BLOCKS) k_project(ProjA
             cv[3 * r + c] = dot3_blas(m[3 * r] * s0, m[3 * r + 1] * s1, m[3 * r + 2] * s2, m[3 * c], m[3 * c + 1],
                                       m[3 * c + 2]);
     const bool live = valid && alpha > kEpsContrib;
+    // threshold-ellipse extent factor 2 max(t, 0), t = ln(al / EPS) (+ outward pad): per primitive
+    const double t2 = live ? 2.0 * fmax(log(alpha / kEpsContrib) * 1.0002 + 2e-4, 0.0) : 0.0;
     // SH degree 0: colour is view independent -- compute once
     double col0[3] = {0.0, 0.0, 0.0};
     if (W == 17 && live) {
@@ -260,9 +262,9 @@ __global__ void __launch_bounds__(kProjThreads, PROJ_MIN_BLOCKS) k_project(ProjA
             rec.al = alpha;
             {
                 // e >= dx^2 / (2 Sxx) with Sigma = cov2d, so |dx| > sqrt(2 t Sxx) => e > t
-                const double t = log(alpha / kEpsContrib) * 1.0002 + 2e-4;
-                const double hx = sqrt(2.0 * fmax(t, 0.0) * (a2 + 1e-9 * a2)) * 1.0002 + 1e-3;
-                const double hy = sqrt(2.0 * fmax(t, 0.0) * (c2 + 1e-9 * c2)) * 1.0002 + 1e-3;
+                // (t2 = 2 max(t, 0), t = ln(al/EPS) padded: view independent, hoisted)
+                const double hx = sqrt(t2 * (a2 + 1e-9 * a2)) * 1.0002 + 1e-3;
+                const double hy = sqrt(t2 * (c2 + 1e-9 * c2)) * 1.0002 + 1e-3;
                 rec.hx = det > 0.0 && isfinite(hx) ? (float)hx * 1.0001f : 1e30f;
                 rec.hy = det > 0.0 && isfinite(hy) ? (float)hy * 1.0001f : 1e30f;
             }
