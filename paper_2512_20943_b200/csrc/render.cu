@@ -670,70 +670,41 @@ __device__ __forceinline__ double alpha_at(const CompShared &sh, int j, double p
 }
 
 // ---- tile-list sort: ascending (depth key, primitive index) -----------------
-// Bitonic network over npad (power of 2) entries in shared memory.  Strides
-// below 64 run in registers on 64-entry warp segments (lane holds entries
-// lane and lane+32, partners via shuffles, no barriers); only strides >= 64
-// touch shared memory with block barriers.
-
-__device__ __forceinline__ bool kv_gt(uint64_t ka, uint32_t va, uint64_t kb, uint32_t vb) {
-    return ka > kb || (ka == kb && va > vb);
-}
+// Bitonic networks on unique 32-bit keys (depth bucket << position bits |
+// list position).  Block variant: strides below 64 run in registers on
+// 64-entry warp segments (lane holds entries lane and lane+32, partners via
+// shuffles, no barriers); only strides >= 64 touch shared memory.
 
 // in-register steps for strides s = smax .. 1 (smax <= 32) of bitonic size `size`
-__device__ __forceinline__ void warp_bitonic_steps(uint64_t &k0, uint32_t &v0, uint64_t &k1, uint32_t &v1, int e0,
-                                                   int size, int smax) {
+__device__ __forceinline__ void warp_bitonic_steps32(uint32_t &k0, uint32_t &k1, int e0, int size, int smax) {
     const int lane = threadIdx.x & 31;
     if (smax >= 32) {  // stride 32: the lane's own pair (e0, e0 + 32)
         const bool asc = (e0 & size) == 0;
-        if (kv_gt(k0, v0, k1, v1) == asc) {
-            const uint64_t tk = k0;
-            const uint32_t tv = v0;
-            k0 = k1;
-            v0 = v1;
-            k1 = tk;
-            v1 = tv;
-        }
+        const uint32_t lo = min(k0, k1), hi = max(k0, k1);
+        k0 = asc ? lo : hi;
+        k1 = asc ? hi : lo;
         smax = 16;
     }
     for (int st = smax; st > 0; st >>= 1) {
         const bool lower = (lane & st) == 0;
-        {
-            const uint64_t pk = __shfl_xor_sync(0xffffffffu, k0, st);
-            const uint32_t pv = __shfl_xor_sync(0xffffffffu, v0, st);
-            const bool asc = (e0 & size) == 0;
-            const bool gt = kv_gt(k0, v0, pk, pv);
-            if ((lower == asc) ? gt : !gt && (pk != k0 || pv != v0)) {
-                k0 = pk;
-                v0 = pv;
-            }
-        }
-        {
-            const uint64_t pk = __shfl_xor_sync(0xffffffffu, k1, st);
-            const uint32_t pv = __shfl_xor_sync(0xffffffffu, v1, st);
-            const bool asc = ((e0 + 32) & size) == 0;
-            const bool gt = kv_gt(k1, v1, pk, pv);
-            if ((lower == asc) ? gt : !gt && (pk != k1 || pv != v1)) {
-                k1 = pk;
-                v1 = pv;
-            }
-        }
+        const uint32_t p0 = __shfl_xor_sync(0xffffffffu, k0, st);
+        const uint32_t p1 = __shfl_xor_sync(0xffffffffu, k1, st);
+        const bool asc0 = (e0 & size) == 0, asc1 = ((e0 + 32) & size) == 0;
+        k0 = (lower == asc0) ? min(k0, p0) : max(k0, p0);
+        k1 = (lower == asc1) ? min(k1, p1) : max(k1, p1);
     }
 }
 
-// Exact path: (64-bit depth key, index) pairs, used when two entries of a
-// tile share a 32-bit depth bucket.
-__device__ __noinline__ void sort_tile_list(uint64_t *k, uint32_t *v, int npad) {
+// Block-wide ascending sort of npad (power of 2, >= 64) unique keys in shared memory.
+__device__ __forceinline__ void block_bitonic32(uint32_t *k, int npad) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // sizes 2..64: each warp sorts whole 64-entry segments in registers
-    for (int seg = w; seg * 64 < npad; seg += kTileThreads / 32) {
+    constexpr int kW = kTileThreads / 32;
+    for (int seg = w; seg * 64 < npad; seg += kW) {  // sizes 2..64 in registers
         const int e0 = seg * 64 + lane;
-        uint64_t k0 = k[e0], k1 = k[e0 + 32];
-        uint32_t v0 = v[e0], v1 = v[e0 + 32];
-        for (int size = 2; size <= 64; size <<= 1) warp_bitonic_steps(k0, v0, k1, v1, e0, size, size >> 1);
+        uint32_t k0 = k[e0], k1 = k[e0 + 32];
+        for (int size = 2; size <= 64; size <<= 1) warp_bitonic_steps32(k0, k1, e0, size, size >> 1);
         k[e0] = k0;
         k[e0 + 32] = k1;
-        v[e0] = v0;
-        v[e0 + 32] = v1;
     }
     __syncthreads();
     for (int size = 128; size <= npad; size <<= 1) {
@@ -742,26 +713,20 @@ __device__ __noinline__ void sort_tile_list(uint64_t *k, uint32_t *v, int npad) 
                 const int lo = ((i & ~(st - 1)) << 1) | (i & (st - 1));
                 const int hi = lo + st;
                 const bool asc = (lo & size) == 0;
-                const uint64_t ka = k[lo], kb = k[hi];
-                const uint32_t va = v[lo], vb = v[hi];
-                if (kv_gt(ka, va, kb, vb) == asc) {
+                const uint32_t ka = k[lo], kb = k[hi];
+                if ((ka > kb) == asc) {
                     k[lo] = kb;
                     k[hi] = ka;
-                    v[lo] = vb;
-                    v[hi] = va;
                 }
             }
             __syncthreads();
         }
-        for (int seg = w; seg * 64 < npad; seg += kTileThreads / 32) {
+        for (int seg = w; seg * 64 < npad; seg += kW) {
             const int e0 = seg * 64 + lane;
-            uint64_t k0 = k[e0], k1 = k[e0 + 32];
-            uint32_t v0 = v[e0], v1 = v[e0 + 32];
-            warp_bitonic_steps(k0, v0, k1, v1, e0, size, 32);
+            uint32_t k0 = k[e0], k1 = k[e0 + 32];
+            warp_bitonic_steps32(k0, k1, e0, size, 32);
             k[e0] = k0;
             k[e0 + 32] = k1;
-            v[e0] = v0;
-            v[e0 + 32] = v1;
         }
         __syncthreads();
     }
@@ -828,6 +793,8 @@ struct TileSortArgs {
     int64_t stride;
     uint32_t *slow_list;       // tiles needing the block-level exact sort
     unsigned int *slow_n;
+    uint32_t *mid_list;        // tiles for k_sort_tiles_long
+    unsigned int *mid_n;
     int64_t Tt;
 };
 
@@ -841,13 +808,18 @@ __device__ __forceinline__ int item_of_tile(const int64_t *__restrict__ tile_bas
 }
 
 // Sort one tile list (n <= 32 R) in registers on 32-bit keys: each entry's
-// fp32 depth bits are re-bucketed to 22 bits over the tile's own range, with
-// the entry's list position in the low 10 bits.  Distinct 22-bit buckets are
-// strictly depth ordered (fp32 rounding and bucketing are monotone); adjacent
-// equal buckets send the tile to the exact (64-bit depth key, index) block sort.
-template <int R>
-__device__ __forceinline__ void warp_sort_tile(const TileSortArgs &a, int64_t g, int n) {
+// fp32 depth bits are re-bucketed to 32 - PB bits over the tile's own range,
+// with the entry's list position in the low PB bits (PB = 10, or 11 for lists
+// above 1024).  Distinct buckets are strictly depth ordered (fp32 rounding and
+// bucketing are monotone), so the bucket sort is the exact order except inside
+// runs of equal buckets, where it is list order: those runs (rare, short) are
+// re-sorted in place on the exact (64-bit depth key, index) afterwards.
+// Only the primitive ids travel on (every consumer of a sorted list reads the
+// low word).
+template <int R, int PB>
+__device__ __forceinline__ void warp_sort_tile(const TileSortArgs &a, int64_t g, int n, uint32_t *sflags) {
     const int lane = threadIdx.x & 31;
+    constexpr uint32_t kPMask = (1u << PB) - 1u;
     uint64_t *lst = a.tl.list(g);
     uint32_t key[R];
     uint32_t bmin = 0xffffffffu, bmax = 0u;
@@ -864,14 +836,14 @@ __device__ __forceinline__ void warp_sort_tile(const TileSortArgs &a, int64_t g,
     bmin = __reduce_min_sync(0xffffffffu, bmin);
     bmax = __reduce_max_sync(0xffffffffu, bmax);
     const uint32_t span = bmax - bmin;
-    const int sh = max(0, (32 - __clz((int)span)) - 22);
+    const int sh = max(0, (32 - __clz((int)span)) - (32 - PB));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = lane + 32 * r;
-        key[r] = e < n ? (((key[r] - bmin) >> sh) << 10) | (uint32_t)e : 0xffffffffu;
+        key[r] = e < n ? (((key[r] - bmin) >> sh) << PB) | (uint32_t)e : 0xffffffffu;
     }
     warp_reg_bitonic<R>(key);
-    // adjacent entries in one 22-bit bucket need the exact comparison
+    // adjacent entries in one bucket: their exact order is fixed below
     bool clash = false;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -879,75 +851,162 @@ __device__ __forceinline__ void warp_sort_tile(const TileSortArgs &a, int64_t g,
         const uint32_t nxt_same = __shfl_down_sync(0xffffffffu, key[r], 1);
         const uint32_t nxt_row = __shfl_sync(0xffffffffu, key[r + 1 < R ? r + 1 : r], 0);
         const uint32_t nx = lane < 31 ? nxt_same : nxt_row;
-        if (e + 1 < n) clash |= (key[r] >> 10) == (nx >> 10);
+        const bool same = e + 1 < n && (key[r] >> PB) == (nx >> PB);
+        clash |= same;
+        if (sflags) {
+            const unsigned m = __ballot_sync(0xffffffffu, same);
+            if (lane == 0) sflags[r] = m;
+        }
     }
-    if (__any_sync(0xffffffffu, clash)) {
-        if (lane == 0) a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
-        return;
-    }
-    uint64_t out[R];
+    // gather the ids in sorted order (in place in key[]), then write them back
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = lane + 32 * r;
-        out[r] = e < n ? lst[key[r] & 1023u] : 0ull;
+        key[r] = e < n ? (uint32_t)lst[key[r] & kPMask] : 0u;
     }
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e = lane + 32 * r;
-        if (e < n) lst[e] = out[r];
+        if (e < n) lst[e] = key[r];
+    }
+    if (!__any_sync(0xffffffffu, clash)) return;
+    if (!sflags) {  // no flag scratch: the exact block sort takes the tile
+        if (lane == 0) a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
+        return;
+    }
+    __syncwarp();  // the written ids and the run flags are visible to the warp
+    const uint64_t *depth = a.depth + (int64_t)item_of_tile(a.tile_base, a.nitems, g) * a.stride;
+    auto same_next = [&](int e) { return (sflags[e >> 5] >> (e & 31)) & 1u; };
+    for (int e = lane; e < n; e += 32) {
+        if (!same_next(e) || (e > 0 && same_next(e - 1))) continue;  // not the start of a run
+        int end = e + 1;
+        while (same_next(end)) ++end;
+        // insertion sort of lst[e..end] on (64-bit depth key, index)
+        for (int i = e + 1; i <= end; ++i) {
+            const uint32_t id = (uint32_t)lst[i];
+            const uint64_t k = depth[id];
+            int j = i - 1;
+            while (j >= e) {
+                const uint32_t pj = (uint32_t)lst[j];
+                const uint64_t kj = depth[pj];
+                if (kj < k || (kj == k && pj < id)) break;
+                lst[j + 1] = pj;
+                --j;
+            }
+            lst[j + 1] = id;
+        }
     }
 }
 
-constexpr int kWarpSortMax = 512;
+#ifndef WARP_SORT_MAX
+#define WARP_SORT_MAX 512
+#endif
+constexpr int kWarpSortMax = WARP_SORT_MAX;  // lists up to this length: k_sort_tiles_warp (<= 64 registers)
 
-__global__ void __launch_bounds__(128) k_sort_tiles_warp(TileSortArgs a) {
+__global__ void __launch_bounds__(128, 8) k_sort_tiles_warp(TileSortArgs a) {
+    __shared__ uint32_t sflags[4][kWarpSortMax / 32];
     const int64_t g = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
     if (g >= a.Tt) return;
     const int n = a.tl.count(a.tcount, g);
     if (n <= 1 || n > kSortCap) return;  // > kSortCap: radix fallback already sorted it
-    if (n > kWarpSortMax) {
-        if ((threadIdx.x & 31) == 0) a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
+    if (n > kWarpSortMax) {  // the long-list warp sort (k_sort_tiles_long) takes it
+        if ((threadIdx.x & 31) == 0) a.mid_list[atomicAdd(a.mid_n, 1u)] = (uint32_t)g;
         return;
     }
-    if (n <= 32) warp_sort_tile<1>(a, g, n);
-    else if (n <= 64) warp_sort_tile<2>(a, g, n);
-    else if (n <= 128) warp_sort_tile<4>(a, g, n);
-    else if (n <= 256) warp_sort_tile<8>(a, g, n);
-    else warp_sort_tile<16>(a, g, n);
+    uint32_t *fl = sflags[threadIdx.x >> 5];
+    if (n <= 32) warp_sort_tile<1, 10>(a, g, n, fl);
+    else if (n <= 64) warp_sort_tile<2, 10>(a, g, n, fl);
+    else if (n <= 128) warp_sort_tile<4, 10>(a, g, n, fl);
+    else if (n <= 256) warp_sort_tile<8, 10>(a, g, n, fl);
+    else warp_sort_tile<16, 10>(a, g, n, fl);
 }
 
-// Exact block-level sort of one slow tile on (64-bit depth key, id).
-__device__ __noinline__ void sort_one_slow_tile(const TileSortArgs &a, int64_t g, uint64_t *skey, uint32_t *sid) {
-    const int n = a.tl.count(a.tcount, g);
-    const uint64_t *depth = a.depth + (int64_t)item_of_tile(a.tile_base, a.nitems, g) * a.stride;
-    uint64_t *lst = a.tl.list(g);
-    int npad = 64;
-    while (npad < n) npad <<= 1;
-    for (int k = threadIdx.x; k < npad; k += kTileThreads) {
-        if (k < n) {
-            const uint32_t id = (uint32_t)lst[k];
-            sid[k] = id;
-            skey[k] = depth[id];
-        } else {
-            sid[k] = 0xffffffffu;
-            skey[k] = ~0ull;
+// Lists of kWarpSortMax < n <= 1024: one warp each, keys in 32 registers,
+// walking the device-side list of such tiles (no host readback); longer lists
+// go on to the block sort.
+__global__ void __launch_bounds__(128, 4) k_sort_tiles_long(TileSortArgs a) {
+    __shared__ uint32_t sflags[4][1024 / 32];
+    const unsigned int nmid = *a.mid_n;
+    uint32_t *fl = sflags[threadIdx.x >> 5];
+    for (unsigned int b = blockIdx.x * 4 + (threadIdx.x >> 5); b < nmid; b += gridDim.x * 4) {
+        const int64_t g = a.mid_list[b];
+        const int n = a.tl.count(a.tcount, g);
+        if (n <= 1024) {
+            warp_sort_tile<32, 10>(a, g, n, fl);
+        } else if ((threadIdx.x & 31) == 0) {
+            a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
         }
     }
-    __syncthreads();
-    sort_tile_list(skey, sid, npad);
-    for (int k = threadIdx.x; k < n; k += kTileThreads) lst[k] = sid[k];
 }
 
-// Exact block-level sort on (64-bit depth key, id) for the slow tiles; a
-// fixed grid strides over the device-side slow list.
+// Block-level sort of one long tile (kSortCap >= n > 1024): 32-bit keys (21-bit
+// depth bucket << 11 | list position) sorted in shared memory, the ids
+// gathered in that order, runs of equal buckets re-sorted on the exact
+// (64-bit depth key, index), written back.
 __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs a) {
-    __shared__ uint64_t skey[kSortCap];
+    __shared__ uint32_t skey[kSortCap];
     __shared__ uint32_t sid[kSortCap];
+    __shared__ uint32_t sred[2][kTileThreads / 32];
     const unsigned int nslow = *a.slow_n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (unsigned int b = blockIdx.x; b < nslow; b += gridDim.x) {
         __syncthreads();
-        sort_one_slow_tile(a, a.slow_list[b], skey, sid);
+        const int64_t g = a.slow_list[b];
+        const int n = a.tl.count(a.tcount, g);
+        uint64_t *lst = a.tl.list(g);
+        int npad = 64;
+        while (npad < n) npad <<= 1;
+        uint32_t bmin = 0xffffffffu, bmax = 0u;
+        for (int e = threadIdx.x; e < n; e += kTileThreads) {
+            const uint32_t hb = (uint32_t)(lst[e] >> 32);
+            skey[e] = hb;
+            bmin = min(bmin, hb);
+            bmax = max(bmax, hb);
+        }
+        bmin = __reduce_min_sync(0xffffffffu, bmin);
+        bmax = __reduce_max_sync(0xffffffffu, bmax);
+        if (lane == 0) {
+            sred[0][w] = bmin;
+            sred[1][w] = bmax;
+        }
+        __syncthreads();
+        bmin = 0xffffffffu;
+        bmax = 0u;
+#pragma unroll
+        for (int k = 0; k < kTileThreads / 32; ++k) {
+            bmin = min(bmin, sred[0][k]);
+            bmax = max(bmax, sred[1][k]);
+        }
+        const int sh = max(0, (32 - __clz((int)(bmax - bmin))) - 21);
+        for (int e = threadIdx.x; e < npad; e += kTileThreads)
+            skey[e] = e < n ? (((skey[e] - bmin) >> sh) << 11) | (uint32_t)e : 0xffffffffu;
+        __syncthreads();
+        block_bitonic32(skey, npad);
+        for (int e = threadIdx.x; e < n; e += kTileThreads) sid[e] = (uint32_t)lst[skey[e] & 2047u];
+        __syncthreads();
+        const uint64_t *depth = a.depth + (int64_t)item_of_tile(a.tile_base, a.nitems, g) * a.stride;
+        auto same_next = [&](int e) { return e + 1 < n && (skey[e] >> 11) == (skey[e + 1] >> 11); };
+        for (int e = threadIdx.x; e < n; e += kTileThreads) {
+            if (!same_next(e) || (e > 0 && same_next(e - 1))) continue;  // not the start of a run
+            int end = e + 1;
+            while (same_next(end)) ++end;
+            for (int i = e + 1; i <= end; ++i) {  // insertion sort on (64-bit depth key, index)
+                const uint32_t id = sid[i];
+                const uint64_t kk = depth[id];
+                int j = i - 1;
+                while (j >= e) {
+                    const uint32_t pj = sid[j];
+                    const uint64_t kj = depth[pj];
+                    if (kj < kk || (kj == kk && pj < id)) break;
+                    sid[j + 1] = pj;
+                    --j;
+                }
+                sid[j + 1] = id;
+            }
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < n; e += kTileThreads) lst[e] = sid[e];
     }
 }
 
@@ -2150,14 +2209,16 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
     if (Tt > 0) {
         // depth-order every tile list: warp-level register sort, block-level exact sort for the rest
         unsigned int *slow_n = (unsigned int *)(stats + 3);
-        uint32_t *slow_list = ctx->scratch_t<uint32_t>(kSlotSlowTiles, (size_t)Tt);
-        AIRGS_CUDA_TRY(cudaMemsetAsync(slow_n, 0, sizeof(unsigned int), st));
-        TileSortArgs ta{tl, tile_count, L.d_tile_base, nitems, depth, L.stride, slow_list, slow_n, Tt};
+        uint32_t *slow_list = ctx->scratch_t<uint32_t>(kSlotSlowTiles, 2 * (size_t)Tt);
+        AIRGS_CUDA_TRY(cudaMemsetAsync(slow_n, 0, 2 * sizeof(unsigned int), st));
+        TileSortArgs ta{tl,          tile_count, L.d_tile_base, nitems,        depth, L.stride,
+                        slow_list,   slow_n,     slow_list + Tt, slow_n + 1,   Tt};
         StageScope t_sort(ctx, st, kStageSort);
         k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
-        // the exact block sort walks the device-side slow list (no host readback)
+        // the long-list warp sort and the exact block sort walk device-side tile lists (no host readback)
+        k_sort_tiles_long<<<(unsigned)std::min<int64_t>(ceil_div(Tt, 4), 1184), 128, 0, st>>>(ta);
         k_sort_tiles_block<<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
-        NL += 2;
+        NL += 3;
         check_launch();
         t_sort.end();
         if (ctx->dump.counts) {  // debug capture of the depth-ordered lists (airgs_debug_tile_lists)
