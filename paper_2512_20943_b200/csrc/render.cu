@@ -922,6 +922,9 @@ __global__ void __launch_bounds__(128, 8) k_sort_tiles_warp(TileSortArgs a) {
     else warp_sort_tile<16, 10>(a, g, n, fl);
 }
 
+#ifndef LONG_WARP_MAX
+#define LONG_WARP_MAX 1024
+#endif
 // Lists of kWarpSortMax < n <= 1024: one warp each, keys in 32 registers,
 // walking the device-side list of such tiles (no host readback); longer lists
 // go on to the block sort.
@@ -932,7 +935,7 @@ __global__ void __launch_bounds__(128, 4) k_sort_tiles_long(TileSortArgs a) {
     for (unsigned int b = blockIdx.x * 4 + (threadIdx.x >> 5); b < nmid; b += gridDim.x * 4) {
         const int64_t g = a.mid_list[b];
         const int n = a.tl.count(a.tcount, g);
-        if (n <= 1024) {
+        if (n <= LONG_WARP_MAX) {
             warp_sort_tile<32, 10>(a, g, n, fl);
         } else if ((threadIdx.x & 31) == 0) {
             a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
