@@ -39,9 +39,9 @@ def test_c2_view_tile_lists_bit_exact():
 
 def test_depth_ties_ordered_by_index():
     """Every primitive at exactly the same camera depth: the reference's
-    stable argsort keeps index order, and so must every tile list (the warp
-    sort's 22-bit buckets all clash and hand the tiles to the exact block
-    sort on (64-bit depth key, index))."""
+    stable argsort keeps index order, and so must every tile list (the
+    sort's depth buckets all clash: each tile is one run, re-sorted in place
+    on the exact (64-bit depth key, index))."""
     from paper_2512_20943_b200.camera import look_at
 
     rng = np.random.default_rng(11)
@@ -59,11 +59,13 @@ def test_depth_ties_ordered_by_index():
     _compare(p, cam)
 
 
-@pytest.mark.parametrize("count", [1500, 6000])
+@pytest.mark.parametrize("count", [800, 1500, 6000])
 def test_crowded_tiles_through_overflow_paths(count):
-    """Lists longer than the bucket capacity (512) and the in-shared-memory
-    sort (2048): the call is redone through scanned ranges and a segmented
-    radix presort; the lists are still the reference order."""
+    """Lists longer than the warp sort (512: the 32-keys-per-lane warp sort
+    up to 1024, the block sort up to 2048), the bucket capacity (512) and the
+    in-shared-memory sort (2048: the call is redone through scanned ranges
+    and a segmented radix presort); with exact depth ties inside the crowd,
+    the lists are still the reference order."""
     from paper_2512_20943_b200.camera import look_at
 
     rng = np.random.default_rng(count)
