@@ -25,6 +25,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <cub/block/block_radix_sort.cuh>
+
 #include "context.h"
 #include "exp_table.h"
 #include "scan_sort.cuh"
@@ -670,67 +672,8 @@ __device__ __forceinline__ double alpha_at(const CompShared &sh, int j, double p
 }
 
 // ---- tile-list sort: ascending (depth key, primitive index) -----------------
-// Bitonic networks on unique 32-bit keys (depth bucket << position bits |
-// list position).  Block variant: strides below 64 run in registers on
-// 64-entry warp segments (lane holds entries lane and lane+32, partners via
-// shuffles, no barriers); only strides >= 64 touch shared memory.
-
-// in-register steps for strides s = smax .. 1 (smax <= 32) of bitonic size `size`
-__device__ __forceinline__ void warp_bitonic_steps32(uint32_t &k0, uint32_t &k1, int e0, int size, int smax) {
-    const int lane = threadIdx.x & 31;
-    if (smax >= 32) {  // stride 32: the lane's own pair (e0, e0 + 32)
-        const bool asc = (e0 & size) == 0;
-        const uint32_t lo = min(k0, k1), hi = max(k0, k1);
-        k0 = asc ? lo : hi;
-        k1 = asc ? hi : lo;
-        smax = 16;
-    }
-    for (int st = smax; st > 0; st >>= 1) {
-        const bool lower = (lane & st) == 0;
-        const uint32_t p0 = __shfl_xor_sync(0xffffffffu, k0, st);
-        const uint32_t p1 = __shfl_xor_sync(0xffffffffu, k1, st);
-        const bool asc0 = (e0 & size) == 0, asc1 = ((e0 + 32) & size) == 0;
-        k0 = (lower == asc0) ? min(k0, p0) : max(k0, p0);
-        k1 = (lower == asc1) ? min(k1, p1) : max(k1, p1);
-    }
-}
-
-// Block-wide ascending sort of npad (power of 2, >= 64) unique keys in shared memory.
-__device__ __forceinline__ void block_bitonic32(uint32_t *k, int npad) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    constexpr int kW = kTileThreads / 32;
-    for (int seg = w; seg * 64 < npad; seg += kW) {  // sizes 2..64 in registers
-        const int e0 = seg * 64 + lane;
-        uint32_t k0 = k[e0], k1 = k[e0 + 32];
-        for (int size = 2; size <= 64; size <<= 1) warp_bitonic_steps32(k0, k1, e0, size, size >> 1);
-        k[e0] = k0;
-        k[e0 + 32] = k1;
-    }
-    __syncthreads();
-    for (int size = 128; size <= npad; size <<= 1) {
-        for (int st = size >> 1; st >= 64; st >>= 1) {
-            for (int i = threadIdx.x; i < (npad >> 1); i += kTileThreads) {
-                const int lo = ((i & ~(st - 1)) << 1) | (i & (st - 1));
-                const int hi = lo + st;
-                const bool asc = (lo & size) == 0;
-                const uint32_t ka = k[lo], kb = k[hi];
-                if ((ka > kb) == asc) {
-                    k[lo] = kb;
-                    k[hi] = ka;
-                }
-            }
-            __syncthreads();
-        }
-        for (int seg = w; seg * 64 < npad; seg += kW) {
-            const int e0 = seg * 64 + lane;
-            uint32_t k0 = k[e0], k1 = k[e0 + 32];
-            warp_bitonic_steps32(k0, k1, e0, size, 32);
-            k[e0] = k0;
-            k[e0 + 32] = k1;
-        }
-        __syncthreads();
-    }
-}
+// All sorts work on unique 32-bit keys (tile-local depth bucket << position
+// bits | list position); see warp_sort_tile and k_sort_tiles_radix.
 
 // ---- per-tile list sort kernels ------------------------------------------------
 // One warp per tile, entries e = lane + 32 r held in registers (R per lane);
@@ -793,7 +736,7 @@ struct TileSortArgs {
     int64_t stride;
     uint32_t *slow_list;       // tiles needing the block-level exact sort
     unsigned int *slow_n;
-    uint32_t *mid_list;        // tiles for k_sort_tiles_long
+    uint32_t *mid_list;        // tiles for k_sort_tiles_long (longer than kWarpSortMax)
     unsigned int *mid_n;
     int64_t Tt;
 };
@@ -943,25 +886,40 @@ __global__ void __launch_bounds__(128, 4) k_sort_tiles_long(TileSortArgs a) {
     }
 }
 
-// Block-level sort of one long tile (kSortCap >= n > 1024): 32-bit keys (21-bit
-// depth bucket << 11 | list position) sorted in shared memory, the ids
-// gathered in that order, runs of equal buckets re-sorted on the exact
-// (64-bit depth key, index), written back.
-__global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs a) {
-    __shared__ uint32_t skey[kSortCap];
-    __shared__ uint32_t sid[kSortCap];
-    __shared__ uint32_t sred[2][kTileThreads / 32];
-    const unsigned int nslow = *a.slow_n;
+// Block-level sort of long tile lists: 32-bit keys (depth bucket << PB | list
+// position, PB = log2 CAP) sorted by a stable block radix sort over the bucket
+// bits only (CUB's BlockRadixSort inside this kernel; the positions are already
+// ascending), the ids gathered in that order, runs of equal buckets re-sorted
+// on the exact (64-bit depth key, index), written back.  MID: the tiles of
+// kWarpSortMax < n <= CAP from the mid list (longer ones are forwarded to the
+// slow list); otherwise the slow list (n <= kSortCap).
+#ifndef SORT_CUB_BITS
+#define SORT_CUB_BITS 5
+#endif
+template <int CAP, int THREADS, bool MID>
+__global__ void __launch_bounds__(THREADS) k_sort_tiles_radix(TileSortArgs a) {
+    constexpr int kItems = CAP / THREADS;
+    constexpr int PB = CAP == 2048 ? 11 : (CAP == 1024 ? 10 : 9);
+    static_assert((1 << PB) == CAP, "power-of-two capacity");
+    using BlockRadix = cub::BlockRadixSort<uint32_t, THREADS, kItems, cub::NullType, SORT_CUB_BITS>;
+    __shared__ typename BlockRadix::TempStorage radix_tmp;
+    __shared__ uint32_t skey[CAP];
+    __shared__ uint32_t sid[CAP];
+    __shared__ uint32_t sred[2][THREADS / 32];
+    const unsigned int nlist = MID ? *a.mid_n : *a.slow_n;
+    const uint32_t *list = MID ? a.mid_list : a.slow_list;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (unsigned int b = blockIdx.x; b < nslow; b += gridDim.x) {
+    for (unsigned int b = blockIdx.x; b < nlist; b += gridDim.x) {
         __syncthreads();
-        const int64_t g = a.slow_list[b];
+        const int64_t g = list[b];
         const int n = a.tl.count(a.tcount, g);
+        if (MID && n > CAP) {
+            if (threadIdx.x == 0) a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
+            continue;
+        }
         uint64_t *lst = a.tl.list(g);
-        int npad = 64;
-        while (npad < n) npad <<= 1;
         uint32_t bmin = 0xffffffffu, bmax = 0u;
-        for (int e = threadIdx.x; e < n; e += kTileThreads) {
+        for (int e = threadIdx.x; e < n; e += THREADS) {
             const uint32_t hb = (uint32_t)(lst[e] >> 32);
             skey[e] = hb;
             bmin = min(bmin, hb);
@@ -977,20 +935,27 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs 
         bmin = 0xffffffffu;
         bmax = 0u;
 #pragma unroll
-        for (int k = 0; k < kTileThreads / 32; ++k) {
+        for (int k = 0; k < THREADS / 32; ++k) {
             bmin = min(bmin, sred[0][k]);
             bmax = max(bmax, sred[1][k]);
         }
-        const int sh = max(0, (32 - __clz((int)(bmax - bmin))) - 21);
-        for (int e = threadIdx.x; e < npad; e += kTileThreads)
-            skey[e] = e < n ? (((skey[e] - bmin) >> sh) << 11) | (uint32_t)e : 0xffffffffu;
+        const int sh = max(0, (32 - __clz((int)(bmax - bmin))) - (32 - PB));
+        uint32_t keys[kItems];  // blocked: thread t holds entries kItems t ..
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const int e = threadIdx.x * kItems + i;
+            keys[i] = e < n ? (((skey[e] - bmin) >> sh) << PB) | (uint32_t)e : 0xffffffffu;
+        }
+        __syncthreads();  // skey reads done before the sort's shared scratch / the write-back below
+        BlockRadix(radix_tmp).Sort(keys, PB, 32);
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) skey[threadIdx.x * kItems + i] = keys[i];
         __syncthreads();
-        block_bitonic32(skey, npad);
-        for (int e = threadIdx.x; e < n; e += kTileThreads) sid[e] = (uint32_t)lst[skey[e] & 2047u];
+        for (int e = threadIdx.x; e < n; e += THREADS) sid[e] = (uint32_t)lst[skey[e] & (CAP - 1)];
         __syncthreads();
         const uint64_t *depth = a.depth + (int64_t)item_of_tile(a.tile_base, a.nitems, g) * a.stride;
-        auto same_next = [&](int e) { return e + 1 < n && (skey[e] >> 11) == (skey[e + 1] >> 11); };
-        for (int e = threadIdx.x; e < n; e += kTileThreads) {
+        auto same_next = [&](int e) { return e + 1 < n && (skey[e] >> PB) == (skey[e + 1] >> PB); };
+        for (int e = threadIdx.x; e < n; e += THREADS) {
             if (!same_next(e) || (e > 0 && same_next(e - 1))) continue;  // not the start of a run
             int end = e + 1;
             while (same_next(end)) ++end;
@@ -1009,7 +974,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tiles_block(TileSortArgs 
             }
         }
         __syncthreads();
-        for (int e = threadIdx.x; e < n; e += kTileThreads) lst[e] = sid[e];
+        for (int e = threadIdx.x; e < n; e += THREADS) lst[e] = sid[e];
     }
 }
 
@@ -2218,9 +2183,9 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
                         slow_list,   slow_n,     slow_list + Tt, slow_n + 1,   Tt};
         StageScope t_sort(ctx, st, kStageSort);
         k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
-        // the long-list warp sort and the exact block sort walk device-side tile lists (no host readback)
+        // the long-list block sorts walk device-side tile lists (no host readback)
         k_sort_tiles_long<<<(unsigned)std::min<int64_t>(ceil_div(Tt, 4), 1184), 128, 0, st>>>(ta);
-        k_sort_tiles_block<<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
+        k_sort_tiles_radix<kSortCap, kTileThreads, false><<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
         NL += 3;
         check_launch();
         t_sort.end();
