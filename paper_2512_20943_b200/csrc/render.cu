@@ -865,6 +865,12 @@ __global__ void __launch_bounds__(128, 8) k_sort_tiles_warp(TileSortArgs a) {
     else warp_sort_tile<16, 10>(a, g, n, fl);
 }
 
+#ifndef BIG_RADIX
+#define BIG_RADIX 128  // threads of the block radix sort for 1025-2048 lists (16 keys each)
+#endif
+#ifndef MID_RADIX
+#define MID_RADIX 128  // threads of the block radix sort for 513-1024 lists (8 keys each; 0: the warp sort)
+#endif
 #ifndef LONG_WARP_MAX
 #define LONG_WARP_MAX 1024
 #endif
@@ -2184,8 +2190,12 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         StageScope t_sort(ctx, st, kStageSort);
         k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
         // the long-list block sorts walk device-side tile lists (no host readback)
+#if MID_RADIX
+        k_sort_tiles_radix<1024, MID_RADIX, true><<<(unsigned)std::min<int64_t>(Tt, 1184), MID_RADIX, 0, st>>>(ta);
+#else
         k_sort_tiles_long<<<(unsigned)std::min<int64_t>(ceil_div(Tt, 4), 1184), 128, 0, st>>>(ta);
-        k_sort_tiles_radix<kSortCap, kTileThreads, false><<<(unsigned)std::min<int64_t>(Tt, 1184), kTileThreads, 0, st>>>(ta);
+#endif
+        k_sort_tiles_radix<kSortCap, BIG_RADIX, false><<<(unsigned)std::min<int64_t>(Tt, 1184), BIG_RADIX, 0, st>>>(ta);
         NL += 3;
         check_launch();
         t_sort.end();
