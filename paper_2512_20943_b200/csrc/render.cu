@@ -736,7 +736,7 @@ struct TileSortArgs {
     int64_t stride;
     uint32_t *slow_list;       // tiles needing the block-level exact sort
     unsigned int *slow_n;
-    uint32_t *mid_list;        // tiles for k_sort_tiles_long (longer than kWarpSortMax)
+    uint32_t *mid_list;        // tiles longer than kWarpSortMax (k_sort_tiles_radix<1024, ...>)
     unsigned int *mid_n;
     int64_t Tt;
 };
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(128, 8) k_sort_tiles_warp(TileSortArgs a) {
     if (g >= a.Tt) return;
     const int n = a.tl.count(a.tcount, g);
     if (n <= 1 || n > kSortCap) return;  // > kSortCap: radix fallback already sorted it
-    if (n > kWarpSortMax) {  // the long-list warp sort (k_sort_tiles_long) takes it
+    if (n > kWarpSortMax) {  // the block radix sort (k_sort_tiles_radix) takes it
         if ((threadIdx.x & 31) == 0) a.mid_list[atomicAdd(a.mid_n, 1u)] = (uint32_t)g;
         return;
     }
@@ -868,29 +868,6 @@ __global__ void __launch_bounds__(128, 8) k_sort_tiles_warp(TileSortArgs a) {
 #ifndef BIG_RADIX
 #define BIG_RADIX 128  // threads of the block radix sort for 1025-2048 lists (16 keys each)
 #endif
-#ifndef MID_RADIX
-#define MID_RADIX 128  // threads of the block radix sort for 513-1024 lists (8 keys each; 0: the warp sort)
-#endif
-#ifndef LONG_WARP_MAX
-#define LONG_WARP_MAX 1024
-#endif
-// Lists of kWarpSortMax < n <= 1024: one warp each, keys in 32 registers,
-// walking the device-side list of such tiles (no host readback); longer lists
-// go on to the block sort.
-__global__ void __launch_bounds__(128, 4) k_sort_tiles_long(TileSortArgs a) {
-    __shared__ uint32_t sflags[4][1024 / 32];
-    const unsigned int nmid = *a.mid_n;
-    uint32_t *fl = sflags[threadIdx.x >> 5];
-    for (unsigned int b = blockIdx.x * 4 + (threadIdx.x >> 5); b < nmid; b += gridDim.x * 4) {
-        const int64_t g = a.mid_list[b];
-        const int n = a.tl.count(a.tcount, g);
-        if (n <= LONG_WARP_MAX) {
-            warp_sort_tile<32, 10>(a, g, n, fl);
-        } else if ((threadIdx.x & 31) == 0) {
-            a.slow_list[atomicAdd(a.slow_n, 1u)] = (uint32_t)g;
-        }
-    }
-}
 
 // Block-level sort of long tile lists: 32-bit keys (depth bucket << PB | list
 // position, PB = log2 CAP) sorted by a stable block radix sort over the bucket
@@ -1616,9 +1593,6 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             }
             __syncwarp();
         }
-#ifdef C2_SKIP_AB  // experiment builds only: time without phases A and B (results wrong)
-        ncomp = 0;
-#endif
         for (int c = 0; c < ncomp; c += kC2Chunk) {
             if (__all_sync(0xffffffffu, all_done())) break;
             // phase A: the NP pixels against two entries per f32x2 sequence (dx shared)
@@ -1777,9 +1751,6 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
                 }
             };
 #undef C2_CAND
-#ifdef C2_SKIP_B  // experiment builds only: time without phase B (results wrong)
-            if (wu == 0x12345678u)
-#endif
             if (C2_NOCLAMP && !batch_clamp)
                 phase_b(std::false_type{});
             else
@@ -2190,11 +2161,7 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         StageScope t_sort(ctx, st, kStageSort);
         k_sort_tiles_warp<<<(unsigned)ceil_div(Tt, 4), 128, 0, st>>>(ta);
         // the long-list block sorts walk device-side tile lists (no host readback)
-#if MID_RADIX
-        k_sort_tiles_radix<1024, MID_RADIX, true><<<(unsigned)std::min<int64_t>(Tt, 1184), MID_RADIX, 0, st>>>(ta);
-#else
-        k_sort_tiles_long<<<(unsigned)std::min<int64_t>(ceil_div(Tt, 4), 1184), 128, 0, st>>>(ta);
-#endif
+        k_sort_tiles_radix<1024, 128, true><<<(unsigned)std::min<int64_t>(Tt, 1184), 128, 0, st>>>(ta);
         k_sort_tiles_radix<kSortCap, BIG_RADIX, false><<<(unsigned)std::min<int64_t>(Tt, 1184), BIG_RADIX, 0, st>>>(ta);
         NL += 3;
         check_launch();
