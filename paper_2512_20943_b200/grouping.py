@@ -384,7 +384,9 @@ def probe_payload_items(space, cams, payloads, payload_devs, targets, items, dev
         for e, f in zip(engs, flags):
             e.call("airgs_defer", 0, ctypes.byref(f))
     if any(f.value for f in flags):
-        run(1)  # checked mode, one lane
+        # checked mode on the same lanes: errors surface in call order, and each
+        # lane engine adapts its tile-bucket capacity after an overflow
+        run(lanes)
     return _in_item_order(pieces, order, len(items), dev)
 
 

@@ -341,15 +341,32 @@ def deferred(dev, run):
     any problem into one device word; if it is set, ``run()`` is repeated in
     checked mode, which raises the reference's exact error or handles the
     condition (bucket overflow).  Returns run()'s result."""
-    eng = _engine(dev)
-    flags = ctypes.c_uint32(0)
-    eng.call("airgs_defer", 1, ctypes.byref(flags))
+    return deferred_lanes(dev, lambda nl: run(), 1)
+
+
+def deferred_lanes(dev, run, lanes):
+    """deferred() over ``lanes`` engine lanes: ``run(nl)`` may spread its calls
+    over nl lanes (grouping's lane streams); every lane engine folds its
+    problems into its own word.  The checked re-run keeps the lanes: a
+    checked call synchronises on its own flags, so errors still surface in
+    call order, and every lane engine adapts its tile-bucket capacity after
+    an overflow (a deferred call cannot)."""
+    from ._lib import engine, engine_lane
+
+    engs, flags = [], []
+    for lane in range(lanes):
+        with engine_lane(lane):
+            engs.append(engine(dev))
+        flags.append(ctypes.c_uint32(0))
+    for e, f in zip(engs, flags):
+        e.call("airgs_defer", 1, ctypes.byref(f))
     try:
-        out = run()
+        out = run(lanes)
     finally:
-        eng.call("airgs_defer", 0, ctypes.byref(flags))
-    if flags.value:
-        out = run()
+        for e, f in zip(engs, flags):
+            e.call("airgs_defer", 0, ctypes.byref(f))
+    if any(f.value for f in flags):
+        out = run(lanes)
     return out
 
 
@@ -380,20 +397,49 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
         todo = [li for li, j in enumerate(t.keep) if t.kmins[j] > 0]
         V = len(cams)
 
-        def run():
+        def run(nl):
+            import torch
+
+            from ._lib import engine_lane
+            from .grouping import _lane_stream
+
             ref = GaussianFrame(device_params=level_frame_planes(p, None), count=p.n, frame_index=frame_index,
                                 group_key=space.key_index)
             rv = render_views([ref], cams, [(0, v) for v in range(V)], want_images=True, device=dev)
             frames = [GaussianFrame(device_params=level_frame_planes(p, t.kmins[t.keep[li]]), count=p.n)
                       for li in todo]
-            items = [(fi, v) for fi in range(len(frames)) for v in range(V)]
-            targets = [rv.images[v] for _ in range(len(frames)) for v in range(V)]
-            out = render_sse_chunked(frames, cams, items, targets, device=dev, host=False)
+            if nl == 1:
+                items = [(fi, v) for fi in range(len(frames)) for v in range(V)]
+                targets = [rv.images[v] for _ in range(len(frames)) for v in range(V)]
+                out = render_sse_chunked(frames, cams, items, targets, device=dev, host=False)
+            else:
+                # one render call per level, alternating over the engine lanes: level
+                # k+1's projection / binning / sort overlap level k's compositing
+                main = torch.cuda.current_stream(dev)
+                streams = [main] + [_lane_stream(dev, k) for k in range(1, nl)]
+                for st in streams[1:]:
+                    st.wait_stream(main)  # the reference images and level planes
+                parts = []
+                for fi, fr in enumerate(frames):
+                    lane = fi % nl
+                    with torch.cuda.stream(streams[lane]), engine_lane(lane):
+                        sse = render_sse_chunked([fr], cams, [(0, v) for v in range(V)],
+                                                 [rv.images[v] for v in range(V)], device=dev, host=False)
+                    if lane:
+                        sse.record_stream(main)
+                        for v in range(V):
+                            rv.images[v].record_stream(streams[lane])
+                    parts.append(sse)
+                for st in streams[1:]:
+                    main.wait_stream(st)
+                out = torch.cat(parts)
             level_removed(t)  # host-only work (after _removed_prepare), overlapping the enqueued renders
             return out
 
+        from .grouping import probe_lanes
+
         _removed_prepare(p, t.delta.overlay())
-        sse_dev = deferred(dev, run) if todo else None
+        sse_dev = deferred_lanes(dev, run, min(probe_lanes(), max(len(todo), 1))) if todo else None
         if todo:
             sse = sse_dev.cpu().numpy()
             sizes_px = [c.resolution[0] * c.resolution[1] * 3 for c in cams]
