@@ -711,6 +711,8 @@ extern "C" int airgs_gsdp_decode_apply(airgs_ctx *ctx, const uint8_t *payload, i
         if (DA_MAP && map_mode_ok(E, ld) && ok && E > 0) {
             const int slot = 0;
             ctx->pre[0].valid = ctx->pre[1].valid = false;  // (a checked call drops any prescan)
+            // ...which may still be writing its map slot on the side stream
+            for (int k = 0; k < 2; ++k) AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->pre_event(k), 0));
             AIRGS_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(unsigned int), st));
             da_scan(ctx, slot, payload, nbytes, E, V, count, ld, flags, st);
             t0.end();  // the scan; the streaming pass is timed as the apply stage
@@ -816,6 +818,9 @@ extern "C" int airgs_gsdp_decode_apply_ahead(airgs_ctx *ctx, const uint8_t *payl
             AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->pre_event(slot), 0));  // scanned ahead on the side stream
         } else {
             ctx->pre[0].valid = ctx->pre[1].valid = false;
+            // a dropped prescan may still be writing its map slot on the side
+            // stream: the scan below (and later side scans) must follow it
+            for (int k = 0; k < 2; ++k) AIRGS_CUDA_TRY(cudaStreamWaitEvent(st, ctx->pre_event(k), 0));
             slot = 0;
             da_scan(ctx, slot, payload, nbytes, E, V, count, ld, flags + 1, st);
         }
