@@ -237,6 +237,38 @@ def test_probe_payloads_device_pipelined_and_checked_rerun():
     assert [q for q, _ in got2] == ref
 
 
+@pytest.mark.parametrize("lanes", [1, 2, 3])
+def test_probe_lanes_equal(monkeypatch, lanes):
+    """Frames of the pipelined probe alternate over engine lanes (own stream,
+    own scratch, own decode-ahead slots); the qualities do not depend on the
+    lane count, including an out-of-order, repeated frame sequence."""
+    import torch
+
+    from paper_2512_20943_b200 import codec, grouping
+    from paper_2512_20943_b200.model import CanonicalSpace, GaussianFrame, diff_frames
+
+    monkeypatch.setenv("AIRGS_PROBE_LANES", str(lanes))
+    base_p, _ = _scene(62, n=1500)
+    cams = _cams(3, (64, 48))
+    space = CanonicalSpace(GaussianFrame(params=base_p), capacity_U=base_p.shape[0])
+    payloads, pdevs, targets, ref = [], [], [], []
+    for s in range(5):
+        moved = base_p.copy()
+        rng = np.random.default_rng(s + 10)
+        moved[::3, 0:3] += rng.normal(0, 0.01 * (s + 1), (moved[::3].shape[0], 3))
+        pay = codec.encode_delta(diff_frames(space.frame, GaussianFrame(params=moved)), 1e-4)
+        imgs = orc.render_with_usage(moved, cams)[0]
+        payloads.append(pay)
+        pdevs.append(torch.frombuffer(bytearray(pay.data), dtype=torch.uint8).cuda())
+        targets.append([torch.from_numpy(im).cuda() for im in imgs])
+        dec = codec.decode_delta(pay, base_p.shape[0], 17)
+        ref.append(grouping.quality_probe(space, dec, grouping.GroundTruth(images=imgs), cams))
+    seq = [0, 1, 2, 4, 3, 3, 0, 1]
+    got = grouping.probe_payloads_device(space, cams, [payloads[i] for i in seq], [pdevs[i] for i in seq],
+                                         [targets[i] for i in seq], tau_db=60.0)
+    assert [q for q, _ in got] == [ref[i] for i in seq]
+
+
 def test_level_space_chunked_render_calls_equal_single_call(monkeypatch):
     """build_level_space splits its (level, view) renders into calls of bounded
     working set (RENDER_PAIRS_PER_CALL); the qualities do not depend on it."""
