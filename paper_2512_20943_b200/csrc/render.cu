@@ -1342,9 +1342,6 @@ k_composite(const CompItem *__restrict__ items, const int64_t *__restrict__ tile
 #ifndef C2_ELLIPSE_CULL
 #define C2_ELLIPSE_CULL 0  // measured slower (profiles/r2_composite_experiments.md): off
 #endif
-#ifndef C2_PERSIST
-#define C2_PERSIST 0  // measured slower (profiles/r2_composite_experiments.md): off
-#endif
 #ifndef C2_EXP_REP
 #define C2_EXP_REP 1  // 2 and 4 copies measured slower (less L1 left for records)
 #endif
@@ -1422,8 +1419,7 @@ __device__ unsigned long long g_c2c[10];
 template <bool USAGE, int NP>
 __global__ void __launch_bounds__(CompNGeom<NP>::kThreads, C2_MIN_BLOCKS)
 k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ tile_base, int nitems,
-             const TileLists tls, const uint32_t *__restrict__ tcount, unsigned int *__restrict__ work,
-             int64_t ntiles_all) {
+             const TileLists tls, const uint32_t *__restrict__ tcount) {
     using G = CompNGeom<NP>;
 #if C2_STATIC_SMEM
     // static shared memory (< 48 KB): constant shared addresses fold into the
@@ -1434,19 +1430,7 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
     CompNShared<NP, USAGE> &sh = *reinterpret_cast<CompNShared<NP, USAGE> *>(compn_smem);
 #endif
     load_exp_table<kC2ExpRep>(sh.exptab, G::kThreads);
-#if C2_PERSIST
-    // persistent CTAs take tiles from a counter: one exp-table load and CTA
-    // start per SM slot instead of per tile (the grab's barrier also separates
-    // a tile's last batch from the next tile's staging)
-    __shared__ unsigned int s_tile;
-    for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(work, 1u);
-    __syncthreads();
-    const int64_t g = s_tile;
-    if (g >= ntiles_all) break;
-#else
     const int64_t g = blockIdx.x;
-#endif
     int lo = 0, hi = nitems - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -1805,33 +1789,22 @@ k_compositeN(const CompItem *__restrict__ items, const int64_t *__restrict__ til
             for (int k = G::kWarps + w; k < kCompWarps; k += G::kWarps) it.sse_tiles[(int64_t)tl * kCompWarps + k] = 0.0;
         }
     }
-#if C2_PERSIST
-    __syncthreads();  // s_tile is read by every thread before the next grab
-    }
-#endif
 }
 
 template <bool USAGE>
 static void launch_composite2(int64_t tiles, cudaStream_t st, const CompItem *items, const int64_t *tile_base,
-                              int nitems, const TileLists &tl, const uint32_t *tcount, unsigned int *work) {
+                              int nitems, const TileLists &tl, const uint32_t *tcount) {
     auto *fn = k_compositeN<USAGE, C2_NP>;
-    unsigned grid = (unsigned)tiles;
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    if (C2_PERSIST) grid = (unsigned)std::min<int64_t>(tiles, (int64_t)sms * C2_MIN_BLOCKS);
+    const unsigned grid = (unsigned)tiles;
     if (C2_STATIC_SMEM) {
         // C2_EXTRA_SMEM (experiments): unused dynamic shared memory that caps the
         // CTAs per SM, leaving registers for kernels of another stream
-        fn<<<grid, CompNGeom<C2_NP>::kThreads, C2_EXTRA_SMEM, st>>>(items, tile_base, nitems, tl, tcount, work, tiles);
+        fn<<<grid, CompNGeom<C2_NP>::kThreads, C2_EXTRA_SMEM, st>>>(items, tile_base, nitems, tl, tcount);
         return;
     }
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CompNShared<C2_NP, USAGE>));
-    fn<<<grid, CompNGeom<C2_NP>::kThreads, sizeof(CompNShared<C2_NP, USAGE>), st>>>(items, tile_base, nitems, tl, tcount,
-                                                                             work, tiles);
+    fn<<<grid, CompNGeom<C2_NP>::kThreads, sizeof(CompNShared<C2_NP, USAGE>), st>>>(items, tile_base, nitems, tl,
+                                                                                     tcount);
 }
 
 // Diagnostic counters: for every (primitive, pixel of its clipped bbox) pair of
@@ -2235,14 +2208,9 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
         rec->cbits = cbits;
         rec->cbase = cbase;
     }
-    // item descriptors, then the persistent compositing kernel's work counter (zero)
-    const size_t ci_bytes = sizeof(CompItem) * nitems;
-    CompItem *d_ci = (CompItem *)ctx->scratch(kSlotMisc1, ci_bytes + 16);
+    CompItem *d_ci = (CompItem *)ctx->scratch(kSlotMisc1, sizeof(CompItem) * nitems);
     uint8_t *d_has = (uint8_t *)ctx->scratch(kSlotMisc2, nitems);
-    std::vector<unsigned char> ci_up(ci_bytes + 16, 0);
-    std::memcpy(ci_up.data(), ci.data(), ci_bytes);
-    h2d_small(ctx, d_ci, ci_up.data(), ci_bytes + 16, st);
-    unsigned int *d_work = reinterpret_cast<unsigned int *>(reinterpret_cast<char *>(d_ci) + ci_bytes);
+    h2d_small(ctx, d_ci, ci.data(), sizeof(CompItem) * nitems, st);
     h2d_small(ctx, d_has, has_t.data(), nitems, st);
     StageScope t_comp(ctx, st, kStageComposite, Tt > 0);
     if (Tt > 0) {
@@ -2270,9 +2238,9 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
                 launch_composite<false, true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         } else if (COMP_PX2) {
             if (any_usage)
-                launch_composite2<true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, d_work);
+                launch_composite2<true>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count);
             else
-                launch_composite2<false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, d_work);
+                launch_composite2<false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count);
         } else if (any_usage) {
             launch_composite<true, false>(Tt, st, d_ci, L.d_tile_base, nitems, tl, tile_count, cs);
         } else {
