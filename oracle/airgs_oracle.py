@@ -311,7 +311,7 @@ def tile_keys(bboxes, width, height, tile=TILE):
     return np.sort(((ty * tx_n + tx) << 32) | p[rep])
 
 
-def threshold_tile_ranges(pr, tile=TILE):
+def threshold_tile_ranges(pr, tile=TILE, with_ext=False):
     """Tile range of each prepared primitive under the B200 binning's
     weight-threshold narrowing (restated from render.cu k_project /
     rec_tile_range): a pixel can pass the reference's weight
@@ -343,25 +343,88 @@ def threshold_tile_ranges(pr, tile=TILE):
     yb = np.where(ny, np.minimum(yb, np.floor(myf + hyf).astype(np.int64)), yb)
     has = (bb[:, 1] > bb[:, 0]) & (bb[:, 3] > bb[:, 2]) & (xa <= xb) & (ya <= yb)
     rng = np.stack([xa // tile, xb // tile, ya // tile, yb // tile], axis=1)
+    if with_ext:
+        return rng, has, nx & ny
     return rng, has
 
 
-def tile_lists_threshold(params, cam, tile=TILE):
+def _quad_rect_min_lb32(A, B, C, rX, rY, x0, x1, y0, y1):
+    """float32 restatement, op for op, of render.cu quad_rect_min_lb (the CUDA
+    code is compiled without FMA contraction): a conservative lower bound of
+    min A dx^2 + B dx dy + C dy^2 over [x0, x1] x [y0, y1], the edge vertices
+    from the reciprocals rX = 1/(2C), rY = 1/(2A).  Arrays."""
+    f = np.float32
+
+    def edge(P, Q, r, X, lo, hi):
+        with np.errstate(invalid="ignore", over="ignore"):
+            t = np.minimum(np.maximum(((-B) * X) * r, lo), hi)
+            a = (P * X) * X
+            b = (B * X) * t
+            c = (Q * t) * t
+            return ((a + b) + c) - (f(1e-4) * ((a + np.abs(b)) + c) + f(1e-3))
+
+    ex = np.minimum(edge(A, C, rX, x0, y0, y1), edge(A, C, rX, x1, y0, y1))
+    ey = np.minimum(edge(C, A, rY, y0, x0, x1), edge(C, A, rY, y1, x0, x1))
+    lb = np.minimum(ex, ey)
+    inside = (x0 <= 0) & (x1 >= 0) & (y0 <= 0) & (y1 >= 0)
+    return np.where(inside, f(0.0), lb).astype(f)
+
+
+def ellipse_tile_keep(pr, rng, ok_ext, tile=TILE):
+    """render.cu make_cull_rec / cull_keep restated: for primitives whose
+    threshold tile range spans 2..4 tiles in both directions (with threshold
+    extents and a positive definite fp32 conic), the binning drops a tile
+    when a lower bound of e over the tile's pixel centres exceeds
+    t = ln(alpha/EPS) (+ pad): no pixel there can pass the weight test.
+    Returns keep(i, u, v), vectorised over primitive positions and tiles."""
+    f32 = np.float32
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t = np.maximum(np.log(pr.alphas / EPS_CONTRIB) * 1.0002 + 2e-4, 0.0)
+    nu = rng[:, 1] - rng[:, 0] + 1
+    nv = rng[:, 3] - rng[:, 2] + 1
+    A = (0.5 * pr.conics[:, 0]).astype(f32)
+    B = pr.conics[:, 1].astype(f32)
+    C = (0.5 * pr.conics[:, 2]).astype(f32)
+    cull = ok_ext & (nu >= 2) & (nv >= 2) & (nu <= 4) & (nv <= 4) & (A > 0) & (C > 0)
+    with np.errstate(divide="ignore"):
+        rX = (f32(1.0) / (f32(2.0) * C)).astype(f32)
+        rY = (f32(1.0) / (f32(2.0) * A)).astype(f32)
+    tf = t.astype(f32)
+    mx = ((pr.means2d[:, 0] - rng[:, 0] * tile).astype(f32) - f32(0.5)).astype(f32)
+    my = ((pr.means2d[:, 1] - rng[:, 2] * tile).astype(f32) - f32(0.5)).astype(f32)
+
+    def keep(i, u, v):
+        du, dv = u - rng[i, 0], v - rng[i, 2]
+        x0 = ((du * tile).astype(f32) - mx[i]).astype(f32)
+        x1 = ((du * tile + tile - 1).astype(f32) - mx[i]).astype(f32)
+        y0 = ((dv * tile).astype(f32) - my[i]).astype(f32)
+        y1 = ((dv * tile + tile - 1).astype(f32) - my[i]).astype(f32)
+        lb = _quad_rect_min_lb32(A[i], B[i], C[i], rX[i], rY[i], x0, x1, y0, y1)
+        return ~cull[i] | ~(lb > tf[i])
+
+    return keep
+
+
+def tile_lists_threshold(params, cam, tile=TILE, ellipse=True):
     """Expected per-tile lists of the B200 binning + sort stage for one view:
     ``tile_keys`` over the reference's clipped bboxes,
-    restricted to the tiles of ``threshold_tile_ranges``, mapped back to
-    primitive indices.  Returns {tile_id: int64 array of primitive indices in
+    restricted to the tiles of ``threshold_tile_ranges`` and (``ellipse``)
+    to the tiles ``ellipse_tile_keep`` keeps, mapped back to primitive
+    indices.  Returns {tile_id: int64 array of primitive indices in
     compositing order (prep.order position ascending)}."""
     pr = prepare(params, cam)
     ct = CamTerms(cam)
     keys = tile_keys(pr.bboxes, ct.W, ct.H, tile)
-    rng, has = threshold_tile_ranges(pr, tile)
+    rng, has, ok_ext = threshold_tile_ranges(pr, tile, with_ext=True)
     tx_n = (ct.W + tile - 1) // tile
     tid = keys >> 32
     pos = keys & 0xFFFFFFFF
     tyy, txx = tid // tx_n, tid % tx_n
     r = rng[pos]
     keep = has[pos] & (txx >= r[:, 0]) & (txx <= r[:, 1]) & (tyy >= r[:, 2]) & (tyy <= r[:, 3])
+    if ellipse:
+        kk = np.nonzero(keep)[0]
+        keep[kk] = ellipse_tile_keep(pr, rng, ok_ext, tile)(pos[kk], txx[kk], tyy[kk])
     tid, pos = tid[keep], pos[keep]
     out = {}
     if tid.size:

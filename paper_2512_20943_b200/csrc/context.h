@@ -216,6 +216,7 @@ enum Slot : int {
     kSlotFusedIdx,
     kSlotFusedMap,
     kSlotFusedAgg,
+    kSlotCullRec,
     kSlotCount
 };
 

@@ -36,6 +36,13 @@ namespace airgs {
 // ---------------------------------------------------------------------------
 // projection
 
+// ellipse-vs-tile cull record of a (view, primitive) (see make_cull_rec)
+constexpr uint32_t kCullFlag = 0x80000000u;
+struct __align__(16) CullRec {
+    float A, B, C, rX;    // 0.5 a, b, 0.5 c (fp32); 1 / (2 C)
+    float rY, mx, my, t;  // 1 / (2 A); mean - 0.5 relative to the range's first pixel; t (fp32)
+};
+
 struct ProjArgs {
     const airgs_frame *frames;
     const airgs_camera *cams;
@@ -47,7 +54,8 @@ struct ProjArgs {
     Rec *recs;                 // [nitems][stride]
     uint64_t *depth;           // [nitems][stride] orderable depth keys
     int32_t *ntiles;           // [nitems][stride] tiles touched (0 = empty bbox, -1 = no tile)
-    uint2 *binrec;             // [nitems][stride] tile range u0 | u1 << 16, v0 | v1 << 16 (when ntiles > 0)
+    uint2 *binrec;             // [nitems][stride] tile range u0 | u1 << 16 (| kCullFlag), v0 | v1 << 16 (when ntiles > 0)
+    CullRec *cullrec;          // [nitems][stride] (flagged ranges only)
     unsigned int *flags;
     int64_t stride;
     unsigned long long *stats;  // diagnostic decision margins (null: off)
@@ -109,6 +117,63 @@ __device__ __forceinline__ bool rec_tile_range(const Rec &r, int &u0, int &u1, i
     u1 = xb / kTile;
     v0 = ya / kTile;
     v1 = yb / kTile;
+    return true;
+}
+
+// Ellipse-vs-tile cull of the binning.  For a primitive-view whose tile range
+// spans 2..4 tiles in both directions (the corners of its threshold AABB are
+// where tiles can miss the ellipse) the projection stores the fp32 inputs of
+// the test in a 32-byte cull record and flags the range (bit 31 of binrec.x);
+// the binning then drops a (primitive, tile) pair when a conservative lower
+// bound of e = 0.5 (a dx^2 + c dy^2) + b dx dy over the tile's pixel centres
+// exceeds t = ln(al / EPS) (+ pad): no pixel of that tile can pass the weight
+// test.  The tests run in the binning, where (primitive, tile) pairs are dealt
+// evenly over the warp's lanes.  oracle/airgs_oracle.py restates it op for op.
+#ifndef TILE_CULL
+#define TILE_CULL 1
+#endif
+
+// Lower bound (conservative by 1e-4 of the terms' magnitude + 1e-3, far above
+// fp32 rounding) of min Q(dx, dy) = A dx^2 + B dx dy + C dy^2 over the
+// rectangle [x0, x1] x [y0, y1] (A, C > 0, positive definite): 0 if the
+// rectangle holds the origin, else the smallest of the four edges' minima,
+// each the 1-D quadratic at its clamped vertex (vertices from the reciprocals
+// rX = 1/(2C), rY = 1/(2A); evaluating a rounded vertex only raises the value
+// by Q delta^2, far inside the slack).  Plain fp32 (-fmad=false).
+__device__ __forceinline__ float quad_rect_min_lb(float A, float B, float C, float rX, float rY, float x0, float x1,
+                                                  float y0, float y1) {
+    if (x0 <= 0.0f && x1 >= 0.0f && y0 <= 0.0f && y1 >= 0.0f) return 0.0f;
+    auto edge = [B](float P, float Q, float r, float X, float lo, float hi) {
+        // min over t in [lo, hi] of P X^2 + B X t + Q t^2
+        const float t = fminf(fmaxf(-B * X * r, lo), hi);
+        const float a = P * X * X, b = B * X * t, c = Q * t * t;
+        return (a + b + c) - (1e-4f * (a + fabsf(b) + c) + 1e-3f);
+    };
+    const float ex = fminf(edge(A, C, rX, x0, y0, y1), edge(A, C, rX, x1, y0, y1));
+    const float ey = fminf(edge(C, A, rY, y0, x0, x1), edge(C, A, rY, y1, x0, x1));
+    return fminf(ex, ey);
+}
+
+// may the ellipse of cull record c reach tile (du, dv) of its range?
+__device__ __forceinline__ bool cull_keep(const CullRec &c, int du, int dv) {
+    const float x0 = (float)(du * kTile) - c.mx, x1 = (float)(du * kTile + kTile - 1) - c.mx;
+    const float y0 = (float)(dv * kTile) - c.my, y1 = (float)(dv * kTile + kTile - 1) - c.my;
+    return !(quad_rect_min_lb(c.A, c.B, c.C, c.rX, c.rY, x0, x1, y0, y1) > c.t);
+}
+
+// the cull record of a projected record with tile range (u0..u1, v0..v1), or false
+__device__ __forceinline__ bool make_cull_rec(const Rec &r, int u0, int u1, int v0, int v1, double t, CullRec &c) {
+    const int nu = u1 - u0 + 1, nv = v1 - v0 + 1;
+    if (!TILE_CULL || nu < 2 || nv < 2 || nu > 4 || nv > 4 || !(r.hx < 1e29f && r.hy < 1e29f)) return false;
+    c.A = (float)(0.5 * r.ca);
+    c.B = (float)r.cb;
+    c.C = (float)(0.5 * r.cc);
+    if (!(c.A > 0.0f && c.C > 0.0f)) return false;
+    c.rX = 1.0f / (2.0f * c.C);
+    c.rY = 1.0f / (2.0f * c.A);
+    c.mx = (float)(r.mx - (double)(u0 * kTile)) - 0.5f;
+    c.my = (float)(r.my - (double)(v0 * kTile)) - 0.5f;
+    c.t = (float)t;
     return true;
 }
 
@@ -274,7 +339,11 @@ __global__ void __launch_bounds__(kProjThreads, PROJ_MIN_BLOCKS) k_project(ProjA
             const bool has_bbox = rec.x1 > rec.x0 && rec.y1 > rec.y0;
             if (has_bbox && rec_tile_range(rec, u0, u1, v0, v1)) {
                 nt = (u1 - u0 + 1) * (v1 - v0 + 1);
-                a.binrec[o] = make_uint2((uint32_t)u0 | ((uint32_t)u1 << 16), (uint32_t)v0 | ((uint32_t)v1 << 16));
+                CullRec cr;
+                const bool cull = a.cullrec && make_cull_rec(rec, u0, u1, v0, v1, 0.5 * t2, cr);
+                if (cull) a.cullrec[o] = cr;
+                a.binrec[o] = make_uint2((uint32_t)u0 | ((uint32_t)u1 << 16) | (cull ? kCullFlag : 0u),
+                                         (uint32_t)v0 | ((uint32_t)v1 << 16));
             }
             const int64_t *fz = a.item_frozen ? a.item_frozen[item] : nullptr;
             const unsigned long long zk = order_key_of(fz, i, tz);
@@ -344,6 +413,7 @@ __global__ void k_bin_counts(const uint32_t *__restrict__ padded, uint32_t *__re
 
 struct BinArgs {
     const uint2 *binrec;
+    const CullRec *cullrec;
     const uint64_t *depth;
     const int32_t *ntiles;
     const int64_t *tile_base;
@@ -365,12 +435,18 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
     const int nt = i < a.count[s] ? max(a.ntiles[o], 0) : 0;
     if (__all_sync(0xffffffffu, nt == 0)) return;
     int u0 = 0, u1 = 0, v0 = 0;  // tile range (the last row follows from nt)
+    bool cull = false;           // this primitive's pairs pass the ellipse test first
+    CullRec cr{};
     uint64_t entry = 0;
     if (nt > 0) {
         const uint2 br = a.binrec[o];  // 8 bytes instead of the 96-byte record
         u0 = (int)(br.x & 0xffffu);
-        u1 = (int)(br.x >> 16);
+        u1 = (int)((br.x & ~kCullFlag) >> 16);
         v0 = (int)(br.y & 0xffffu);
+        if (br.x & kCullFlag) {
+            cull = true;
+            cr = a.cullrec[o];
+        }
         const uint64_t zk = a.depth[o];
         // 32-bit order key: small keys (frozen positions, the seam's input order)
         // as they are; depth keys (z > 0) as their fp32 bits, monotone, behind them
@@ -391,7 +467,8 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
     const int txn = a.tiles_x[s];
     // two rounds of 32 pairs per iteration: both counter atomics are in flight
     // before either result is consumed
-    auto resolve = [&](int k, int64_t &g, uint64_t &oent) {
+    const bool any_cull = __any_sync(0xffffffffu, cull);
+    auto resolve = [&](int k, int64_t &g, uint64_t &oent) -> bool {
         // owner lane: the last lane whose first pair index is <= k
         int L = 0;
 #pragma unroll
@@ -405,14 +482,26 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
         oent = __shfl_sync(0xffffffffu, entry, L);
         const int dv = j / onu;
         g = tb + (int64_t)(ov0 + dv) * txn + ou0 + (j - dv * onu);
+        if (!any_cull) return true;  // warp-uniform
+        CullRec oc;
+        oc.A = __shfl_sync(0xffffffffu, cr.A, L);
+        oc.B = __shfl_sync(0xffffffffu, cr.B, L);
+        oc.C = __shfl_sync(0xffffffffu, cr.C, L);
+        oc.rX = __shfl_sync(0xffffffffu, cr.rX, L);
+        oc.rY = __shfl_sync(0xffffffffu, cr.rY, L);
+        oc.mx = __shfl_sync(0xffffffffu, cr.mx, L);
+        oc.my = __shfl_sync(0xffffffffu, cr.my, L);
+        oc.t = __shfl_sync(0xffffffffu, cr.t, L);
+        const bool oculled = __shfl_sync(0xffffffffu, cull, L);
+        return !oculled || cull_keep(oc, j - dv * onu, dv);
     };
     for (int k0 = 0; k0 < total; k0 += 64) {
         const int ka = k0 + lane, kb = k0 + 32 + lane;
         int64_t ga = 0, gb = 0;
         uint64_t ea = 0, eb = 0;
-        resolve(ka, ga, ea);
-        resolve(kb, gb, eb);
-        const bool va = ka < total, vb = kb < total;
+        const bool keepa = resolve(ka, ga, ea);
+        const bool keepb = resolve(kb, gb, eb);
+        const bool va = ka < total && keepa, vb = kb < total && keepb;
         const uint32_t pa = va ? atomicAdd(a.tile_count + ga * kBinCountStride, 1u) : 0u;
         const uint32_t pb = vb ? atomicAdd(a.tile_count + gb * kBinCountStride, 1u) : 0u;
         if (va) {
@@ -447,6 +536,8 @@ struct TileScanOut {
 
 struct EmitArgs {
     const Rec *recs;
+    const uint2 *binrec;       // cull flag (bit 31 of x)
+    const CullRec *cullrec;
     const uint64_t *depth;
     const int32_t *ntiles;
     const int64_t *tile_base;
@@ -475,8 +566,12 @@ __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     const int txn = a.tiles_x[s];
     int u0, u1, v0, v1;
     rec_tile_range(r, u0, u1, v0, v1);
+    const bool cull = a.binrec && (a.binrec[o].x & kCullFlag);  // the binning's pairs exactly
+    CullRec cr{};
+    if (cull) cr = a.cullrec[o];
     for (int v = v0; v <= v1; ++v)
         for (int u = u0; u <= u1; ++u) {
+            if (cull && !cull_keep(cr, u - u0, v - v0)) continue;
             const int64_t g = tb + v * txn + u;
             a.ids[a.tstart[g] + atomicAdd(a.cursor + g, 1u)] = entry;
         }
@@ -1991,7 +2086,7 @@ struct Layout {
 // segmented radix sort.  Also adapts the bucket capacity for the next call.
 static TileLists scanned_lists(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L, const Rec *recs,
                                const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count, int index_order,
-                               uint32_t cap, cudaStream_t st) {
+                               uint32_t cap, cudaStream_t st, const uint2 *binrec, const CullRec *cullrec) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
@@ -2031,8 +2126,8 @@ static TileLists scanned_lists(airgs_ctx *ctx, const std::vector<ItemHost> &item
     uint32_t *cursor = ctx->scratch_t<uint32_t>(kSlotPairKeys, (size_t)Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * Tt, st));
     if (P > 0) {
-        EmitArgs ea{recs, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, tstart, cursor, ids, L.stride,
-                    index_order};
+        EmitArgs ea{recs,     binrec,  cullrec, depth,  ntiles,   L.d_tile_base, L.d_tiles_x, L.d_count,
+                    tstart,   cursor,  ids,     L.stride, index_order};
         k_emit<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ea);
         ++NL;
         check_launch();
@@ -2270,7 +2365,7 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
 static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items, const Layout &L,
                               const Rec *recs, const uint64_t *depth, const int32_t *ntiles, uint32_t *tile_count,
                               int index_order, double *sse, cudaStream_t st, unsigned int *flags,
-                              const uint2 *binrec, RecordOut *rec = nullptr) {
+                              const uint2 *binrec, const CullRec *cullrec, RecordOut *rec = nullptr) {
     const int nitems = L.nitems;
     int64_t &NL = ctx->launches;
     const int64_t Tt = L.Tt;
@@ -2286,8 +2381,8 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
             pad = ctx->scratch_t<uint32_t>(kSlotBinCount, (size_t)Tt * kBinCountStride);
             AIRGS_CUDA_TRY(cudaMemsetAsync(pad, 0, sizeof(uint32_t) * (size_t)Tt * kBinCountStride, st));
         }
-        BinArgs ba{binrec, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, pad, bucket, cap, flags, L.stride,
-                   index_order};
+        BinArgs ba{binrec, cullrec, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, pad, bucket, cap, flags,
+                   L.stride, index_order};
         StageScope t_bin(ctx, st, kStageBin);
         k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
         ++NL;
@@ -2359,7 +2454,8 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
                 if (h.usage == usage_map[k].first) n = h.count;
             AIRGS_CUDA_TRY(cudaMemsetAsync(usage_map[k].second, 0, sizeof(int64_t) * n, st));
         }
-        const TileLists tl2 = scanned_lists(ctx, items, L, recs, depth, ntiles, tile_count, index_order, cap, st);
+        const TileLists tl2 =
+            scanned_lists(ctx, items, L, recs, depth, ntiles, tile_count, index_order, cap, st, binrec, cullrec);
         sort_composite_sse(ctx, work, L, tl2, recs, depth, ntiles, tile_count, sse, st, rec, index_order != 0);
     }
     for (const auto &m : usage_map) {
@@ -2490,6 +2586,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     uint64_t *depth = ctx->scratch_t<uint64_t>(kSlotDepth, per);
     int32_t *ntiles = ctx->scratch_t<int32_t>(kSlotNtiles, per);
     uint2 *binrec = ctx->scratch_t<uint2>(kSlotBinRec, per);
+    CullRec *cullrec = TILE_CULL ? ctx->scratch_t<CullRec>(kSlotCullRec, per) : nullptr;
     uint32_t *tile_count = ctx->scratch_t<uint32_t>(kSlotTileCount, (size_t)L.Tt);
     AIRGS_CUDA_TRY(cudaMemsetAsync(tile_count, 0, sizeof(uint32_t) * L.Tt, st));
 
@@ -2506,6 +2603,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
     pa.depth = depth;
     pa.ntiles = ntiles;
     pa.binrec = binrec;
+    pa.cullrec = cullrec;
     pa.flags = flags;
     pa.stride = stride;
     pa.stats = (ctx->stats && ctx->d_stats) ? ctx->d_stats : nullptr;
@@ -2522,7 +2620,7 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         check_launch();
     }
     t_proj.end();
-    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags, binrec,
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 0, sse, st, flags, binrec, cullrec,
                       bwd ? &bwd->rec : nullptr);
     if (bwd) {
         bwd->recs = recs;
@@ -3043,7 +3141,7 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
         check_launch();
     }
     // every in-image pixel of every tile is written by the composite kernel
-    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 1, nullptr, st, flags, binrec, rec);
+    bin_and_composite(ctx, ih, L, recs, depth, ntiles, tile_count, 1, nullptr, st, flags, binrec, nullptr, rec);
     if (recs_out) *recs_out = recs;
     if (Tt_out) *Tt_out = L.Tt;
     if (tcount_out) *tcount_out = tile_count;
