@@ -45,6 +45,7 @@ metric/config.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -84,6 +85,23 @@ def _dist():
     return rank, world, local
 
 
+def gc_pause():
+    """The timed regions run without Python's cyclic garbage collector (as
+    timeit does): a gen-2 pass over the process's objects while the frames
+    are being enqueued would leave the GPU idle for milliseconds.
+    AIRGS_BENCH_GC=1 keeps it on."""
+    was = gc.isenabled()
+    if os.environ.get("AIRGS_BENCH_GC", "0") != "1":
+        gc.collect()
+        gc.disable()
+    return was
+
+
+def gc_resume(was):
+    if was:
+        gc.enable()
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -113,6 +131,16 @@ class ClockSampler:
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # wait for the first sample: nvidia-smi's NVML start-up (slow on a fresh
+        # box) stalls this process's CUDA calls for milliseconds, which must not
+        # land inside the timed region
+        t0 = time.time()
+        while time.time() - t0 < 3.0 and self.proc.poll() is None:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.01)
+        time.sleep(0.05)
 
     def stop(self):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
@@ -371,6 +399,10 @@ def run_gpu(args):
             launches0 = sum(e.launches for e in lane_engs)
             ev0 = torch.cuda.Event(enable_timing=True)
             ev1 = torch.cuda.Event(enable_timing=True)
+            if os.environ.get("AIRGS_TRACE_GROW"):
+                print(f"[bench] timed region start (lanes {lanes})", file=sys.stderr, flush=True)
+            gc_was = gc_pause()
+            h0 = time.perf_counter()
             ev0.record(stream)
             if args.per_step:  # one synchronising evaluate_frame per step
                 qs = [evaluate_frame(space, cams, payload_dev[i % nf], payloads[i % nf].data, targets[i % nf],
@@ -379,8 +411,13 @@ def run_gpu(args):
                 qs = [q for q, _ in probe_payloads_sharded(space, cams, *frames(args.warmup, total), tau_db=TAU_DB,
                                                            device=device)]
             ev1.record(stream)
+            h1 = time.perf_counter()
             barrier()
             torch.cuda.synchronize(device)
+            gc_resume(gc_was)
+            if os.environ.get("AIRGS_TRACE_GROW"):
+                print(f"[bench] timed region end: host enqueue {1e3 * (h1 - h0):.2f} ms, "
+                      f"to sync {1e3 * (time.perf_counter() - h0):.2f} ms", file=sys.stderr, flush=True)
             clk = sampler.stop() if sampler else None
             kts = [e.timing(0) for e in lane_engs]
             kt = {k: sum(t[k] for t in kts) for k in kts[0]}
@@ -617,11 +654,13 @@ def run_e2e(space, cams, payloads, targets, device, args, world):
     steps = args.steps
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    gc_was = gc_pause()
     ev0.record(stream)
     probe_sequence_sharded(space, cams, [host_p[i % pool] for i in range(steps)],
                            [host_t[i % pool] for i in range(steps)], device=device)
     ev1.record(stream)
     torch.cuda.synchronize(device)
+    gc_resume(gc_was)
     ms = ev0.elapsed_time(ev1)
     if world > 1:
         import torch.distributed as dist

@@ -1,5 +1,7 @@
 // Per-device context: grow-only HBM workspace + pinned staging.
 #pragma once
+#include <cstdio>
+#include <cstdlib>
 
 #include <string>
 #include <vector>
@@ -124,6 +126,7 @@ struct airgs_ctx {
         if (b.cap < bytes) {
             size_t want = std::max(bytes, b.cap + b.cap / 4);
             want = (want + 255) & ~size_t(255);
+            if (std::getenv("AIRGS_TRACE_GROW")) std::fprintf(stderr, "[airgs] scratch %d grows %zu -> %zu\n", id, b.cap, want);
             AIRGS_CUDA_TRY(cudaDeviceSynchronize());
             if (b.p) AIRGS_CUDA_TRY(cudaFree(b.p));
             b.p = nullptr;
@@ -142,6 +145,7 @@ struct airgs_ctx {
     void *staging(size_t bytes) {
         if (host_cap < bytes) {
             size_t want = std::max(bytes, size_t(1) << 16);
+            if (std::getenv("AIRGS_TRACE_GROW")) std::fprintf(stderr, "[airgs] staging grows %zu -> %zu\n", host_cap, want);
             if (host) AIRGS_CUDA_TRY(cudaFreeHost(host));
             host = nullptr;
             host_cap = 0;
