@@ -94,6 +94,18 @@ __device__ __forceinline__ unsigned long long order_key(double z) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+// 32-bit list-entry key, monotone in the 64-bit order key: frozen positions
+// and the seam's input indices (< 2^30) first, then negative depths (a
+// near_clip < 0 camera keeps near_clip < z <= 0, ss/rasterizer.py:126), then
+// positive depths; fp32 depth bits (ties between distinct 64-bit keys are
+// resolved by the tile sort's exact-key run fix)
+__device__ __forceinline__ uint32_t list_key32(unsigned long long zk) {
+    if (zk >> 63) return 0x80000000u | (__float_as_uint((float)__longlong_as_double((long long)(zk & 0x7fffffffffffffffull))) >> 1);
+    if (zk < (1ull << 30)) return (uint32_t)zk;
+    const float f = (float)__longlong_as_double((long long)~zk);  // z <= -0
+    return 0x40000000u | (~__float_as_uint(f) >> 1);
+}
+
 __device__ __forceinline__ unsigned long long order_key_of(const int64_t *frozen, int64_t i, double tz) {
     if (frozen && frozen[i] >= 0) return (unsigned long long)frozen[i];
     return order_key(tz);
@@ -447,12 +459,7 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
             cull = true;
             cr = a.cullrec[o];
         }
-        const uint64_t zk = a.depth[o];
-        // 32-bit order key: small keys (frozen positions, the seam's input order)
-        // as they are; depth keys (z > 0) as their fp32 bits, monotone, behind them
-        const double z = __longlong_as_double((long long)(zk & 0x7fffffffffffffffull));
-        const uint32_t hi = (zk >> 63) ? (0x80000000u | (__float_as_uint((float)z) >> 1)) : (uint32_t)zk;
-        entry = ((uint64_t)hi << 32) | (uint32_t)i;
+        entry = ((uint64_t)list_key32(a.depth[o]) << 32) | (uint32_t)i;
     }
     const int nu = u1 - u0 + 1;
     int incl = nt;
@@ -558,11 +565,7 @@ __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     if (a.ntiles[o] <= 0) return;
     const Rec &r = a.recs[o];
     const int64_t tb = a.tile_base[s];
-    // fp32 depth from the orderable key (z > 0: key = bits | sign bit)
-    const double z = __longlong_as_double((long long)(a.depth[o] & 0x7fffffffffffffffull));
-    const uint64_t zk = a.depth[o];
-    const uint32_t hi = (zk >> 63) ? (0x80000000u | (__float_as_uint((float)z) >> 1)) : (uint32_t)zk;
-    const uint64_t entry = ((uint64_t)hi << 32) | (uint32_t)i;
+    const uint64_t entry = ((uint64_t)list_key32(a.depth[o]) << 32) | (uint32_t)i;
     const int txn = a.tiles_x[s];
     int u0, u1, v0, v1;
     rec_tile_range(r, u0, u1, v0, v1);
@@ -2524,7 +2527,8 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         if (f.count <= 0) throw ApiFailure(AIRGS_E_STRUCTURAL, "cannot render an empty frame");
         if (f.width != 17 && f.width != 26)
             throw ApiFailure(AIRGS_E_STRUCTURAL, "no sh degree yields parameter width " + std::to_string(f.width));
-        if (f.count > 0x7fffffffLL) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");
+        // (list keys hold frozen positions below 2^30)
+        if (f.count >= (1LL << 30)) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");
         const airgs_camera &c = cams[v.camera];
         if (c.width < 1 || c.height < 1) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad camera resolution");
         if (c.width > (65535 * kTile) || c.height > (65535 * kTile))
@@ -3107,7 +3111,7 @@ static void seam_impl(airgs_ctx *ctx, int64_t k, const double *means2d, const do
                       int64_t *Tt_out = nullptr, uint32_t **tcount_out = nullptr) {
     if (h < 1 || w < 1) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad image size");
     if (w > 65535 * kTile || h > 65535 * kTile) throw ApiFailure(AIRGS_E_CAPACITY, "image beyond the tile index range");
-    if (k > 0x7fffffffLL) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");
+    if (k >= (1LL << 30)) throw ApiFailure(AIRGS_E_CAPACITY, "too many primitives");  // list keys: index < 2^30
     std::vector<ItemHost> ih(1);
     ItemHost &it = ih[0];
     it.frame = 0;

@@ -100,15 +100,17 @@ def test_camera_validation():
     assert Camera.from_dict(c.to_dict()) == c
 
 
-def test_negative_near_clip_rejected_before_launch():
-    """Depth keys assume kept depths z > near_clip >= 0 (render.cu order_key);
-    a negative near plane is refused with the reference's ValidationError
-    class instead of silently mis-ordering tile lists."""
+def test_near_clip_must_be_finite():
+    """A negative near plane is accepted as the reference accepts it (kept
+    depths near_clip < z <= 0 order before positive ones, render.cu
+    list_key32; tests/test_gpu_render.py::test_negative_near_clip_matches_oracle);
+    a non-finite one is refused with the reference's ValidationError class."""
     from paper_2512_20943_b200.camera import camera_struct, look_at
     from paper_2512_20943_b200.errors import ValidationError
 
     camera_struct(look_at((0.0, 0.0, -2.5), (0.0, 0.0, 0.0), near_clip=0.0))
-    for bad in (-0.01, float("nan"), float("inf")):
+    camera_struct(look_at((0.0, 0.0, -2.5), (0.0, 0.0, 0.0), near_clip=-0.25))
+    for bad in (float("nan"), float("inf"), float("-inf")):
         with pytest.raises(ValidationError):
             camera_struct(look_at((0.0, 0.0, -2.5), (0.0, 0.0, 0.0), near_clip=bad))
 

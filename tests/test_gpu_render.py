@@ -40,6 +40,32 @@ def test_render_with_usage_matches_oracle(deg, n, res):
         assert np.max(np.abs(a.pixels - b)) <= PIX_TOL
 
 
+@pytest.mark.parametrize("near", [-0.2, -1.0])
+def test_negative_near_clip_matches_oracle(near):
+    """Cameras inside the cloud with a negative near plane: primitives at
+    near_clip < z <= 0 are kept and composited first, as the reference's
+    stable depth argsort orders them (ss/rasterizer.py:126-127); their
+    32-bit list keys sit between frozen positions and positive depths."""
+    from paper_2512_20943_b200 import rasterizer
+    from paper_2512_20943_b200.camera import Camera
+    from paper_2512_20943_b200.model import GaussianFrame
+
+    rng = np.random.default_rng(7)
+    p = random_params(rng, 3000, 0, spread=0.6)
+    base = _cams(3, (96, 72))
+    from paper_2512_20943_b200.camera import ring_rig
+
+    inner = ring_rig(3, radius=0.35, height=0.1, focal=80.0, resolution=(96, 72))
+    cams = [Camera(c.pose, c.focal, c.resolution, near_clip=near) for c in inner + base[:1]]
+    z = [(p[:, :3] @ np.asarray(c.pose)[:3, :3].T + np.asarray(c.pose)[:3, 3])[:, 2] for c in cams]
+    assert any(np.count_nonzero((zz > near) & (zz < 0)) > 50 for zz in z)  # negative depths are present
+    imgs, usage = rasterizer.render_with_usage(GaussianFrame(params=p), cams)
+    ref_imgs, ref_usage = orc.render_with_usage(p, cams)
+    np.testing.assert_array_equal(usage.counts, ref_usage)
+    for a, b in zip(imgs, ref_imgs):
+        assert np.max(np.abs(a.pixels - b)) <= PIX_TOL
+
+
 def test_render_single_view(rng, frame_factory, cam32):
     from paper_2512_20943_b200 import rasterizer
 
