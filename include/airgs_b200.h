@@ -78,6 +78,15 @@ typedef struct airgs_view_item {
                                 * (ss/rasterizer.py:128-142): position of each primitive
                                 * in the frozen order, -1 if absent (kept primitives
                                 * absent from it are appended in depth order) */
+    const int32_t *tile_minrank; /* int32[tiles] or NULL: clean-tile skip of the
+                                * pruning-level sweep (SSE-only items: target set,
+                                * image and usage NULL).  16x16 tile g (row-major)
+                                * with tile_minrank[g] >= tile_keep_min is known to
+                                * render identically to the target, so its SSE
+                                * contribution is exactly 0 and it is not composited
+                                * (airgs_tile_footprint builds the array) */
+    int32_t tile_keep_min;
+    int32_t reserved;
 } airgs_view_item;
 
 /* ---- context ------------------------------------------------------------ */
@@ -199,6 +208,22 @@ AIRGS_API int airgs_render(airgs_ctx *ctx, const airgs_frame *frames, int32_t nf
                  const airgs_camera *cams, int32_t ncams,
                  const airgs_view_item *items, int32_t nitems,
                  double *sse, void *stream);
+
+/* Tile footprint for the pruning-level sweep's clean-tile skip
+ * (ss/pruning.py:122-131 re-renders every level; only the tiles a pruned
+ * primitive reaches can differ from the unpruned reference render).  For
+ * every camera v and primitive i with rank[i] < rank_cap, the 16x16 tiles of
+ * its clipped bbox (widened by one pixel; the binning's tile set is a subset)
+ * receive minrank[v * tile_stride + g] = min(., rank[i]).  Run it over the
+ * unpruned frame and over the frame with every ranked entry pruned: a level
+ * that prunes ranks < k changes no primitive reaching tile g when
+ * minrank[g] >= k, so that tile's pixels equal the reference's bit for bit.
+ * Primitives that the renderer would refuse (zero quaternion, non-finite)
+ * are skipped: the render of that frame fails anyway.  The caller fills
+ * minrank with INT32_MAX first; device buffers, asynchronous. */
+AIRGS_API int airgs_tile_footprint(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cams,
+                                   int32_t ncams, const int32_t *rank, int32_t rank_cap, int32_t *minrank,
+                                   int64_t tile_stride, void *stream);
 
 /* Debug capture of one view's depth-ordered tile lists (the binning + sort
  * stage that precedes compositing; SURVEY.md s8(c) tile keys): for every

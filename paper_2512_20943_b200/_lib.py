@@ -55,6 +55,9 @@ class ItemC(ctypes.Structure):
         ("image", ctypes.c_void_p),
         ("usage", ctypes.c_void_p),
         ("frozen_pos", ctypes.c_void_p),
+        ("tile_minrank", ctypes.c_void_p),
+        ("tile_keep_min", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -66,6 +69,8 @@ SIGNATURES = {
     "airgs_launch_count": (i64, [vp]),
     "airgs_timing": (ctypes.c_int, [vp, i32, c_double_p, c_i64_p, c_double_p, c_i64_p]),
     "airgs_timing_stages": (ctypes.c_int, [vp, i32, c_double_p, c_i64_p, i32]),
+    "airgs_tile_footprint": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), ctypes.POINTER(CameraC), i32, vp, i32, vp,
+                                            i64, vp]),
     "airgs_debug_tile_lists": (ctypes.c_int, [vp, ctypes.POINTER(FrameC), ctypes.POINTER(CameraC), i64, vp, vp, vp]),
     "airgs_eval_stats": (ctypes.c_int, [vp, i32, c_i64_p]),
     "airgs_eval_margins": (ctypes.c_int, [vp, c_double_p]),

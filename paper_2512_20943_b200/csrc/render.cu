@@ -437,6 +437,8 @@ struct BinArgs {
     unsigned int *flags;
     int64_t stride;
     int index_order;
+    const int32_t *const *minrank;  // per item clean-tile skip arrays, or null
+    const int32_t *keep_min;
 };
 
 __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
@@ -472,6 +474,9 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     const int64_t tb = a.tile_base[s];
     const int txn = a.tiles_x[s];
+    // clean tiles of a pruning level take no pairs (k_compositeN skips them)
+    const int32_t *mr = a.minrank ? a.minrank[s] : nullptr;
+    const int32_t kmin = mr ? a.keep_min[s] : 0;
     // two rounds of 32 pairs per iteration: both counter atomics are in flight
     // before either result is consumed
     const bool any_cull = __any_sync(0xffffffffu, cull);
@@ -489,7 +494,9 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
         oent = __shfl_sync(0xffffffffu, entry, L);
         const int dv = j / onu;
         g = tb + (int64_t)(ov0 + dv) * txn + ou0 + (j - dv * onu);
-        if (!any_cull) return true;  // warp-uniform
+        // (no early return before the shuffles below: they take the full warp)
+        const bool clean = mr && k < total && mr[g - tb] >= kmin;
+        if (!any_cull) return !clean;  // warp-uniform
         CullRec oc;
         oc.A = __shfl_sync(0xffffffffu, cr.A, L);
         oc.B = __shfl_sync(0xffffffffu, cr.B, L);
@@ -500,7 +507,7 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
         oc.my = __shfl_sync(0xffffffffu, cr.my, L);
         oc.t = __shfl_sync(0xffffffffu, cr.t, L);
         const bool oculled = __shfl_sync(0xffffffffu, cull, L);
-        return !oculled || cull_keep(oc, j - dv * onu, dv);
+        return !clean && (!oculled || cull_keep(oc, j - dv * onu, dv));
     };
     for (int k0 = 0; k0 < total; k0 += 64) {
         const int ka = k0 + lane, kb = k0 + 32 + lane;
@@ -555,6 +562,8 @@ struct EmitArgs {
     uint64_t *ids;             // list entries (fp32 depth bits << 32 | id) in tile ranges
     int64_t stride;
     int index_order;           // (informational: the keys themselves decide, see k_bin)
+    const int32_t *const *minrank;  // per item clean-tile skip arrays (the pairs k_bin counted), or null
+    const int32_t *keep_min;
 };
 
 __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
@@ -572,9 +581,12 @@ __global__ void __launch_bounds__(256) k_emit(EmitArgs a) {
     const bool cull = a.binrec && (a.binrec[o].x & kCullFlag);  // the binning's pairs exactly
     CullRec cr{};
     if (cull) cr = a.cullrec[o];
+    const int32_t *mr = a.minrank ? a.minrank[s] : nullptr;
+    const int32_t kmin = mr ? a.keep_min[s] : 0;
     for (int v = v0; v <= v1; ++v)
         for (int u = u0; u <= u1; ++u) {
             if (cull && !cull_keep(cr, u - u0, v - v0)) continue;
+            if (mr && mr[v * txn + u] >= kmin) continue;
             const int64_t g = tb + v * txn + u;
             a.ids[a.tstart[g] + atomicAdd(a.cursor + g, 1u)] = entry;
         }
@@ -1937,6 +1949,23 @@ k_count_pairs(const CompItem *__restrict__ items, const int32_t *__restrict__ nt
 // one block per item: fixed-order reduction of that item's tile partials
 // (1024 threads, four independent accumulators each: the item's ~45k partials
 // are read with enough loads in flight; the order is fixed by the layout)
+// Clean tiles of a pruning-level item (airgs_view_item.tile_minrank): the
+// binning gave them no pairs, and their pixels equal the target's bit for bit
+// (no primitive the level changes reaches them), so their SSE partials are
+// exactly 0 -- the same partials compositing their full lists would give.
+__global__ void __launch_bounds__(256) k_zero_clean(double *__restrict__ sse_tiles, const int64_t *__restrict__ tile_base,
+                                                    const int32_t *const *__restrict__ minrank,
+                                                    const int32_t *__restrict__ keep_min) {
+    const int s = blockIdx.y;
+    const int32_t *mr = minrank[s];
+    if (!mr) return;
+    const int64_t tl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tl >= tile_base[s + 1] - tile_base[s] || mr[tl] < keep_min[s]) return;
+    double *o = sse_tiles + (tile_base[s] + tl) * kCompWarps;
+#pragma unroll
+    for (int k = 0; k < kCompWarps; ++k) o[k] = 0.0;
+}
+
 constexpr int kSseThreads = 1024;
 __global__ void __launch_bounds__(kSseThreads)
 k_sse_items(const double *__restrict__ sse_tiles, const int64_t *__restrict__ tile_base,
@@ -2068,6 +2097,8 @@ struct ItemHost {
     int64_t *usage;
     int clip;
     const int64_t *frozen = nullptr;  // frozen compositing order positions, or null
+    const int32_t *minrank = nullptr; // clean-tile skip (airgs_view_item.tile_minrank), or null
+    int32_t keep_min = 0;
 };
 
 // Device layout of the per-call descriptors shared by project / emit / composite.
@@ -2080,6 +2111,8 @@ struct Layout {
     const int32_t *d_tiles_x = nullptr;
     const int64_t *d_count = nullptr;
     const int32_t *d_tile_item = nullptr;
+    const int32_t *const *d_minrank = nullptr;  // per item: clean-tile skip array or null (null: none at all)
+    const int32_t *d_keep_min = nullptr;
 };
 
 // Stage B: histogram (already accumulated in tile_count) -> ranges -> emit ->
@@ -2130,7 +2163,7 @@ static TileLists scanned_lists(airgs_ctx *ctx, const std::vector<ItemHost> &item
     AIRGS_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * Tt, st));
     if (P > 0) {
         EmitArgs ea{recs,     binrec,  cullrec, depth,  ntiles,   L.d_tile_base, L.d_tiles_x, L.d_count,
-                    tstart,   cursor,  ids,     L.stride, index_order};
+                    tstart,   cursor,  ids,     L.stride, index_order, L.d_minrank, L.d_keep_min};
         k_emit<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ea);
         ++NL;
         check_launch();
@@ -2357,6 +2390,13 @@ static void sort_composite_sse(airgs_ctx *ctx, const std::vector<ItemHost> &item
     t_comp.end();
     if (sse && any_target) {
         StageScope t_sse(ctx, st, kStageSse);
+        if (L.d_minrank) {  // clean tiles of a pruning level: their pixels equal the target, SSE exactly 0
+            int64_t maxt = 0;
+            for (int s = 0; s < nitems; ++s) maxt = std::max(maxt, L.tile_base[s + 1] - L.tile_base[s]);
+            k_zero_clean<<<dim3((unsigned)ceil_div(maxt, 256), (unsigned)nitems), 256, 0, st>>>(
+                sse_tiles, L.d_tile_base, L.d_minrank, L.d_keep_min);
+            ++NL;
+        }
         k_sse_items<<<nitems, kSseThreads, 0, st>>>(sse_tiles, L.d_tile_base, d_has, sse);
         ++NL;
         check_launch();
@@ -2385,7 +2425,7 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
             AIRGS_CUDA_TRY(cudaMemsetAsync(pad, 0, sizeof(uint32_t) * (size_t)Tt * kBinCountStride, st));
         }
         BinArgs ba{binrec, cullrec, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, pad, bucket, cap, flags,
-                   L.stride, index_order};
+                   L.stride, index_order, L.d_minrank, L.d_keep_min};
         StageScope t_bin(ctx, st, kStageBin);
         k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
         ++NL;
@@ -2485,12 +2525,20 @@ static void upload_layout(airgs_ctx *ctx, const std::vector<ItemHost> &items, La
     const size_t o_tb = off; off = align(off + sizeof(int64_t) * (nitems + 1));
     const size_t o_tx = off; off = align(off + sizeof(int32_t) * nitems);
     const size_t o_cnt = off; off = align(off + sizeof(int64_t) * nitems);
+    bool any_skip = false;
+    for (const ItemHost &h : items) any_skip |= h.minrank != nullptr;
+    const size_t o_mr = off; off = align(off + (any_skip ? sizeof(void *) * nitems : 0));
+    const size_t o_km = off; off = align(off + (any_skip ? sizeof(int32_t) * nitems : 0));
     std::vector<char> hbuf(off);
     memcpy(hbuf.data() + o_tb, L.tile_base.data(), sizeof(int64_t) * (nitems + 1));
     for (int s = 0; s < nitems; ++s) {
         const int32_t tx = items[s].tiles_x;
         memcpy(hbuf.data() + o_tx + sizeof(int32_t) * s, &tx, sizeof(int32_t));
         memcpy(hbuf.data() + o_cnt + sizeof(int64_t) * s, &items[s].count, sizeof(int64_t));
+        if (any_skip) {
+            memcpy(hbuf.data() + o_mr + sizeof(void *) * s, &items[s].minrank, sizeof(void *));
+            memcpy(hbuf.data() + o_km + sizeof(int32_t) * s, &items[s].keep_min, sizeof(int32_t));
+        }
     }
     char *d = (char *)ctx->scratch(kSlotMisc0, off);
     h2d_small(ctx, d, hbuf.data(), off, st);
@@ -2498,6 +2546,8 @@ static void upload_layout(airgs_ctx *ctx, const std::vector<ItemHost> &items, La
     L.d_tiles_x = (const int32_t *)(d + o_tx);
     L.d_count = (const int64_t *)(d + o_cnt);
     L.d_tile_item = nullptr;  // built on device when the oversized-tile path needs it
+    L.d_minrank = any_skip ? (const int32_t *const *)(d + o_mr) : nullptr;
+    L.d_keep_min = any_skip ? (const int32_t *)(d + o_km) : nullptr;
 }
 
 
@@ -2546,6 +2596,10 @@ static void render_impl(airgs_ctx *ctx, const airgs_frame *frames, int nframes, 
         h.trans = bwd ? bwd->t_final : nullptr;
         h.usage = v.usage;
         h.frozen = v.frozen_pos;
+        h.minrank = v.tile_minrank;
+        h.keep_min = v.tile_keep_min;
+        if (h.minrank && (!h.target || h.image || h.usage || bwd))
+            throw ApiFailure(AIRGS_E_STRUCTURAL, "tile_minrank needs an SSE-only item (target set, no image or usage)");
         h.clip = bwd ? 0 : 1;  // the forward of render_forward returns the unclipped image
         per_frame[v.frame].push_back(s);
         stride = std::max(stride, f.count);
@@ -3211,6 +3265,131 @@ static void sse_impl(airgs_ctx *ctx, const double *a, const double *b, int64_t n
 }  // namespace airgs
 
 using namespace airgs;
+
+// ---------------------------------------------------------------------------
+// tile footprint (pruning-level sweep, clean-tile skip; include/airgs_b200.h)
+
+// The projection of k_project restated for the clipped bbox alone (same fp64
+// expressions, so the same bbox), widened by one pixel: every tile the
+// binning gives the primitive (clipped bbox ∩ threshold-ellipse AABB) is
+// marked.  Non-finite geometry marks the whole view.
+__global__ void __launch_bounds__(128) k_tile_footprint(airgs_frame fr, const airgs_camera *__restrict__ cams,
+                                                         const int32_t *__restrict__ rank, int32_t rank_cap,
+                                                         int32_t *__restrict__ minrank, int64_t tile_stride) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= fr.count) return;
+    const int32_t rk = rank[i];
+    if (rk >= rank_cap) return;
+    const airgs_camera &cam = cams[blockIdx.y];
+    const int64_t ld = fr.ld;
+    double p[11];
+    bool finite = true;
+#pragma unroll
+    for (int c = 0; c < 11; ++c) {
+        p[c] = fr.params[i + c * ld];
+        finite &= isfinite(p[c]);
+    }
+    for (int c = 11; c < fr.width; ++c) finite &= isfinite(fr.params[i + c * ld]);
+    const double qn = sqrt(((p[3] * p[3] + p[4] * p[4]) + p[5] * p[5]) + p[6] * p[6]);
+    if (!finite || qn == 0.0) return;  // the render of this frame fails (ss/rasterizer.py:105-106)
+    const double alpha = sigmoid_ref(p[10]);
+    if (!(alpha > kEpsContrib * (1.0 - 1e-12))) return;  // not kept by either render
+    const double *R = cam.rot;
+    const double tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
+    if (!(tz > cam.near_clip - 1e-9 * (1.0 + fabs(cam.near_clip)))) return;
+    const int txn = (cam.width + kTile - 1) / kTile, tyn = (cam.height + kTile - 1) / kTile;
+    int32_t *mr = minrank + (int64_t)blockIdx.y * tile_stride;
+    const double w_ = p[3] / qn, x_ = p[4] / qn, y_ = p[5] / qn, z_ = p[6] / qn;
+    const double s0 = exp(2.0 * p[7]), s1 = exp(2.0 * p[8]), s2 = exp(2.0 * p[9]);
+    double m[9];
+    m[0] = 1.0 - 2.0 * (y_ * y_ + z_ * z_);
+    m[1] = 2.0 * (x_ * y_ - w_ * z_);
+    m[2] = 2.0 * (x_ * z_ + w_ * y_);
+    m[3] = 2.0 * (x_ * y_ + w_ * z_);
+    m[4] = 1.0 - 2.0 * (x_ * x_ + z_ * z_);
+    m[5] = 2.0 * (y_ * z_ - w_ * x_);
+    m[6] = 2.0 * (x_ * z_ - w_ * y_);
+    m[7] = 2.0 * (y_ * z_ + w_ * x_);
+    m[8] = 1.0 - 2.0 * (x_ * x_ + y_ * y_);
+    double cv[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            cv[3 * r + c] = dot3_blas(m[3 * r] * s0, m[3 * r + 1] * s1, m[3 * r + 2] * s2, m[3 * c], m[3 * c + 1],
+                                      m[3 * c + 2]);
+    const double tx = dot3_blas(p[0], p[1], p[2], R[0], R[1], R[2]) + cam.trans[0];
+    const double ty = dot3_blas(p[0], p[1], p[2], R[3], R[4], R[5]) + cam.trans[1];
+    const double fl = cam.focal;
+    const double mx = fl * tx / tz + 0.5 * (double)cam.width;
+    const double my = fl * ty / tz + 0.5 * (double)cam.height;
+    const double j00 = fl / tz, zz = tz * tz, j02 = -fl * tx / zz, j12 = -fl * ty / zz;
+    double M[6];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        M[c] = dot3_blas(j00, 0.0, j02, R[c], R[3 + c], R[6 + c]);
+        M[3 + c] = dot3_blas(0.0, j00, j12, R[c], R[3 + c], R[6 + c]);
+    }
+    double MC[6];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            MC[3 * r + c] = dot3_blas(M[3 * r], M[3 * r + 1], M[3 * r + 2], cv[c], cv[3 + c], cv[6 + c]);
+    const double a2 = dot3_blas(MC[0], MC[1], MC[2], M[0], M[1], M[2]) + kCovBlur;
+    const double b2 = dot3_blas(MC[0], MC[1], MC[2], M[3], M[4], M[5]);
+    const double c2 = dot3_blas(MC[3], MC[4], MC[5], M[3], M[4], M[5]) + kCovBlur;
+    const double dd = a2 - c2;
+    const double eig = 0.5 * (a2 + c2) + sqrt(fmax(0.25 * (dd * dd) + b2 * b2, 0.0));
+    const double rad = kRadiusSigma * sqrt(eig);
+    const double Wd = (double)cam.width, Hd = (double)cam.height;
+    int u0 = 0, u1 = txn - 1, v0 = 0, v1 = tyn - 1;
+    if (isfinite(mx) && isfinite(my) && isfinite(rad)) {
+        const int x0 = (int)fmin(fmax(floor(mx - rad) - 1.0, 0.0), Wd);
+        const int x1 = (int)fmin(fmax(ceil(mx + rad) + 2.0, 0.0), Wd);
+        const int y0 = (int)fmin(fmax(floor(my - rad) - 1.0, 0.0), Hd);
+        const int y1 = (int)fmin(fmax(ceil(my + rad) + 2.0, 0.0), Hd);
+        if (x1 <= x0 || y1 <= y0) return;
+        u0 = x0 / kTile;
+        u1 = (x1 - 1) / kTile;
+        v0 = y0 / kTile;
+        v1 = (y1 - 1) / kTile;
+    }
+    for (int v = v0; v <= v1; ++v)
+        for (int u = u0; u <= u1; ++u) {
+            int32_t *q = mr + (int64_t)v * txn + u;
+            if (*q > rk) atomicMin(q, rk);
+        }
+}
+
+static void tile_footprint_impl(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cams, int ncams,
+                                const int32_t *rank, int32_t rank_cap, int32_t *minrank, int64_t tile_stride,
+                                cudaStream_t st) {
+    if (ncams <= 0 || frame->count <= 0 || rank_cap <= 0) return;
+    if (frame->width != 17 && frame->width != 26)
+        throw ApiFailure(AIRGS_E_STRUCTURAL, "no sh degree yields parameter width " + std::to_string(frame->width));
+    for (int v = 0; v < ncams; ++v) {
+        const airgs_camera &c = cams[v];
+        if (c.width < 1 || c.height < 1) throw ApiFailure(AIRGS_E_STRUCTURAL, "bad camera resolution");
+        if (ceil_div(c.width, kTile) * ceil_div(c.height, kTile) > tile_stride)
+            throw ApiFailure(AIRGS_E_CAPACITY, "tile_stride below a camera's tile count");
+    }
+    if (ncams > 65535) throw ApiFailure(AIRGS_E_CAPACITY, "too many cameras");
+    airgs_camera *d_cams = ctx->scratch_t<airgs_camera>(kSlotMisc1, (size_t)ncams);
+    h2d_small(ctx, d_cams, cams, sizeof(airgs_camera) * ncams, st);
+    const dim3 grid((unsigned)ceil_div(frame->count, 128), (unsigned)ncams);
+    k_tile_footprint<<<grid, 128, 0, st>>>(*frame, d_cams, rank, rank_cap, minrank, tile_stride);
+    ++ctx->launches;
+    check_launch();
+}
+
+extern "C" int airgs_tile_footprint(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cams, int32_t ncams,
+                                    const int32_t *rank, int32_t rank_cap, int32_t *minrank, int64_t tile_stride,
+                                    void *stream) {
+    return guarded(ctx, [&] {
+        tile_footprint_impl(ctx, frame, cams, ncams, rank, rank_cap, minrank, tile_stride, (cudaStream_t)stream);
+    });
+}
 
 extern "C" int airgs_render(airgs_ctx *ctx, const airgs_frame *frames, int32_t nframes, const airgs_camera *cams,
                             int32_t ncams, const airgs_view_item *items, int32_t nitems, double *sse, void *stream) {

@@ -316,7 +316,7 @@ def level_removed(t: LevelTable):
     return t.removed
 
 
-def render_sse_chunked(frames, cams, items, targets, device=None, host=True):
+def render_sse_chunked(frames, cams, items, targets, device=None, host=True, tile_skip=None):
     """SSE of (frame, view) items against their targets, at most
     RENDER_PAIRS_PER_CALL (item, primitive) records per render call (C5: 2M
     primitives x 8 levels x 32 views would not fit one call's scratch).
@@ -329,10 +329,46 @@ def render_sse_chunked(frames, cams, items, targets, device=None, host=True):
         return np.zeros(0) if host else None
     n = max(fr.count for fr in frames)
     per_call = max(1, RENDER_PAIRS_PER_CALL // max(n, 1))
-    parts = [render_views(frames, cams, items[k:k + per_call], targets=targets[k:k + per_call], device=device).sse
+    parts = [render_views(frames, cams, items[k:k + per_call], targets=targets[k:k + per_call], device=device,
+                          tile_skip=None if tile_skip is None else tile_skip[k:k + per_call]).sse
              for k in range(0, len(items), per_call)]
     sse = torch.cat(parts) if len(parts) > 1 else parts[0]
     return sse.cpu().numpy() if host else sse
+
+
+def tile_skip_enabled() -> bool:
+    """Clean-tile skip of the level renders (default on; AIRGS_LEVEL_TILE_SKIP=0
+    renders every tile, for A/B checks -- the qualities are bit-identical)."""
+    import os
+
+    return os.environ.get("AIRGS_LEVEL_TILE_SKIP", "1") != "0"
+
+
+def tile_footprint(p: LevelPlan, cams, rank_cap: int):
+    """minrank[v] (device int32 [tiles of view v]): the lowest prune rank of
+    an entry whose primitive reaches that tile of view v in the unpruned
+    reference render or with its entry pruned.  A level pruning ranks < k
+    changes only primitives of rank < k, so every tile with minrank >= k
+    composites exactly as in the reference render: SSE 0 without rendering
+    (the reference re-renders whole levels, ss/pruning.py:122-131)."""
+    import torch
+
+    from ._lib import CameraC, FrameC
+    from .camera import camera_struct
+
+    dev = p.canon.device
+    eng = _engine(dev)
+    cams = list(cams)
+    tiles = [((c.resolution[0] + 15) // 16) * ((c.resolution[1] + 15) // 16) for c in cams]
+    stride = max(tiles)
+    minrank = torch.full((len(cams), stride), 2**31 - 1, dtype=torch.int32, device=dev)
+    cc = (CameraC * len(cams))(*[camera_struct(c) for c in cams])
+    planes = [level_frame_planes(p, None), level_frame_planes(p, 2**31 - 1)]
+    for pl in planes:
+        fc = FrameC(pl.data_ptr(), p.n, pl.shape[1], p.width, 0)
+        eng.call("airgs_tile_footprint", ctypes.byref(fc), cc, len(cams), _ptr(p.rank), int(rank_cap),
+                 _ptr(minrank), stride, eng.stream())
+    return [minrank[v, :tiles[v]] for v in range(len(cams))], planes
 
 
 def deferred(dev, run):
@@ -396,6 +432,7 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
         # ss/pruning.py:102-104)
         todo = [li for li, j in enumerate(t.keep) if t.kmins[j] > 0]
         V = len(cams)
+        skip = tile_skip_enabled()
 
         def run(nl):
             import torch
@@ -403,15 +440,24 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
             from ._lib import engine_lane
             from .grouping import _lane_stream
 
-            ref = GaussianFrame(device_params=level_frame_planes(p, None), count=p.n, frame_index=frame_index,
+            kmins = [t.kmins[t.keep[li]] for li in todo]
+            if skip:
+                minrank, (ref_planes, _) = tile_footprint(p, cams, max(kmins))
+            else:
+                minrank, ref_planes = None, level_frame_planes(p, None)
+            ref = GaussianFrame(device_params=ref_planes, count=p.n, frame_index=frame_index,
                                 group_key=space.key_index)
             rv = render_views([ref], cams, [(0, v) for v in range(V)], want_images=True, device=dev)
-            frames = [GaussianFrame(device_params=level_frame_planes(p, t.kmins[t.keep[li]]), count=p.n)
-                      for li in todo]
+            frames = [GaussianFrame(device_params=level_frame_planes(p, k), count=p.n) for k in kmins]
+
+            def level_skip(fi):
+                return None if minrank is None else [(minrank[v], kmins[fi]) for v in range(V)]
+
             if nl == 1:
                 items = [(fi, v) for fi in range(len(frames)) for v in range(V)]
                 targets = [rv.images[v] for _ in range(len(frames)) for v in range(V)]
-                out = render_sse_chunked(frames, cams, items, targets, device=dev, host=False)
+                sk = None if minrank is None else [x for fi in range(len(frames)) for x in level_skip(fi)]
+                out = render_sse_chunked(frames, cams, items, targets, device=dev, host=False, tile_skip=sk)
             else:
                 # one render call per level, alternating over the engine lanes: level
                 # k+1's projection / binning / sort overlap level k's compositing
@@ -424,11 +470,14 @@ def build_level_space(delta: DeltaTensor, space: CanonicalSpace, cams, ratios, u
                     lane = fi % nl
                     with torch.cuda.stream(streams[lane]), engine_lane(lane):
                         sse = render_sse_chunked([fr], cams, [(0, v) for v in range(V)],
-                                                 [rv.images[v] for v in range(V)], device=dev, host=False)
+                                                 [rv.images[v] for v in range(V)], device=dev, host=False,
+                                                 tile_skip=level_skip(fi))
                     if lane:
                         sse.record_stream(main)
                         for v in range(V):
                             rv.images[v].record_stream(streams[lane])
+                            if minrank is not None:
+                                minrank[v].record_stream(streams[lane])
                     parts.append(sse)
                 for st in streams[1:]:
                     main.wait_stream(st)

@@ -101,7 +101,7 @@ def _frame_planes(frame, dev):
 
 
 def render_views(frames, cams, items, targets=None, want_images=False, usage_frames=None, device=None,
-                 frozen=None):
+                 frozen=None, tile_skip=None):
     """Render ``items`` = [(frame_idx, cam_idx), ...] in one pipeline pass.
 
     targets: optional list (per item) of device (h, w, 3) float64 tensors;
@@ -111,6 +111,10 @@ def render_views(frames, cams, items, targets=None, want_images=False, usage_fra
       counts; ``.usage[f]`` is an int64 device tensor over the frame.
     frozen: optional list (per item) of frozen-order position tensors
       (``frozen_positions``) or None (ss/rasterizer.py:128-142).
+    tile_skip: optional list (per item) of (minrank, keep_min) or None, for
+      SSE-only items of a pruning-level sweep: tiles g with minrank[g] >=
+      keep_min are known to equal the target and are not composited
+      (``pruning.tile_footprint``; airgs_view_item.tile_minrank).
     """
     import torch
 
@@ -152,6 +156,10 @@ def render_views(frames, cams, items, targets=None, want_images=False, usage_fra
             ic[s].usage = usage[fi].data_ptr()
         if frozen is not None and frozen[s] is not None:
             ic[s].frozen_pos = frozen[s].data_ptr()
+        if tile_skip is not None and tile_skip[s] is not None:
+            mr, km = tile_skip[s]
+            ic[s].tile_minrank = mr.data_ptr()
+            ic[s].tile_keep_min = int(km)
     sse = torch.zeros((len(items),), dtype=torch.float64, device=dev)
     before = eng.launches
     eng.call("airgs_render", fc, len(frames), cc, len(cams), ic, len(items), ptr(sse), eng.stream())

@@ -49,7 +49,8 @@ def test_struct_layouts_match_header():
 
     assert ctypes.sizeof(_lib.CameraC) == 9 * 8 + 3 * 8 + 3 * 8 + 8 + 8 + 4 + 4
     assert ctypes.sizeof(_lib.FrameC) == 8 + 8 + 8 + 4 + 4
-    assert ctypes.sizeof(_lib.ItemC) == 4 + 4 + 8 + 8 + 8 + 8
+    assert ctypes.sizeof(_lib.ItemC) == 4 + 4 + 8 + 8 + 8 + 8 + 8 + 4 + 4
+    assert _lib.ItemC.tile_minrank.offset == 40 and _lib.ItemC.tile_keep_min.offset == 48
 
 
 def test_status_codes_map_to_reference_taxonomy():

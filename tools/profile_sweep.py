@@ -49,3 +49,10 @@ for rep in range(3):
     lv = t("level renders (batched)", lambda: render_views(frames, cams, items, targets=targets))
     t("sse readback", lambda: lv.sse.cpu().numpy())
     t("build_level_space total", lambda: pruning.build_level_space(gap, space, cams, ratios, usage, 1e-4))
+    os.environ["AIRGS_LEVEL_TILE_SKIP"] = "0"
+    t("build_level_space (no skip)", lambda: pruning.build_level_space(gap, space, cams, ratios, usage, 1e-4))
+    os.environ["AIRGS_LEVEL_TILE_SKIP"] = "1"
+    mr, _ = pruning.tile_footprint(p, cams, max(kmins))
+    tot = sum(int(m.numel()) for m in mr)
+    print("clean tile share per level:",
+          " ".join("%.3f" % (sum(int((m >= k).sum()) for m in mr) / tot) for k in kmins[1:]), flush=True)
