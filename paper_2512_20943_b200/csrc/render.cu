@@ -3269,10 +3269,11 @@ using namespace airgs;
 // ---------------------------------------------------------------------------
 // tile footprint (pruning-level sweep, clean-tile skip; include/airgs_b200.h)
 
-// The projection of k_project restated for the clipped bbox alone (same fp64
-// expressions, so the same bbox), widened by one pixel: every tile the
-// binning gives the primitive (clipped bbox ∩ threshold-ellipse AABB) is
-// marked.  Non-finite geometry marks the whole view.
+// The projection of k_project restated for the clipped bbox and the
+// threshold-ellipse AABB alone (same fp64 expressions, so the same extents),
+// each widened by a pixel or more: every tile the binning gives the primitive
+// (clipped bbox ∩ threshold-ellipse AABB, rec_tile_range) is marked.
+// Non-finite geometry marks the whole view.
 __global__ void __launch_bounds__(128) k_tile_footprint(airgs_frame fr, const airgs_camera *__restrict__ cams,
                                                          const int32_t *__restrict__ rank, int32_t rank_cap,
                                                          int32_t *__restrict__ minrank, int64_t tile_stride) {
@@ -3350,10 +3351,23 @@ __global__ void __launch_bounds__(128) k_tile_footprint(airgs_frame fr, const ai
         const int y0 = (int)fmin(fmax(floor(my - rad) - 1.0, 0.0), Hd);
         const int y1 = (int)fmin(fmax(ceil(my + rad) + 2.0, 0.0), Hd);
         if (x1 <= x0 || y1 <= y0) return;
-        u0 = x0 / kTile;
-        u1 = (x1 - 1) / kTile;
-        v0 = y0 / kTile;
-        v1 = (y1 - 1) / kTile;
+        int xa = x0, xb = x1 - 1, ya = y0, yb = y1 - 1;
+        const double det = a2 * c2 - b2 * b2;
+        const double t2 = 2.0 * fmax(log(alpha / kEpsContrib) * 1.0002 + 2e-4, 0.0);
+        const double hx = sqrt(t2 * (a2 + 1e-9 * a2)) * 1.0002 + 1e-3;
+        const double hy = sqrt(t2 * (c2 + 1e-9 * c2)) * 1.0002 + 1e-3;
+        if (det > 0.0 && isfinite(hx) && isfinite(hy)) {  // k_project's rec.hx / rec.hy, padded outward
+            const double ex = hx * 1.001 + 2.0, ey = hy * 1.001 + 2.0;
+            xa = max(xa, (int)fmax(floor(mx - 0.5 - ex), -1.0));
+            xb = min(xb, (int)fmin(ceil(mx - 0.5 + ex), Wd));
+            ya = max(ya, (int)fmax(floor(my - 0.5 - ey), -1.0));
+            yb = min(yb, (int)fmin(ceil(my - 0.5 + ey), Hd));
+            if (xa > xb || ya > yb) return;
+        }
+        u0 = xa / kTile;
+        u1 = xb / kTile;
+        v0 = ya / kTile;
+        v1 = yb / kTile;
     }
     for (int v = v0; v <= v1; ++v)
         for (int u = u0; u <= u1; ++u) {

@@ -238,13 +238,20 @@ def build_level_space_sharded(delta, space, cams, ratios, usage, quant_step, bas
     def run():
         # reference images only for the views this rank needs
         need_views = sorted({int(i) % V for i in mine})
-        ref = GaussianFrame(device_params=pruning.level_frame_planes(p, None), count=p.n)
+        need_levels = sorted({int(i) // V for i in mine})
+        kmin = {li: t.kmins[t.keep[li]] for li in need_levels}
+        minrank = None
+        if need_levels and pruning.tile_skip_enabled() and max(kmin.values()) > 0:
+            # clean-tile skip, as in pruning.build_level_space
+            minrank, (ref_planes, _) = pruning.tile_footprint(p, cams, max(kmin.values()))
+        else:
+            ref_planes = pruning.level_frame_planes(p, None)
+        ref = GaussianFrame(device_params=ref_planes, count=p.n)
         refs = {}
         if need_views:
             rv = render_views([ref], cams, [(0, v) for v in need_views], want_images=True, device=dev)
             refs = dict(zip(need_views, rv.images))
-        need_levels = sorted({int(i) // V for i in mine})
-        frames = {li: GaussianFrame(device_params=pruning.level_frame_planes(p, t.kmins[t.keep[li]]), count=p.n)
+        frames = {li: GaussianFrame(device_params=pruning.level_frame_planes(p, kmin[li]), count=p.n)
                   for li in need_levels}
         if mine.size == 0:
             local = torch.zeros((0,), dtype=torch.float64, device=dev)
@@ -252,8 +259,10 @@ def build_level_space_sharded(delta, space, cams, ratios, usage, quant_step, bas
             order = sorted(frames)
             pos = {li: k for k, li in enumerate(order)}
             items = [(pos[int(i) // V], int(i) % V) for i in mine]
+            skip = None if minrank is None else [(minrank[int(i) % V], kmin[int(i) // V]) for i in mine]
             local = pruning.render_sse_chunked([frames[li] for li in order], cams, items,
-                                               [refs[int(i) % V] for i in mine], device=dev, host=False)
+                                               [refs[int(i) % V] for i in mine], device=dev, host=False,
+                                               tile_skip=skip)
         pruning.level_removed(t)  # host-only work overlapping the enqueued renders
         return local
 
