@@ -441,6 +441,9 @@ struct BinArgs {
     const int32_t *keep_min;
 };
 
+// SKIP: the clean-tile test of a pruning-level sweep (a separate instantiation:
+// the per-pair test costs the probe's binning ~10%)
+template <bool SKIP>
 __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
     const int s = blockIdx.y;
     const int lane = threadIdx.x & 31;
@@ -475,8 +478,8 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
     const int64_t tb = a.tile_base[s];
     const int txn = a.tiles_x[s];
     // clean tiles of a pruning level take no pairs (k_compositeN skips them)
-    const int32_t *mr = a.minrank ? a.minrank[s] : nullptr;
-    const int32_t kmin = mr ? a.keep_min[s] : 0;
+    const int32_t *mr = SKIP ? a.minrank[s] : nullptr;
+    const int32_t kmin = SKIP && mr ? a.keep_min[s] : 0;
     // two rounds of 32 pairs per iteration: both counter atomics are in flight
     // before either result is consumed
     const bool any_cull = __any_sync(0xffffffffu, cull);
@@ -495,7 +498,7 @@ __global__ void __launch_bounds__(256) k_bin(BinArgs a) {
         const int dv = j / onu;
         g = tb + (int64_t)(ov0 + dv) * txn + ou0 + (j - dv * onu);
         // (no early return before the shuffles below: they take the full warp)
-        const bool clean = mr && k < total && mr[g - tb] >= kmin;
+        const bool clean = SKIP && mr && k < total && mr[g - tb] >= kmin;
         if (!any_cull) return !clean;  // warp-uniform
         CullRec oc;
         oc.A = __shfl_sync(0xffffffffu, cr.A, L);
@@ -2427,7 +2430,11 @@ static void bin_and_composite(airgs_ctx *ctx, const std::vector<ItemHost> &items
         BinArgs ba{binrec, cullrec, depth, ntiles, L.d_tile_base, L.d_tiles_x, L.d_count, pad, bucket, cap, flags,
                    L.stride, index_order, L.d_minrank, L.d_keep_min};
         StageScope t_bin(ctx, st, kStageBin);
-        k_bin<<<dim3((unsigned)ceil_div(maxc, 256), (unsigned)nitems), 256, 0, st>>>(ba);
+        const dim3 bgrid((unsigned)ceil_div(maxc, 256), (unsigned)nitems);
+        if (L.d_minrank)
+            k_bin<true><<<bgrid, 256, 0, st>>>(ba);
+        else
+            k_bin<false><<<bgrid, 256, 0, st>>>(ba);
         ++NL;
         if (kBinCountStride > 1) {
             k_bin_counts<<<(unsigned)ceil_div(Tt, 256), 256, 0, st>>>(pad, tile_count, Tt);
