@@ -78,6 +78,22 @@ def test_c3_level_space_identical_with_and_without_tile_skip(monkeypatch):
         assert a.quality_db == b.quality_db  # bit for bit
 
 
+@pytest.mark.parametrize("views,count", [(4, 20_000), (2, 60_000)])
+def test_small_level_space_identical_with_and_without_tile_skip(monkeypatch, views, count):
+    """Reduced C3 scenes (fast enough for compute-sanitizer): the skip path
+    (k_tile_footprint, k_bin<true>, k_zero_clean) against full renders."""
+    from paper_2512_20943_b200.pruning import build_level_space
+
+    gap, space, cams, usage = _c3_gap(views=views, count=count, seed=5)
+    ratios = [0.0, 0.05, 0.2, 0.5, 0.9]
+    monkeypatch.setenv("AIRGS_LEVEL_TILE_SKIP", "0")
+    off = build_level_space(gap, space, cams, ratios, usage, 1e-4)
+    monkeypatch.setenv("AIRGS_LEVEL_TILE_SKIP", "1")
+    on = build_level_space(gap, space, cams, ratios, usage, 1e-4)
+    assert [x.quality_db for x in on.levels] == [x.quality_db for x in off.levels]
+    assert [x.size_bytes for x in on.levels] == [x.size_bytes for x in off.levels]
+
+
 def test_tile_skip_refused_for_items_with_pixels_or_usage():
     import torch
 

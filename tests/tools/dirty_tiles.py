@@ -1,6 +1,8 @@
 """Fraction of a view's tiles touched by the pruned rows of each pruning level
 (C3, CPU, oracle projection): the upper bound on what dirty-tile reuse across
-levels could skip.  python tools/dirty_tiles.py"""
+levels could skip -- with UNIFORM RANDOM usage, which the real
+sweep does not have (its measured clean shares: DESIGN.md s4, level sweep).
+python tools/dirty_tiles.py"""
 import os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
