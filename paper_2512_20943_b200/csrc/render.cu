@@ -3282,13 +3282,13 @@ using namespace airgs;
 // (clipped bbox ∩ threshold-ellipse AABB, rec_tile_range) is marked.
 // Non-finite geometry marks the whole view.
 __global__ void __launch_bounds__(128) k_tile_footprint(airgs_frame fr, const airgs_camera *__restrict__ cams,
-                                                         const int32_t *__restrict__ rank, int32_t rank_cap,
+                                                         int ncams, const int32_t *__restrict__ rank, int32_t rank_cap,
                                                          int32_t *__restrict__ minrank, int64_t tile_stride) {
+    // one thread per primitive, its view-independent terms once, then every view
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= fr.count) return;
     const int32_t rk = rank[i];
     if (rk >= rank_cap) return;
-    const airgs_camera &cam = cams[blockIdx.y];
     const int64_t ld = fr.ld;
     double p[11];
     bool finite = true;
@@ -3302,11 +3302,6 @@ __global__ void __launch_bounds__(128) k_tile_footprint(airgs_frame fr, const ai
     if (!finite || qn == 0.0) return;  // the render of this frame fails (ss/rasterizer.py:105-106)
     const double alpha = sigmoid_ref(p[10]);
     if (!(alpha > kEpsContrib * (1.0 - 1e-12))) return;  // not kept by either render
-    const double *R = cam.rot;
-    const double tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
-    if (!(tz > cam.near_clip - 1e-9 * (1.0 + fabs(cam.near_clip)))) return;
-    const int txn = (cam.width + kTile - 1) / kTile, tyn = (cam.height + kTile - 1) / kTile;
-    int32_t *mr = minrank + (int64_t)blockIdx.y * tile_stride;
     const double w_ = p[3] / qn, x_ = p[4] / qn, y_ = p[5] / qn, z_ = p[6] / qn;
     const double s0 = exp(2.0 * p[7]), s1 = exp(2.0 * p[8]), s2 = exp(2.0 * p[9]);
     double m[9];
@@ -3326,61 +3321,69 @@ __global__ void __launch_bounds__(128) k_tile_footprint(airgs_frame fr, const ai
         for (int c = 0; c < 3; ++c)
             cv[3 * r + c] = dot3_blas(m[3 * r] * s0, m[3 * r + 1] * s1, m[3 * r + 2] * s2, m[3 * c], m[3 * c + 1],
                                       m[3 * c + 2]);
-    const double tx = dot3_blas(p[0], p[1], p[2], R[0], R[1], R[2]) + cam.trans[0];
-    const double ty = dot3_blas(p[0], p[1], p[2], R[3], R[4], R[5]) + cam.trans[1];
-    const double fl = cam.focal;
-    const double mx = fl * tx / tz + 0.5 * (double)cam.width;
-    const double my = fl * ty / tz + 0.5 * (double)cam.height;
-    const double j00 = fl / tz, zz = tz * tz, j02 = -fl * tx / zz, j12 = -fl * ty / zz;
-    double M[6];
+    const double t2 = 2.0 * fmax(log(alpha / kEpsContrib) * 1.0002 + 2e-4, 0.0);
+    for (int v = 0; v < ncams; ++v) {
+        const airgs_camera &cam = cams[v];
+        const double *R = cam.rot;
+        const double tz = dot3_blas(p[0], p[1], p[2], R[6], R[7], R[8]) + cam.trans[2];
+        if (!(tz > cam.near_clip - 1e-9 * (1.0 + fabs(cam.near_clip)))) continue;
+        const int txn = (cam.width + kTile - 1) / kTile, tyn = (cam.height + kTile - 1) / kTile;
+        int32_t *mr = minrank + (int64_t)v * tile_stride;
+        const double tx = dot3_blas(p[0], p[1], p[2], R[0], R[1], R[2]) + cam.trans[0];
+        const double ty = dot3_blas(p[0], p[1], p[2], R[3], R[4], R[5]) + cam.trans[1];
+        const double fl = cam.focal;
+        const double mx = fl * tx / tz + 0.5 * (double)cam.width;
+        const double my = fl * ty / tz + 0.5 * (double)cam.height;
+        const double j00 = fl / tz, zz = tz * tz, j02 = -fl * tx / zz, j12 = -fl * ty / zz;
+        double M[6];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        M[c] = dot3_blas(j00, 0.0, j02, R[c], R[3 + c], R[6 + c]);
-        M[3 + c] = dot3_blas(0.0, j00, j12, R[c], R[3 + c], R[6 + c]);
-    }
-    double MC[6];
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            MC[3 * r + c] = dot3_blas(M[3 * r], M[3 * r + 1], M[3 * r + 2], cv[c], cv[3 + c], cv[6 + c]);
-    const double a2 = dot3_blas(MC[0], MC[1], MC[2], M[0], M[1], M[2]) + kCovBlur;
-    const double b2 = dot3_blas(MC[0], MC[1], MC[2], M[3], M[4], M[5]);
-    const double c2 = dot3_blas(MC[3], MC[4], MC[5], M[3], M[4], M[5]) + kCovBlur;
-    const double dd = a2 - c2;
-    const double eig = 0.5 * (a2 + c2) + sqrt(fmax(0.25 * (dd * dd) + b2 * b2, 0.0));
-    const double rad = kRadiusSigma * sqrt(eig);
-    const double Wd = (double)cam.width, Hd = (double)cam.height;
-    int u0 = 0, u1 = txn - 1, v0 = 0, v1 = tyn - 1;
-    if (isfinite(mx) && isfinite(my) && isfinite(rad)) {
-        const int x0 = (int)fmin(fmax(floor(mx - rad) - 1.0, 0.0), Wd);
-        const int x1 = (int)fmin(fmax(ceil(mx + rad) + 2.0, 0.0), Wd);
-        const int y0 = (int)fmin(fmax(floor(my - rad) - 1.0, 0.0), Hd);
-        const int y1 = (int)fmin(fmax(ceil(my + rad) + 2.0, 0.0), Hd);
-        if (x1 <= x0 || y1 <= y0) return;
-        int xa = x0, xb = x1 - 1, ya = y0, yb = y1 - 1;
-        const double det = a2 * c2 - b2 * b2;
-        const double t2 = 2.0 * fmax(log(alpha / kEpsContrib) * 1.0002 + 2e-4, 0.0);
-        const double hx = sqrt(t2 * (a2 + 1e-9 * a2)) * 1.0002 + 1e-3;
-        const double hy = sqrt(t2 * (c2 + 1e-9 * c2)) * 1.0002 + 1e-3;
-        if (det > 0.0 && isfinite(hx) && isfinite(hy)) {  // k_project's rec.hx / rec.hy, padded outward
-            const double ex = hx * 1.001 + 2.0, ey = hy * 1.001 + 2.0;
-            xa = max(xa, (int)fmax(floor(mx - 0.5 - ex), -1.0));
-            xb = min(xb, (int)fmin(ceil(mx - 0.5 + ex), Wd));
-            ya = max(ya, (int)fmax(floor(my - 0.5 - ey), -1.0));
-            yb = min(yb, (int)fmin(ceil(my - 0.5 + ey), Hd));
-            if (xa > xb || ya > yb) return;
+        for (int c = 0; c < 3; ++c) {
+            M[c] = dot3_blas(j00, 0.0, j02, R[c], R[3 + c], R[6 + c]);
+            M[3 + c] = dot3_blas(0.0, j00, j12, R[c], R[3 + c], R[6 + c]);
         }
-        u0 = xa / kTile;
-        u1 = xb / kTile;
-        v0 = ya / kTile;
-        v1 = yb / kTile;
-    }
-    for (int v = v0; v <= v1; ++v)
-        for (int u = u0; u <= u1; ++u) {
-            int32_t *q = mr + (int64_t)v * txn + u;
-            if (*q > rk) atomicMin(q, rk);
+        double MC[6];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                MC[3 * r + c] = dot3_blas(M[3 * r], M[3 * r + 1], M[3 * r + 2], cv[c], cv[3 + c], cv[6 + c]);
+        const double a2 = dot3_blas(MC[0], MC[1], MC[2], M[0], M[1], M[2]) + kCovBlur;
+        const double b2 = dot3_blas(MC[0], MC[1], MC[2], M[3], M[4], M[5]);
+        const double c2 = dot3_blas(MC[3], MC[4], MC[5], M[3], M[4], M[5]) + kCovBlur;
+        const double dd = a2 - c2;
+        const double eig = 0.5 * (a2 + c2) + sqrt(fmax(0.25 * (dd * dd) + b2 * b2, 0.0));
+        const double rad = kRadiusSigma * sqrt(eig);
+        const double Wd = (double)cam.width, Hd = (double)cam.height;
+        int u0 = 0, u1 = txn - 1, v0 = 0, v1 = tyn - 1;
+        if (isfinite(mx) && isfinite(my) && isfinite(rad)) {
+            const int x0 = (int)fmin(fmax(floor(mx - rad) - 1.0, 0.0), Wd);
+            const int x1 = (int)fmin(fmax(ceil(mx + rad) + 2.0, 0.0), Wd);
+            const int y0 = (int)fmin(fmax(floor(my - rad) - 1.0, 0.0), Hd);
+            const int y1 = (int)fmin(fmax(ceil(my + rad) + 2.0, 0.0), Hd);
+            if (x1 <= x0 || y1 <= y0) continue;
+            int xa = x0, xb = x1 - 1, ya = y0, yb = y1 - 1;
+            const double det = a2 * c2 - b2 * b2;
+            const double hx = sqrt(t2 * (a2 + 1e-9 * a2)) * 1.0002 + 1e-3;
+            const double hy = sqrt(t2 * (c2 + 1e-9 * c2)) * 1.0002 + 1e-3;
+            if (det > 0.0 && isfinite(hx) && isfinite(hy)) {  // k_project's rec.hx / rec.hy, padded outward
+                const double ex = hx * 1.001 + 2.0, ey = hy * 1.001 + 2.0;
+                xa = max(xa, (int)fmax(floor(mx - 0.5 - ex), -1.0));
+                xb = min(xb, (int)fmin(ceil(mx - 0.5 + ex), Wd));
+                ya = max(ya, (int)fmax(floor(my - 0.5 - ey), -1.0));
+                yb = min(yb, (int)fmin(ceil(my - 0.5 + ey), Hd));
+                if (xa > xb || ya > yb) continue;
+            }
+            u0 = xa / kTile;
+            u1 = xb / kTile;
+            v0 = ya / kTile;
+            v1 = yb / kTile;
         }
+        for (int y = v0; y <= v1; ++y)
+            for (int x = u0; x <= u1; ++x) {
+                int32_t *q = mr + (int64_t)y * txn + x;
+                if (*q > rk) atomicMin(q, rk);
+            }
+    }
 }
 
 static void tile_footprint_impl(airgs_ctx *ctx, const airgs_frame *frame, const airgs_camera *cams, int ncams,
@@ -3395,11 +3398,10 @@ static void tile_footprint_impl(airgs_ctx *ctx, const airgs_frame *frame, const 
         if (ceil_div(c.width, kTile) * ceil_div(c.height, kTile) > tile_stride)
             throw ApiFailure(AIRGS_E_CAPACITY, "tile_stride below a camera's tile count");
     }
-    if (ncams > 65535) throw ApiFailure(AIRGS_E_CAPACITY, "too many cameras");
     airgs_camera *d_cams = ctx->scratch_t<airgs_camera>(kSlotMisc1, (size_t)ncams);
     h2d_small(ctx, d_cams, cams, sizeof(airgs_camera) * ncams, st);
-    const dim3 grid((unsigned)ceil_div(frame->count, 128), (unsigned)ncams);
-    k_tile_footprint<<<grid, 128, 0, st>>>(*frame, d_cams, rank, rank_cap, minrank, tile_stride);
+    k_tile_footprint<<<(unsigned)ceil_div(frame->count, 128), 128, 0, st>>>(*frame, d_cams, ncams, rank, rank_cap,
+                                                                            minrank, tile_stride);
     ++ctx->launches;
     check_launch();
 }
